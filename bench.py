@@ -1,0 +1,407 @@
+"""Benchmark of the approximate-activation training step (BASELINE.json).
+
+    python bench.py [--gpus N --steps K --warmup W] [--impl reference] [--config C2]
+
+Default workload (BASELINE.json configs[1]): ResNet-164
+CIFAR-10 shape, batch 128 per GPU (weak scaling), 4-bit approx tapes, one
+full iteration per step = forward + softmax-xent + backward + (all-reduce)
++ momentum SGD, replayed from one CUDA graph.  Synthetic N(0,1) images, seed 0.
+
+Prints ONE JSON line (rank 0).  ``value`` = whole-job images/s with inputs
+resident in HBM; ``e2e`` = the same through the public Trainer.step() with
+pinned-host H2D of every batch and a D2H of the loss inside the timed
+region; ``roofline`` = the dominant kernel's algorithmic bytes / measured
+time against MEASURED_PEAKS.json; ``cpu_baseline`` = the oracle port of the
+reference (with the reference's own compiled C conv kernel from
+oracle/_ref) timed on this host on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "train images/sec + stored-activation bytes/sample at 4-bit, 1/2/4/8 B200"
+CONFIGS = {
+    "C1": dict(builder="make_residual_spec", batch=32, bits=4, classes=10,
+               workload="C1 small CIFAR ResNet make_residual_spec(8,3,3), batch 32/GPU, 4-bit"),
+    "C2": dict(builder="resnet164_spec", batch=128, bits=4, classes=10,
+               workload="C2 ResNet-164 CIFAR-10 32x32, batch 128/GPU, 4-bit approx tapes"),
+    "C3": dict(builder="resnet1001_spec", batch=128, bits=4, classes=100,
+               workload="C3 ResNet-1001 CIFAR-100 32x32, batch 128/GPU, 4-bit approx tapes"),
+    "C4": dict(builder="resnet152_spec", batch=64, bits=4, classes=1000,
+               workload="C4 ResNet-152 224x224, batch 64/GPU, 4-bit approx tapes"),
+}
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), float(d["bf16_tflops_sustained"]), "measured"
+    except Exception:
+        return 6650.0, 1590.0, "fallback"
+
+
+# ------------------------------------------------------------ cost model
+
+def _geo(args, off):
+    n, ci, h, w, co, kh, kw, s, p = (int(args[off + i]) for i in range(9))
+    oh = (h + 2 * p - kh) // s + 1
+    ow = (w + 2 * p - kw) // s + 1
+    return n, ci, h, w, co, kh, kw, oh, ow
+
+
+def algo_cost(name, a):
+    """(algorithmic HBM bytes, useful FLOPs) of one qt_* call."""
+    if name == "qt_bn_stats":
+        return 4 * a[1] * a[2] * a[3], 0
+    if name == "qt_bn_relu_forward":
+        numel = a[1] * a[2] * a[3]
+        b = 4 * numel + (4 * numel if a[11] else 0) + (4 * numel if a[12] else 0)
+        b += (a[10] * numel + 7) // 8 if a[10] else 0
+        return b, 0
+    if name == "qt_conv_forward":
+        n, ci, h, w, co, kh, kw, oh, ow = _geo(a, 3)
+        b = 4 * (n * ci * h * w + n * co * oh * ow + co * ci * kh * kw)
+        if a[12]:
+            b += 4 * n * int(a[13]) * oh * ow
+        return b, 2 * n * oh * ow * co * ci * kh * kw
+    if name == "qt_conv_dgrad":
+        n, ci, h, w, co, kh, kw, oh, ow = _geo(a, 3)
+        return (4 * (n * co * oh * ow + n * ci * h * w + co * ci * kh * kw),
+                2 * n * oh * ow * co * ci * kh * kw)
+    if name == "qt_conv_wgrad":
+        n, ci, h, w, co, kh, kw, oh, ow = _geo(a, 4)
+        tape = a[1]
+        act = n * ci * h * w
+        ab = (tape.bits * act + 7) // 8 if (tape.codes and not a[2]) else 4 * act
+        return (4 * n * co * oh * ow + ab + 8 * co * ci * kh * kw,
+                2 * n * oh * ow * co * ci * kh * kw)
+    if name in ("qt_bn_backward_reduce", "qt_bn_backward_apply"):
+        tape = a[1]
+        numel = a[2] * a[3] * a[4] * (a[5] if name == "qt_bn_backward_apply" else 1)
+        tb = (tape.bits * numel + 7) // 8 if tape.codes else 4 * numel
+        b = 4 * numel + tb + (4 * numel if name == "qt_bn_backward_apply" else 0)
+        if name == "qt_bn_backward_apply" and a[10]:
+            b += 4 * numel // (int(a[12]) ** 2)
+        return b, 0
+    if name == "qt_copy":
+        return 8 * a[2], 0
+    if name == "qt_sgd":
+        return 16 * a[3], 0
+    return 0, 0
+
+
+class KernelTimer:
+    """_native hook: CUDA events around every qt_* launch on the launching
+    (current) stream."""
+
+    def __init__(self, torch):
+        self.torch = torch
+        self.rec = []
+
+    def before(self, name, args):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record()
+        self._cur = (name, args, e)
+
+    def after(self, name, args):
+        e = self.torch.cuda.Event(enable_timing=True)
+        e.record()
+        self.rec.append((self._cur[0], self._cur[1], self._cur[2], e))
+
+    def summary(self):
+        self.torch.cuda.synchronize()
+        agg = {}
+        for name, args, e0, e1 in self.rec:
+            ms = e0.elapsed_time(e1)
+            b, f = algo_cost(name, args)
+            d = agg.setdefault(name, {"ms": 0.0, "launches": 0, "bytes": 0, "flops": 0})
+            d["ms"] += ms
+            d["launches"] += 1
+            d["bytes"] += b
+            d["flops"] += f
+        return agg
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------- CPU baseline
+
+def _cpu_worker(cfg_name, batch, steps, warmup, q):
+    os.environ["OMP_NUM_THREADS"] = "1"
+    os.environ["OPENBLAS_NUM_THREADS"] = "1"
+    import numpy as np
+    import oracle as O
+    from paper_1901_07988_b200 import engine as E
+    c = CONFIGS[cfg_name]
+    spec = getattr(E, c["builder"])().to_json()
+    rng = np.random.default_rng(0)
+    x = rng.standard_normal((batch,) + tuple(spec["input_shape"])).astype(np.float32)
+    y = rng.integers(0, spec["num_classes"], batch)
+    params = O.init_params(spec, 0)
+    times = []
+    for i in range(warmup + steps):
+        t0 = time.perf_counter()
+        O.train_step(spec, params, x, y, "approx", c["bits"])
+        if i >= warmup:
+            times.append(time.perf_counter() - t0)
+    q.put(times)
+
+
+def cpu_reference(cfg_name, batch, steps, warmup, procs):
+    """Oracle port (+ reference C kernel) on `procs` single-thread replicas;
+    returns (aggregate images/s, median step seconds)."""
+    import multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    ps = [ctx.Process(target=_cpu_worker, args=(cfg_name, batch, steps, warmup, q))
+          for _ in range(procs)]
+    for p in ps:
+        p.start()
+    res = [q.get() for _ in ps]
+    for p in ps:
+        p.join()
+    med = [sorted(t)[len(t) // 2] for t in res]
+    return sum(batch / m for m in med), sorted(med)[len(med) // 2]
+
+
+# ------------------------------------------------------------------ main
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
+    ap.add_argument("--bits", type=int, default=None)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-batch", type=int, default=4)
+    args = ap.parse_args()
+    cfg = CONFIGS[args.config]
+    bits = args.bits or cfg["bits"]
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        procs = max(1, len(os.sched_getaffinity(0)))
+        steps = max(1, args.steps)
+        ips, med = cpu_reference(args.config, args.cpu_batch, steps, max(0, min(args.warmup, 1)),
+                                 procs)
+        line = {
+            "metric": METRIC, "value": ips, "unit": "images/s", "impl": "reference",
+            "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
+            "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (f64 accumulation)", "data": "synthetic",
+            "config": {"workload": cfg["workload"], "sample_batch_per_process": args.cpu_batch,
+                       "processes": procs},
+            "cpu_baseline": {"value": ips, "unit": "images/s", "cores": procs, "kind": "port",
+                             "sample": f"{procs} single-thread replicas x {steps} steps of "
+                                       f"batch {args.cpu_batch} ({args.config} spec)"},
+            "e2e": {"value": ips, "unit": "images/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0},
+        }
+        print(json.dumps(line), flush=True)
+        return
+
+    import numpy as np
+    import torch
+    import paper_1901_07988_b200 as P
+    from paper_1901_07988_b200 import _native as N
+    from paper_1901_07988_b200 import dist as D
+    from paper_1901_07988_b200 import engine as E
+
+    group = None
+    local = 0
+    if world > 1:
+        rank, world, local = D.init_from_env("nccl")
+        group = torch.distributed.group.WORLD
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    spec = getattr(E, cfg["builder"])()
+    n = cfg["batch"]
+    tr = P.Trainer(spec, n, mode="approx", bits=bits, lr=0.1, momentum=0.9,
+                   weight_decay=2e-4 if args.config != "C4" else 1e-4, seed=0, device=dev,
+                   process_group=group)
+    if group is not None:
+        D.broadcast_(tr.params.values, 0)
+    rng = np.random.default_rng(rank)
+    x_host = rng.standard_normal((n,) + tuple(spec.input_shape)).astype(np.float32)
+    y_host = rng.integers(0, spec.num_classes, n).astype(np.int64)
+    tr.load_batch(x_host, y_host)
+    tr.capture()
+
+    # launches per step: count one eager step
+    c0 = N.launch_count[0]
+    tr._body()
+    launches_per_step = N.launch_count[0] - c0
+    torch.cuda.synchronize()
+
+    for _ in range(max(3, args.warmup)):
+        tr.step_device()
+    torch.cuda.synchronize()
+
+    def barrier():
+        if group is not None:
+            torch.distributed.barrier()
+        torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        tr.step_device()
+    e1.record()
+    barrier()
+    ms = e0.elapsed_time(e1) / args.steps
+    ms = D.max_over_ranks(ms, group, dev)
+
+    # end to end through the public API: host batch -> H2D -> step -> D2H loss
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        tr.step(x_host, y_host)
+    barrier()
+    e2e_s = (time.perf_counter() - t0) / args.steps
+    e2e_s = D.max_over_ranks(e2e_s, group, dev)
+    clk = clocks.stop()
+
+    # per-kernel timing of one instrumented eager step (CUDA events on the
+    # launching stream) -> dominant kernel and its roofline
+    timer = KernelTimer(torch)
+    N.hook = timer
+    tr._body()
+    N.hook = None
+    agg = timer.summary()
+    hbm, tc, peak_kind = _peaks()
+    total_ms = sum(d["ms"] for d in agg.values())
+    top = max(agg.items(), key=lambda kv: kv[1]["ms"])
+    name, d = top
+    ai = d["flops"] / d["bytes"] if d["bytes"] else float("inf")
+    ridge = tc * 1e12 / (hbm * 1e9)
+    if d["flops"] and ai > ridge:
+        achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12
+        roof = {"bound": "tensor", "achieved": achieved, "peak": tc, "unit": "TFLOP/s",
+                "frac": achieved / tc}
+    else:
+        achieved = d["bytes"] / (d["ms"] * 1e-3) / 1e9
+        roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
+                "frac": achieved / hbm}
+    roof.update({"kernel": name, "launches_per_step": d["launches"],
+                 "share_of_step": d["ms"] / total_ms if total_ms else None,
+                 "traffic": None, "peak_kind": peak_kind})
+    # step roofline: every launch at its own bound (HBM or tensor), summed
+    step_roof_ms = 0.0
+    for nm, dd in agg.items():
+        step_roof_ms += max(dd["bytes"] / (hbm * 1e9), dd["flops"] / (tc * 1e12)) * 1e3
+    kernels = sorted(({"kernel": k, "ms": v["ms"], "launches": v["launches"],
+                       "GBps": v["bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] else None}
+                      for k, v in agg.items()), key=lambda r: -r["ms"])[:8]
+
+    rep = E.memory_report(spec, (n,) + tuple(spec.input_shape), mode="approx", bits=bits)
+    rep_exact = E.memory_report(spec, (n,) + tuple(spec.input_shape), mode="exact", bits=None)
+    images = n * world
+    value = images / (ms * 1e-3)
+    line = {
+        "metric": METRIC, "value": value, "unit": "images/s", "n_gpus": world,
+        "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "f32", "data": "synthetic N(0,1) images, seed 0, random-init weights",
+        "config": {"workload": cfg["workload"], "global_batch": images, "per_gpu_batch": n,
+                   "bits": bits, "mode": "approx", "parallelism": f"dp{world}",
+                   "l2": f"step working set > L2 (tape arena {tr.arena.code_arena_bytes >> 20} MiB, "
+                         f"{len(spec.layers)} layers streamed per step)"},
+        "stored_activation_bytes_per_sample": rep.persistent_tape_bytes // n,
+        "exact_activation_bytes_per_sample": rep_exact.persistent_tape_bytes // n,
+        "activation_reduction": rep_exact.persistent_tape_bytes / rep.persistent_tape_bytes,
+        "e2e": {"value": images / e2e_s, "unit": "images/s",
+                "h2d_bytes_per_step": tr.h2d_bytes, "d2h_bytes_per_step": tr.d2h_bytes},
+        "gpu_launches": launches_per_step * args.steps,
+        "roofline": roof,
+        "step_roofline": {"ms": step_roof_ms, "frac": step_roof_ms / ms},
+        "kernels": kernels,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        procs = 1
+        ips, med = cpu_reference(args.config, args.cpu_batch, 2, 1, procs)
+        line["cpu_baseline"] = {"value": ips, "unit": "images/s", "cores": procs, "kind": "port",
+                                "sample": f"1 warm-up + 2 steps at batch {args.cpu_batch} of the "
+                                          f"{args.config} network, oracle port + reference C "
+                                          f"conv kernel, 1 thread ({med:.1f} s/step)"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if group is not None:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,205 @@
+/*
+ * qtape_b200 -- C ABI of the B200-native approximate-activation training step
+ * (arXiv 1901.07988).  Built from paper_1901_07988_b200/csrc into
+ * paper_1901_07988_b200/libqtape_b200.so (sm_100a).
+ *
+ * Conventions
+ *   - every pointer is a DEVICE pointer (cudaMalloc'd / torch.cuda storage)
+ *     unless stated; tensors are C-contiguous NCHW float32 ("rank 4") or
+ *     (N, C) ("rank 2", pass hw = 1);
+ *   - packed codes use the reference bit layout exactly: code i of the flat
+ *     NCHW tensor at bits [i*K, (i+1)*K), little-endian inside a byte, tail
+ *     of the last byte zero (reference codec.py:59-78);
+ *   - `stream` is a cudaStream_t (the caller's current torch stream); every
+ *     call is stream-ordered, never synchronises, never allocates, and is
+ *     safe inside CUDA-graph capture;
+ *   - workspaces are caller-owned; their size comes from qt_*_workspace();
+ *   - return value: 0 (QT_OK), a negative QT_E* code for an argument error
+ *     detected before launch, or a positive cudaError_t from the launch.
+ *     There is no CPU fallback anywhere.
+ *
+ * Each entry point names the reference interface it replaces
+ * (/root/reference/pkg/src/qtape/<file>:<line>).
+ */
+#ifndef QTAPE_B200_H
+#define QTAPE_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define QT_OK 0
+#define QT_EINVAL (-1)        /* bad extents / pointer / bit width          */
+#define QT_EUNSUPPORTED (-2)  /* shape outside what the kernels implement  */
+
+typedef void *qt_stream_t;    /* cudaStream_t */
+
+int qt_version(void);
+const char *qt_error_string(int status);
+int qt_num_sms(void);
+
+/* ---------------------------------------------------------------- codec ---
+ * Per-channel codec constants (codec.py:27-29, :101-104, :117):
+ *   step[c]   = 6*max(|gamma_c|,1e-8) * 2^-K           (float64)
+ *   offset[c] = floor(beta_c * 2^K/(6*max(|gamma_c|,1e-8)))  (int64, x86 cast)
+ */
+int qt_codec_constants(const float *gamma, const float *beta, int64_t c, int bits,
+                       double *step, int64_t *offset, qt_stream_t stream);
+
+/* Quantize + pack a pre-ReLU activation tensor a (N,C,HW).
+ * Replaces codec.quantize (codec.py:123-143) incl. raw_codes (:107-120) and
+ * pack_codes (:59-78).  clip_count (one int64, device) is ACCUMULATED into. */
+int qt_quantize_pack(const float *a, int64_t n, int64_t c, int64_t hw,
+                     const float *gamma, const float *beta, int bits,
+                     uint8_t *codes, double *step, int64_t *offset,
+                     int64_t *clip_count, qt_stream_t stream);
+
+/* Decode a tape to interval medians (codec.dequantize, codec.py:146-156;
+ * unpack_codes :81-98).  relu != 0 additionally applies max(.,0). */
+int qt_unpack_dequant(const uint8_t *codes, int64_t n, int64_t c, int64_t hw,
+                      int bits, const double *step, const int64_t *offset,
+                      int relu, float *out, qt_stream_t stream);
+
+/* Raw bit packing of uint8 codes (pack_codes / unpack_codes, codec.py:59-98).
+ * qt_pack_codes writes ceil(count*K/8) bytes; out-of-range codes set
+ * *bad (device int32) to 1 (caller raises CodecError). */
+int qt_pack_codes(const uint8_t *codes, int64_t count, int bits, uint8_t *packed,
+                  int32_t *bad, qt_stream_t stream);
+int qt_unpack_codes(const uint8_t *packed, int64_t count, int bits, uint8_t *codes,
+                    qt_stream_t stream);
+
+/* ------------------------------------------------------------------- BN ---
+ * Per-channel population mean/var over (N,HW), float64 (ops.channel_moments,
+ * ops.py:186-196).  If running_mean/var are non-NULL they are updated as
+ * layer.py:237-241 (r = 0.9 r; r += (1-0.9) batch).  ws: qt_bn_stats_workspace. */
+int64_t qt_bn_stats_workspace(int64_t n, int64_t c, int64_t hw);
+int qt_bn_stats(const float *x, int64_t n, int64_t c, int64_t hw,
+                double *mean, double *var, double *running_mean, double *running_var,
+                void *ws, qt_stream_t stream);
+
+/* Per-channel float64 sum over (N,HW) (ops.channel_sum, ops.py:199-201);
+ * ws: qt_bn_stats_workspace. */
+int qt_channel_sum(const float *x, int64_t n, int64_t c, int64_t hw, double *out,
+                   void *ws, qt_stream_t stream);
+
+/* Fused forward K1: BN apply (4 rounded fp32 ops, layer.py:245-249) ->
+ * tape -> ReLU (layer.py:264).  mode: 0 exact, 1 approx, 2 naive
+ * (layer.py:32); bits 0 = identity bypass (layer.py:256-258).
+ *   a3_out      : ReLU'd activations for the linear transform (the `work` slot)
+ *   a2_tape     : fp32 pre-ReLU copy (exact / bypass tapes), else NULL
+ *   codes/step/offset/clip_count : K-bit tape (approx / naive), else NULL
+ * training == 0 uses mean/var as given (running stats) and writes no tape. */
+int qt_bn_relu_forward(const float *x, int64_t n, int64_t c, int64_t hw,
+                       const double *mean, const double *var, double eps,
+                       const float *gamma, const float *beta, int mode, int bits,
+                       float *a3_out, float *a2_tape, uint8_t *codes, double *step,
+                       int64_t *offset, int64_t *clip_count, qt_stream_t stream);
+
+/* Tape source descriptor used by the backward kernels: either a fp32 pre-ReLU
+ * tape (a2 != NULL) or packed codes + frozen constants. */
+typedef struct {
+    const float *a2;        /* exact tape, or NULL                     */
+    const uint8_t *codes;   /* packed codes, or NULL                   */
+    const double *step;     /* [C] frozen decode step                  */
+    const int64_t *offset;  /* [C] frozen decode offset                */
+    int bits;
+} qt_tape_t;
+
+/* Rebuild (a1, a2, a3) from a tape (layer.reconstruct_from_tape,
+ * layer.py:269-283).  Any output may be NULL. */
+int qt_reconstruct(qt_tape_t tape, int64_t n, int64_t c, int64_t hw,
+                   const float *gamma_tape, const float *beta_tape,
+                   float *a1, float *a2, float *a3, qt_stream_t stream);
+
+/* Backward of mask + scale/bias + normalization (layer.py:353-381 and
+ * bn_input_gradient :286-308), in two launches.
+ *   g3  : gradient w.r.t. the rectified activations (dgrad output), (N,C,HW)
+ *   reduce: accumulates grad_beta += sum(g3*mask), grad_gamma += sum(a1*g3*mask)
+ *           and writes stats[3*C] = {t2[C], t3[C], inv[C]} (float32)
+ *   apply : g_in = ((g1 - t2) - a1v*t3) * inv, g1 = g3*mask*gamma, in place
+ *           allowed (g_in == g3); if res_g != NULL also adds the shortcut
+ *           adjoint (engine.py:272-279): res_g has shape (N,CR,HR,WR) with
+ *           HR = H/sc, CR >= C.
+ * variance_a1 (nullable) replaces a1 in the variance term (diagnostics). */
+int64_t qt_bn_backward_workspace(int64_t n, int64_t c, int64_t hw);
+int qt_bn_backward_reduce(const float *g3, qt_tape_t tape, int64_t n, int64_t c,
+                          int64_t hw, const float *gamma_tape, const float *beta_tape,
+                          const double *sigma2, double eps, const float *variance_a1,
+                          float *grad_gamma, float *grad_beta, float *stats, void *ws,
+                          qt_stream_t stream);
+int qt_bn_backward_apply(const float *g3, qt_tape_t tape, int64_t n, int64_t c,
+                         int64_t h, int64_t w, const float *gamma_tape,
+                         const float *beta_tape, const float *variance_a1,
+                         const float *stats, const float *res_g, int64_t cr,
+                         int64_t sc, float *g_in, qt_stream_t stream);
+
+/* ----------------------------------------------------------------- conv ---
+ * Cross-correlation with zero padding; integral extents are validated by the
+ * caller (ops.conv2d_out_shape, ops.py:80-94).
+ * Forward (ops.conv2d_forward ops.py:106-138; _kernels.c:10-52):
+ *   out = conv(x, w) (+ shortcut(res) if res != NULL, engine.py:262-269;
+ *   res is (N, CR, HR, WR) with CR <= Co and HR = OH*sr). */
+int qt_conv_forward(const float *x, const float *w, float *out,
+                    int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co,
+                    int64_t kh, int64_t kw, int64_t stride, int64_t pad,
+                    const float *res, int64_t cr, int64_t sr, qt_stream_t stream);
+
+/* Data gradient (ops.conv2d_backward g_x path, ops.py:168-183). */
+int qt_conv_dgrad(const float *g, const float *w, float *gx,
+                  int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co,
+                  int64_t kh, int64_t kw, int64_t stride, int64_t pad,
+                  qt_stream_t stream);
+
+/* Weight gradient, accumulated: grad_w += fp32(sum) (ops.py:164-167,
+ * layer.py:167).  The activation operand comes from `act`:
+ *   act.a2 with relu   -> exact tape
+ *   act.codes          -> relu(decode(codes)) fused into operand staging
+ *   x_plain != NULL    -> the plain input (stem, layer.py:340-342). */
+int64_t qt_conv_wgrad_workspace(int64_t n, int64_t ci, int64_t h, int64_t wd,
+                                int64_t co, int64_t kh, int64_t kw, int64_t stride,
+                                int64_t pad);
+int qt_conv_wgrad(const float *g, qt_tape_t act, const float *x_plain, float *grad_w,
+                  int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co,
+                  int64_t kh, int64_t kw, int64_t stride, int64_t pad,
+                  void *ws, qt_stream_t stream);
+
+/* ---------------------------------------------------------- dense / head ---
+ * C[M,N] (=|+=) fp32( sum_k A[m,k] B[k,n] ) with float64 accumulation in
+ * ascending k, one rounding per multiply and add: bit-identical to
+ * ops.matmul (ops.py:54-77).  ta/tb: operand stored transposed. */
+int qt_matmul(const float *a, const float *b, float *c, int64_t m, int64_t k,
+              int64_t nn, int ta, int tb, int accumulate, qt_stream_t stream);
+/* Global average pool (N,C,HW)->(N,C), float64 mean (layer._gap :154-157). */
+int qt_gap(const float *x, int64_t n, int64_t c, int64_t hw, float *out,
+           qt_stream_t stream);
+/* out[n,c,:] = fp32(g[n,c] / hw) broadcast (layer.py:173-179). */
+int qt_gap_backward(const float *g, int64_t n, int64_t c, int64_t hw, float *out,
+                    qt_stream_t stream);
+/* Mean softmax cross-entropy (training.softmax_xent, training.py:120-134).
+ * loss: float64 buffer of 1 + N slots (slot 0 = loss, the rest per-row nll
+ * scratch); grad (N,C) fp32; labels int64; *bad_label set to 1 if a label
+ * lies outside [0, C) (caller raises DataError). */
+int qt_softmax_xent(const float *logits, const int64_t *labels, int64_t n, int64_t c,
+                    double *loss, float *grad, int32_t *bad_label, qt_stream_t stream);
+/* Momentum SGD on a contiguous slab (training.sgd_step, training.py:98-117);
+ * zeroes grad afterwards.  If lr_dev != NULL the learning rate is read from
+ * device memory (so a captured CUDA graph follows a schedule). */
+int qt_sgd(float *value, float *grad, float *vel, int64_t count, float lr,
+           const float *lr_dev, float momentum, float weight_decay, qt_stream_t stream);
+
+/* ------------------------------------------------------------ engine glue ---
+ * res = copy(x) and shortcut add / adjoint (engine.py:262-279) as standalone
+ * kernels (the fused forms live in qt_conv_forward / qt_bn_backward_apply). */
+int qt_copy(const float *src, float *dst, int64_t count, qt_stream_t stream);
+int qt_shortcut_add(float *cur, const float *res, int64_t n, int64_t c, int64_t h,
+                    int64_t w, int64_t cr, int64_t sr, qt_stream_t stream);
+int qt_shortcut_adjoint(float *g_in, const float *g_res, int64_t n, int64_t c,
+                        int64_t h, int64_t w, int64_t cres, int64_t sr,
+                        qt_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* QTAPE_B200_H */

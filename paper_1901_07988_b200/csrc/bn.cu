@@ -1,0 +1,483 @@
+// Batch-norm statistics, the BN/ReLU backward from the tape, reconstruction,
+// global average pooling and the parameter-free shortcut kernels.
+//
+// Reductions are deterministic: a fixed element->thread->block partition,
+// float64 partials, and a last-block-per-channel finalize that reads the
+// partials in block order (no float atomics anywhere).
+#include "common.cuh"
+
+namespace qt {
+
+constexpr int kRThreads = 256;
+constexpr int64_t kTargetPerBlock = 8192;
+// Workspace layout of every reduction: [kCounterBytes of per-channel
+// completion counters (always left at zero)][float64 partials].  Keeping the
+// counters at a fixed offset lets differently-shaped launches share one
+// grow-only buffer.
+constexpr int64_t kMaxChannels = 65535;
+constexpr int64_t kCounterBytes = 65536 * 4;
+
+struct Part {
+    int64_t planes_per_block;  // (n) planes one block reduces for a channel
+    int64_t blocks;            // blocks per channel
+};
+
+static Part partition(int64_t n, int64_t hw) {
+    Part p;
+    p.planes_per_block = std::max<int64_t>(1, kTargetPerBlock / hw);
+    if (p.planes_per_block > n) p.planes_per_block = n;
+    p.blocks = qt_cdiv(n, p.planes_per_block);
+    return p;
+}
+
+// Block-wide deterministic sum of NV doubles; result valid in thread 0.
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double (*smem)[kRThreads / 32]) {
+#pragma unroll
+    for (int j = 0; j < NV; ++j) v[j] = warp_sum(v[j]);
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) smem[j][w] = v[j];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+            double t = 0.0;
+            for (int q = 0; q < kRThreads / 32; ++q) t += smem[j][q];
+            v[j] = t;
+        }
+    }
+}
+
+// Returns true in thread 0 of the last block to finish channel `ch`.
+__device__ __forceinline__ bool last_block(unsigned *counter, unsigned nblocks) {
+    __shared__ bool s_last;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        unsigned prev = atomicAdd(counter, 1u);
+        s_last = (prev == nblocks - 1);
+        if (s_last) *counter = 0;  // re-arm for the next launch / graph replay
+    }
+    __syncthreads();
+    return s_last;
+}
+
+// ------------------------------------------------------------- BN stats ---
+
+struct StatsArgs {
+    const float *x;
+    int64_t n, c, hw;
+    int64_t ppb, nb;
+    double *mean, *var, *rmean, *rvar;
+    double *part;       // [c][nb][2]
+    unsigned *counter;  // [c]
+};
+
+__global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
+    __shared__ double red[2][kRThreads / 32];
+    const int64_t ch = blockIdx.y;
+    const int64_t p0 = (int64_t)blockIdx.x * a.ppb;
+    const int64_t p1 = min(p0 + a.ppb, a.n);
+    const double shift = (double)a.x[ch * a.hw];  // x[0, c, 0]: shifted sums
+    double v[2] = {0.0, 0.0};
+    const int64_t cnt = (p1 - p0) * a.hw;
+    if ((a.hw & 3) == 0) {
+        const int64_t hw4 = a.hw >> 2;
+        for (int64_t e = threadIdx.x; e < cnt / 4; e += kRThreads) {
+            int64_t pl = e / hw4, off = e - pl * hw4;
+            float4 q = __ldg(reinterpret_cast<const float4 *>(a.x + ((p0 + pl) * a.c + ch) * a.hw) + off);
+            double d0 = (double)q.x - shift, d1 = (double)q.y - shift;
+            double d2 = (double)q.z - shift, d3 = (double)q.w - shift;
+            v[0] += (d0 + d1) + (d2 + d3);
+            v[1] += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+        }
+    } else {
+        for (int64_t e = threadIdx.x; e < cnt; e += kRThreads) {
+            int64_t pl = e / a.hw, off = e - pl * a.hw;
+            double d = (double)a.x[((p0 + pl) * a.c + ch) * a.hw + off] - shift;
+            v[0] += d;
+            v[1] += d * d;
+        }
+    }
+    block_sum<2>(v, red);
+    if (threadIdx.x == 0) {
+        double *pp = a.part + (ch * a.nb + blockIdx.x) * 2;
+        pp[0] = v[0];
+        pp[1] = v[1];
+    }
+    if (!last_block(a.counter + ch, (unsigned)a.nb)) return;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        double s1 = 0.0, s2 = 0.0;
+        const volatile double *pp = a.part + ch * a.nb * 2;
+        for (int64_t b = 0; b < a.nb; ++b) {
+            s1 += pp[2 * b];
+            s2 += pp[2 * b + 1];
+        }
+        const double cntd = (double)(a.n * a.hw);
+        const double dm = s1 / cntd;
+        double var = (s2 - s1 * dm) / cntd;
+        if (!(var > 0.0)) var = var != var ? var : 0.0;
+        const double mean = shift + dm;
+        a.mean[ch] = mean;
+        a.var[ch] = var;
+        if (a.rmean) {  // layer.py:237-241
+            const double m = 0.9;
+            a.rmean[ch] = __dadd_rn(__dmul_rn(a.rmean[ch], m), __dmul_rn(1.0 - m, mean));
+            a.rvar[ch] = __dadd_rn(__dmul_rn(a.rvar[ch], m), __dmul_rn(1.0 - m, var));
+        }
+    }
+}
+
+// Plain per-channel float64 sum (ops.channel_sum, ops.py:199-201).
+__global__ void __launch_bounds__(kRThreads) chan_sum_kernel(StatsArgs a) {
+    __shared__ double red[1][kRThreads / 32];
+    const int64_t ch = blockIdx.y;
+    const int64_t p0 = (int64_t)blockIdx.x * a.ppb;
+    const int64_t p1 = min(p0 + a.ppb, a.n);
+    double v[1] = {0.0};
+    const int64_t cnt = (p1 - p0) * a.hw;
+    for (int64_t e = threadIdx.x; e < cnt; e += kRThreads) {
+        int64_t pl = e / a.hw, off = e - pl * a.hw;
+        v[0] += (double)a.x[((p0 + pl) * a.c + ch) * a.hw + off];
+    }
+    block_sum<1>(v, red);
+    if (threadIdx.x == 0) a.part[ch * a.nb + blockIdx.x] = v[0];
+    if (!last_block(a.counter + ch, (unsigned)a.nb)) return;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        double s1 = 0.0;
+        const volatile double *pp = a.part + ch * a.nb;
+        for (int64_t b = 0; b < a.nb; ++b) s1 += pp[b];
+        a.mean[ch] = s1;
+    }
+}
+
+// --------------------------------------------------------- BN backward ---
+
+struct BwdArgs {
+    const float *g3;
+    qt_tape_t tape;
+    int64_t n, c, hw;
+    const float *gamma, *beta;
+    const double *sigma2;
+    double eps;
+    const float *va1;
+    float *grad_gamma, *grad_beta, *stats;
+    int64_t ppb, nb;
+    double *part;       // [c][nb][4]
+    unsigned *counter;  // [c]
+};
+
+struct ElemBwd {
+    float g3m, a1g3m, g1, a1vg1, a1v;
+};
+
+__device__ __forceinline__ ElemBwd bwd_elem(const qt_tape_t &t, const float *va1, int64_t i,
+                                            int ch, float g3, float gam, float bet, float sg) {
+    ElemBwd r;
+    float a2 = tape_value(t, i, ch);
+    float a1 = __fdiv_rn(__fsub_rn(a2, bet), sg);                 // layer.py:364-366
+    r.g3m = __fmul_rn(g3, a2 > 0.f ? 1.f : 0.f);                 // layer.py:355, :368
+    r.a1g3m = __fmul_rn(a1, r.g3m);                              // layer.py:372
+    r.g1 = __fmul_rn(r.g3m, gam);                                // layer.py:373
+    r.a1v = va1 ? va1[i] : a1;
+    r.a1vg1 = __fmul_rn(r.a1v, r.g1);                            // layer.py:301
+    return r;
+}
+
+__global__ void __launch_bounds__(kRThreads) bn_bwd_reduce_kernel(BwdArgs a) {
+    __shared__ double red[4][kRThreads / 32];
+    const int64_t ch = blockIdx.y;
+    const int64_t p0 = (int64_t)blockIdx.x * a.ppb;
+    const int64_t p1 = min(p0 + a.ppb, a.n);
+    const float gam = a.gamma[ch], bet = a.beta[ch], sg = safe_gamma(gam);
+    double v[4] = {0.0, 0.0, 0.0, 0.0};
+    const int64_t cnt = (p1 - p0) * a.hw;
+    for (int64_t e = threadIdx.x; e < cnt; e += kRThreads) {
+        int64_t pl = e / a.hw, off = e - pl * a.hw;
+        int64_t i = ((p0 + pl) * a.c + ch) * a.hw + off;
+        ElemBwd r = bwd_elem(a.tape, a.va1, i, (int)ch, a.g3[i], gam, bet, sg);
+        v[0] += (double)r.g3m;
+        v[1] += (double)r.a1g3m;
+        v[2] += (double)r.g1;
+        v[3] += (double)r.a1vg1;
+    }
+    block_sum<4>(v, red);
+    if (threadIdx.x == 0) {
+        double *pp = a.part + (ch * a.nb + blockIdx.x) * 4;
+        for (int j = 0; j < 4; ++j) pp[j] = v[j];
+    }
+    if (!last_block(a.counter + ch, (unsigned)a.nb)) return;
+    if (threadIdx.x == 0) {
+        __threadfence();
+        double s[4] = {0.0, 0.0, 0.0, 0.0};
+        const volatile double *pp = a.part + ch * a.nb * 4;
+        for (int64_t b = 0; b < a.nb; ++b)
+            for (int j = 0; j < 4; ++j) s[j] += pp[4 * b + j];
+        const double cntd = (double)(a.n * a.hw);
+        if (a.grad_beta) a.grad_beta[ch] = __double2float_rn((double)a.grad_beta[ch] + s[0]);
+        if (a.grad_gamma) a.grad_gamma[ch] = __double2float_rn((double)a.grad_gamma[ch] + s[1]);
+        a.stats[ch] = __double2float_rn(s[2] / cntd);                         // t2
+        a.stats[a.c + ch] = __double2float_rn(s[3] / cntd);                   // t3
+        a.stats[2 * a.c + ch] =
+            __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(a.sigma2[ch], a.eps))));  // inv
+    }
+}
+
+struct ApplyArgs {
+    const float *g3;
+    qt_tape_t tape;
+    int64_t n, c, h, w;
+    const float *gamma, *beta, *va1, *stats, *res;
+    int64_t cr, sc;
+    float *g_in;
+};
+
+__global__ void __launch_bounds__(kRThreads) bn_bwd_apply_kernel(ApplyArgs a) {
+    const int64_t hw = a.h * a.w;
+    const int64_t numel = a.n * a.c * hw;
+    for (int64_t i = (int64_t)blockIdx.x * kRThreads + threadIdx.x; i < numel;
+         i += (int64_t)gridDim.x * kRThreads) {
+        const int64_t pl = i / hw;
+        const int ch = (int)(pl % a.c);
+        const float gam = a.gamma[ch];
+        ElemBwd r = bwd_elem(a.tape, a.va1, i, ch, a.g3[i], gam, a.beta[ch], safe_gamma(gam));
+        float o = __fsub_rn(r.g1, a.stats[ch]);                           // layer.py:305
+        o = __fsub_rn(o, __fmul_rn(r.a1v, a.stats[a.c + ch]));            // :306
+        o = __fmul_rn(o, a.stats[2 * a.c + ch]);                          // :307
+        if (a.res) {  // shortcut adjoint, engine.py:272-279
+            const int64_t p = i - pl * hw;
+            const int64_t y = p / a.w, x = p - y * a.w;
+            if (a.sc == 1 && a.cr == a.c) {
+                o = __fadd_rn(o, a.res[i]);
+            } else if (y % a.sc == 0 && x % a.sc == 0) {
+                const int64_t nn = pl / a.c;
+                const int64_t hr = a.h / a.sc, wr = a.w / a.sc;
+                o = __fadd_rn(o, a.res[((nn * a.cr + ch) * hr + y / a.sc) * wr + x / a.sc]);
+            }
+        }
+        a.g_in[i] = o;
+    }
+}
+
+// ------------------------------------------------------- reconstruct ---
+
+__global__ void reconstruct_kernel(qt_tape_t t, int64_t numel, int64_t c, int64_t hw,
+                                   const float *gamma, const float *beta, float *a1, float *a2,
+                                   float *a3) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < numel;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int ch = (int)((i / hw) % c);
+        float v = tape_value(t, i, ch);
+        if (a2) a2[i] = v;
+        if (a3) a3[i] = (v >= 0.f || isnan(v)) ? v : 0.f;
+        if (a1) a1[i] = __fdiv_rn(__fsub_rn(v, beta[ch]), safe_gamma(gamma[ch]));
+    }
+}
+
+// -------------------------------------------------------------- GAP ---
+
+__global__ void gap_kernel(const float *x, int64_t planes, int64_t hw, float *out) {
+    const int64_t pl = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
+    if (pl >= planes) return;
+    const int lane = threadIdx.x & 31;
+    double s = 0.0;
+    for (int64_t e = lane; e < hw; e += 32) s += (double)x[pl * hw + e];
+    s = warp_sum(s);
+    if (lane == 0) out[pl] = __double2float_rn(s / (double)hw);
+}
+
+__global__ void gap_bwd_kernel(const float *g, int64_t planes, int64_t hw, float *out) {
+    const int64_t numel = planes * hw;
+    const float fhw = (float)hw;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < numel;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = __fdiv_rn(g[i / hw], fhw);
+}
+
+// --------------------------------------------------------- shortcut ---
+
+__global__ void copy_kernel(const float4 *src, float4 *dst, int64_t n4) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+__global__ void copy1_kernel(const float *src, float *dst, int64_t n) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        dst[i] = src[i];
+}
+
+// cur (N,C,H,W) += res (N,CR,H*sr,W*sr) on channels < CR (engine.py:262-269)
+__global__ void shortcut_add_kernel(float *cur, const float *res, int64_t n, int64_t c, int64_t h,
+                                    int64_t w, int64_t cr, int64_t sr) {
+    const int64_t numel = n * c * h * w;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < numel;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t x = i % w, t = i / w;
+        int64_t y = t % h;
+        t /= h;
+        int64_t ch = t % c, nn = t / c;
+        if (ch >= cr) continue;
+        float r = res[((nn * cr + ch) * (h * sr) + y * sr) * (w * sr) + x * sr];
+        cur[i] = __fadd_rn(cur[i], r);
+    }
+}
+
+// g_in (N,C,H,W)[:, :, ::s, ::s] += g_res (N,CRES,H/s,W/s)[:, :C] (engine.py:272-279)
+__global__ void shortcut_adj_kernel(float *g_in, const float *g_res, int64_t n, int64_t c,
+                                    int64_t h, int64_t w, int64_t cres, int64_t sr) {
+    const int64_t hr = h / sr, wr = w / sr;
+    const int64_t numel = n * c * hr * wr;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < numel;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t x = i % wr, t = i / wr;
+        int64_t y = t % hr;
+        t /= hr;
+        int64_t ch = t % c, nn = t / c;
+        float *d = g_in + ((nn * c + ch) * h + y * sr) * w + x * sr;
+        *d = __fadd_rn(*d, g_res[((nn * cres + ch) * hr + y) * wr + x]);
+    }
+}
+
+static unsigned grid_for(int64_t n, int threads) {
+    int64_t b = qt_cdiv(n, threads);
+    if (b > 148 * 64) b = 148 * 64;
+    return (unsigned)std::max<int64_t>(b, 1);
+}
+
+}  // namespace qt
+
+using namespace qt;
+
+extern "C" int64_t qt_bn_stats_workspace(int64_t n, int64_t c, int64_t hw) {
+    Part p = partition(n, hw);
+    return kCounterBytes + c * p.blocks * 2 * (int64_t)sizeof(double);
+}
+
+extern "C" int qt_bn_stats(const float *x, int64_t n, int64_t c, int64_t hw, double *mean,
+                           double *var, double *running_mean, double *running_var, void *ws,
+                           qt_stream_t stream) {
+    QT_REQUIRE(x && mean && var && ws && n > 0 && c > 0 && hw > 0 && c <= kMaxChannels);
+    QT_REQUIRE((running_mean == nullptr) == (running_var == nullptr));
+    Part p = partition(n, hw);
+    StatsArgs a{x, n, c, hw, p.planes_per_block, p.blocks, mean, var, running_mean, running_var,
+                (double *)((char *)ws + kCounterBytes), (unsigned *)ws};
+    dim3 grid((unsigned)p.blocks, (unsigned)c);
+    bn_stats_kernel<<<grid, kRThreads, 0, qt_s(stream)>>>(a);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+extern "C" int qt_channel_sum(const float *x, int64_t n, int64_t c, int64_t hw, double *out,
+                              void *ws, qt_stream_t stream) {
+    QT_REQUIRE(x && out && ws && n > 0 && c > 0 && hw > 0 && c <= kMaxChannels);
+    Part p = partition(n, hw);
+    StatsArgs a{x, n, c, hw, p.planes_per_block, p.blocks, out, nullptr, nullptr, nullptr,
+                (double *)((char *)ws + kCounterBytes), (unsigned *)ws};
+    dim3 grid((unsigned)p.blocks, (unsigned)c);
+    chan_sum_kernel<<<grid, kRThreads, 0, qt_s(stream)>>>(a);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+extern "C" int64_t qt_bn_backward_workspace(int64_t n, int64_t c, int64_t hw) {
+    Part p = partition(n, hw);
+    return kCounterBytes + c * p.blocks * 4 * (int64_t)sizeof(double);
+}
+
+extern "C" int qt_bn_backward_reduce(const float *g3, qt_tape_t tape, int64_t n, int64_t c,
+                                     int64_t hw, const float *gamma_tape, const float *beta_tape,
+                                     const double *sigma2, double eps, const float *variance_a1,
+                                     float *grad_gamma, float *grad_beta, float *stats, void *ws,
+                                     qt_stream_t stream) {
+    QT_REQUIRE(g3 && gamma_tape && beta_tape && sigma2 && stats && ws);
+    QT_REQUIRE(n > 0 && c > 0 && hw > 0 && c <= kMaxChannels);
+    QT_REQUIRE(tape.a2 || (tape.codes && tape.step && tape.offset && qt_bits_ok(tape.bits)));
+    Part p = partition(n, hw);
+    BwdArgs a{g3, tape, n, c, hw, gamma_tape, beta_tape, sigma2, eps, variance_a1, grad_gamma,
+              grad_beta, stats, p.planes_per_block, p.blocks,
+              (double *)((char *)ws + kCounterBytes), (unsigned *)ws};
+    dim3 grid((unsigned)p.blocks, (unsigned)c);
+    bn_bwd_reduce_kernel<<<grid, kRThreads, 0, qt_s(stream)>>>(a);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+extern "C" int qt_bn_backward_apply(const float *g3, qt_tape_t tape, int64_t n, int64_t c,
+                                    int64_t h, int64_t w, const float *gamma_tape,
+                                    const float *beta_tape, const float *variance_a1,
+                                    const float *stats, const float *res_g, int64_t cr, int64_t sc,
+                                    float *g_in, qt_stream_t stream) {
+    QT_REQUIRE(g3 && gamma_tape && beta_tape && stats && g_in && n > 0 && c > 0 && h > 0 && w > 0);
+    QT_REQUIRE(tape.a2 || (tape.codes && tape.step && tape.offset && qt_bits_ok(tape.bits)));
+    QT_REQUIRE(!res_g || (sc >= 1 && h % sc == 0 && w % sc == 0 && cr >= c));
+    ApplyArgs a{g3, tape, n, c, h, w, gamma_tape, beta_tape, variance_a1, stats, res_g, cr, sc, g_in};
+    bn_bwd_apply_kernel<<<grid_for(n * c * h * w, kRThreads), kRThreads, 0, qt_s(stream)>>>(a);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+extern "C" int qt_reconstruct(qt_tape_t tape, int64_t n, int64_t c, int64_t hw,
+                              const float *gamma_tape, const float *beta_tape, float *a1,
+                              float *a2, float *a3, qt_stream_t stream) {
+    QT_REQUIRE(n > 0 && c > 0 && hw > 0 && gamma_tape && beta_tape);
+    QT_REQUIRE(tape.a2 || (tape.codes && tape.step && tape.offset && qt_bits_ok(tape.bits)));
+    int64_t numel = n * c * hw;
+    reconstruct_kernel<<<grid_for(numel, 256), 256, 0, qt_s(stream)>>>(tape, numel, c, hw, gamma_tape,
+                                                                    beta_tape, a1, a2, a3);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+extern "C" int qt_gap(const float *x, int64_t n, int64_t c, int64_t hw, float *out,
+                      qt_stream_t stream) {
+    QT_REQUIRE(x && out && n > 0 && c > 0 && hw > 0);
+    int64_t planes = n * c;
+    gap_kernel<<<(unsigned)qt_cdiv(planes, 8), 256, 0, qt_s(stream)>>>(x, planes, hw, out);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+extern "C" int qt_gap_backward(const float *g, int64_t n, int64_t c, int64_t hw, float *out,
+                               qt_stream_t stream) {
+    QT_REQUIRE(g && out && n > 0 && c > 0 && hw > 0);
+    gap_bwd_kernel<<<grid_for(n * c * hw, 256), 256, 0, qt_s(stream)>>>(g, n * c, hw, out);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+extern "C" int qt_copy(const float *src, float *dst, int64_t count, qt_stream_t stream) {
+    QT_REQUIRE(count >= 0 && (count == 0 || (src && dst)));
+    if (count == 0) return QT_OK;
+    if ((count & 3) == 0 && (((uintptr_t)src | (uintptr_t)dst) & 15) == 0)
+        copy_kernel<<<grid_for(count / 4, 256), 256, 0, qt_s(stream)>>>(
+            (const float4 *)src, (float4 *)dst, count / 4);
+    else
+        copy1_kernel<<<grid_for(count, 256), 256, 0, qt_s(stream)>>>(src, dst, count);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+extern "C" int qt_shortcut_add(float *cur, const float *res, int64_t n, int64_t c, int64_t h,
+                               int64_t w, int64_t cr, int64_t sr, qt_stream_t stream) {
+    QT_REQUIRE(cur && res && n > 0 && c > 0 && h > 0 && w > 0 && cr > 0 && cr <= c && sr >= 1);
+    shortcut_add_kernel<<<grid_for(n * c * h * w, 256), 256, 0, qt_s(stream)>>>(cur, res, n, c, h, w,
+                                                                             cr, sr);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+extern "C" int qt_shortcut_adjoint(float *g_in, const float *g_res, int64_t n, int64_t c, int64_t h,
+                                   int64_t w, int64_t cres, int64_t sr, qt_stream_t stream) {
+    QT_REQUIRE(g_in && g_res && n > 0 && c > 0 && h > 0 && w > 0 && cres >= c && sr >= 1);
+    QT_REQUIRE(h % sr == 0 && w % sr == 0);
+    shortcut_adj_kernel<<<grid_for(n * c * (h / sr) * (w / sr), 256), 256, 0, qt_s(stream)>>>(
+        g_in, g_res, n, c, h, w, cres, sr);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}

@@ -1,0 +1,406 @@
+// K-bit activation codec and the fused forward K1 (BN apply -> tape -> ReLU).
+//
+// Bit-exact with the reference codec (codec.py:59-156) and BN apply
+// (layer.py:245-264): every float op is an explicit round-to-nearest
+// intrinsic (no FMA contraction, no FTZ) and the float64 -> int64 cast
+// emulates x86 numpy (see common.cuh).
+//
+// Layout: a thread owns a group of 8 consecutive flat-NCHW elements, i.e.
+// K bytes of packed codes (K in {1,2,4,8}); a 256-thread block owns 2048
+// consecutive elements.  Loads/stores are 128-bit for the fp32 streams and
+// one K-byte store for the codes, so a warp writes 32*K contiguous code
+// bytes.  Per-(n,c)-plane constants (mean/inv/gamma/beta/scale/offset) are
+// computed once per block into shared memory.
+#include "common.cuh"
+
+namespace qt {
+
+constexpr int kThreads = 256;
+constexpr int kGroup = 8;
+constexpr int kBlockElems = kThreads * kGroup;
+constexpr int kMaxPlanes = 258;  // planes a 2048-element block can touch for hw >= 8
+
+struct PlaneConst {
+    double scale;
+    double step;
+    int64_t off;
+    float m32, inv32, g, b;
+};
+
+enum { MODE_EXACT = 0, MODE_APPROX = 1, MODE_NAIVE = 2 };
+
+struct FwdArgs {
+    const float *x;
+    int64_t numel, c, hw;
+    const double *mean, *var;
+    double eps;
+    const float *gamma, *beta;
+    int mode, bits;  // bits == 0: identity bypass (no codes)
+    float *a3_out;
+    float *a2_tape;
+    uint8_t *codes;
+    double *step;
+    int64_t *offset;
+    unsigned long long *clip_count;
+};
+
+__device__ __forceinline__ PlaneConst make_plane(const FwdArgs &a, int64_t ch, bool apply_bn) {
+    PlaneConst p;
+    if (apply_bn) {
+        double inv = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(a.var[ch], a.eps)));  // layer.py:245
+        p.m32 = __double2float_rn(a.mean[ch]);
+        p.inv32 = __double2float_rn(inv);
+    } else {
+        p.m32 = 0.f;
+        p.inv32 = 1.f;
+    }
+    p.g = a.gamma[ch];
+    p.b = a.beta[ch];
+    if (a.bits) {
+        ChanCode cc = chan_code(p.g, p.b, a.bits);
+        p.scale = cc.scale;
+        p.step = cc.step;
+        p.off = cc.off;
+    }
+    return p;
+}
+
+__device__ __forceinline__ float relu_np(float v) {
+    // np.maximum(v, 0): keeps NaN and -0.0 (layer.py:264)
+    return (v >= 0.f || isnan(v)) ? v : 0.f;
+}
+
+template <bool APPLY_BN>
+__global__ void __launch_bounds__(kThreads) bn_relu_quant_kernel(FwdArgs a) {
+    __shared__ PlaneConst sp[kMaxPlanes];
+    __shared__ unsigned long long s_clip[kThreads / 32];
+
+    const int64_t blk0 = (int64_t)blockIdx.x * kBlockElems;
+    const int64_t blk1 = min(blk0 + kBlockElems, a.numel);
+    const int64_t plane0 = blk0 / a.hw;
+    const int64_t nplanes = (blk1 - 1) / a.hw - plane0 + 1;
+    const bool staged = nplanes <= kMaxPlanes;
+    if (staged) {
+        for (int64_t q = threadIdx.x; q < nplanes; q += kThreads)
+            sp[q] = make_plane(a, (plane0 + q) % a.c, APPLY_BN);
+    }
+    // tape constants: frozen step/offset per channel (codec.py:137-143)
+    if (a.bits && a.step) {
+        for (int64_t ch = (int64_t)blockIdx.x * kThreads + threadIdx.x; ch < a.c;
+             ch += (int64_t)gridDim.x * kThreads) {
+            ChanCode cc = chan_code(a.gamma[ch], a.beta[ch], a.bits);
+            a.step[ch] = cc.step;
+            a.offset[ch] = cc.off;
+        }
+    }
+    __syncthreads();
+
+    const int64_t i0 = blk0 + (int64_t)threadIdx.x * kGroup;
+    unsigned long long clip = 0;
+    if (i0 < a.numel) {
+        const int cnt = (int)min((int64_t)kGroup, a.numel - i0);
+        float xv[kGroup];
+        const bool vec = (cnt == kGroup) && ((((uintptr_t)(a.x + i0)) & 15) == 0);
+        if (vec) {
+            float4 u = __ldg(reinterpret_cast<const float4 *>(a.x + i0));
+            float4 v = __ldg(reinterpret_cast<const float4 *>(a.x + i0) + 1);
+            xv[0] = u.x; xv[1] = u.y; xv[2] = u.z; xv[3] = u.w;
+            xv[4] = v.x; xv[5] = v.y; xv[6] = v.z; xv[7] = v.w;
+        } else {
+#pragma unroll
+            for (int j = 0; j < kGroup; ++j) xv[j] = j < cnt ? a.x[i0 + j] : 0.f;
+        }
+        float a2v[kGroup], a3v[kGroup];
+        uint64_t word = 0;
+        int64_t pl = i0 / a.hw;
+        int64_t rem = i0 - pl * a.hw;
+        PlaneConst pc = staged ? sp[pl - plane0] : make_plane(a, pl % a.c, APPLY_BN);
+#pragma unroll
+        for (int j = 0; j < kGroup; ++j) {
+            if (j < cnt) {
+                if (rem == a.hw) {  // crossed into the next (n,c) plane
+                    ++pl;
+                    rem = 0;
+                    pc = staged ? sp[pl - plane0] : make_plane(a, pl % a.c, APPLY_BN);
+                }
+                float v = xv[j];
+                if (APPLY_BN) {  // four separately rounded ops, layer.py:246-249
+                    v = __fsub_rn(v, pc.m32);
+                    v = __fmul_rn(v, pc.inv32);
+                    v = __fmul_rn(v, pc.g);
+                    v = __fadd_rn(v, pc.b);
+                }
+                a2v[j] = v;
+                float pre = v;
+                if (a.bits) {
+                    int64_t raw = raw_code(v, pc.scale, pc.off, a.bits);
+                    const int64_t top = (1ll << a.bits) - 1;
+                    clip += (raw < 0 || raw > top);
+                    uint32_t code = (uint32_t)(raw < 0 ? 0 : (raw > top ? top : raw));
+                    word |= (uint64_t)code << (j * a.bits);
+                    if (a.mode == MODE_NAIVE) pre = decode(code, pc.step, pc.off, a.bits);
+                }
+                a3v[j] = relu_np(pre);
+                ++rem;
+            } else {
+                a2v[j] = 0.f;
+                a3v[j] = 0.f;
+            }
+        }
+        if (vec) {
+            if (a.a2_tape) {
+                float4 *d = reinterpret_cast<float4 *>(a.a2_tape + i0);
+                d[0] = make_float4(a2v[0], a2v[1], a2v[2], a2v[3]);
+                d[1] = make_float4(a2v[4], a2v[5], a2v[6], a2v[7]);
+            }
+            if (a.a3_out) {
+                float4 *d = reinterpret_cast<float4 *>(a.a3_out + i0);
+                d[0] = make_float4(a3v[0], a3v[1], a3v[2], a3v[3]);
+                d[1] = make_float4(a3v[4], a3v[5], a3v[6], a3v[7]);
+            }
+        } else {
+            for (int j = 0; j < cnt; ++j) {
+                if (a.a2_tape) a.a2_tape[i0 + j] = a2v[j];
+                if (a.a3_out) a.a3_out[i0 + j] = a3v[j];
+            }
+        }
+        if (a.bits && a.codes) {
+            // group g = i0/8 owns bytes [g*K, g*K + K)
+            uint8_t *dst = a.codes + (i0 / kGroup) * a.bits;
+            if (cnt == kGroup) {
+                switch (a.bits) {
+                    case 8: *reinterpret_cast<uint2 *>(dst) = make_uint2((uint32_t)word, (uint32_t)(word >> 32)); break;
+                    case 4: *reinterpret_cast<uint32_t *>(dst) = (uint32_t)word; break;
+                    case 2: *reinterpret_cast<uint16_t *>(dst) = (uint16_t)word; break;
+                    default: *dst = (uint8_t)word; break;
+                }
+            } else {
+                const int nbytes = (cnt * a.bits + 7) / 8;
+                for (int b = 0; b < nbytes; ++b) dst[b] = (uint8_t)(word >> (8 * b));
+            }
+        }
+    }
+    if (a.clip_count) {
+        clip = warp_sum(clip);
+        if ((threadIdx.x & 31) == 0) s_clip[threadIdx.x >> 5] = clip;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            for (int w = 0; w < kThreads / 32; ++w) t += s_clip[w];
+            if (t) atomicAdd(a.clip_count, t);
+        }
+    }
+}
+
+struct DecArgs {
+    const uint8_t *codes;
+    int64_t numel, c, hw;
+    int bits;
+    const double *step;
+    const int64_t *offset;
+    int relu;
+    float *out;
+};
+
+__global__ void __launch_bounds__(kThreads) unpack_dequant_kernel(DecArgs a) {
+    __shared__ double s_step[kMaxPlanes];
+    __shared__ int64_t s_off[kMaxPlanes];
+    const int64_t blk0 = (int64_t)blockIdx.x * kBlockElems;
+    const int64_t blk1 = min(blk0 + kBlockElems, a.numel);
+    const int64_t plane0 = blk0 / a.hw;
+    const int64_t nplanes = (blk1 - 1) / a.hw - plane0 + 1;
+    const bool staged = nplanes <= kMaxPlanes;
+    if (staged) {
+        for (int64_t q = threadIdx.x; q < nplanes; q += kThreads) {
+            int64_t ch = (plane0 + q) % a.c;
+            s_step[q] = a.step[ch];
+            s_off[q] = a.offset[ch];
+        }
+    }
+    __syncthreads();
+    const int64_t i0 = blk0 + (int64_t)threadIdx.x * kGroup;
+    if (i0 >= a.numel) return;
+    const int cnt = (int)min((int64_t)kGroup, a.numel - i0);
+    const uint8_t *src = a.codes + (i0 / kGroup) * a.bits;
+    uint64_t word = 0;
+    if (cnt == kGroup) {
+        switch (a.bits) {
+            case 8: { uint2 u = *reinterpret_cast<const uint2 *>(src); word = u.x | ((uint64_t)u.y << 32); break; }
+            case 4: word = *reinterpret_cast<const uint32_t *>(src); break;
+            case 2: word = *reinterpret_cast<const uint16_t *>(src); break;
+            default: word = *src; break;
+        }
+    } else {
+        const int nbytes = (cnt * a.bits + 7) / 8;
+        for (int b = 0; b < nbytes; ++b) word |= (uint64_t)src[b] << (8 * b);
+    }
+    float v[kGroup];
+    int64_t pl = i0 / a.hw;
+    int64_t rem = i0 - pl * a.hw;
+    const uint32_t mask = (1u << a.bits) - 1u;
+#pragma unroll
+    for (int j = 0; j < kGroup; ++j) {
+        if (j < cnt) {
+            if (rem == a.hw) { ++pl; rem = 0; }
+            double st;
+            int64_t of;
+            if (staged) { st = s_step[pl - plane0]; of = s_off[pl - plane0]; }
+            else { int64_t ch = pl % a.c; st = a.step[ch]; of = a.offset[ch]; }
+            float d = decode((uint32_t)(word >> (j * a.bits)) & mask, st, of, a.bits);
+            v[j] = a.relu ? relu_np(d) : d;
+            ++rem;
+        } else {
+            v[j] = 0.f;
+        }
+    }
+    if (cnt == kGroup && ((((uintptr_t)(a.out + i0)) & 15) == 0)) {
+        float4 *d = reinterpret_cast<float4 *>(a.out + i0);
+        d[0] = make_float4(v[0], v[1], v[2], v[3]);
+        d[1] = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+        for (int j = 0; j < cnt; ++j) a.out[i0 + j] = v[j];
+    }
+}
+
+__global__ void codec_constants_kernel(const float *gamma, const float *beta, int64_t c,
+                                       int bits, double *step, int64_t *offset) {
+    int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (ch >= c) return;
+    ChanCode cc = chan_code(gamma[ch], beta[ch], bits);
+    step[ch] = cc.step;
+    offset[ch] = cc.off;
+}
+
+__global__ void pack_kernel(const uint8_t *codes, int64_t count, int bits, uint8_t *packed,
+                            int64_t nbytes, int32_t *bad) {
+    int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (b >= nbytes) return;
+    const int per = 8 / bits;
+    uint32_t out = 0;
+    bool oob = false;
+    for (int j = 0; j < per; ++j) {
+        int64_t i = b * per + j;
+        if (i < count) {
+            uint32_t v = codes[i];
+            oob |= v >= (1u << bits);
+            out |= (v & ((1u << bits) - 1u)) << (j * bits);
+        }
+    }
+    packed[b] = (uint8_t)out;
+    if (oob && bad) *bad = 1;
+}
+
+__global__ void unpack_kernel(const uint8_t *packed, int64_t count, int bits, uint8_t *codes) {
+    int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= count) return;
+    codes[i] = (uint8_t)get_code(packed, i, bits);
+}
+
+static int launch_fwd(const FwdArgs &a, bool apply_bn, cudaStream_t s) {
+    if (a.numel == 0) return QT_OK;
+    int64_t blocks = qt_cdiv(a.numel, kBlockElems);
+    if (blocks > 0x7fffffff) return QT_EUNSUPPORTED;
+    if (apply_bn)
+        bn_relu_quant_kernel<true><<<(unsigned)blocks, kThreads, 0, s>>>(a);
+    else
+        bn_relu_quant_kernel<false><<<(unsigned)blocks, kThreads, 0, s>>>(a);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+}  // namespace qt
+
+using namespace qt;
+
+extern "C" int qt_codec_constants(const float *gamma, const float *beta, int64_t c, int bits,
+                                  double *step, int64_t *offset, qt_stream_t stream) {
+    QT_REQUIRE(qt_bits_ok(bits) && c >= 0 && gamma && beta && step && offset);
+    if (c == 0) return QT_OK;
+    codec_constants_kernel<<<(unsigned)qt_cdiv(c, 256), 256, 0, qt_s(stream)>>>(gamma, beta, c, bits,
+                                                                              step, offset);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+extern "C" int qt_quantize_pack(const float *a, int64_t n, int64_t c, int64_t hw,
+                                const float *gamma, const float *beta, int bits, uint8_t *codes,
+                                double *step, int64_t *offset, int64_t *clip_count,
+                                qt_stream_t stream) {
+    QT_REQUIRE(qt_bits_ok(bits) && n >= 0 && c > 0 && hw > 0 && a && gamma && beta && codes);
+    FwdArgs f{};
+    f.x = a;
+    f.numel = n * c * hw;
+    f.c = c;
+    f.hw = hw;
+    f.gamma = gamma;
+    f.beta = beta;
+    f.mode = MODE_APPROX;
+    f.bits = bits;
+    f.codes = codes;
+    f.step = step;
+    f.offset = offset;
+    f.clip_count = reinterpret_cast<unsigned long long *>(clip_count);
+    return launch_fwd(f, false, qt_s(stream));
+}
+
+extern "C" int qt_bn_relu_forward(const float *x, int64_t n, int64_t c, int64_t hw,
+                                  const double *mean, const double *var, double eps,
+                                  const float *gamma, const float *beta, int mode, int bits,
+                                  float *a3_out, float *a2_tape, uint8_t *codes, double *step,
+                                  int64_t *offset, int64_t *clip_count, qt_stream_t stream) {
+    QT_REQUIRE(n >= 0 && c > 0 && hw > 0 && x && mean && var && gamma && beta);
+    QT_REQUIRE(mode >= 0 && mode <= 2);
+    QT_REQUIRE(bits == 0 || qt_bits_ok(bits));
+    QT_REQUIRE(bits == 0 || codes);
+    FwdArgs f{};
+    f.x = x;
+    f.numel = n * c * hw;
+    f.c = c;
+    f.hw = hw;
+    f.mean = mean;
+    f.var = var;
+    f.eps = eps;
+    f.gamma = gamma;
+    f.beta = beta;
+    f.mode = mode;
+    f.bits = bits;
+    f.a3_out = a3_out;
+    f.a2_tape = a2_tape;
+    f.codes = codes;
+    f.step = step;
+    f.offset = offset;
+    f.clip_count = reinterpret_cast<unsigned long long *>(clip_count);
+    return launch_fwd(f, true, qt_s(stream));
+}
+
+extern "C" int qt_unpack_dequant(const uint8_t *codes, int64_t n, int64_t c, int64_t hw, int bits,
+                                 const double *step, const int64_t *offset, int relu, float *out,
+                                 qt_stream_t stream) {
+    QT_REQUIRE(qt_bits_ok(bits) && n >= 0 && c > 0 && hw > 0 && codes && step && offset && out);
+    DecArgs d{codes, n * c * hw, c, hw, bits, step, offset, relu, out};
+    if (d.numel == 0) return QT_OK;
+    int64_t blocks = qt_cdiv(d.numel, kBlockElems);
+    unpack_dequant_kernel<<<(unsigned)blocks, kThreads, 0, qt_s(stream)>>>(d);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+extern "C" int qt_pack_codes(const uint8_t *codes, int64_t count, int bits, uint8_t *packed,
+                             int32_t *bad, qt_stream_t stream) {
+    QT_REQUIRE(qt_bits_ok(bits) && count >= 0 && (count == 0 || (codes && packed)));
+    int64_t nbytes = (count * bits + 7) / 8;
+    if (nbytes == 0) return QT_OK;
+    pack_kernel<<<(unsigned)qt_cdiv(nbytes, 256), 256, 0, qt_s(stream)>>>(codes, count, bits, packed,
+                                                                        nbytes, bad);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+extern "C" int qt_unpack_codes(const uint8_t *packed, int64_t count, int bits, uint8_t *codes,
+                               qt_stream_t stream) {
+    QT_REQUIRE(qt_bits_ok(bits) && count >= 0 && (count == 0 || (codes && packed)));
+    if (count == 0) return QT_OK;
+    unpack_kernel<<<(unsigned)qt_cdiv(count, 256), 256, 0, qt_s(stream)>>>(packed, count, bits, codes);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}

@@ -1,0 +1,104 @@
+// Shared device helpers for the qtape_b200 kernels (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "../../include/qtape_b200.h"
+
+#define QT_CHECK_LAUNCH()                              \
+    do {                                               \
+        cudaError_t e__ = cudaGetLastError();          \
+        if (e__ != cudaSuccess) return (int)e__;       \
+    } while (0)
+
+#define QT_REQUIRE(cond)                               \
+    do {                                               \
+        if (!(cond)) return QT_EINVAL;                 \
+    } while (0)
+
+static inline cudaStream_t qt_s(qt_stream_t s) { return (cudaStream_t)s; }
+
+static inline bool qt_bits_ok(int b) { return b == 1 || b == 2 || b == 4 || b == 8; }
+
+static inline int64_t qt_cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+namespace qt {
+
+constexpr double kGammaFloor = 1e-8;   // codec.py:24
+constexpr float kGammaFloorF = 1e-8f;  // layer.py:134 (dtype.type(GAMMA_FLOOR))
+
+// x86 numpy float64 -> int64 cast: cvttsd2si yields INT64_MIN ("integer
+// indefinite") for NaN, +-inf and anything outside [-2^63, 2^63).
+__device__ __forceinline__ int64_t x86_f64_to_i64(double d) {
+    if (d >= -9223372036854775808.0 && d < 9223372036854775808.0) return (int64_t)d;
+    return INT64_MIN;
+}
+
+// Codec constants for one channel, bit-exact with codec._scales and the
+// offset computation (codec.py:101-104, :117).
+struct ChanCode {
+    double scale;   // 2^K / (6 g)
+    double step;    // 6 g 2^-K
+    int64_t off;    // floor(beta * scale) via x86 cast
+};
+
+__device__ __forceinline__ ChanCode chan_code(float gamma, float beta, int bits) {
+    double g = fabs((double)gamma);
+    g = g > kGammaFloor ? g : kGammaFloor;           // np.maximum (NaN-propagating
+    if (isnan((double)gamma)) g = (double)gamma;     //  like numpy)
+    double g6 = __dmul_rn(6.0, g);
+    ChanCode r;
+    r.scale = __ddiv_rn(ldexp(1.0, bits), g6);
+    r.step = __dmul_rn(g6, ldexp(1.0, -bits));
+    r.off = x86_f64_to_i64(floor(__dmul_rn((double)beta, r.scale)));
+    return r;
+}
+
+// Unclipped code with wrapping int64 arithmetic (codec.py:118-120).
+__device__ __forceinline__ int64_t raw_code(float a, double scale, int64_t off, int bits) {
+    int64_t u = x86_f64_to_i64(floor(__dmul_rn((double)a, scale)));
+    uint64_t r = (uint64_t)u + (uint64_t)(1ll << (bits - 1)) - (uint64_t)off;
+    return (int64_t)r;
+}
+
+// Interval-median decode (codec.py:149-154), rounded to the tape dtype.
+__device__ __forceinline__ float decode(uint32_t code, double step, int64_t off, int bits) {
+    double half = (double)(1 << (bits - 1));
+    double inner = __dadd_rn((double)code, 0.5 - half);
+    inner = __dadd_rn(inner, (double)off);
+    return __double2float_rn(__dmul_rn(step, inner));
+}
+
+__device__ __forceinline__ uint32_t get_code(const uint8_t *codes, int64_t i, int bits) {
+    if (bits == 8) return codes[i];
+    int64_t bit = i * bits;
+    return (codes[bit >> 3] >> (bit & 7)) & ((1u << bits) - 1u);
+}
+
+// Pre-ReLU activation of element i from a tape (fp32 copy or codes).
+__device__ __forceinline__ float tape_value(const qt_tape_t &t, int64_t i, int c) {
+    if (t.a2) return t.a2[i];
+    return decode(get_code(t.codes, i, t.bits), t.step[c], t.offset[c], t.bits);
+}
+
+__device__ __forceinline__ float safe_gamma(float g) {
+    float mag = fabsf(g);
+    mag = mag > kGammaFloorF ? mag : kGammaFloorF;
+    if (isnan(g)) mag = g;
+    return g < 0.f ? -mag : mag;
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// Convolution geometry (NCHW input n x ci x h x w, kernel co x ci x kh x kw).
+struct ConvGeo {
+    int64_t n, ci, h, w, co, kh, kw, s, pad, oh, ow;
+};
+
+}  // namespace qt

@@ -1,0 +1,191 @@
+"""Layer forward/backward parity (reference golden vectors + oracle)."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from gpu_util import LAYER_TOL, dev, host, norm_err
+
+pytestmark = pytest.mark.gpu
+
+import paper_1901_07988_b200 as P  # noqa: E402
+from paper_1901_07988_b200 import _native as N  # noqa: E402
+from paper_1901_07988_b200 import layer as L  # noqa: E402
+from paper_1901_07988_b200.errors import StateError  # noqa: E402
+
+
+def _bits(v):
+    v = int(v)
+    return None if v < 0 else v
+
+
+def _params(g, k):
+    kind = str(g[k + "_kind"])
+    kind = "conv" if kind == "plain_conv" else kind
+    gamma = g.get(k + "_gamma")
+    return L.LayerParams(kind=kind, weight=dev(g[k + "_w"]), stride=int(g[k + "_stride"]),
+                         pad=int(g[k + "_pad"]),
+                         gamma=None if gamma is None else dev(gamma),
+                         beta=None if gamma is None else dev(g[k + "_beta"]))
+
+
+def test_bn_relu_forward_bit_exact_given_moments():
+    """K1 fed the oracle's float64 moments reproduces the reference's A2,
+    codes and ReLU output bit for bit (layer.py:245-264, codec.py:107-143)."""
+    rng = np.random.default_rng(11)
+    for shape, bits in [((4, 5, 8, 8), 4), ((3, 16, 7, 7), 8), ((6, 7), 2), ((2, 3, 5, 5), 1),
+                        ((8, 64, 16, 16), 4)]:
+        c = shape[1]
+        x = (rng.standard_normal(shape) * 2 + 0.5).astype(np.float32)
+        gamma = rng.uniform(0.5, 1.5, c).astype(np.float32)
+        beta = rng.uniform(-0.3, 0.3, c).astype(np.float32)
+        mean, var = O.moments(x)
+        p = O.new_params("conv", np.zeros((1, c, 1, 1), np.float32), gamma=gamma, beta=beta)
+        for mode in ("approx", "naive", "exact"):
+            _, tape = O.layer_fwd(x, dict(p, running_mean=np.zeros(c), running_var=np.ones(c)),
+                                  mode, bits)
+            a2w = ((((x - O.qtape_oracle._b(mean.astype(np.float32), x.ndim))
+                     * O.qtape_oracle._b((1.0 / np.sqrt(var + 1e-5)).astype(np.float32), x.ndim))
+                    * O.qtape_oracle._b(gamma, x.ndim)) + O.qtape_oracle._b(beta, x.ndim))
+            n_, c_, hw = P.ops.nchw(torch.empty(shape, device="meta"))
+            a3 = torch.empty(shape, device="cuda")
+            a2 = torch.empty(shape, device="cuda")
+            nb = (bits * x.size + 7) // 8
+            codes = torch.empty(nb, dtype=torch.uint8, device="cuda")
+            step = torch.empty(c, dtype=torch.float64, device="cuda")
+            off = torch.empty(c, dtype=torch.int64, device="cuda")
+            clip = torch.zeros(1, dtype=torch.int64, device="cuda")
+            nm = {"exact": 0, "approx": 1, "naive": 2}[mode]
+            kb = 0 if mode == "exact" else bits
+            N.call("qt_bn_relu_forward", N.ptr(dev(x)), n_, c_, hw, N.ptr(dev(mean)),
+                   N.ptr(dev(var)), 1e-5, N.ptr(dev(gamma)), N.ptr(dev(beta)), nm, kb, N.ptr(a3),
+                   N.ptr(a2 if mode == "exact" else None), N.ptr(codes if kb else None),
+                   N.ptr(step if kb else None), N.ptr(off if kb else None),
+                   N.ptr(clip if kb else None))
+            if mode == "exact":
+                assert np.array_equal(host(a2), tape["a2"])
+                assert np.array_equal(host(a3), np.maximum(a2w, np.float32(0)))
+            else:
+                assert np.array_equal(host(codes), tape["q"]["codes"]), (shape, bits, mode)
+                assert int(clip.item()) == tape["q"]["clip_count"]
+                pre = O.dequantize(tape["q"]) if mode == "naive" else a2w
+                assert np.array_equal(host(a3), np.maximum(pre, np.float32(0))), (shape, mode)
+
+
+def test_golden_layers(golden_layers):
+    g = golden_layers
+    for i in range(int(g["n_layer"])):
+        k = f"l{i}"
+        p = _params(g, k)
+        mode, bits = str(g[k + "_mode"]), _bits(g[k + "_bits"])
+        y, tape = L.layer_forward(dev(g[k + "_x"]), p, mode=mode, bits=bits)
+        assert norm_err(host(y), g[k + "_y"]) < LAYER_TOL, k
+        if p.preact:
+            assert norm_err(host(tape.sigma2), g[k + "_sigma2"]) < 1e-12, k
+            assert norm_err(host(p.running_mean), g[k + "_rmean"]) < 1e-12, k
+            if tape.is_quantized:
+                mine = O.unpack(host(tape.stored.codes), bits, tape.stored.numel)
+                ref = O.unpack(g[k + "_codes"], bits, tape.stored.numel)
+                assert np.mean(mine == ref) > 0.999, k      # moments differ in the last ulp
+                assert np.array_equal(host(tape.stored.offset), g[k + "_offset"]), k
+                assert np.array_equal(host(tape.stored.step), g[k + "_step"]), k
+            else:
+                assert norm_err(host(tape.stored), g[k + "_a2"]) < LAYER_TOL, k
+        gin = L.layer_backward(dev(g[k + "_g"]), tape, p)
+        assert norm_err(host(gin), g[k + "_gin"]) < LAYER_TOL, k
+        assert norm_err(host(p.grad_weight), g[k + "_gw"]) < LAYER_TOL, k
+        if p.preact:
+            assert norm_err(host(p.grad_gamma), g[k + "_ggamma"]) < LAYER_TOL, k
+            assert norm_err(host(p.grad_beta), g[k + "_gbeta"]) < LAYER_TOL, k
+
+
+def _conv_params(ci, co, seed, gamma=None, beta=None):
+    rng = np.random.default_rng(seed)
+    w = (rng.standard_normal((co, ci, 3, 3)) * 0.3).astype(np.float32)
+    gamma = np.ones(ci, np.float32) if gamma is None else gamma.astype(np.float32)
+    beta = np.zeros(ci, np.float32) if beta is None else beta.astype(np.float32)
+    return L.LayerParams(kind="conv", weight=dev(w), stride=1, pad=1, gamma=dev(gamma),
+                         beta=dev(beta))
+
+
+def test_approx_forward_equals_exact_forward_bitwise():
+    rng = np.random.default_rng(2)
+    x = dev(rng.standard_normal((4, 3, 8, 8)).astype(np.float32))
+    ye, _ = L.layer_forward(x, _conv_params(3, 5, 1), mode="exact")
+    ya, ta = L.layer_forward(x, _conv_params(3, 5, 1), mode="approx", bits=4)
+    assert torch.equal(ye, ya) and ta.is_quantized
+
+
+def test_identity_bypass_bitwise():
+    rng = np.random.default_rng(1)
+    x = dev(rng.standard_normal((2, 2, 5, 5)).astype(np.float32))
+    ye, te = L.layer_forward(x, _conv_params(2, 3, 4), mode="exact")
+    ya, ta = L.layer_forward(x, _conv_params(2, 3, 4), mode="approx", bits=None)
+    yn, _ = L.layer_forward(x, _conv_params(2, 3, 4), mode="naive", bits=None)
+    assert torch.equal(ye, ya) and torch.equal(ye, yn)
+    assert torch.equal(te.stored, ta.stored) and ta.identity
+
+
+def test_naive_uses_reconstruction():
+    rng = np.random.default_rng(3)
+    x = dev(rng.standard_normal((4, 3, 8, 8)).astype(np.float32))
+    p = _conv_params(3, 5, 7)
+    ye, _ = L.layer_forward(x, _conv_params(3, 5, 7), mode="exact")
+    yn, tn = L.layer_forward(x, p, mode="naive", bits=4)
+    assert not torch.equal(ye, yn)
+    _, _, a3 = L.reconstruct_from_tape(tn)
+    assert torch.equal(yn, P.ops.conv2d_forward(a3, p.weight, 1, 1))
+
+
+def test_exactness_decomposition():
+    """reference tests/test_layer.py:173-202 on the device."""
+    rng = np.random.default_rng(9)
+    gamma, beta = rng.uniform(0.8, 1.2, 3), rng.uniform(-0.2, 0.2, 3)
+    x = dev(rng.standard_normal((4, 3, 8, 8)).astype(np.float32))
+    p = _conv_params(3, 4, 9, gamma, beta)
+    out, te = L.layer_forward(x, p, mode="exact")
+    _, ta = L.layer_forward(x, p, mode="approx", bits=8)
+    g = dev(rng.standard_normal(tuple(out.shape)).astype(np.float32))
+    ie, ia = {}, {}
+    pe, pa = _conv_params(3, 4, 9, gamma, beta), _conv_params(3, 4, 9, gamma, beta)
+    gin_e = L.layer_backward(g, te, pe, internals=ie)
+    gin_a = L.layer_backward(g, ta, pa, internals=ia)
+    assert torch.equal(ie["mask"], ia["mask"])
+    assert torch.equal(ie["grad_linear_in"], ia["grad_linear_in"])
+    assert torch.equal(pe.grad_beta, pa.grad_beta)
+    assert torch.equal(ie["grad_normalized"], ia["grad_normalized"])
+    assert not torch.equal(pe.grad_weight, pa.grad_weight)
+    assert not torch.equal(pe.grad_gamma, pa.grad_gamma)
+    assert not torch.equal(gin_e, gin_a)
+    pa2 = _conv_params(3, 4, 9, gamma, beta)
+    gin_sub = L.layer_backward(g, ta, pa2, variance_a1=ie["a1"])
+    assert torch.equal(gin_sub, gin_e)
+
+
+def test_eval_mode_and_errors():
+    rng = np.random.default_rng(5)
+    p = _conv_params(2, 2, 5)
+    x = dev(rng.standard_normal((4, 2, 6, 6)).astype(np.float32))
+    for _ in range(3):
+        L.layer_forward(x, p, mode="exact")
+    y1, tape = L.layer_forward(x, p, training=False)
+    assert tape is None
+    rm = p.running_mean.clone()
+    y2, _ = L.layer_forward(x, p, training=False)
+    assert torch.equal(y1, y2) and torch.equal(rm, p.running_mean)
+    with pytest.raises(StateError):
+        L.layer_backward(torch.zeros((1, 2, 4, 4), device="cuda"), None, p)
+    _, t = L.layer_forward(x, p, mode="exact")
+    with pytest.raises(StateError):
+        L.layer_backward(torch.zeros((4, 2, 9, 9), device="cuda"), t, p)
+
+
+def test_zero_gradient():
+    rng = np.random.default_rng(6)
+    p = _conv_params(2, 3, 6)
+    x = dev(rng.standard_normal((2, 2, 5, 5)).astype(np.float32))
+    out, tape = L.layer_forward(x, p, mode="approx", bits=4)
+    gin = L.layer_backward(torch.zeros_like(out), tape, p)
+    assert not bool(gin.any()) and not bool(p.grad_weight.any())
+    assert not bool(p.grad_gamma.any()) and not bool(p.grad_beta.any())

@@ -1,0 +1,113 @@
+"""Conv / matmul / moment parity against the oracle (tolerances in gpu_util)."""
+
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from gpu_util import CONV_TOL, MOMENT_TOL, dev, host, norm_err
+
+pytestmark = pytest.mark.gpu
+
+from paper_1901_07988_b200 import ops  # noqa: E402
+from paper_1901_07988_b200.errors import ShapeError  # noqa: E402
+
+GEOS = [  # (n, ci, h, co, k, s, p)
+    (2, 3, 9, 4, 3, 1, 1), (2, 5, 8, 6, 3, 1, 1), (3, 4, 8, 8, 2, 2, 0), (2, 16, 8, 16, 1, 1, 0),
+    (2, 3, 16, 8, 4, 4, 0), (2, 8, 7, 5, 3, 2, 0), (1, 32, 16, 64, 1, 1, 0), (4, 64, 8, 16, 1, 1, 0),
+    (2, 16, 16, 16, 3, 1, 1), (2, 12, 14, 24, 2, 2, 0), (3, 7, 5, 9, 3, 1, 2), (2, 4, 12, 4, 4, 2, 1),
+]
+
+
+@pytest.mark.parametrize("geo", GEOS)
+def test_conv_forward(geo):
+    n, ci, h, co, k, s, p = geo
+    rng = np.random.default_rng(sum(geo))
+    x = rng.standard_normal((n, ci, h, h)).astype(np.float32)
+    w = rng.standard_normal((co, ci, k, k)).astype(np.float32)
+    want = O.conv_fwd(x, w, s, p)
+    got = host(ops.conv2d_forward(dev(x), dev(w), s, p))
+    assert got.shape == want.shape
+    assert norm_err(got, want) < CONV_TOL
+
+
+@pytest.mark.parametrize("geo", GEOS)
+def test_conv_backward(geo):
+    n, ci, h, co, k, s, p = geo
+    rng = np.random.default_rng(100 + sum(geo))
+    x = rng.standard_normal((n, ci, h, h)).astype(np.float32)
+    w = rng.standard_normal((co, ci, k, k)).astype(np.float32)
+    g = rng.standard_normal(O.conv_out_shape(x.shape, w.shape, s, p)).astype(np.float32)
+    gx_w, gk_w = O.conv_bwd(x, w, g, s, p)
+    gx, gk = ops.conv2d_backward(dev(x), dev(w), dev(g), s, p)
+    assert norm_err(host(gx), gx_w) < CONV_TOL
+    assert norm_err(host(gk), gk_w) < CONV_TOL
+    none, gk2 = ops.conv2d_backward(dev(x), dev(w), dev(g), s, p, need_g_x=False)
+    assert none is None and np.array_equal(host(gk2), host(gk))
+
+
+def test_conv_adjoint_identity():
+    rng = np.random.default_rng(3)
+    x = dev(rng.standard_normal((2, 3, 8, 8)).astype(np.float32))
+    w = dev(rng.standard_normal((4, 3, 3, 3)).astype(np.float32))
+    y = dev(rng.standard_normal((2, 4, 8, 8)).astype(np.float32))
+    gx, _ = ops.conv2d_backward(x, w, y, 1, 1)
+    lhs = float((ops.conv2d_forward(x, w, 1, 1).double() * y.double()).sum())
+    rhs = float((x.double() * gx.double()).sum())
+    assert abs(lhs - rhs) / abs(lhs) < 1e-5
+
+
+def test_conv_residual_fused():
+    rng = np.random.default_rng(4)
+    x = rng.standard_normal((2, 8, 8, 8)).astype(np.float32)
+    w = rng.standard_normal((16, 8, 2, 2)).astype(np.float32)
+    res = rng.standard_normal((2, 4, 8, 8)).astype(np.float32)
+    y = O.conv_fwd(x, w, 2, 0)
+    want = y.copy()
+    want[:, :4] += res[:, :, ::2, ::2]
+    got = host(ops.conv2d_forward(dev(x), dev(w), 2, 0, residual=dev(res)))
+    assert norm_err(got, want) < CONV_TOL
+
+
+def test_shape_errors():
+    with pytest.raises(ShapeError):
+        ops.conv2d_forward(torch.zeros((1, 3, 8, 8), device="cuda"),
+                           torch.zeros((4, 3, 3, 3), device="cuda"), 2, 1)
+    with pytest.raises(ShapeError):
+        ops.conv2d_forward(torch.zeros((1, 3, 8, 8), device="cuda"),
+                           torch.zeros((4, 2, 3, 3), device="cuda"), 1, 1)
+
+
+@pytest.mark.parametrize("shape", [(5, 7, 3), (64, 256, 10), (16, 2048, 1000), (1, 1, 1)])
+def test_matmul_bit_exact(shape):
+    n, k, m = shape
+    rng = np.random.default_rng(n + k + m)
+    a = rng.standard_normal((n, k)).astype(np.float32)
+    b = rng.standard_normal((k, m)).astype(np.float32)
+    got = host(ops.matmul(dev(a), dev(b)))
+    assert np.array_equal(got, O.matmul_fixed(a, b))
+    # transposed operands read in place
+    assert np.array_equal(host(ops.matmul(dev(a.T.copy()), dev(b), ta=True)), got)
+    assert np.array_equal(host(ops.matmul(dev(a), dev(b.T.copy()), tb=True)), got)
+
+
+@pytest.mark.parametrize("shape", [(8, 4, 12, 12), (128, 64, 8, 8), (6, 7), (3, 5, 7, 7),
+                                   (2, 16, 112, 112)])
+def test_moments(shape):
+    rng = np.random.default_rng(len(shape))
+    x = (rng.standard_normal(shape) * 3 + 1).astype(np.float32)
+    m, v = ops.channel_moments(dev(x))
+    mw, vw = O.moments(x)
+    assert np.max(np.abs(host(m) - mw) / (np.abs(mw) + 1e-3)) < MOMENT_TOL
+    assert np.max(np.abs(host(v) - vw) / vw) < MOMENT_TOL
+    s = host(ops.channel_sum(dev(x)))
+    assert np.max(np.abs(s - O.chan_sum(x)) / (np.abs(O.chan_sum(x)) + 1)) < 1e-12
+
+
+def test_moments_constant_and_two_point():
+    x = torch.full((4, 3, 5, 5), 2.5, device="cuda")
+    m, v = ops.channel_moments(x)
+    assert np.all(host(m) == 2.5) and np.all(host(v) == 0.0)
+    x = dev(np.array([[1.0], [3.0]], np.float32))
+    m, v = ops.channel_moments(x)
+    assert host(m)[0] == 2.0 and host(v)[0] == 1.0
