@@ -82,10 +82,17 @@ def lib():
     global _lib
     if _lib is not None:
         return _lib
-    if not _SO.exists():
-        raise StateError(
-            f"{_SO.name} is not built; run `python -m paper_1901_07988_b200.build` "
-            "(there is no CPU fallback)")
+    from . import build as _build
+    if not _build.is_current():
+        # stale or missing: rebuild in-tree when nvcc is available, else fail
+        try:
+            _build.build()
+        except Exception as exc:  # noqa: BLE001
+            if not _SO.exists():
+                raise StateError(
+                    f"{_SO.name} is not built and the build failed ({exc}); "
+                    "there is no CPU fallback") from exc
+            raise StateError(f"{_SO.name} is stale and could not be rebuilt: {exc}") from exc
     so = ctypes.CDLL(str(_SO))
     for name, (res, args) in SIGNATURES.items():
         fn = getattr(so, name)

@@ -48,6 +48,12 @@ def _digest() -> str:
     return h.hexdigest()[:16]
 
 
+def is_current() -> bool:
+    """True if libqtape_b200.so was built from the present sources/flags."""
+    stamp = BUILD / "stamp"
+    return OUT.exists() and stamp.exists() and stamp.read_text() == _digest()
+
+
 def build(force: bool = False, verbose: bool = False) -> Path:
     stamp = BUILD / "stamp"
     dig = _digest()

@@ -41,7 +41,8 @@ def test_bn_relu_forward_bit_exact_given_moments():
         gamma = rng.uniform(0.5, 1.5, c).astype(np.float32)
         beta = rng.uniform(-0.3, 0.3, c).astype(np.float32)
         mean, var = O.moments(x)
-        p = O.new_params("conv", np.zeros((1, c, 1, 1), np.float32), gamma=gamma, beta=beta)
+        kind, wshape = ("dense", (c, 1)) if len(shape) == 2 else ("conv", (1, c, 1, 1))
+        p = O.new_params(kind, np.zeros(wshape, np.float32), gamma=gamma, beta=beta)
         for mode in ("approx", "naive", "exact"):
             _, tape = O.layer_fwd(x, dict(p, running_mean=np.zeros(c), running_var=np.ones(c)),
                                   mode, bits)
@@ -58,8 +59,9 @@ def test_bn_relu_forward_bit_exact_given_moments():
             clip = torch.zeros(1, dtype=torch.int64, device="cuda")
             nm = {"exact": 0, "approx": 1, "naive": 2}[mode]
             kb = 0 if mode == "exact" else bits
-            N.call("qt_bn_relu_forward", N.ptr(dev(x)), n_, c_, hw, N.ptr(dev(mean)),
-                   N.ptr(dev(var)), 1e-5, N.ptr(dev(gamma)), N.ptr(dev(beta)), nm, kb, N.ptr(a3),
+            keep = [dev(x), dev(mean), dev(var), dev(gamma), dev(beta)]   # keep alive
+            N.call("qt_bn_relu_forward", N.ptr(keep[0]), n_, c_, hw, N.ptr(keep[1]),
+                   N.ptr(keep[2]), 1e-5, N.ptr(keep[3]), N.ptr(keep[4]), nm, kb, N.ptr(a3),
                    N.ptr(a2 if mode == "exact" else None), N.ptr(codes if kb else None),
                    N.ptr(step if kb else None), N.ptr(off if kb else None),
                    N.ptr(clip if kb else None))
