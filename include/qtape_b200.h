@@ -144,13 +144,26 @@ int qt_bn_backward_apply(const float *g3, qt_tape_t tape, int64_t n, int64_t c,
 int qt_conv_forward(const float *x, const float *w, float *out,
                     int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co,
                     int64_t kh, int64_t kw, int64_t stride, int64_t pad,
-                    const float *res, int64_t cr, int64_t sr, qt_stream_t stream);
+                    const float *res, int64_t cr, int64_t sr, void *ws,
+                    qt_stream_t stream);
 
 /* Data gradient (ops.conv2d_backward g_x path, ops.py:168-183). */
 int qt_conv_dgrad(const float *g, const float *w, float *gx,
                   int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co,
-                  int64_t kh, int64_t kw, int64_t stride, int64_t pad,
+                  int64_t kh, int64_t kw, int64_t stride, int64_t pad, void *ws,
                   qt_stream_t stream);
+
+/* Scratch for qt_conv_forward / qt_conv_dgrad: the tensor-core path keeps the
+ * (hi, lo) TF32 split of the re-laid-out kernel there (2*ci*co*kh*kw floats).
+ * The tensor-core path serves stride-1 convs whose output rows are 8, 16 or
+ * 32 pixels wide with ci % 8 == 0 and co % 16 == 0 (every CIFAR ResNet conv
+ * except the stem and the 2x2/s2 transitions); other shapes run on the
+ * CUDA-core implicit GEMM.  QTAPE_NO_TC=1 forces the CUDA-core path. */
+int64_t qt_conv_workspace(int64_t ci, int64_t co, int64_t kh, int64_t kw);
+/* 1 if qt_conv_forward (dgrad = 0) / qt_conv_dgrad (dgrad = 1) of this shape
+ * runs on the tensor cores, 0 if on the CUDA cores (host-side query). */
+int qt_conv_uses_tc(int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co, int64_t kh,
+                    int64_t kw, int64_t stride, int64_t pad, int dgrad);
 
 /* Weight gradient, accumulated: grad_w += fp32(sum) (ops.py:164-167,
  * layer.py:167).  The activation operand comes from `act`:

@@ -53,8 +53,10 @@ SIGNATURES = {
     "qt_bn_backward_apply": (I32, [P, Tape, I64, I64, I64, I64, P, P, P, P, P, I64,
                                    I64, P, P]),
     "qt_conv_forward": (I32, [P, P, P, I64, I64, I64, I64, I64, I64, I64, I64, I64,
-                              P, I64, I64, P]),
-    "qt_conv_dgrad": (I32, [P, P, P, I64, I64, I64, I64, I64, I64, I64, I64, I64, P]),
+                              P, I64, I64, P, P]),
+    "qt_conv_dgrad": (I32, [P, P, P, I64, I64, I64, I64, I64, I64, I64, I64, I64, P, P]),
+    "qt_conv_workspace": (I64, [I64, I64, I64, I64]),
+    "qt_conv_uses_tc": (I32, [I64] * 9 + [I32]),
     "qt_conv_wgrad_workspace": (I64, [I64] * 9),
     "qt_conv_wgrad": (I32, [P, Tape, P, P, I64, I64, I64, I64, I64, I64, I64, I64,
                             I64, P, P]),

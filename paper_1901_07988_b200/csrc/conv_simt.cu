@@ -313,16 +313,18 @@ using namespace qt;
 
 // Tensor-core paths (conv_tc.cu); return QT_EUNSUPPORTED for shapes they do not take.
 int qt_tc_conv_forward(const float *x, const float *w, float *out, const qt::ConvGeo &g,
-                       const float *res, int64_t cr, int64_t sr, cudaStream_t s);
+                       const float *res, int64_t cr, int64_t sr, void *ws, cudaStream_t s);
+int qt_tc_conv_dgrad(const float *gr, const float *w, float *gx, const qt::ConvGeo &g, void *ws,
+                     cudaStream_t s);
 
 extern "C" int qt_conv_forward(const float *x, const float *w, float *out, int64_t n, int64_t ci,
                                int64_t h, int64_t wd, int64_t co, int64_t kh, int64_t kw,
                                int64_t stride, int64_t pad, const float *res, int64_t cr,
-                               int64_t sr, qt_stream_t stream) {
+                               int64_t sr, void *ws, qt_stream_t stream) {
     ConvGeo g = make_geo(n, ci, h, wd, co, kh, kw, stride, pad);
     QT_REQUIRE(x && w && out && geo_ok(g));
     QT_REQUIRE(!res || (cr > 0 && cr <= co && sr >= 1));
-    int rc = qt_tc_conv_forward(x, w, out, g, res, cr, sr, qt_s(stream));
+    int rc = qt_tc_conv_forward(x, w, out, g, res, cr, sr, ws, qt_s(stream));
     if (rc != QT_EUNSUPPORTED) return rc;
     FwdA la{x, g};
     FwdB lb{w, ci * kh * kw};
@@ -333,9 +335,11 @@ extern "C" int qt_conv_forward(const float *x, const float *w, float *out, int64
 
 extern "C" int qt_conv_dgrad(const float *gr, const float *w, float *gx, int64_t n, int64_t ci,
                              int64_t h, int64_t wd, int64_t co, int64_t kh, int64_t kw,
-                             int64_t stride, int64_t pad, qt_stream_t stream) {
+                             int64_t stride, int64_t pad, void *ws, qt_stream_t stream) {
     ConvGeo g = make_geo(n, ci, h, wd, co, kh, kw, stride, pad);
     QT_REQUIRE(gr && w && gx && geo_ok(g));
+    int rc = qt_tc_conv_dgrad(gr, w, gx, g, ws, qt_s(stream));
+    if (rc != QT_EUNSUPPORTED) return rc;
     DgradA la{gr, g};
     DgradB lb{w, g};
     StoreNCHW ep{gx, h * wd, ci, wd, nullptr, 0, 1};

@@ -195,10 +195,11 @@ def _gap(a3: torch.Tensor) -> torch.Tensor:
     return out
 
 
-def _linear_forward(a3, p: LayerParams, out, residual=None):
+def _linear_forward(a3, p: LayerParams, out, residual=None, ws=None):
     """layer.py:138-151; ``residual`` fuses the block-end shortcut add."""
     if p.kind == "conv":
-        return ops.conv2d_forward(a3, p.weight, p.stride, p.pad, out=out, residual=residual)
+        return ops.conv2d_forward(a3, p.weight, p.stride, p.pad, out=out, residual=residual,
+                                  ws=None if ws is None else ws.conv)
     if p.kind == "dense":
         src = a3
     elif p.kind == "gap_dense":
@@ -227,7 +228,7 @@ def layer_forward(a_in: torch.Tensor, p: LayerParams, mode: str = "exact",
         raise ConfigError(f"bits must be one of (1, 2, 4, 8), got {bits}")
     _dev_f32(a_in, "a_in")
     if not p.preact:
-        a_out = _linear_forward(a_in, p, out, residual)
+        a_out = _linear_forward(a_in, p, out, residual, ws)
         return a_out, LayerTape(mode="plain", stored=None, input_ref=a_in)
 
     n, c, hw = ops.nchw(a_in)
@@ -278,7 +279,7 @@ def layer_forward(a_in: torch.Tensor, p: LayerParams, mode: str = "exact",
         tape = LayerTape(mode=mode, stored=stored, sigma2=var, gamma=slot.gamma,
                          beta=slot.beta, bn_epsilon=p.bn_epsilon,
                          identity=(bits is None and mode != "exact"))
-    a_out = _linear_forward(work, p, out, residual)
+    a_out = _linear_forward(work, p, out, residual, ws)
     ops._check_finite(a_out)
     return a_out, tape
 
@@ -352,7 +353,8 @@ def layer_backward(g_out: torch.Tensor, tape: LayerTape, p: LayerParams,
             if not need_input_grad:
                 return None
             g_in = out if out is not None else torch.empty_like(a_in)
-            ops.conv2d_dgrad(g_out, p.weight, tuple(a_in.shape), p.stride, p.pad, g_in)
+            ops.conv2d_dgrad(g_out, p.weight, tuple(a_in.shape), p.stride, p.pad, g_in,
+                             ws=None if ws is None else ws.conv)
         if residual_grad is not None:
             _apply_adjoint(g_in, residual_grad)
         return g_in
@@ -370,7 +372,8 @@ def layer_backward(g_out: torch.Tensor, tape: LayerTape, p: LayerParams,
     if p.kind == "conv":
         ops.conv2d_wgrad(g_out, tuple(p.weight.shape), p.stride, p.pad, p.grad_weight,
                          tape=nt, in_shape=in_shape, ws=None if ws is None else ws.wgrad)
-        ops.conv2d_dgrad(g_out, p.weight, in_shape, p.stride, p.pad, g3)
+        ops.conv2d_dgrad(g_out, p.weight, in_shape, p.stride, p.pad, g3,
+                         ws=None if ws is None else ws.conv)
     else:
         _, _, a3 = reconstruct_from_tape(tape)
         if p.kind == "dense":

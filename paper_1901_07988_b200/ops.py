@@ -106,9 +106,17 @@ def conv2d_out_shape(in_shape: tuple, k_shape: tuple, stride: int, pad: int) -> 
     return n, co, oh, ow
 
 
+def _conv_ws(k, ws):
+    co, ci, kh, kw = k.shape
+    need = N.query("qt_conv_workspace", ci, co, kh, kw)
+    if ws is None or ws.numel() < need:
+        ws = workspace(need, k.device, "conv")
+    return ws
+
+
 def conv2d_forward(x: torch.Tensor, k: torch.Tensor, stride: int = 1, pad: int = 0,
-                   out: Optional[torch.Tensor] = None, residual: Optional[torch.Tensor] = None
-                   ) -> torch.Tensor:
+                   out: Optional[torch.Tensor] = None, residual: Optional[torch.Tensor] = None,
+                   ws=None) -> torch.Tensor:
     """Cross-correlation with zero padding (ops.py:106-138).
 
     ``residual`` (engine use) fuses the parameter-free shortcut add of
@@ -127,7 +135,7 @@ def conv2d_forward(x: torch.Tensor, k: torch.Tensor, stride: int = 1, pad: int =
         cr = residual.shape[1]
         sr = residual.shape[2] // oh
     N.call("qt_conv_forward", N.ptr(x), N.ptr(k), N.ptr(out), n, ci, x.shape[2], x.shape[3], co,
-           kh, kw, stride, pad, N.ptr(residual), cr, sr)
+           kh, kw, stride, pad, N.ptr(residual), cr, sr, N.ptr(_conv_ws(k, ws)))
     _check_finite(out)
     return out
 
@@ -160,11 +168,11 @@ def conv2d_wgrad(g_out, k_shape, stride, pad, grad_w, x_plain=None, tape=None, i
            kw, stride, pad, N.ptr(ws))
 
 
-def conv2d_dgrad(g_out, k, in_shape, stride, pad, g_x_out):
+def conv2d_dgrad(g_out, k, in_shape, stride, pad, g_x_out, ws=None):
     n, ci, h, w = in_shape
     co, _, kh, kw = k.shape
     N.call("qt_conv_dgrad", N.ptr(g_out), N.ptr(k), N.ptr(g_x_out), n, ci, h, w, co, kh, kw,
-           stride, pad)
+           stride, pad, N.ptr(_conv_ws(k, ws)))
 
 
 def conv2d_backward(x: torch.Tensor, k: torch.Tensor, g_out: torch.Tensor, stride: int = 1,

@@ -16,7 +16,20 @@ GEOS = [  # (n, ci, h, co, k, s, p)
     (2, 3, 9, 4, 3, 1, 1), (2, 5, 8, 6, 3, 1, 1), (3, 4, 8, 8, 2, 2, 0), (2, 16, 8, 16, 1, 1, 0),
     (2, 3, 16, 8, 4, 4, 0), (2, 8, 7, 5, 3, 2, 0), (1, 32, 16, 64, 1, 1, 0), (4, 64, 8, 16, 1, 1, 0),
     (2, 16, 16, 16, 3, 1, 1), (2, 12, 14, 24, 2, 2, 0), (3, 7, 5, 9, 3, 1, 2), (2, 4, 12, 4, 4, 2, 1),
+    # tensor-core (tcgen05) shapes: rows of 8/16/32 px, ci % 8 == 0, co % 16 == 0
+    (4, 16, 32, 16, 3, 1, 1), (2, 32, 32, 64, 1, 1, 0), (2, 64, 8, 256, 1, 1, 0),
+    (4, 256, 8, 64, 1, 1, 0), (2, 64, 8, 64, 3, 1, 1), (2, 128, 16, 32, 1, 1, 0),
+    (2, 32, 16, 32, 3, 1, 1), (2, 16, 32, 64, 1, 1, 0), (6, 8, 8, 16, 3, 1, 1),
 ]
+
+
+def test_tensor_core_path_is_selected():
+    from paper_1901_07988_b200 import _native as N
+    assert N.query("qt_conv_uses_tc", 128, 16, 32, 32, 16, 3, 3, 1, 1, 0) == 1
+    assert N.query("qt_conv_uses_tc", 128, 16, 32, 32, 16, 3, 3, 1, 1, 1) == 1
+    assert N.query("qt_conv_uses_tc", 128, 64, 8, 8, 256, 1, 1, 1, 0, 0) == 1
+    assert N.query("qt_conv_uses_tc", 128, 3, 32, 32, 16, 3, 3, 1, 1, 0) == 0   # stem
+    assert N.query("qt_conv_uses_tc", 128, 32, 32, 32, 32, 2, 2, 2, 0, 0) == 0  # 2x2/s2
 
 
 @pytest.mark.parametrize("geo", GEOS)
