@@ -119,6 +119,7 @@ int qt_reconstruct(qt_tape_t tape, int64_t n, int64_t c, int64_t hw,
  *   reduce: accumulates grad_beta += sum(g3*mask), grad_gamma += sum(a1*g3*mask)
  *           and writes stats[3*C] = {t2[C], t3[C], inv[C]} (float32)
  *   apply : g_in = ((g1 - t2) - a1v*t3) * inv, g1 = g3*mask*gamma, in place
+ *           (ws = the workspace the reduce wrote its per-code tables into)
  *           allowed (g_in == g3); if res_g != NULL also adds the shortcut
  *           adjoint (engine.py:272-279): res_g has shape (N,CR,HR,WR) with
  *           HR = H/sc, CR >= C.
@@ -133,7 +134,7 @@ int qt_bn_backward_apply(const float *g3, qt_tape_t tape, int64_t n, int64_t c,
                          int64_t h, int64_t w, const float *gamma_tape,
                          const float *beta_tape, const float *variance_a1,
                          const float *stats, const float *res_g, int64_t cr,
-                         int64_t sc, float *g_in, qt_stream_t stream);
+                         int64_t sc, const void *ws, float *g_in, qt_stream_t stream);
 
 /* ----------------------------------------------------------------- conv ---
  * Cross-correlation with zero padding; integral extents are validated by the

@@ -51,7 +51,7 @@ SIGNATURES = {
     "qt_bn_backward_reduce": (I32, [P, Tape, I64, I64, I64, P, P, P, F64, P, P, P,
                                     P, P, P]),
     "qt_bn_backward_apply": (I32, [P, Tape, I64, I64, I64, I64, P, P, P, P, P, I64,
-                                   I64, P, P]),
+                                   I64, P, P, P]),
     "qt_conv_forward": (I32, [P, P, P, I64, I64, I64, I64, I64, I64, I64, I64, I64,
                               P, I64, I64, P, P]),
     "qt_conv_dgrad": (I32, [P, P, P, I64, I64, I64, I64, I64, I64, I64, I64, I64, P, P]),

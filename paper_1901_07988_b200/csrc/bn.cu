@@ -155,114 +155,6 @@ __global__ void __launch_bounds__(kRThreads) chan_sum_kernel(StatsArgs a) {
     }
 }
 
-// --------------------------------------------------------- BN backward ---
-
-struct BwdArgs {
-    const float *g3;
-    qt_tape_t tape;
-    int64_t n, c, hw;
-    const float *gamma, *beta;
-    const double *sigma2;
-    double eps;
-    const float *va1;
-    float *grad_gamma, *grad_beta, *stats;
-    int64_t ppb, nb;
-    double *part;       // [c][nb][4]
-    unsigned *counter;  // [c]
-};
-
-struct ElemBwd {
-    float g3m, a1g3m, g1, a1vg1, a1v;
-};
-
-__device__ __forceinline__ ElemBwd bwd_elem(const qt_tape_t &t, const float *va1, int64_t i,
-                                            int ch, float g3, float gam, float bet, float sg) {
-    ElemBwd r;
-    float a2 = tape_value(t, i, ch);
-    float a1 = __fdiv_rn(__fsub_rn(a2, bet), sg);                 // layer.py:364-366
-    r.g3m = __fmul_rn(g3, a2 > 0.f ? 1.f : 0.f);                 // layer.py:355, :368
-    r.a1g3m = __fmul_rn(a1, r.g3m);                              // layer.py:372
-    r.g1 = __fmul_rn(r.g3m, gam);                                // layer.py:373
-    r.a1v = va1 ? va1[i] : a1;
-    r.a1vg1 = __fmul_rn(r.a1v, r.g1);                            // layer.py:301
-    return r;
-}
-
-__global__ void __launch_bounds__(kRThreads) bn_bwd_reduce_kernel(BwdArgs a) {
-    __shared__ double red[4][kRThreads / 32];
-    const int64_t ch = blockIdx.y;
-    const int64_t p0 = (int64_t)blockIdx.x * a.ppb;
-    const int64_t p1 = min(p0 + a.ppb, a.n);
-    const float gam = a.gamma[ch], bet = a.beta[ch], sg = safe_gamma(gam);
-    double v[4] = {0.0, 0.0, 0.0, 0.0};
-    const int64_t cnt = (p1 - p0) * a.hw;
-    for (int64_t e = threadIdx.x; e < cnt; e += kRThreads) {
-        int64_t pl = e / a.hw, off = e - pl * a.hw;
-        int64_t i = ((p0 + pl) * a.c + ch) * a.hw + off;
-        ElemBwd r = bwd_elem(a.tape, a.va1, i, (int)ch, a.g3[i], gam, bet, sg);
-        v[0] += (double)r.g3m;
-        v[1] += (double)r.a1g3m;
-        v[2] += (double)r.g1;
-        v[3] += (double)r.a1vg1;
-    }
-    block_sum<4>(v, red);
-    if (threadIdx.x == 0) {
-        double *pp = a.part + (ch * a.nb + blockIdx.x) * 4;
-        for (int j = 0; j < 4; ++j) pp[j] = v[j];
-    }
-    if (!last_block(a.counter + ch, (unsigned)a.nb)) return;
-    if (threadIdx.x == 0) {
-        __threadfence();
-        double s[4] = {0.0, 0.0, 0.0, 0.0};
-        const volatile double *pp = a.part + ch * a.nb * 4;
-        for (int64_t b = 0; b < a.nb; ++b)
-            for (int j = 0; j < 4; ++j) s[j] += pp[4 * b + j];
-        const double cntd = (double)(a.n * a.hw);
-        if (a.grad_beta) a.grad_beta[ch] = __double2float_rn((double)a.grad_beta[ch] + s[0]);
-        if (a.grad_gamma) a.grad_gamma[ch] = __double2float_rn((double)a.grad_gamma[ch] + s[1]);
-        a.stats[ch] = __double2float_rn(s[2] / cntd);                         // t2
-        a.stats[a.c + ch] = __double2float_rn(s[3] / cntd);                   // t3
-        a.stats[2 * a.c + ch] =
-            __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(a.sigma2[ch], a.eps))));  // inv
-    }
-}
-
-struct ApplyArgs {
-    const float *g3;
-    qt_tape_t tape;
-    int64_t n, c, h, w;
-    const float *gamma, *beta, *va1, *stats, *res;
-    int64_t cr, sc;
-    float *g_in;
-};
-
-__global__ void __launch_bounds__(kRThreads) bn_bwd_apply_kernel(ApplyArgs a) {
-    const int64_t hw = a.h * a.w;
-    const int64_t numel = a.n * a.c * hw;
-    for (int64_t i = (int64_t)blockIdx.x * kRThreads + threadIdx.x; i < numel;
-         i += (int64_t)gridDim.x * kRThreads) {
-        const int64_t pl = i / hw;
-        const int ch = (int)(pl % a.c);
-        const float gam = a.gamma[ch];
-        ElemBwd r = bwd_elem(a.tape, a.va1, i, ch, a.g3[i], gam, a.beta[ch], safe_gamma(gam));
-        float o = __fsub_rn(r.g1, a.stats[ch]);                           // layer.py:305
-        o = __fsub_rn(o, __fmul_rn(r.a1v, a.stats[a.c + ch]));            // :306
-        o = __fmul_rn(o, a.stats[2 * a.c + ch]);                          // :307
-        if (a.res) {  // shortcut adjoint, engine.py:272-279
-            const int64_t p = i - pl * hw;
-            const int64_t y = p / a.w, x = p - y * a.w;
-            if (a.sc == 1 && a.cr == a.c) {
-                o = __fadd_rn(o, a.res[i]);
-            } else if (y % a.sc == 0 && x % a.sc == 0) {
-                const int64_t nn = pl / a.c;
-                const int64_t hr = a.h / a.sc, wr = a.w / a.sc;
-                o = __fadd_rn(o, a.res[((nn * a.cr + ch) * hr + y / a.sc) * wr + x / a.sc]);
-            }
-        }
-        a.g_in[i] = o;
-    }
-}
-
 // ------------------------------------------------------- reconstruct ---
 
 __global__ void reconstruct_kernel(qt_tape_t t, int64_t numel, int64_t c, int64_t hw,
@@ -381,43 +273,6 @@ extern "C" int qt_channel_sum(const float *x, int64_t n, int64_t c, int64_t hw, 
                 (double *)((char *)ws + kCounterBytes), (unsigned *)ws};
     dim3 grid((unsigned)p.blocks, (unsigned)c);
     chan_sum_kernel<<<grid, kRThreads, 0, qt_s(stream)>>>(a);
-    QT_CHECK_LAUNCH();
-    return QT_OK;
-}
-
-extern "C" int64_t qt_bn_backward_workspace(int64_t n, int64_t c, int64_t hw) {
-    Part p = partition(n, hw);
-    return kCounterBytes + c * p.blocks * 4 * (int64_t)sizeof(double);
-}
-
-extern "C" int qt_bn_backward_reduce(const float *g3, qt_tape_t tape, int64_t n, int64_t c,
-                                     int64_t hw, const float *gamma_tape, const float *beta_tape,
-                                     const double *sigma2, double eps, const float *variance_a1,
-                                     float *grad_gamma, float *grad_beta, float *stats, void *ws,
-                                     qt_stream_t stream) {
-    QT_REQUIRE(g3 && gamma_tape && beta_tape && sigma2 && stats && ws);
-    QT_REQUIRE(n > 0 && c > 0 && hw > 0 && c <= kMaxChannels);
-    QT_REQUIRE(tape.a2 || (tape.codes && tape.step && tape.offset && qt_bits_ok(tape.bits)));
-    Part p = partition(n, hw);
-    BwdArgs a{g3, tape, n, c, hw, gamma_tape, beta_tape, sigma2, eps, variance_a1, grad_gamma,
-              grad_beta, stats, p.planes_per_block, p.blocks,
-              (double *)((char *)ws + kCounterBytes), (unsigned *)ws};
-    dim3 grid((unsigned)p.blocks, (unsigned)c);
-    bn_bwd_reduce_kernel<<<grid, kRThreads, 0, qt_s(stream)>>>(a);
-    QT_CHECK_LAUNCH();
-    return QT_OK;
-}
-
-extern "C" int qt_bn_backward_apply(const float *g3, qt_tape_t tape, int64_t n, int64_t c,
-                                    int64_t h, int64_t w, const float *gamma_tape,
-                                    const float *beta_tape, const float *variance_a1,
-                                    const float *stats, const float *res_g, int64_t cr, int64_t sc,
-                                    float *g_in, qt_stream_t stream) {
-    QT_REQUIRE(g3 && gamma_tape && beta_tape && stats && g_in && n > 0 && c > 0 && h > 0 && w > 0);
-    QT_REQUIRE(tape.a2 || (tape.codes && tape.step && tape.offset && qt_bits_ok(tape.bits)));
-    QT_REQUIRE(!res_g || (sc >= 1 && h % sc == 0 && w % sc == 0 && cr >= c));
-    ApplyArgs a{g3, tape, n, c, h, w, gamma_tape, beta_tape, variance_a1, stats, res_g, cr, sc, g_in};
-    bn_bwd_apply_kernel<<<grid_for(n * c * h * w, kRThreads), kRThreads, 0, qt_s(stream)>>>(a);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }

@@ -1,0 +1,364 @@
+// BN / ReLU backward from the tape (layer.py:353-381, bn_input_gradient
+// :286-308) -- two HBM passes over g3, both reading the packed codes:
+//
+//   reduce : per channel  S0 = sum g3m, S1 = sum a1*g3m, S2 = sum g1,
+//            S3 = sum a1v*g1   (g3m = g3*mask, g1 = g3m*gamma; float64)
+//            -> grad_beta += S0, grad_gamma += S1, t2 = S2/n, t3 = S3/n, inv
+//   apply  : g_in = ((g1 - t2) - a1v*t3) * inv  (+ shortcut adjoint)
+//
+// For a K-bit tape every per-element quantity that depends on the stored
+// activation (mask = decoded > 0, a1 = (decoded - beta)/safe_gamma) is a
+// function of the code alone, so each channel's 2^K-entry table is built
+// once (with exactly the reference's float64 decode and fp32 rounding) and
+// the element loops are table lookups: no per-element float64 decode or
+// IEEE division, 8 elements per thread with 128-bit g3 loads and one K-byte
+// code load.  Reductions stay deterministic (fixed partition, float64
+// partials, last-block finalize in block order).
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace qt {
+
+constexpr int kBT = 256;
+constexpr int64_t kBwdCounterBytes = 65536 * 4;
+constexpr int64_t kMaxLut = 256;
+
+struct BwdPart {
+    int64_t ppb, nb;
+};
+
+static BwdPart bwd_partition(int64_t n, int64_t hw) {
+    BwdPart p;
+    p.ppb = std::max<int64_t>(1, 4096 / hw);
+    if (p.ppb > n) p.ppb = n;
+    p.nb = qt_cdiv(n, p.ppb);
+    return p;
+}
+
+// ws layout: [counters 256 KiB][lut: C x 2 x 256 floats][partials C x nb x 4 doubles]
+static inline float *lut_base(void *ws) { return (float *)((char *)ws + kBwdCounterBytes); }
+static inline double *part_base(void *ws, int64_t c) {
+    return (double *)((char *)ws + kBwdCounterBytes + c * 2 * kMaxLut * sizeof(float));
+}
+
+struct BwdArgs {
+    const float *g3;
+    qt_tape_t tape;
+    int64_t n, c, hw;
+    const float *gamma, *beta;
+    const double *sigma2;
+    double eps;
+    const float *va1;
+    float *grad_gamma, *grad_beta, *stats;
+    int64_t ppb, nb;
+    double *part;
+    unsigned *counter;
+    float *lut;      // [C][2][256]: mask, a1 per code
+};
+
+// mask (1/0) and a1 for one code of channel ch (layer.py:354-366)
+__device__ __forceinline__ void lut_entry(const qt_tape_t &t, int ch, uint32_t code, float bet,
+                                          float sg, float &m, float &a1) {
+    const float a2 = decode(code, t.step[ch], t.offset[ch], t.bits);
+    m = a2 > 0.f ? 1.f : 0.f;
+    a1 = __fdiv_rn(__fsub_rn(a2, bet), sg);
+}
+
+__device__ __forceinline__ uint64_t load_code_word(const uint8_t *codes, int64_t i0, int bits) {
+    const uint8_t *src = codes + (i0 >> 3) * bits;   // i0 multiple of 8
+    switch (bits) {
+        case 8: { uint2 u = *reinterpret_cast<const uint2 *>(src); return u.x | ((uint64_t)u.y << 32); }
+        case 4: return *reinterpret_cast<const uint32_t *>(src);
+        case 2: return *reinterpret_cast<const uint16_t *>(src);
+        default: return *src;
+    }
+}
+
+template <bool CODES, bool VA1>
+__global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
+    __shared__ float s_m[kMaxLut], s_a1[kMaxLut];
+    __shared__ double red[4][kBT / 32];
+    __shared__ bool s_last;
+    const int ch = blockIdx.y;
+    const float gam = a.gamma[ch], bet = a.beta[ch], sg = safe_gamma(gam);
+    const int ncode = CODES ? (1 << a.tape.bits) : 0;
+    if (CODES) {
+        for (int code = threadIdx.x; code < ncode; code += kBT)
+            lut_entry(a.tape, ch, code, bet, sg, s_m[code], s_a1[code]);
+        __syncthreads();
+    }
+    const int64_t p0 = (int64_t)blockIdx.x * a.ppb;
+    const int64_t p1 = min(p0 + a.ppb, a.n);
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    const uint32_t cmask = (1u << a.tape.bits) - 1u;
+    // The summation order depends only on the shape (never on the tape
+    // type), so an exact tape and a K-bit tape with variance_a1 substituted
+    // produce bit-identical sums (reference test_layer.py:173-202).
+    if ((a.hw & 7) == 0) {
+        const int64_t groups = (p1 - p0) * (a.hw >> 3);
+        const int64_t gpp = a.hw >> 3;
+        for (int64_t gi = threadIdx.x; gi < groups; gi += kBT) {
+            const int64_t pl = gi / gpp, off = (gi - pl * gpp) << 3;
+            const int64_t i0 = ((p0 + pl) * a.c + ch) * a.hw + off;
+            const float4 ga = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0));
+            const float4 gb = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0) + 1);
+            const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+            float mv[8], av[8];
+            if (CODES) {
+                const uint64_t word = load_code_word(a.tape.codes, i0, a.tape.bits);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t code = (uint32_t)(word >> (j * a.tape.bits)) & cmask;
+                    mv[j] = s_m[code];
+                    av[j] = s_a1[code];
+                }
+            } else {
+                const float4 xa = __ldg(reinterpret_cast<const float4 *>(a.tape.a2 + i0));
+                const float4 xb = __ldg(reinterpret_cast<const float4 *>(a.tape.a2 + i0) + 1);
+                const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    mv[j] = xv[j] > 0.f ? 1.f : 0.f;
+                    av[j] = __fdiv_rn(__fsub_rn(xv[j], bet), sg);
+                }
+            }
+            double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float g3m = __fmul_rn(gv[j], mv[j]);
+                const float g1 = __fmul_rn(g3m, gam);
+                const float a1v = VA1 ? a.va1[i0 + j] : av[j];
+                d0 += (double)g3m;
+                d1 += (double)__fmul_rn(av[j], g3m);
+                d2 += (double)g1;
+                d3 += (double)__fmul_rn(a1v, g1);
+            }
+            v0 += d0; v1 += d1; v2 += d2; v3 += d3;
+        }
+    } else {
+        const int64_t cnt = (p1 - p0) * a.hw;
+        for (int64_t e = threadIdx.x; e < cnt; e += kBT) {
+            const int64_t pl = e / a.hw, off = e - pl * a.hw;
+            const int64_t i = ((p0 + pl) * a.c + ch) * a.hw + off;
+            float m, a1;
+            if (CODES) {
+                const uint32_t code = get_code(a.tape.codes, i, a.tape.bits);
+                m = s_m[code];
+                a1 = s_a1[code];
+            } else {
+                const float a2 = a.tape.a2[i];
+                m = a2 > 0.f ? 1.f : 0.f;
+                a1 = __fdiv_rn(__fsub_rn(a2, bet), sg);
+            }
+            const float g3m = __fmul_rn(a.g3[i], m);
+            const float g1 = __fmul_rn(g3m, gam);
+            const float a1v = VA1 ? a.va1[i] : a1;
+            v0 += (double)g3m;
+            v1 += (double)__fmul_rn(a1, g3m);
+            v2 += (double)g1;
+            v3 += (double)__fmul_rn(a1v, g1);
+        }
+    }
+    v0 = warp_sum(v0); v1 = warp_sum(v1); v2 = warp_sum(v2); v3 = warp_sum(v3);
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red[0][w] = v0; red[1][w] = v1; red[2][w] = v2; red[3][w] = v3;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double *pp = a.part + (ch * a.nb + blockIdx.x) * 4;
+        for (int j = 0; j < 4; ++j) {
+            double t = 0.0;
+            for (int q = 0; q < kBT / 32; ++q) t += red[j][q];
+            pp[j] = t;
+        }
+        __threadfence();
+        const unsigned prev = atomicAdd(a.counter + ch, 1u);
+        s_last = prev == (unsigned)a.nb - 1;
+        if (s_last) a.counter[ch] = 0;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    // last block of this channel: publish the code table for the apply pass
+    if (CODES) {
+        float *lut = a.lut + (int64_t)ch * 2 * kMaxLut;
+        for (int code = threadIdx.x; code < ncode; code += kBT) {
+            lut[code] = s_m[code];
+            lut[kMaxLut + code] = s_a1[code];
+        }
+    }
+    if (threadIdx.x == 0) {
+        __threadfence();
+        double s[4] = {0.0, 0.0, 0.0, 0.0};
+        const volatile double *pp = a.part + ch * a.nb * 4;
+        for (int64_t b = 0; b < a.nb; ++b)
+            for (int j = 0; j < 4; ++j) s[j] += pp[4 * b + j];
+        const double cntd = (double)(a.n * a.hw);
+        if (a.grad_beta) a.grad_beta[ch] = __double2float_rn((double)a.grad_beta[ch] + s[0]);
+        if (a.grad_gamma) a.grad_gamma[ch] = __double2float_rn((double)a.grad_gamma[ch] + s[1]);
+        a.stats[ch] = __double2float_rn(s[2] / cntd);                         // t2
+        a.stats[a.c + ch] = __double2float_rn(s[3] / cntd);                   // t3
+        a.stats[2 * a.c + ch] =
+            __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(a.sigma2[ch], a.eps))));  // inv
+    }
+}
+
+struct ApplyArgs {
+    const float *g3;
+    qt_tape_t tape;
+    int64_t n, c, h, w;
+    const float *gamma, *beta, *va1, *stats, *res;
+    const float *lut;
+    int64_t cr, sc;
+    float *g_in;
+};
+
+__device__ __forceinline__ float res_value(const ApplyArgs &a, int64_t i, int64_t pl, int ch,
+                                           int64_t hw) {
+    if (a.sc == 1 && a.cr == a.c) return a.res[i];
+    const int64_t p = i - pl * hw;
+    const int64_t y = p / a.w, x = p - y * a.w;
+    if (y % a.sc || x % a.sc) return 0.f;
+    const int64_t nn = pl / a.c;
+    const int64_t hr = a.h / a.sc, wr = a.w / a.sc;
+    return a.res[((nn * a.cr + ch) * hr + y / a.sc) * wr + x / a.sc];
+}
+
+template <bool CODES, bool VA1>
+__global__ void __launch_bounds__(kBT) bn_bwd_apply_kernel(ApplyArgs a) {
+    const int64_t hw = a.h * a.w;
+    const int64_t numel = a.n * a.c * hw;
+    const uint32_t cmask = (1u << a.tape.bits) - 1u;
+    if (CODES && (hw & 7) == 0) {
+        const int64_t groups = numel >> 3;
+        for (int64_t gi = (int64_t)blockIdx.x * kBT + threadIdx.x; gi < groups;
+             gi += (int64_t)gridDim.x * kBT) {
+            const int64_t i0 = gi << 3;
+            const int64_t pl = i0 / hw;
+            const int ch = (int)(pl % a.c);
+            const float gam = __ldg(a.gamma + ch);
+            const float t2 = __ldg(a.stats + ch), t3 = __ldg(a.stats + a.c + ch);
+            const float inv = __ldg(a.stats + 2 * a.c + ch);
+            const float *lm = a.lut + (int64_t)ch * 2 * kMaxLut;
+            const float4 ga = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0));
+            const float4 gb = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0) + 1);
+            const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
+            const uint64_t word = load_code_word(a.tape.codes, i0, a.tape.bits);
+            float o[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t code = (uint32_t)(word >> (j * a.tape.bits)) & cmask;
+                const float m = __ldg(lm + code), a1 = __ldg(lm + kMaxLut + code);
+                const float g1 = __fmul_rn(__fmul_rn(gv[j], m), gam);
+                const float a1v = VA1 ? a.va1[i0 + j] : a1;
+                float r = __fsub_rn(g1, t2);                       // layer.py:305
+                r = __fsub_rn(r, __fmul_rn(a1v, t3));              // :306
+                o[j] = __fmul_rn(r, inv);                          // :307
+            }
+            if (a.res) {
+                if (a.sc == 1 && a.cr == a.c) {
+                    const float4 ra = __ldg(reinterpret_cast<const float4 *>(a.res + i0));
+                    const float4 rb = __ldg(reinterpret_cast<const float4 *>(a.res + i0) + 1);
+                    const float rv[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) o[j] = __fadd_rn(o[j], rv[j]);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        o[j] = __fadd_rn(o[j], res_value(a, i0 + j, pl, ch, hw));
+                }
+            }
+            float4 *dst = reinterpret_cast<float4 *>(a.g_in + i0);
+            dst[0] = make_float4(o[0], o[1], o[2], o[3]);
+            dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+        }
+        return;
+    }
+    for (int64_t i = (int64_t)blockIdx.x * kBT + threadIdx.x; i < numel;
+         i += (int64_t)gridDim.x * kBT) {
+        const int64_t pl = i / hw;
+        const int ch = (int)(pl % a.c);
+        const float gam = a.gamma[ch];
+        float m, a1;
+        if (CODES) {
+            const uint32_t code = get_code(a.tape.codes, i, a.tape.bits);
+            const float *lm = a.lut + (int64_t)ch * 2 * kMaxLut;
+            m = lm[code];
+            a1 = lm[kMaxLut + code];
+        } else {
+            const float a2 = a.tape.a2[i];
+            m = a2 > 0.f ? 1.f : 0.f;
+            a1 = __fdiv_rn(__fsub_rn(a2, a.beta[ch]), safe_gamma(gam));
+        }
+        const float g1 = __fmul_rn(__fmul_rn(a.g3[i], m), gam);
+        const float a1v = VA1 ? a.va1[i] : a1;
+        float r = __fsub_rn(g1, a.stats[ch]);
+        r = __fsub_rn(r, __fmul_rn(a1v, a.stats[a.c + ch]));
+        r = __fmul_rn(r, a.stats[2 * a.c + ch]);
+        if (a.res) r = __fadd_rn(r, res_value(a, i, pl, ch, hw));
+        a.g_in[i] = r;
+    }
+}
+
+}  // namespace qt
+
+using namespace qt;
+
+extern "C" int64_t qt_bn_backward_workspace(int64_t n, int64_t c, int64_t hw) {
+    BwdPart p = bwd_partition(n, hw);
+    return kBwdCounterBytes + c * 2 * kMaxLut * (int64_t)sizeof(float) +
+           c * p.nb * 4 * (int64_t)sizeof(double);
+}
+
+extern "C" int qt_bn_backward_reduce(const float *g3, qt_tape_t tape, int64_t n, int64_t c,
+                                     int64_t hw, const float *gamma_tape, const float *beta_tape,
+                                     const double *sigma2, double eps, const float *variance_a1,
+                                     float *grad_gamma, float *grad_beta, float *stats, void *ws,
+                                     qt_stream_t stream) {
+    QT_REQUIRE(g3 && gamma_tape && beta_tape && sigma2 && stats && ws);
+    QT_REQUIRE(n > 0 && c > 0 && hw > 0 && c <= 65535);
+    QT_REQUIRE(tape.a2 || (tape.codes && tape.step && tape.offset && qt_bits_ok(tape.bits)));
+    BwdPart p = bwd_partition(n, hw);
+    const bool codes = tape.a2 == nullptr;
+    if (!codes) tape.bits = 1;
+    BwdArgs a{g3, tape, n, c, hw, gamma_tape, beta_tape, sigma2, eps, variance_a1, grad_gamma,
+              grad_beta, stats, p.ppb, p.nb, part_base(ws, c), (unsigned *)ws, lut_base(ws)};
+    dim3 grid((unsigned)p.nb, (unsigned)c);
+    cudaStream_t s = qt_s(stream);
+    if (codes)
+        variance_a1 ? bn_bwd_reduce_kernel<true, true><<<grid, kBT, 0, s>>>(a)
+                    : bn_bwd_reduce_kernel<true, false><<<grid, kBT, 0, s>>>(a);
+    else
+        variance_a1 ? bn_bwd_reduce_kernel<false, true><<<grid, kBT, 0, s>>>(a)
+                    : bn_bwd_reduce_kernel<false, false><<<grid, kBT, 0, s>>>(a);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+extern "C" int qt_bn_backward_apply(const float *g3, qt_tape_t tape, int64_t n, int64_t c,
+                                    int64_t h, int64_t w, const float *gamma_tape,
+                                    const float *beta_tape, const float *variance_a1,
+                                    const float *stats, const float *res_g, int64_t cr, int64_t sc,
+                                    const void *ws, float *g_in, qt_stream_t stream) {
+    QT_REQUIRE(g3 && gamma_tape && beta_tape && stats && g_in && ws && n > 0 && c > 0 && h > 0 &&
+               w > 0);
+    QT_REQUIRE(tape.a2 || (tape.codes && tape.step && tape.offset && qt_bits_ok(tape.bits)));
+    QT_REQUIRE(!res_g || (sc >= 1 && h % sc == 0 && w % sc == 0 && cr >= c));
+    const bool codes = tape.a2 == nullptr;
+    if (!codes) tape.bits = 1;
+    ApplyArgs a{g3, tape, n, c, h, w, gamma_tape, beta_tape, variance_a1, stats, res_g,
+                lut_base((void *)ws), cr, sc, g_in};
+    const int64_t work = codes && ((h * w) & 7) == 0 ? (n * c * h * w) >> 3 : n * c * h * w;
+    int64_t blocks = std::min<int64_t>(qt_cdiv(work, kBT), 148 * 16);
+    blocks = std::max<int64_t>(blocks, 1);
+    cudaStream_t s = qt_s(stream);
+    if (codes)
+        variance_a1 ? bn_bwd_apply_kernel<true, true><<<(unsigned)blocks, kBT, 0, s>>>(a)
+                    : bn_bwd_apply_kernel<true, false><<<(unsigned)blocks, kBT, 0, s>>>(a);
+    else
+        variance_a1 ? bn_bwd_apply_kernel<false, true><<<(unsigned)blocks, kBT, 0, s>>>(a)
+                    : bn_bwd_apply_kernel<false, false><<<(unsigned)blocks, kBT, 0, s>>>(a);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}

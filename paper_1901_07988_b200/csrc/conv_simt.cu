@@ -270,16 +270,6 @@ static int run_gemm(LA la, LB lb, EP ep, int64_t M, int64_t N, int64_t K, int64_
     return QT_OK;
 }
 
-// grad_w[i] = fp32(grad_w[i] + fp32(sum_z ws[z][i]))  (layer.py:167)
-__global__ void splitk_reduce(const float *ws, int64_t splits, int64_t count, float *grad_w) {
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        for (int64_t z = 0; z < splits; ++z) s += (double)ws[z * count + i];
-        grad_w[i] = __fadd_rn(grad_w[i], __double2float_rn(s));
-    }
-}
-
 static ConvGeo make_geo(int64_t n, int64_t ci, int64_t h, int64_t w, int64_t co, int64_t kh,
                         int64_t kw, int64_t s, int64_t pad) {
     ConvGeo g{n, ci, h, w, co, kh, kw, s, pad, 0, 0};
@@ -316,6 +306,11 @@ int qt_tc_conv_forward(const float *x, const float *w, float *out, const qt::Con
                        const float *res, int64_t cr, int64_t sr, void *ws, cudaStream_t s);
 int qt_tc_conv_dgrad(const float *gr, const float *w, float *gx, const qt::ConvGeo &g, void *ws,
                      cudaStream_t s);
+int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
+                     const qt::ConvGeo &g, void *ws, cudaStream_t st);
+int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g);
+int qt_tc_wgrad_reduce(const float *partial, int64_t splits, int64_t count, float *grad_w,
+                       cudaStream_t st);
 
 extern "C" int qt_conv_forward(const float *x, const float *w, float *out, int64_t n, int64_t ci,
                                int64_t h, int64_t wd, int64_t co, int64_t kh, int64_t kw,
@@ -353,7 +348,8 @@ extern "C" int64_t qt_conv_wgrad_workspace(int64_t n, int64_t ci, int64_t h, int
     if (!geo_ok(g)) return 0;
     int64_t kps, splits;
     wgrad_plan(g, kps, splits);
-    return splits * co * ci * kh * kw * (int64_t)sizeof(float) + 256;
+    return std::max(splits * co * ci * kh * kw * (int64_t)sizeof(float), qt_tc_wgrad_workspace(g)) +
+           256;
 }
 
 extern "C" int qt_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
@@ -363,6 +359,8 @@ extern "C" int qt_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plai
     ConvGeo g = make_geo(n, ci, h, wd, co, kh, kw, stride, pad);
     QT_REQUIRE(gr && grad_w && ws && geo_ok(g));
     QT_REQUIRE(x_plain || act.a2 || (act.codes && act.step && act.offset && qt_bits_ok(act.bits)));
+    int rc0 = qt_tc_conv_wgrad(gr, act, x_plain, grad_w, g, ws, qt_s(stream));
+    if (rc0 != QT_EUNSUPPORTED) return rc0;
     const int64_t M = co, N = ci * kh * kw, K = n * g.oh * g.ow;
     int64_t kps, splits;
     wgrad_plan(g, kps, splits);
@@ -371,9 +369,5 @@ extern "C" int qt_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plai
     StorePartial ep{(float *)ws, M, N};
     int rc = run_gemm<true, true>(la, lb, ep, M, N, K, kps, qt_s(stream));
     if (rc) return rc;
-    const int64_t count = M * N;
-    splitk_reduce<<<(unsigned)std::min<int64_t>(qt_cdiv(count, 256), 4096), 256, 0, qt_s(stream)>>>(
-        (const float *)ws, splits, count, grad_w);
-    QT_CHECK_LAUNCH();
-    return QT_OK;
+    return qt_tc_wgrad_reduce((const float *)ws, splits, M * N, grad_w, qt_s(stream));
 }

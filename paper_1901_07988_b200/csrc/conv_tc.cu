@@ -45,8 +45,8 @@ struct FwdCfg {
     // raw activation box (TMA, MN-major) + KW taps x (hi, lo) K-major + KW x weights (hi, lo)
     static constexpr int STAGE_BYTES = A_BYTES * (1 + 2 * KW) + 2 * KW * B_SLOT;
     static constexpr int S0 = (200 * 1024) / STAGE_BYTES;
-    static constexpr int S = S0 > 4 ? 4 : (S0 < 1 ? 1 : S0);
-    static constexpr int SMEM = S * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+    static constexpr int S_MAX = S0 > 4 ? 4 : (S0 < 1 ? 1 : S0);
+    static int smem_bytes(int stages) { return stages * STAGE_BYTES + 1024 /*align*/ + 256; }
     static constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
     static constexpr int A_SW = OWT * 4;     // swizzle bytes of the raw activation box
     static constexpr int K_SW = KC * 4;      // swizzle bytes of the K-major operand tiles
@@ -55,6 +55,7 @@ struct FwdCfg {
 struct FwdGeo {
     int n, ci, h, w, co, kh, kw, pad, oh, ow;
     int rows, nimg, tiles_per_img;  // tile = nimg images x rows x OW pixels
+    int stages;                     // smem ring depth (<= the K loop length)
 };
 
 struct EpiParams {
@@ -69,12 +70,12 @@ struct EpiParams {
 // by the transform warps (TMA cannot start a tile at an unaligned innermost
 // coordinate, so the +-1 column shift and its zero padding happen in smem).
 template <int BN, int OWT, int KC, int KW>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTcThreads, 2)
     conv_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmBh,
                        const __grid_constant__ CUtensorMap tmBl, FwdGeo g, EpiParams ep) {
     using C = FwdCfg<BN, OWT, KC, KW>;
-    constexpr int S = C::S;
+    const int S = g.stages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
     uint64_t *full = (uint64_t *)(smem + S * C::STAGE_BYTES);
@@ -322,10 +323,17 @@ static int launch_fwd(const CUtensorMap &a, const CUtensorMap &bh, const CUtenso
     auto kern = conv_fwd_tc_kernel<BN, OWT, KC, KW>;
     static bool attr = false;
     if (!attr) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::SMEM);
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    kern<<<dim3(tiles, ntiles), kTcThreads, C::SMEM, st>>>(a, bh, bl, g, ep);
+    // ring depth: no deeper than the K loop, and small enough that 2+ CTAs
+    // share an SM (one CTA's epilogue / prologue overlaps another's mainloop)
+    FwdGeo gg = g;
+    const int nst = g.kh * (g.ci / KC);
+    int S = std::min(nst, C::S_MAX);
+    while (S > 1 && C::smem_bytes(S) > 112 * 1024) --S;
+    gg.stages = S;
+    kern<<<dim3(tiles, ntiles), kTcThreads, C::smem_bytes(S), st>>>(a, bh, bl, gg, ep);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }

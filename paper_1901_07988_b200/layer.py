@@ -419,6 +419,6 @@ def layer_backward(g_out: torch.Tensor, tape: LayerTape, p: LayerParams,
         cr = residual_grad.shape[1]
         sc = h // residual_grad.shape[2] if g3.dim() == 4 else 1
     N.call("qt_bn_backward_apply", N.ptr(g3), nt, n, c, h, w, N.ptr(tape.gamma), N.ptr(tape.beta),
-           N.ptr(variance_a1), N.ptr(stats), N.ptr(residual_grad), cr, sc, N.ptr(g3))
+           N.ptr(variance_a1), N.ptr(stats), N.ptr(residual_grad), cr, sc, N.ptr(bws), N.ptr(g3))
     ops._check_finite(g3)
     return g3

@@ -191,3 +191,40 @@ def test_zero_gradient():
     gin = L.layer_backward(torch.zeros_like(out), tape, p)
     assert not bool(gin.any()) and not bool(p.grad_weight.any())
     assert not bool(p.grad_gamma.any()) and not bool(p.grad_beta.any())
+
+
+@pytest.mark.parametrize("cfg", [
+    # (n, ci, co, hw, k, pad, bits, mode) -- tensor-core shapes (wgrad decodes the codes in smem)
+    (4, 16, 16, 32, 3, 1, 4, "approx"), (8, 64, 16, 8, 1, 0, 4, "approx"),
+    (4, 16, 64, 16, 1, 0, 8, "approx"), (2, 32, 32, 16, 3, 1, 2, "approx"),
+    (4, 16, 16, 32, 3, 1, 4, "exact"), (4, 32, 128, 8, 1, 0, 1, "approx"),
+])
+def test_backward_given_device_tape(cfg):
+    """Backward parity with the oracle fed OUR tape (codes, step, offset,
+    sigma2, frozen gamma/beta): isolates the backward kernels (TC wgrad with
+    fused decode, TC dgrad, BN/ReLU backward) from forward-moment ulps."""
+    n, ci, co, hw, k, pad, bits, mode = cfg
+    rng = np.random.default_rng(sum(cfg[:7]))
+    w = (rng.standard_normal((co, ci, k, k)) * 0.3).astype(np.float32)
+    gamma = rng.uniform(0.5, 1.5, ci).astype(np.float32)
+    beta = rng.uniform(-0.3, 0.3, ci).astype(np.float32)
+    x = (rng.standard_normal((n, ci, hw, hw)) * 2 + 0.5).astype(np.float32)
+    p = L.LayerParams(kind="conv", weight=dev(w), stride=1, pad=pad, gamma=dev(gamma),
+                      beta=dev(beta))
+    y, tape = L.layer_forward(dev(x), p, mode=mode, bits=bits)
+    g = rng.standard_normal(tuple(y.shape)).astype(np.float32)
+    gin = L.layer_backward(dev(g), tape, p)
+    ot = {"mode": mode, "sigma2": host(tape.sigma2), "gamma": host(tape.gamma),
+          "beta": host(tape.beta), "eps": 1e-5}
+    if tape.is_quantized:
+        q = tape.stored
+        ot["q"] = {"codes": host(q.codes), "bits": bits, "shape": tuple(q.shape),
+                   "dtype": np.dtype(np.float32), "step": host(q.step), "offset": host(q.offset)}
+    else:
+        ot["a2"] = host(tape.stored)
+    op = O.new_params("conv", w, 1, pad, gamma.copy(), beta.copy())
+    ogin = O.layer_bwd(g, ot, op)
+    assert norm_err(host(gin), ogin) < LAYER_TOL
+    assert norm_err(host(p.grad_weight), op["grad_weight"]) < LAYER_TOL
+    assert norm_err(host(p.grad_gamma), op["grad_gamma"]) < LAYER_TOL
+    assert norm_err(host(p.grad_beta), op["grad_beta"]) < LAYER_TOL
