@@ -95,7 +95,18 @@ int qt_bn_relu_forward(const float *x, int64_t n, int64_t c, int64_t hw,
                        const double *mean, const double *var, double eps,
                        const float *gamma, const float *beta, int mode, int bits,
                        float *a3_out, float *a2_tape, uint8_t *codes, double *step,
-                       int64_t *offset, int64_t *clip_count, qt_stream_t stream);
+                       int64_t *offset, int64_t *clip_count, const void *consts,
+                       qt_stream_t stream);
+
+/* Training-mode fusion of the layer's per-channel work in ONE launch:
+ * qt_bn_stats + the constants of qt_bn_relu_forward (pass the same `consts`
+ * buffer, 48 bytes per channel, to it) + the frozen gamma/beta tape copies
+ * + the tape's step/offset + zeroing the clip counter (layer.py:236-255). */
+int qt_bn_stats_prep(const float *x, int64_t n, int64_t c, int64_t hw, double eps,
+                     const float *gamma, const float *beta, int bits, double *mean,
+                     double *var, double *running_mean, double *running_var,
+                     float *gamma_copy, float *beta_copy, double *step, int64_t *offset,
+                     int64_t *clip_count, void *consts, void *ws, qt_stream_t stream);
 
 /* Tape source descriptor used by the backward kernels: either a fp32 pre-ReLU
  * tape (a2 != NULL) or packed codes + frozen constants. */

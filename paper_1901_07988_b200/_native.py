@@ -45,7 +45,9 @@ SIGNATURES = {
     "qt_bn_stats": (I32, [P, I64, I64, I64, P, P, P, P, P, P]),
     "qt_channel_sum": (I32, [P, I64, I64, I64, P, P, P]),
     "qt_bn_relu_forward": (I32, [P, I64, I64, I64, P, P, F64, P, P, I32, I32,
-                                 P, P, P, P, P, P, P]),
+                                 P, P, P, P, P, P, P, P]),
+    "qt_bn_stats_prep": (I32, [P, I64, I64, I64, F64, P, P, I32, P, P, P, P, P, P, P, P, P,
+                               P, P, P]),
     "qt_reconstruct": (I32, [Tape, I64, I64, I64, P, P, P, P, P, P]),
     "qt_bn_backward_workspace": (I64, [I64, I64, I64]),
     "qt_bn_backward_reduce": (I32, [P, Tape, I64, I64, I64, P, P, P, F64, P, P, P,

@@ -9,7 +9,7 @@
 namespace qt {
 
 constexpr int kRThreads = 256;
-constexpr int64_t kTargetPerBlock = 8192;
+constexpr int64_t kTargetPerBlock = 4096;
 // Workspace layout of every reduction: [kCounterBytes of per-channel
 // completion counters (always left at zero)][float64 partials].  Keeping the
 // counters at a fixed offset lets differently-shaped launches share one
@@ -73,6 +73,15 @@ struct StatsArgs {
     double *mean, *var, *rmean, *rvar;
     double *part;       // [c][nb][2]
     unsigned *counter;  // [c]
+    // optional fused preparation of the layer's forward (qt_bn_stats_prep)
+    const float *gamma, *beta;
+    int bits;
+    double eps;
+    BnConst *consts;
+    float *gcopy, *bcopy;
+    double *step;
+    int64_t *offset;
+    int64_t *clip;
 };
 
 __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
@@ -83,7 +92,21 @@ __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
     const double shift = (double)a.x[ch * a.hw];  // x[0, c, 0]: shifted sums
     double v[2] = {0.0, 0.0};
     const int64_t cnt = (p1 - p0) * a.hw;
-    if ((a.hw & 3) == 0) {
+    if ((a.hw & 7) == 0) {
+        const int64_t hw8 = a.hw >> 3;
+        for (int64_t e = threadIdx.x; e < cnt / 8; e += kRThreads) {
+            int64_t pl = e / hw8, off = e - pl * hw8;
+            const float4 *src = reinterpret_cast<const float4 *>(a.x + ((p0 + pl) * a.c + ch) * a.hw) + 2 * off;
+            const float4 q = __ldg(src), r = __ldg(src + 1);
+            double d0 = (double)q.x - shift, d1 = (double)q.y - shift;
+            double d2 = (double)q.z - shift, d3 = (double)q.w - shift;
+            double d4 = (double)r.x - shift, d5 = (double)r.y - shift;
+            double d6 = (double)r.z - shift, d7 = (double)r.w - shift;
+            v[0] += ((d0 + d1) + (d2 + d3)) + ((d4 + d5) + (d6 + d7));
+            v[1] += ((d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3)) +
+                    ((d4 * d4 + d5 * d5) + (d6 * d6 + d7 * d7));
+        }
+    } else if ((a.hw & 3) == 0) {
         const int64_t hw4 = a.hw >> 2;
         for (int64_t e = threadIdx.x; e < cnt / 4; e += kRThreads) {
             int64_t pl = e / hw4, off = e - pl * hw4;
@@ -127,6 +150,17 @@ __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
             const double m = 0.9;
             a.rmean[ch] = __dadd_rn(__dmul_rn(a.rmean[ch], m), __dmul_rn(1.0 - m, mean));
             a.rvar[ch] = __dadd_rn(__dmul_rn(a.rvar[ch], m), __dmul_rn(1.0 - m, var));
+        }
+        if (a.consts) {  // per-channel constants of the fused forward (K1)
+            const float g = a.gamma[ch], b = a.beta[ch];
+            a.consts[ch] = bn_const(mean, var, a.eps, g, b, a.bits);
+            a.gcopy[ch] = g;          // frozen tape copies (layer.py:253-255)
+            a.bcopy[ch] = b;
+            if (a.bits) {
+                a.step[ch] = a.consts[ch].step;
+                a.offset[ch] = a.consts[ch].off;
+            }
+            if (ch == 0 && a.clip) *a.clip = 0;
         }
     }
 }
@@ -258,7 +292,28 @@ extern "C" int qt_bn_stats(const float *x, int64_t n, int64_t c, int64_t hw, dou
     QT_REQUIRE((running_mean == nullptr) == (running_var == nullptr));
     Part p = partition(n, hw);
     StatsArgs a{x, n, c, hw, p.planes_per_block, p.blocks, mean, var, running_mean, running_var,
-                (double *)((char *)ws + kCounterBytes), (unsigned *)ws};
+                (double *)((char *)ws + kCounterBytes), (unsigned *)ws,
+                nullptr, nullptr, 0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    dim3 grid((unsigned)p.blocks, (unsigned)c);
+    bn_stats_kernel<<<grid, kRThreads, 0, qt_s(stream)>>>(a);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+extern "C" int qt_bn_stats_prep(const float *x, int64_t n, int64_t c, int64_t hw, double eps,
+                                const float *gamma, const float *beta, int bits, double *mean,
+                                double *var, double *running_mean, double *running_var,
+                                float *gamma_copy, float *beta_copy, double *step, int64_t *offset,
+                                int64_t *clip_count, void *consts, void *ws, qt_stream_t stream) {
+    QT_REQUIRE(x && mean && var && ws && consts && gamma && beta && gamma_copy && beta_copy);
+    QT_REQUIRE(n > 0 && c > 0 && hw > 0 && c <= kMaxChannels);
+    QT_REQUIRE(bits == 0 || (qt_bits_ok(bits) && step && offset));
+    QT_REQUIRE((running_mean == nullptr) == (running_var == nullptr));
+    Part p = partition(n, hw);
+    StatsArgs a{x, n, c, hw, p.planes_per_block, p.blocks, mean, var, running_mean, running_var,
+                (double *)((char *)ws + kCounterBytes), (unsigned *)ws,
+                gamma, beta, bits, eps, (BnConst *)consts, gamma_copy, beta_copy, step, offset,
+                clip_count};
     dim3 grid((unsigned)p.blocks, (unsigned)c);
     bn_stats_kernel<<<grid, kRThreads, 0, qt_s(stream)>>>(a);
     QT_CHECK_LAUNCH();
@@ -270,7 +325,8 @@ extern "C" int qt_channel_sum(const float *x, int64_t n, int64_t c, int64_t hw, 
     QT_REQUIRE(x && out && ws && n > 0 && c > 0 && hw > 0 && c <= kMaxChannels);
     Part p = partition(n, hw);
     StatsArgs a{x, n, c, hw, p.planes_per_block, p.blocks, out, nullptr, nullptr, nullptr,
-                (double *)((char *)ws + kCounterBytes), (unsigned *)ws};
+                (double *)((char *)ws + kCounterBytes), (unsigned *)ws,
+                nullptr, nullptr, 0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     dim3 grid((unsigned)p.blocks, (unsigned)c);
     chan_sum_kernel<<<grid, kRThreads, 0, qt_s(stream)>>>(a);
     QT_CHECK_LAUNCH();

@@ -42,10 +42,22 @@ struct FwdArgs {
     double *step;
     int64_t *offset;
     unsigned long long *clip_count;
+    const BnConst *consts;   // optional: per-channel constants from qt_bn_stats_prep
 };
 
 __device__ __forceinline__ PlaneConst make_plane(const FwdArgs &a, int64_t ch, bool apply_bn) {
     PlaneConst p;
+    if (a.consts) {
+        const BnConst k = a.consts[ch];
+        p.m32 = k.m32;
+        p.inv32 = k.inv32;
+        p.g = k.g;
+        p.b = k.b;
+        p.scale = k.scale;
+        p.step = k.step;
+        p.off = k.off;
+        return p;
+    }
     if (apply_bn) {
         double inv = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(a.var[ch], a.eps)));  // layer.py:245
         p.m32 = __double2float_rn(a.mean[ch]);
@@ -85,7 +97,7 @@ __global__ void __launch_bounds__(kThreads) bn_relu_quant_kernel(FwdArgs a) {
             sp[q] = make_plane(a, (plane0 + q) % a.c, APPLY_BN);
     }
     // tape constants: frozen step/offset per channel (codec.py:137-143)
-    if (a.bits && a.step) {
+    if (a.bits && a.step && !a.consts) {
         for (int64_t ch = (int64_t)blockIdx.x * kThreads + threadIdx.x; ch < a.c;
              ch += (int64_t)gridDim.x * kThreads) {
             ChanCode cc = chan_code(a.gamma[ch], a.beta[ch], a.bits);
@@ -347,8 +359,9 @@ extern "C" int qt_bn_relu_forward(const float *x, int64_t n, int64_t c, int64_t 
                                   const double *mean, const double *var, double eps,
                                   const float *gamma, const float *beta, int mode, int bits,
                                   float *a3_out, float *a2_tape, uint8_t *codes, double *step,
-                                  int64_t *offset, int64_t *clip_count, qt_stream_t stream) {
-    QT_REQUIRE(n >= 0 && c > 0 && hw > 0 && x && mean && var && gamma && beta);
+                                  int64_t *offset, int64_t *clip_count, const void *consts,
+                                  qt_stream_t stream) {
+    QT_REQUIRE(n >= 0 && c > 0 && hw > 0 && x && ((mean && var) || consts) && gamma && beta);
     QT_REQUIRE(mode >= 0 && mode <= 2);
     QT_REQUIRE(bits == 0 || qt_bits_ok(bits));
     QT_REQUIRE(bits == 0 || codes);
@@ -370,6 +383,7 @@ extern "C" int qt_bn_relu_forward(const float *x, int64_t n, int64_t c, int64_t 
     f.step = step;
     f.offset = offset;
     f.clip_count = reinterpret_cast<unsigned long long *>(clip_count);
+    f.consts = (const BnConst *)consts;
     return launch_fwd(f, true, qt_s(stream));
 }
 

@@ -55,6 +55,36 @@ __device__ __forceinline__ ChanCode chan_code(float gamma, float beta, int bits)
     return r;
 }
 
+// Per-channel constants of the fused BN-apply + quantize (32 bytes).
+struct BnConst {
+    float m32, inv32, g, b;   // (float)mean, (float)(1/sqrt(var+eps)), gamma, beta
+    double scale;             // 2^K / (6 g)       (codec.py:101-104)
+    double step;              // 6 g 2^-K
+    int64_t off;              // floor(beta * scale) via x86 cast
+    int64_t pad_;
+};
+
+__device__ __forceinline__ BnConst bn_const(double mean, double var, double eps, float gamma,
+                                            float beta, int bits) {
+    BnConst k;
+    const double inv = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var, eps)));   // layer.py:245
+    k.m32 = __double2float_rn(mean);
+    k.inv32 = __double2float_rn(inv);
+    k.g = gamma;
+    k.b = beta;
+    k.scale = 0.0;
+    k.step = 0.0;
+    k.off = 0;
+    k.pad_ = 0;
+    if (bits) {
+        ChanCode cc = chan_code(gamma, beta, bits);
+        k.scale = cc.scale;
+        k.step = cc.step;
+        k.off = cc.off;
+    }
+    return k;
+}
+
 // Unclipped code with wrapping int64 arithmetic (codec.py:118-120).
 __device__ __forceinline__ int64_t raw_code(float a, double scale, int64_t off, int bits) {
     int64_t u = x86_f64_to_i64(floor(__dmul_rn((double)a, scale)));

@@ -46,7 +46,8 @@ struct FwdCfg {
     static constexpr int STAGE_BYTES = A_BYTES * (1 + 2 * KW) + 2 * KW * B_SLOT;
     static constexpr int S0 = (200 * 1024) / STAGE_BYTES;
     static constexpr int S_MAX = S0 > 4 ? 4 : (S0 < 1 ? 1 : S0);
-    static int smem_bytes(int stages) { return stages * STAGE_BYTES + 1024 /*align*/ + 256; }
+    static constexpr int OUT_BYTES = BM * BN * 4;                   // output staging tile
+    static int smem_bytes(int stages) { return stages * STAGE_BYTES + OUT_BYTES + 1024 + 256; }
     static constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
     static constexpr int A_SW = OWT * 4;     // swizzle bytes of the raw activation box
     static constexpr int K_SW = KC * 4;      // swizzle bytes of the K-major operand tiles
@@ -62,6 +63,7 @@ struct EpiParams {
     float *out;
     const float *res;
     int cr, sr;
+    int res_tma;   // 1: residual tile TMA-loaded into the output staging buffer
 };
 
 // One CTA = one 128-pixel x BN-channel output tile.  K loop: for each kernel
@@ -73,16 +75,21 @@ template <int BN, int OWT, int KC, int KW>
 __global__ void __launch_bounds__(kTcThreads, 2)
     conv_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmBh,
-                       const __grid_constant__ CUtensorMap tmBl, FwdGeo g, EpiParams ep) {
+                       const __grid_constant__ CUtensorMap tmBl,
+                       const __grid_constant__ CUtensorMap tmOut,
+                       const __grid_constant__ CUtensorMap tmRes, FwdGeo g, EpiParams ep) {
     using C = FwdCfg<BN, OWT, KC, KW>;
     const int S = g.stages;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t *full = (uint64_t *)(smem + S * C::STAGE_BYTES);
+    // output staging tile [nimg][BN][rows][OWT] fp32 (TMA-store box layout)
+    float *s_out = (float *)(smem + S * C::STAGE_BYTES);
+    uint64_t *full = (uint64_t *)(smem + S * C::STAGE_BYTES + C::OUT_BYTES);
     uint64_t *ready = full + S;
     uint64_t *empty = ready + S;
     uint64_t *done = empty + S;
-    uint32_t *tmem_slot = (uint32_t *)(done + 1);
+    uint64_t *resbar = done + 1;
+    uint32_t *tmem_slot = (uint32_t *)(resbar + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int tile = blockIdx.x;
@@ -99,6 +106,7 @@ __global__ void __launch_bounds__(kTcThreads, 2)
             mbar_init(&empty[s], 1);
         }
         mbar_init(done, 1);
+        mbar_init(resbar, 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
@@ -106,6 +114,7 @@ __global__ void __launch_bounds__(kTcThreads, 2)
         tma_prefetch(&tmA);
         tma_prefetch(&tmBh);
         tma_prefetch(&tmBl);
+        tma_prefetch(&tmOut);
     }
     tc_fence_before();
     __syncthreads();
@@ -124,6 +133,10 @@ __global__ void __launch_bounds__(kTcThreads, 2)
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------------------------- TMA producer
+            if (ep.res_tma) {  // shortcut tile straight into the output staging buffer
+                mbar_expect_tx(resbar, C::OUT_BYTES);
+                tma_load_4d(s_out, &tmRes, resbar, 0, h0, co0, n0);
+            }
             for (int i = 0; i < nstages; ++i) {
                 const int s = i % S;
                 const uint32_t ph = (uint32_t)(i / S) & 1u;
@@ -215,26 +228,48 @@ __global__ void __launch_bounds__(kTcThreads, 2)
         const int ratom = row / OWT, wcol = row % OWT;
         const int img = ratom / g.rows, rr = ratom % g.rows;
         const int nn = n0 + img, y = h0 + rr;
-        const int64_t ohw = (int64_t)g.oh * g.ow;
-        const int64_t pix = (int64_t)y * g.ow + wcol;
         const uint32_t tbase = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
+        // staging index of (channel j, this pixel): [img][BN][rows][OWT]
+        float *so = s_out + ((size_t)img * BN * g.rows + rr) * OWT + wcol;
+        const size_t cstride = (size_t)g.rows * OWT;
+        if (ep.res_tma) mbar_wait(resbar, 0);
+        const bool res_ldg = ep.res && !ep.res_tma;
 #pragma unroll 1
         for (int cb = 0; cb < BN; cb += 16) {
+            float rv[16];
+            if (res_ldg) {  // strided shortcut (sr > 1): gather, all loads in flight
+                const int64_t hr = (int64_t)g.oh * ep.sr, wr = (int64_t)g.ow * ep.sr;
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    const int co = co0 + cb + j;
+                    rv[j] = co < ep.cr ? __ldg(ep.res + (((int64_t)nn * ep.cr + co) * hr +
+                                                         (int64_t)y * ep.sr) * wr +
+                                                (int64_t)wcol * ep.sr)
+                                       : 0.f;
+                }
+            }
             uint32_t r[16];
             tmem_ld16(tbase + cb, r);
             tmem_wait_ld();
 #pragma unroll
             for (int j = 0; j < 16; ++j) {
-                const int co = co0 + cb + j;
-                if (co >= g.co) break;
                 float v = __uint_as_float(r[j]);
-                if (ep.res && co < ep.cr) {
-                    const int64_t hr = (int64_t)g.oh * ep.sr, wr = (int64_t)g.ow * ep.sr;
-                    v = __fadd_rn(v, ep.res[(((int64_t)nn * ep.cr + co) * hr + (int64_t)y * ep.sr) * wr +
-                                            (int64_t)wcol * ep.sr]);
+                float *dst = so + (size_t)(cb + j) * cstride;
+                // out = fp32(conv); cur += shortcut(res)  (engine.py:262-269)
+                if (ep.res_tma) {
+                    if (co0 + cb + j < ep.cr) v = __fadd_rn(v, *dst);
+                } else if (res_ldg && co0 + cb + j < ep.cr) {
+                    v = __fadd_rn(v, rv[j]);
                 }
-                ep.out[((int64_t)nn * g.co + co) * ohw + pix] = v;
+                *dst = v;
             }
+        }
+        fence_async_smem();
+        asm volatile("bar.sync 1, 128;" ::: "memory");   // the 4 epilogue warps
+        if (threadIdx.x == 64) {
+            tma_store_4d(&tmOut, s_out, 0, h0, co0, n0);
+            bulk_commit();
+            bulk_wait_read0();
         }
     }
     tc_fence_before();
@@ -316,9 +351,13 @@ static bool make_map_w(CUtensorMap *m, const float *b, int rows, int kdim, int b
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+struct Maps {
+    CUtensorMap a, bh, bl, out, res;
+};
+
 template <int BN, int OWT, int KC, int KW>
-static int launch_fwd(const CUtensorMap &a, const CUtensorMap &bh, const CUtensorMap &bl,
-                      const FwdGeo &g, const EpiParams &ep, int tiles, int ntiles, cudaStream_t st) {
+static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, int tiles, int ntiles,
+                      cudaStream_t st) {
     using C = FwdCfg<BN, OWT, KC, KW>;
     auto kern = conv_fwd_tc_kernel<BN, OWT, KC, KW>;
     static bool attr = false;
@@ -333,41 +372,54 @@ static int launch_fwd(const CUtensorMap &a, const CUtensorMap &bh, const CUtenso
     int S = std::min(nst, C::S_MAX);
     while (S > 1 && C::smem_bytes(S) > 112 * 1024) --S;
     gg.stages = S;
-    kern<<<dim3(tiles, ntiles), kTcThreads, C::smem_bytes(S), st>>>(a, bh, bl, gg, ep);
+    kern<<<dim3(tiles, ntiles), kTcThreads, C::smem_bytes(S), st>>>(m.a, m.bh, m.bl, m.out, m.res,
+                                                                   gg, ep);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
 
 template <int OWT, int KC, int KW>
-static int dispatch_bn(int bn, const CUtensorMap &a, const CUtensorMap &bh, const CUtensorMap &bl,
-                       const FwdGeo &g, const EpiParams &ep, int tiles, int ntiles,
-                       cudaStream_t st) {
+static int dispatch_bn(int bn, const Maps &m, const FwdGeo &g, const EpiParams &ep, int tiles,
+                       int ntiles, cudaStream_t st) {
     switch (bn) {
-        case 16: return launch_fwd<16, OWT, KC, KW>(a, bh, bl, g, ep, tiles, ntiles, st);
-        case 32: return launch_fwd<32, OWT, KC, KW>(a, bh, bl, g, ep, tiles, ntiles, st);
-        case 64: return launch_fwd<64, OWT, KC, KW>(a, bh, bl, g, ep, tiles, ntiles, st);
-        case 128: return launch_fwd<128, OWT, KC, KW>(a, bh, bl, g, ep, tiles, ntiles, st);
+        case 16: return launch_fwd<16, OWT, KC, KW>(m, g, ep, tiles, ntiles, st);
+        case 32: return launch_fwd<32, OWT, KC, KW>(m, g, ep, tiles, ntiles, st);
+        case 64: return launch_fwd<64, OWT, KC, KW>(m, g, ep, tiles, ntiles, st);
+        case 128: return launch_fwd<128, OWT, KC, KW>(m, g, ep, tiles, ntiles, st);
         default: return QT_EUNSUPPORTED;
     }
 }
 
 template <int OWT>
-static int dispatch_kc(int kc, int kw, int bn, const CUtensorMap &a, const CUtensorMap &bh,
-                       const CUtensorMap &bl, const FwdGeo &g, const EpiParams &ep, int tiles,
-                       int ntiles, cudaStream_t st) {
+static int dispatch_kc(int kc, int kw, int bn, const Maps &m, const FwdGeo &g,
+                       const EpiParams &ep, int tiles, int ntiles, cudaStream_t st) {
     if (kw == 1) {
         switch (kc) {
-            case 8: return dispatch_bn<OWT, 8, 1>(bn, a, bh, bl, g, ep, tiles, ntiles, st);
-            case 16: return dispatch_bn<OWT, 16, 1>(bn, a, bh, bl, g, ep, tiles, ntiles, st);
-            case 32: return dispatch_bn<OWT, 32, 1>(bn, a, bh, bl, g, ep, tiles, ntiles, st);
+            case 8: return dispatch_bn<OWT, 8, 1>(bn, m, g, ep, tiles, ntiles, st);
+            case 16: return dispatch_bn<OWT, 16, 1>(bn, m, g, ep, tiles, ntiles, st);
+            case 32: return dispatch_bn<OWT, 32, 1>(bn, m, g, ep, tiles, ntiles, st);
         }
     } else if (kw == 3) {
         switch (kc) {
-            case 8: return dispatch_bn<OWT, 8, 3>(bn, a, bh, bl, g, ep, tiles, ntiles, st);
-            case 16: return dispatch_bn<OWT, 16, 3>(bn, a, bh, bl, g, ep, tiles, ntiles, st);
+            case 8: return dispatch_bn<OWT, 8, 3>(bn, m, g, ep, tiles, ntiles, st);
+            case 16: return dispatch_bn<OWT, 16, 3>(bn, m, g, ep, tiles, ntiles, st);
         }
     }
     return QT_EUNSUPPORTED;
+}
+
+// (w, h, c, n) view of an NCHW fp32 tensor, box = one output tile of BN channels
+static bool make_map_nchw(CUtensorMap *m, const float *t, int n, int c, int h, int w, int rows,
+                          int bn, int nimg) {
+    auto enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)w, (cuuint64_t)h, (cuuint64_t)c, (cuuint64_t)n};
+    cuuint64_t strides[3] = {(cuuint64_t)w * 4, (cuuint64_t)h * w * 4, (cuuint64_t)c * h * w * 4};
+    cuuint32_t box[4] = {(cuuint32_t)w, (cuuint32_t)rows, (cuuint32_t)bn, (cuuint32_t)nimg};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void *)t, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // Shape predicate of the tensor-core path (also used by qt_conv_uses_tc).
@@ -411,17 +463,25 @@ static int tc_conv_s1(const float *x, const float *w, float *out, int n, int ci,
     weight_prep_kernel<<<(unsigned)std::min<int64_t>(qt_cdiv((int64_t)co * kdim, 256), 1024), 256, 0,
                          st>>>(w, co, ci, kh, kw, flip, bhi, blo);
     QT_CHECK_LAUNCH();
-    CUtensorMap ma, mbh, mbl;
-    if (!make_map_act(&ma, x, g, g.ow, kc) || !make_map_w(&mbh, bhi, co, kdim, bn, kc) ||
-        !make_map_w(&mbl, blo, co, kdim, bn, kc))
+    Maps mp;
+    if (!make_map_act(&mp.a, x, g, g.ow, kc) || !make_map_w(&mp.bh, bhi, co, kdim, bn, kc) ||
+        !make_map_w(&mp.bl, blo, co, kdim, bn, kc) ||
+        !make_map_nchw(&mp.out, out, n, co, g.oh, g.ow, g.rows, bn, g.nimg))
         return QT_EUNSUPPORTED;
-    EpiParams ep{out, res, cr, sr};
+    EpiParams ep{out, res, cr, sr, 0};
+    if (res && sr == 1) {  // same-resolution shortcut: one TMA box per tile (OOB channels -> 0)
+        if (!make_map_nchw(&mp.res, res, n, cr, g.oh, g.ow, g.rows, bn, g.nimg))
+            return QT_EUNSUPPORTED;
+        ep.res_tma = 1;
+    } else {
+        mp.res = mp.out;   // unused
+    }
     const int tiles = (n / g.nimg) * g.tiles_per_img;
     const int ntiles = co / bn;
     switch (g.ow) {
-        case 8: return dispatch_kc<8>(kc, kw, bn, ma, mbh, mbl, g, ep, tiles, ntiles, st);
-        case 16: return dispatch_kc<16>(kc, kw, bn, ma, mbh, mbl, g, ep, tiles, ntiles, st);
-        case 32: return dispatch_kc<32>(kc, kw, bn, ma, mbh, mbl, g, ep, tiles, ntiles, st);
+        case 8: return dispatch_kc<8>(kc, kw, bn, mp, g, ep, tiles, ntiles, st);
+        case 16: return dispatch_kc<16>(kc, kw, bn, mp, g, ep, tiles, ntiles, st);
+        case 32: return dispatch_kc<32>(kc, kw, bn, mp, g, ep, tiles, ntiles, st);
     }
     return QT_EUNSUPPORTED;
 }

@@ -48,7 +48,10 @@ struct WgParams {
     int total_chunks, chunks_per_split, splits;
     int stages;
     uint32_t tmem_cols;
+    int lut_ch;              // >0: channels per CTA covered by the smem code table
 };
+
+constexpr int kWgLutEntries = 4096;   // (channels x 2^K) entries of (hi, lo) = 32 KiB
 
 __device__ __forceinline__ float act_value(const WgParams &p, int nn, int c, int y, int x) {
     if (y < 0 || y >= p.h || x < 0 || x >= p.w) return 0.f;  // conv zero padding
@@ -60,7 +63,7 @@ __device__ __forceinline__ float act_value(const WgParams &p, int nn, int c, int
     return (a >= 0.f || isnan(a)) ? a : 0.f;  // ReLU as np.maximum (layer.py:356)
 }
 
-template <int BN>
+template <int BN, int KW>
 __global__ void __launch_bounds__(kWgThreads, 1)
     conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmG, WgParams p) {
     using C = WgCfg<BN>;
@@ -159,6 +162,21 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         const int kk = p.kh * p.kw;
         const int quads_per_chunk = 8;    // 32 px / 4
         const int tasks = (c_end - c_begin) * p.kh * quads_per_chunk;
+        // per-CTA code table: relu(decode(code)) of every channel in range,
+        // pre-split into TF32 (hi, lo) -- exactly the reference's fp32 a3
+        float *s_lut = reinterpret_cast<float *>(smem + S * stage_bytes + 1024);
+        const bool use_lut = p.lut_ch > 0;
+        if (use_lut) {
+            const int nc = c_end - c_begin, ncode = 1 << p.tape.bits;
+            for (int e = t; e < nc * ncode; e += 256) {
+                const int c = c_begin + e / ncode, code = e % ncode;
+                float a = decode((uint32_t)code, p.tape.step[c], p.tape.offset[c], p.tape.bits);
+                a = (a >= 0.f || isnan(a)) ? a : 0.f;
+                split_tf32(a, s_lut[2 * e], s_lut[2 * e + 1]);
+            }
+            // the 8 transform warps sync among themselves (named barrier 1)
+            asm volatile("bar.sync 1, 256;" ::: "memory");
+        }
         for (int i = 0; i < nk; ++i) {
             const int s = i % S;
             const uint32_t ph = (uint32_t)(i / S) & 1u;
@@ -188,24 +206,48 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const int pix = q * 4;                           // pixel within chunk
                 const int oy = y0 + pix / p.ow, ox0 = pix % p.ow;
                 const int iy = oy + u - p.pad;
-                float vals[4 + 2 * 2];                            // up to pad 2 halo
-                const int span = 4 + p.kw - 1;
+                constexpr int span = 4 + KW - 1;                 // 4 px + halo
+                float vh[span], vl[span];
+                if (iy < 0 || iy >= p.h) {
 #pragma unroll
-                for (int e = 0; e < 8; ++e)
-                    if (e < span) vals[e] = act_value(p, nn, c, iy, ox0 + e - p.pad);
-                for (int v = 0; v < p.kw; ++v) {
-                    const int r = (c * p.kh + u) * p.kw + v - row0;  // local row
+                    for (int e = 0; e < span; ++e) vh[e] = vl[e] = 0.f;
+                } else if (use_lut) {
+                    // codes of the 4 core pixels in one aligned load, halo codes apart
+                    const int64_t rowi = (((int64_t)nn * p.ci + c) * p.h + iy) * p.w;
+                    const int64_t i0 = rowi + ox0;               // multiple of 4
+                    const int bits = p.tape.bits;
+                    uint32_t w4;
+                    if (bits == 4) w4 = *reinterpret_cast<const uint16_t *>(p.tape.codes + (i0 >> 1));
+                    else if (bits == 2) w4 = p.tape.codes[i0 >> 2];
+                    else w4 = (uint32_t)(p.tape.codes[i0 >> 3] >> (i0 & 7));
+                    const float *lh = s_lut + (c - c_begin) * (2 << bits);
+                    const uint32_t cm = (1u << bits) - 1u;
+#pragma unroll
+                    for (int e = 0; e < span; ++e) {
+                        const int x = ox0 + e - p.pad;
+                        uint32_t code;
+                        bool inb = x >= 0 && x < p.w;
+                        if (e >= p.pad && e < p.pad + 4) code = (w4 >> ((e - p.pad) * bits)) & cm;
+                        else code = inb ? get_code(p.tape.codes, rowi + x, bits) : 0u;
+                        vh[e] = inb ? lh[2 * code] : 0.f;
+                        vl[e] = inb ? lh[2 * code + 1] : 0.f;
+                    }
+                } else {
+#pragma unroll
+                    for (int e = 0; e < span; ++e)
+                        split_tf32(act_value(p, nn, c, iy, ox0 + e - p.pad), vh[e], vl[e]);
+                }
+#pragma unroll
+                for (int v = 0; v < KW; ++v) {
+                    const int r = (c * p.kh + u) * KW + v - row0;  // local row
                     if (r < 0 || r >= nrows) continue;
-                    float4 hi, lo;
-                    split_tf32(vals[v + 0], hi.x, lo.x);
-                    split_tf32(vals[v + 1], hi.y, lo.y);
-                    split_tf32(vals[v + 2], hi.z, lo.z);
-                    split_tf32(vals[v + 3], hi.w, lo.w);
                     const int tt = r >> 7, rr = r & 127;
                     const uint32_t off = swz_off<128>((uint32_t)(rr >> 3) * 1024 +
                                                       (uint32_t)(rr & 7) * 128 + (uint32_t)q * 16);
-                    *reinterpret_cast<float4 *>(sAh(s, tt) + off) = hi;
-                    *reinterpret_cast<float4 *>(sAl(s, tt) + off) = lo;
+                    *reinterpret_cast<float4 *>(sAh(s, tt) + off) =
+                        make_float4(vh[v], vh[v + 1], vh[v + 2], vh[v + 3]);
+                    *reinterpret_cast<float4 *>(sAl(s, tt) + off) =
+                        make_float4(vl[v], vl[v + 1], vl[v + 2], vl[v + 3]);
                 }
             }
             (void)kk;
@@ -251,29 +293,29 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 // grad_w[i] = fp32(grad_w[i] + fp32(sum_z partial[z][i])) -- the 8 warps of
 // a block sum interleaved split subsets for 32 consecutive outputs, then
 // combine in warp order: fixed order, deterministic (layer.py:167).
-__global__ void __launch_bounds__(256) wgrad_reduce_kernel(const float *partial, int64_t splits,
-                                                          int64_t count, float *grad_w) {
-    __shared__ double red[8][32];
+__global__ void __launch_bounds__(1024) wgrad_reduce_kernel(const float *partial, int64_t splits,
+                                                           int64_t count, float *grad_w) {
+    __shared__ double red[32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * 32 + lane;
     double s = 0.0;
     if (i < count) {
         int64_t z = warp;
-        for (; z + 24 < splits; z += 32) {
-            const float a = partial[z * count + i], b = partial[(z + 8) * count + i];
-            const float c = partial[(z + 16) * count + i], d = partial[(z + 24) * count + i];
+        for (; z + 96 < splits; z += 128) {
+            const float a = partial[z * count + i], b = partial[(z + 32) * count + i];
+            const float c = partial[(z + 64) * count + i], d = partial[(z + 96) * count + i];
             s += (double)a;
             s += (double)b;
             s += (double)c;
             s += (double)d;
         }
-        for (; z < splits; z += 8) s += (double)partial[z * count + i];
+        for (; z < splits; z += 32) s += (double)partial[z * count + i];
     }
     red[warp][lane] = s;
     __syncthreads();
     if (warp == 0 && i < count) {
         double t = 0.0;
-        for (int w = 0; w < 8; ++w) t += red[w][lane];
+        for (int w = 0; w < 32; ++w) t += red[w][lane];
         grad_w[i] = __fadd_rn(grad_w[i], __double2float_rn(t));
     }
 }
@@ -304,13 +346,14 @@ static WgPlan wg_plan(const ConvGeo &g) {
     const int64_t ow = g.ow, oh = g.oh;
     if (ow != 8 && ow != 16 && ow != 32) return pl;
     if ((oh * ow) % 32 || oh % (32 / ow)) return pl;
-    if (g.co % 16 || g.co > 256 || g.kw > 5 || g.pad > 2) return pl;
+    if (g.co % 16 || g.co > 256 || !(g.kw == 1 || g.kw == 3) || g.pad > 1) return pl;
+    if (g.kw == 1 && g.pad != 0) return pl;
     if (g.n * oh * ow / 32 > INT32_MAX) return pl;
     pl.bn = g.co <= 16 ? 16 : g.co <= 32 ? 32 : g.co <= 64 ? 64 : g.co <= 128 ? 128 : 256;
     if (g.co % pl.bn) return pl;
     const int64_t R = g.ci * g.kh * g.kw;
     const int64_t mt = (R + 127) / 128;
-    int mtg = (int)std::min<int64_t>(mt, pl.bn >= 256 ? 2 : 4);
+    int mtg = (int)std::min<int64_t>(mt, pl.bn >= 256 ? 2 : 3);
     while (mtg > 1 && mtg * pl.bn > 512) --mtg;
     // smem: stages x (g hi/lo + mtg x (a hi/lo) x 16 KiB)
     int stage = 2 * pl.bn * 128 + 2 * mtg * 128 * 128;
@@ -320,22 +363,29 @@ static WgPlan wg_plan(const ConvGeo &g) {
     }
     pl.mtg = mtg;
     pl.mgroups = (int)((mt + mtg - 1) / mtg);
-    pl.stages = std::max(1, std::min(4, (200 * 1024) / stage));
-    pl.smem = pl.stages * stage + 1024 + 256;
+    pl.stages = std::max(1, std::min(4, (190 * 1024) / stage));
+    pl.smem = pl.stages * stage + 1024 + 1024 + kWgLutEntries * 8;
     uint32_t cols = 32;
     while (cols < (uint32_t)(mtg * pl.bn)) cols <<= 1;
     pl.cols = cols;
     pl.total = (int)(g.n * oh * ow / 32);
-    const int want = std::max(1, (2 * 148) / pl.mgroups);
+    // split-K count: enough CTAs to cover the SMs twice, but the fp32
+    // partials (splits x R x co x 4 B) must stay well below the operand
+    // bytes the split reads (g: 128*co B and codes per 32-pixel chunk).
+    int want = std::max(1, (2 * 148) / pl.mgroups);
+    const double chunk_bytes = 128.0 * g.co + 32.0 * g.ci * 1.0;
+    const double part_bytes = 4.0 * R * g.co;
+    const int cap = std::max(48, (int)(4.0 * pl.total * chunk_bytes / part_bytes));
+    want = std::min(want, cap);
     pl.cps = std::max(1, (pl.total + want - 1) / want);
     pl.splits = (pl.total + pl.cps - 1) / pl.cps;
     pl.ok = true;
     return pl;
 }
 
-template <int BN>
+template <int BN, int KW>
 static int launch_wg(const CUtensorMap &m, const WgParams &p, const WgPlan &pl, cudaStream_t st) {
-    auto kern = conv_wgrad_tc_kernel<BN>;
+    auto kern = conv_wgrad_tc_kernel<BN, KW>;
     static int attr = 0;
     if (attr < pl.smem) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
@@ -363,8 +413,8 @@ int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g) {
 
 int qt_tc_wgrad_reduce(const float *partial, int64_t splits, int64_t count, float *grad_w,
                        cudaStream_t st) {
-    wgrad_reduce_kernel<<<(unsigned)qt_cdiv(count, 32), 256, 0, st>>>(partial, splits, count,
-                                                                     grad_w);
+    wgrad_reduce_kernel<<<(unsigned)qt_cdiv(count, 32), 1024, 0, st>>>(partial, splits, count,
+                                                                      grad_w);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -405,15 +455,29 @@ int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float
     p.splits = pl.splits;
     p.stages = pl.stages;
     p.tmem_cols = pl.cols;
-    int rc;
-    switch (pl.bn) {
-        case 16: rc = launch_wg<16>(m, p, pl, st); break;
-        case 32: rc = launch_wg<32>(m, p, pl, st); break;
-        case 64: rc = launch_wg<64>(m, p, pl, st); break;
-        case 128: rc = launch_wg<128>(m, p, pl, st); break;
-        case 256: rc = launch_wg<256>(m, p, pl, st); break;
-        default: return QT_EUNSUPPORTED;
+    {
+        // smem code table when every CTA's channel range fits (K <= 4)
+        const int kk = (int)(g.kh * g.kw);
+        const int max_ch = (pl.mtg * 128 + kk - 1) / kk + (kk > 1 ? 1 : 0);
+        p.lut_ch = (!x_plain && !act.a2 && act.bits <= 4 && max_ch * (1 << act.bits) <= kWgLutEntries)
+                       ? max_ch : 0;
     }
+    int rc;
+#define QT_WG_CASES(KW)                                          \
+    switch (pl.bn) {                                             \
+        case 16: rc = launch_wg<16, KW>(m, p, pl, st); break;    \
+        case 32: rc = launch_wg<32, KW>(m, p, pl, st); break;    \
+        case 64: rc = launch_wg<64, KW>(m, p, pl, st); break;    \
+        case 128: rc = launch_wg<128, KW>(m, p, pl, st); break;  \
+        case 256: rc = launch_wg<256, KW>(m, p, pl, st); break;  \
+        default: return QT_EUNSUPPORTED;                         \
+    }
+    if (g.kw == 1) {
+        QT_WG_CASES(1)
+    } else {
+        QT_WG_CASES(3)
+    }
+#undef QT_WG_CASES
     if (rc) return rc;
     return qt_tc_wgrad_reduce((const float *)ws, pl.splits, g.co * p.R, grad_w, st);
 }

@@ -156,6 +156,7 @@ class TapeSlot:
         self.var = torch.empty(c, dtype=torch.float64, device=device)
         self.gamma = torch.empty(c, dtype=torch.float32, device=device)
         self.beta = torch.empty(c, dtype=torch.float32, device=device)
+        self.consts = torch.empty(c * 48, dtype=torch.uint8, device=device)  # BnConst[C]
         if exact:
             self.a2 = a2 if a2 is not None else torch.empty(shape, dtype=torch.float32,
                                                              device=device)
@@ -167,6 +168,9 @@ class TapeSlot:
             self.a2 = None
             self.codes = codes if codes is not None else torch.empty(
                 packed_nbytes(numel, bits), dtype=torch.uint8, device=device)
+        if exact:
+            self.step = self.offset = self.clip = None
+        else:
             self.step = torch.empty(c, dtype=torch.float64, device=device)
             self.offset = torch.empty(c, dtype=torch.int64, device=device)
             self.clip = torch.zeros(1, dtype=torch.int64, device=device)
@@ -242,34 +246,37 @@ def layer_forward(a_in: torch.Tensor, p: LayerParams, mode: str = "exact",
         raise StateError("work may not alias a_in")
 
     quantized = training and mode != "exact" and bits is not None
-    if training:
-        if slot is None:
-            slot = TapeSlot(a_in.shape, c, bits, not quantized, dev)
-        mean, var = ops.channel_moments(a_in, running=(p.running_mean, p.running_var),
-                                        out=(slot.mean, slot.var),
-                                        ws=None if ws is None else ws.stats)
-    else:
-        mean, var = p.running_mean, p.running_var
-
-    a2_tape = codes = step = offset = clip = None
+    a2_tape = codes = step = offset = clip = consts = None
     kbits = 0
     nmode = 0
     if training:
+        if slot is None:
+            slot = TapeSlot(a_in.shape, c, bits, not quantized, dev)
         if quantized:
             codes, step, offset, clip = slot.codes, slot.step, slot.offset, slot.clip
-            clip.zero_()
             kbits = bits
             nmode = _NATIVE_MODE[mode]
         else:
             a2_tape = slot.a2
+        # one launch: moments + running stats + K1 constants + frozen gamma/beta
+        # + tape step/offset + clip-counter reset (layer.py:236-255)
+        mean, var, consts = slot.mean, slot.var, slot.consts
+        if ws is not None:
+            sws = ws.stats
+        else:
+            sws = ops.workspace(N.query("qt_bn_stats_workspace", n, c, hw), dev, "stats")
+        N.call("qt_bn_stats_prep", N.ptr(a_in), n, c, hw, float(p.bn_epsilon), N.ptr(p.gamma),
+               N.ptr(p.beta), kbits, N.ptr(mean), N.ptr(var), N.ptr(p.running_mean),
+               N.ptr(p.running_var), N.ptr(slot.gamma), N.ptr(slot.beta), N.ptr(step),
+               N.ptr(offset), N.ptr(clip), N.ptr(consts), N.ptr(sws))
+    else:
+        mean, var = p.running_mean, p.running_var
     N.call("qt_bn_relu_forward", N.ptr(a_in), n, c, hw, N.ptr(mean), N.ptr(var),
            float(p.bn_epsilon), N.ptr(p.gamma), N.ptr(p.beta), nmode, kbits, N.ptr(work),
-           N.ptr(a2_tape), N.ptr(codes), N.ptr(step), N.ptr(offset), N.ptr(clip))
+           N.ptr(a2_tape), N.ptr(codes), N.ptr(step), N.ptr(offset), N.ptr(clip), N.ptr(consts))
 
     tape = None
     if training:
-        N.call("qt_copy", N.ptr(p.gamma), N.ptr(slot.gamma), c)
-        N.call("qt_copy", N.ptr(p.beta), N.ptr(slot.beta), c)
         if quantized:
             stored = QuantizedTape(codes=codes, bits=bits, shape=tuple(a_in.shape),
                                    dtype=torch.float32, step=step, offset=offset, sigma2=var,

@@ -64,7 +64,7 @@ def test_bn_relu_forward_bit_exact_given_moments():
                    N.ptr(keep[2]), 1e-5, N.ptr(keep[3]), N.ptr(keep[4]), nm, kb, N.ptr(a3),
                    N.ptr(a2 if mode == "exact" else None), N.ptr(codes if kb else None),
                    N.ptr(step if kb else None), N.ptr(off if kb else None),
-                   N.ptr(clip if kb else None))
+                   N.ptr(clip if kb else None), None)
             if mode == "exact":
                 assert np.array_equal(host(a2), tape["a2"])
                 assert np.array_equal(host(a3), np.maximum(a2w, np.float32(0)))
