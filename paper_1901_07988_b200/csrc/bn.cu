@@ -22,9 +22,13 @@ struct Part {
     int64_t blocks;            // blocks per channel
 };
 
-static Part partition(int64_t n, int64_t hw) {
+static Part partition(int64_t n, int64_t c, int64_t hw) {
+    // ~4 blocks per SM overall, at least kTargetPerBlock/2 elements per block
     Part p;
-    p.planes_per_block = std::max<int64_t>(1, kTargetPerBlock / hw);
+    const int64_t want_nb = std::max<int64_t>(1, (4 * 148 + c - 1) / c);
+    p.planes_per_block = std::max<int64_t>(1, qt_cdiv(n, want_nb));
+    p.planes_per_block = std::max<int64_t>(p.planes_per_block,
+                                           std::max<int64_t>(1, kTargetPerBlock / 2 / hw));
     if (p.planes_per_block > n) p.planes_per_block = n;
     p.blocks = qt_cdiv(n, p.planes_per_block);
     return p;
@@ -281,7 +285,7 @@ static unsigned grid_for(int64_t n, int threads) {
 using namespace qt;
 
 extern "C" int64_t qt_bn_stats_workspace(int64_t n, int64_t c, int64_t hw) {
-    Part p = partition(n, hw);
+    Part p = partition(n, c, hw);
     return kCounterBytes + c * p.blocks * 2 * (int64_t)sizeof(double);
 }
 
@@ -290,7 +294,7 @@ extern "C" int qt_bn_stats(const float *x, int64_t n, int64_t c, int64_t hw, dou
                            qt_stream_t stream) {
     QT_REQUIRE(x && mean && var && ws && n > 0 && c > 0 && hw > 0 && c <= kMaxChannels);
     QT_REQUIRE((running_mean == nullptr) == (running_var == nullptr));
-    Part p = partition(n, hw);
+    Part p = partition(n, c, hw);
     StatsArgs a{x, n, c, hw, p.planes_per_block, p.blocks, mean, var, running_mean, running_var,
                 (double *)((char *)ws + kCounterBytes), (unsigned *)ws,
                 nullptr, nullptr, 0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
@@ -309,7 +313,7 @@ extern "C" int qt_bn_stats_prep(const float *x, int64_t n, int64_t c, int64_t hw
     QT_REQUIRE(n > 0 && c > 0 && hw > 0 && c <= kMaxChannels);
     QT_REQUIRE(bits == 0 || (qt_bits_ok(bits) && step && offset));
     QT_REQUIRE((running_mean == nullptr) == (running_var == nullptr));
-    Part p = partition(n, hw);
+    Part p = partition(n, c, hw);
     StatsArgs a{x, n, c, hw, p.planes_per_block, p.blocks, mean, var, running_mean, running_var,
                 (double *)((char *)ws + kCounterBytes), (unsigned *)ws,
                 gamma, beta, bits, eps, (BnConst *)consts, gamma_copy, beta_copy, step, offset,
@@ -323,7 +327,7 @@ extern "C" int qt_bn_stats_prep(const float *x, int64_t n, int64_t c, int64_t hw
 extern "C" int qt_channel_sum(const float *x, int64_t n, int64_t c, int64_t hw, double *out,
                               void *ws, qt_stream_t stream) {
     QT_REQUIRE(x && out && ws && n > 0 && c > 0 && hw > 0 && c <= kMaxChannels);
-    Part p = partition(n, hw);
+    Part p = partition(n, c, hw);
     StatsArgs a{x, n, c, hw, p.planes_per_block, p.blocks, out, nullptr, nullptr, nullptr,
                 (double *)((char *)ws + kCounterBytes), (unsigned *)ws,
                 nullptr, nullptr, 0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};

@@ -28,9 +28,14 @@ struct BwdPart {
     int64_t ppb, nb;
 };
 
-static BwdPart bwd_partition(int64_t n, int64_t hw) {
+// ~4 blocks per SM in total, each reducing a contiguous run of planes of one
+// channel (enough work per thread that the block's deterministic
+// last-block-finalize tail is amortised)
+static BwdPart bwd_partition(int64_t n, int64_t c, int64_t hw) {
     BwdPart p;
-    p.ppb = std::max<int64_t>(1, 4096 / hw);
+    const int64_t want_nb = std::max<int64_t>(1, (4 * 148 + c - 1) / c);
+    p.ppb = std::max<int64_t>(1, qt_cdiv(n, want_nb));
+    p.ppb = std::max<int64_t>(p.ppb, std::max<int64_t>(1, 2048 / hw));
     if (p.ppb > n) p.ppb = n;
     p.nb = qt_cdiv(n, p.ppb);
     return p;
@@ -98,15 +103,17 @@ __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
     if ((a.hw & 7) == 0) {
         const int64_t groups = (p1 - p0) * (a.hw >> 3);
         const int64_t gpp = a.hw >> 3;
+#pragma unroll 2
         for (int64_t gi = threadIdx.x; gi < groups; gi += kBT) {
             const int64_t pl = gi / gpp, off = (gi - pl * gpp) << 3;
             const int64_t i0 = ((p0 + pl) * a.c + ch) * a.hw + off;
             const float4 ga = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0));
             const float4 gb = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0) + 1);
+            const uint64_t word0 = CODES ? load_code_word(a.tape.codes, i0, a.tape.bits) : 0;
             const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
             float mv[8], av[8];
             if (CODES) {
-                const uint64_t word = load_code_word(a.tape.codes, i0, a.tape.bits);
+                const uint64_t word = word0;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
                     const uint32_t code = (uint32_t)(word >> (j * a.tape.bits)) & cmask;
@@ -306,7 +313,7 @@ __global__ void __launch_bounds__(kBT) bn_bwd_apply_kernel(ApplyArgs a) {
 using namespace qt;
 
 extern "C" int64_t qt_bn_backward_workspace(int64_t n, int64_t c, int64_t hw) {
-    BwdPart p = bwd_partition(n, hw);
+    BwdPart p = bwd_partition(n, c, hw);
     return kBwdCounterBytes + c * 2 * kMaxLut * (int64_t)sizeof(float) +
            c * p.nb * 4 * (int64_t)sizeof(double);
 }
@@ -319,7 +326,7 @@ extern "C" int qt_bn_backward_reduce(const float *g3, qt_tape_t tape, int64_t n,
     QT_REQUIRE(g3 && gamma_tape && beta_tape && sigma2 && stats && ws);
     QT_REQUIRE(n > 0 && c > 0 && hw > 0 && c <= 65535);
     QT_REQUIRE(tape.a2 || (tape.codes && tape.step && tape.offset && qt_bits_ok(tape.bits)));
-    BwdPart p = bwd_partition(n, hw);
+    BwdPart p = bwd_partition(n, c, hw);
     const bool codes = tape.a2 == nullptr;
     if (!codes) tape.bits = 1;
     BwdArgs a{g3, tape, n, c, hw, gamma_tape, beta_tape, sigma2, eps, variance_a1, grad_gamma,

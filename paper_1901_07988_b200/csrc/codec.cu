@@ -11,6 +11,8 @@
 // one K-byte store for the codes, so a warp writes 32*K contiguous code
 // bytes.  Per-(n,c)-plane constants (mean/inv/gamma/beta/scale/offset) are
 // computed once per block into shared memory.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace qt {
@@ -308,8 +310,118 @@ __global__ void unpack_kernel(const uint8_t *packed, int64_t count, int bits, ui
     codes[i] = (uint8_t)get_code(packed, i, bits);
 }
 
+// Streaming K1 for the training path (per-channel constants precomputed by
+// qt_bn_stats_prep, hw % 8 == 0): grid-stride over 8-element groups, two
+// groups per iteration with all four 128-bit loads issued before any math,
+// constants through the read-only cache -- no block prologue, no smem.
+template <int BITS, int MODE, bool A2, bool CLIP>
+__global__ void __launch_bounds__(kThreads) bn_relu_quant_stream(FwdArgs a) {
+    const int64_t ngroups = a.numel >> 3;
+    const int64_t hw8 = a.hw >> 3;
+    const int64_t stride = (int64_t)gridDim.x * kThreads;
+    unsigned long long clip = 0;
+    for (int64_t g0 = (int64_t)blockIdx.x * kThreads + threadIdx.x; g0 < ngroups; g0 += 2 * stride) {
+        const int64_t gs[2] = {g0, g0 + stride};
+        float4 xa[2], xb[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (gs[u] < ngroups) {
+                const float4 *src = reinterpret_cast<const float4 *>(a.x) + 2 * gs[u];
+                xa[u] = __ldg(src);
+                xb[u] = __ldg(src + 1);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t gg = gs[u];
+            if (gg >= ngroups) break;
+            const int64_t ch = (gg / hw8) % a.c;
+            const BnConst k = a.consts[ch];
+            const float xv[8] = {xa[u].x, xa[u].y, xa[u].z, xa[u].w, xb[u].x, xb[u].y, xb[u].z, xb[u].w};
+            float a2v[8], a3v[8];
+            uint64_t word = 0;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                float v = __fsub_rn(xv[j], k.m32);       // layer.py:246-249
+                v = __fmul_rn(v, k.inv32);
+                v = __fmul_rn(v, k.g);
+                v = __fadd_rn(v, k.b);
+                a2v[j] = v;
+                float pre = v;
+                if (BITS) {
+                    const int64_t raw = raw_code(v, k.scale, k.off, BITS);
+                    constexpr int64_t top = (1ll << BITS) - 1;
+                    if (CLIP) clip += (raw < 0 || raw > top);
+                    const uint32_t code = (uint32_t)(raw < 0 ? 0 : (raw > top ? top : raw));
+                    word |= (uint64_t)code << (j * BITS);
+                    if (MODE == MODE_NAIVE) pre = decode(code, k.step, k.off, BITS);
+                }
+                a3v[j] = relu_np(pre);
+            }
+            float4 *d3 = reinterpret_cast<float4 *>(a.a3_out) + 2 * gg;
+            d3[0] = make_float4(a3v[0], a3v[1], a3v[2], a3v[3]);
+            d3[1] = make_float4(a3v[4], a3v[5], a3v[6], a3v[7]);
+            if (A2) {
+                float4 *d2 = reinterpret_cast<float4 *>(a.a2_tape) + 2 * gg;
+                d2[0] = make_float4(a2v[0], a2v[1], a2v[2], a2v[3]);
+                d2[1] = make_float4(a2v[4], a2v[5], a2v[6], a2v[7]);
+            }
+            if (BITS) {
+                uint8_t *dst = a.codes + gg * BITS;
+                if (BITS == 8) *reinterpret_cast<uint2 *>(dst) = make_uint2((uint32_t)word, (uint32_t)(word >> 32));
+                else if (BITS == 4) *reinterpret_cast<uint32_t *>(dst) = (uint32_t)word;
+                else if (BITS == 2) *reinterpret_cast<uint16_t *>(dst) = (uint16_t)word;
+                else *dst = (uint8_t)word;
+            }
+        }
+    }
+    if (CLIP) {
+        __shared__ unsigned long long s_clip[kThreads / 32];
+        clip = warp_sum(clip);
+        if ((threadIdx.x & 31) == 0) s_clip[threadIdx.x >> 5] = clip;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            for (int w = 0; w < kThreads / 32; ++w) t += s_clip[w];
+            if (t) atomicAdd(a.clip_count, t);
+        }
+    }
+}
+
+template <int BITS>
+static void launch_stream(const FwdArgs &a, unsigned blocks, cudaStream_t s) {
+    const bool clip = a.clip_count != nullptr;
+    if (a.mode == MODE_NAIVE) {
+        if (clip) bn_relu_quant_stream<BITS, MODE_NAIVE, false, true><<<blocks, kThreads, 0, s>>>(a);
+        else bn_relu_quant_stream<BITS, MODE_NAIVE, false, false><<<blocks, kThreads, 0, s>>>(a);
+    } else {
+        if (clip) bn_relu_quant_stream<BITS, MODE_APPROX, false, true><<<blocks, kThreads, 0, s>>>(a);
+        else bn_relu_quant_stream<BITS, MODE_APPROX, false, false><<<blocks, kThreads, 0, s>>>(a);
+    }
+}
+
 static int launch_fwd(const FwdArgs &a, bool apply_bn, cudaStream_t s) {
     if (a.numel == 0) return QT_OK;
+    const bool aligned = ((((uintptr_t)a.x) | ((uintptr_t)a.a3_out) | ((uintptr_t)a.a2_tape)) & 15) == 0;
+    if (apply_bn && a.consts && a.a3_out && (a.hw & 7) == 0 && aligned &&
+        (a.bits == 0 || a.codes)) {
+        const int64_t ngroups = a.numel >> 3;
+        int64_t blocks = std::min<int64_t>(qt_cdiv(ngroups, 2 * kThreads), 148 * 8);
+        blocks = std::max<int64_t>(blocks, 1);
+        const unsigned b = (unsigned)blocks;
+        switch (a.bits) {
+            case 0:
+                if (a.a2_tape) bn_relu_quant_stream<0, MODE_EXACT, true, false><<<b, kThreads, 0, s>>>(a);
+                else bn_relu_quant_stream<0, MODE_EXACT, false, false><<<b, kThreads, 0, s>>>(a);
+                break;
+            case 1: launch_stream<1>(a, b, s); break;
+            case 2: launch_stream<2>(a, b, s); break;
+            case 4: launch_stream<4>(a, b, s); break;
+            case 8: launch_stream<8>(a, b, s); break;
+        }
+        QT_CHECK_LAUNCH();
+        return QT_OK;
+    }
     int64_t blocks = qt_cdiv(a.numel, kBlockElems);
     if (blocks > 0x7fffffff) return QT_EUNSUPPORTED;
     if (apply_bn)

@@ -34,249 +34,304 @@ namespace qt {
 
 using namespace tc;
 
-constexpr int kTcThreads = 192;
 
 template <int BN, int OWT, int KC, int KW>
 struct FwdCfg {
     static constexpr int BM = 128;
-    static constexpr int A_BYTES = BM * KC * 4;                     // one tap's K-chunk
-    static constexpr int B_BYTES = BN * KC * 4;
-    static constexpr int B_SLOT = (B_BYTES + 1023) / 1024 * 1024;   // keep every tile 1 KiB aligned
-    // raw activation box (TMA, MN-major) + KW taps x (hi, lo) K-major + KW x weights (hi, lo)
-    static constexpr int STAGE_BYTES = A_BYTES * (1 + 2 * KW) + 2 * KW * B_SLOT;
-    static constexpr int S0 = (200 * 1024) / STAGE_BYTES;
-    static constexpr int S_MAX = S0 > 4 ? 4 : (S0 < 1 ? 1 : S0);
-    static constexpr int OUT_BYTES = BM * BN * 4;                   // output staging tile
-    static int smem_bytes(int stages) { return stages * STAGE_BYTES + OUT_BYTES + 1024 + 256; }
-    static constexpr uint32_t TMEM_COLS = BN <= 32 ? 32 : (BN <= 64 ? 64 : (BN <= 128 ? 128 : 256));
+    static constexpr int NM = KW * BN;                               // MMA N: (column tap, channel)
+    static constexpr int A_BYTES = BM * KC * 4;                      // raw activation box
+    static constexpr int B_BYTES = NM * KC * 4;                      // weights, one of (hi, lo)
+    static constexpr int B_SLOT = (B_BYTES + 1023) / 1024 * 1024;    // keep every tile 1 KiB aligned
+    static constexpr int RAW_BYTES = A_BYTES + 2 * B_SLOT;           // raw ring slot
+    static constexpr int OUT_BYTES = BM * BN * 4;                    // output staging tile
+    static constexpr int ACC_COLS = 2 * NM;                          // double-buffered accumulator
+    static constexpr int OP_COLS = 2 * KC;                           // one A operand stage (hi, lo)
+    static constexpr int OP = (512 - ACC_COLS) / OP_COLS >= 2 ? 2 : 1;
+    static_assert(NM <= 256 && NM % 16 == 0, "UMMA N");
+    static_assert(ACC_COLS + OP_COLS <= 512, "TMEM budget");
     static constexpr int A_SW = OWT * 4;     // swizzle bytes of the raw activation box
-    static constexpr int K_SW = KC * 4;      // swizzle bytes of the K-major operand tiles
+    static constexpr int K_SW = KC * 4;      // swizzle bytes of the weight tiles
 };
 
 struct FwdGeo {
     int n, ci, h, w, co, kh, kw, pad, oh, ow;
     int rows, nimg, tiles_per_img;  // tile = nimg images x rows x OW pixels
-    int stages;                     // smem ring depth (<= the K loop length)
+    int mtiles, ntiles;             // output tiles along pixels / channels
+    int R, NOUT;                    // raw ring and output staging depths
 };
 
 struct EpiParams {
     float *out;
     const float *res;
     int cr, sr;
-    int res_tma;   // 1: residual tile TMA-loaded into the output staging buffer
+    int res_tma;   // 1: shortcut tile TMA-loaded into the output staging buffer
 };
 
-// One CTA = one 128-pixel x BN-channel output tile.  K loop: for each kernel
-// row u and channel chunk: ONE TMA box of KC channels x (rows of the tile
-// shifted by u) whole image rows; the KW column taps v are produced from it
-// by the transform warps (TMA cannot start a tile at an unaligned innermost
-// coordinate, so the +-1 column shift and its zero padding happen in smem).
+constexpr int kFwdThreads = 320;   // w0 TMA, w1 TMEM+MMA, w2-5 split, w6-9 epilogue
+
+// Persistent implicit-GEMM conv: each CTA walks output tiles (128 pixels x BN
+// channels) with a grid-stride loop.
+//
+// Column taps as MMA columns: for kernel row u and a channel chunk the A
+// operand is the UNSHIFTED input box (whole image rows shifted by u -- TMA
+// handles the row offset and the zero rows); the B operand stacks the KW
+// column taps, D[p][(v, co)] = sum_ci x[p][ci] W[co][ci][u][v], and the
+// epilogue forms out[x] = D_0[x-1] + D_1[x] + D_2[x+1] with warp shuffles
+// (a warp holds whole image rows, so neighbours are lanes +-1 and the zero
+// padding is a lane mask).  This keeps N = KW*BN large and the MMA count per
+// tile small (each tcgen05.mma costs ~46 cycles whatever N <= 64).
+//   raw ring (TMA -> split / MMA): activation box + (hi, lo) weight tiles;
+//            freed by the MMA commit.
+//   A in TMEM (split -> MMA): each split thread owns one pixel = one TMEM lane
+//            and writes its TF32 (hi, lo) halves with tcgen05.st.
+//   TMEM acc x2 (MMA -> epilogue): tile j's epilogue (TMEM -> regs -> taps ->
+//            + shortcut (TMA-prefetched) -> smem -> TMA store) overlaps tile
+//            j+1's main loop.
+// Precision: 3xTF32 (hi*hi + hi*lo + lo*hi).
 template <int BN, int OWT, int KC, int KW>
-__global__ void __launch_bounds__(kTcThreads, 2)
+__global__ void __launch_bounds__(kFwdThreads, 1)
     conv_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmBh,
                        const __grid_constant__ CUtensorMap tmBl,
                        const __grid_constant__ CUtensorMap tmOut,
                        const __grid_constant__ CUtensorMap tmRes, FwdGeo g, EpiParams ep) {
     using C = FwdCfg<BN, OWT, KC, KW>;
-    const int S = g.stages;
+    constexpr int OP = C::OP;
+    const int R = g.R, NOUT = g.NOUT;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    // output staging tile [nimg][BN][rows][OWT] fp32 (TMA-store box layout)
-    float *s_out = (float *)(smem + S * C::STAGE_BYTES);
-    uint64_t *full = (uint64_t *)(smem + S * C::STAGE_BYTES + C::OUT_BYTES);
-    uint64_t *ready = full + S;
-    uint64_t *empty = ready + S;
-    uint64_t *done = empty + S;
-    uint64_t *resbar = done + 1;
-    uint32_t *tmem_slot = (uint32_t *)(resbar + 1);
+    uint8_t *raw_base = smem;
+    float *out_base = (float *)(raw_base + R * C::RAW_BYTES);
+    uint64_t *bars = (uint64_t *)((uint8_t *)out_base + NOUT * C::OUT_BYTES);
+    uint64_t *raw_full = bars, *raw_empty = bars + R;
+    uint64_t *op_full = bars + 2 * R, *op_empty = op_full + OP;
+    uint64_t *acc_full = op_empty + OP, *acc_empty = acc_full + 2;
+    uint64_t *res_full = acc_empty + 2;
+    uint32_t *tmem_slot = (uint32_t *)(res_full + 2);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int tile = blockIdx.x;
-    const int co0 = blockIdx.y * BN;
-    const int n0 = (g.nimg > 1) ? tile * g.nimg : tile / g.tiles_per_img;
-    const int h0 = (g.nimg > 1) ? 0 : (tile % g.tiles_per_img) * g.rows;
     const int kchunks = g.ci / KC;
-    const int nstages = g.kh * kchunks;     // (u, channel chunk) pairs
+    const int nst = g.kh * kchunks;             // (u, channel chunk) stages per tile
+    const int total = g.mtiles * g.ntiles;
 
     if (threadIdx.x == 0) {
-        for (int s = 0; s < S; ++s) {
-            mbar_init(&full[s], 1);
-            mbar_init(&ready[s], 128);
-            mbar_init(&empty[s], 1);
+        for (int s = 0; s < R; ++s) { mbar_init(&raw_full[s], 1); mbar_init(&raw_empty[s], 1); }
+        for (int s = 0; s < OP; ++s) { mbar_init(&op_full[s], 128); mbar_init(&op_empty[s], 1); }
+        for (int a = 0; a < 2; ++a) {
+            mbar_init(&acc_full[a], 1);
+            mbar_init(&acc_empty[a], 128);
+            mbar_init(&res_full[a], 1);
         }
-        mbar_init(done, 1);
-        mbar_init(resbar, 1);
         fence_barrier_init();
     }
-    if (warp == 1) tmem_alloc<C::TMEM_COLS>(tmem_slot);
+    if (warp == 1) tmem_alloc<512>(tmem_slot);
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
         tma_prefetch(&tmBh);
         tma_prefetch(&tmBl);
         tma_prefetch(&tmOut);
+        if (ep.res_tma) tma_prefetch(&tmRes);
     }
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    auto sRaw = [&](int s) { return smem + s * C::STAGE_BYTES; };
-    auto sAh = [&](int s, int v) { return smem + s * C::STAGE_BYTES + (1 + v) * C::A_BYTES; };
-    auto sAl = [&](int s, int v) { return smem + s * C::STAGE_BYTES + (1 + KW + v) * C::A_BYTES; };
-    auto sBh = [&](int s, int v) {
-        return smem + s * C::STAGE_BYTES + (1 + 2 * KW) * C::A_BYTES + v * C::B_SLOT;
+    auto tile_coords = [&](int T, int &n0, int &h0, int &co0) {
+        const int mt = T / g.ntiles;
+        co0 = (T - mt * g.ntiles) * BN;
+        n0 = (g.nimg > 1) ? mt * g.nimg : mt / g.tiles_per_img;
+        h0 = (g.nimg > 1) ? 0 : (mt % g.tiles_per_img) * g.rows;
     };
-    auto sBl = [&](int s, int v) {
-        return smem + s * C::STAGE_BYTES + (1 + 2 * KW) * C::A_BYTES + (KW + v) * C::B_SLOT;
-    };
+    auto sRaw = [&](int s) { return raw_base + s * C::RAW_BYTES; };
+    auto sBh = [&](int s) { return raw_base + s * C::RAW_BYTES + C::A_BYTES; };
+    auto sBl = [&](int s) { return raw_base + s * C::RAW_BYTES + C::A_BYTES + C::B_SLOT; };
+    auto a_col = [&](int o) { return (uint32_t)(C::ACC_COLS + o * C::OP_COLS); };
 
     if (warp == 0) {
-        if (lane == 0) {  // ---------------------------------- TMA producer
-            if (ep.res_tma) {  // shortcut tile straight into the output staging buffer
-                mbar_expect_tx(resbar, C::OUT_BYTES);
-                tma_load_4d(s_out, &tmRes, resbar, 0, h0, co0, n0);
-            }
-            for (int i = 0; i < nstages; ++i) {
-                const int s = i % S;
-                const uint32_t ph = (uint32_t)(i / S) & 1u;
-                mbar_wait(&empty[s], ph ^ 1u);
-                const int u = i / kchunks, c0 = (i % kchunks) * KC;
-                mbar_expect_tx(&full[s], C::A_BYTES + 2 * KW * C::B_BYTES);
-                tma_load_4d(sRaw(s), &tmA, &full[s], 0, c0, h0 + u - g.pad, n0);
-#pragma unroll
-                for (int v = 0; v < KW; ++v) {
-                    const int kcol = (u * g.kw + v) * g.ci + c0;
-                    tma_load_2d(sBh(s, v), &tmBh, &full[s], kcol, co0);
-                    tma_load_2d(sBl(s, v), &tmBl, &full[s], kcol, co0);
+        if (lane == 0) {  // ---------------------------------------- TMA producer
+            int gi = 0;
+            for (int T = blockIdx.x; T < total; T += gridDim.x) {
+                int n0, h0, co0;
+                tile_coords(T, n0, h0, co0);
+                for (int i = 0; i < nst; ++i, ++gi) {
+                    const int s = gi % R;
+                    mbar_wait(&raw_empty[s], ((uint32_t)(gi / R) & 1u) ^ 1u);
+                    const int u = i / kchunks, c0 = (i % kchunks) * KC;
+                    mbar_expect_tx(&raw_full[s], C::A_BYTES + 2 * C::B_BYTES);
+                    tma_load_4d(sRaw(s), &tmA, &raw_full[s], 0, c0, h0 + u - g.pad, n0);
+                    tma_load_3d(sBh(s), &tmBh, &raw_full[s], c0, co0, u * KW);
+                    tma_load_3d(sBl(s), &tmBl, &raw_full[s], c0, co0, u * KW);
                 }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // ----------------------------------- MMA issuer
-            constexpr uint32_t idesc = instr_desc(128, BN, 2, 0, 0);   // both K-major
+        if (lane == 0) {  // ----------------------------------------- MMA issuer
+            constexpr uint32_t idesc = instr_desc(128, C::NM, 2, 0, 0);  // A (TMEM) x B (K-major)
             constexpr uint32_t k_sbo = 8 * KC * 4;        // stride between 8-row groups
             constexpr uint32_t lay = swizzle_layout(C::K_SW);
-            for (int i = 0; i < nstages; ++i) {
-                const int s = i % S;
-                const uint32_t ph = (uint32_t)(i / S) & 1u;
-                mbar_wait(&ready[s], ph);
+            int gi = 0, lt = 0;
+            for (int T = blockIdx.x; T < total; T += gridDim.x, ++lt) {
+                const int acc = lt & 1;
+                mbar_wait(&acc_empty[acc], ((uint32_t)(lt >> 1) & 1u) ^ 1u);
                 tc_fence_after();
-#pragma unroll
-                for (int v = 0; v < KW; ++v) {
-                    const uint32_t ah = smem_u32(sAh(s, v)), al = smem_u32(sAl(s, v));
-                    const uint32_t bh = smem_u32(sBh(s, v)), bl = smem_u32(sBl(s, v));
+                const uint32_t d = tmem + (uint32_t)(acc * C::NM);
+                for (int i = 0; i < nst; ++i, ++gi) {
+                    const int s = gi % R, o = gi % OP;
+                    mbar_wait(&op_full[o], (uint32_t)(gi / OP) & 1u);
+                    tc_fence_after();
+                    const uint32_t ah = tmem + a_col(o), al = ah + KC;
+                    const uint32_t bh = smem_u32(sBh(s)), bl = smem_u32(sBl(s));
 #pragma unroll
                     for (int j = 0; j < KC / 8; ++j) {
-                        const uint64_t dah = smem_desc(ah + j * 32, 16, k_sbo, lay);
-                        const uint64_t dal = smem_desc(al + j * 32, 16, k_sbo, lay);
                         const uint64_t dbh = smem_desc(bh + j * 32, 16, k_sbo, lay);
                         const uint64_t dbl = smem_desc(bl + j * 32, 16, k_sbo, lay);
-                        mma_tf32(tmem, dah, dbh, idesc, (i | v | j) ? 1u : 0u);
-                        mma_tf32(tmem, dah, dbl, idesc, 1u);
-                        mma_tf32(tmem, dal, dbh, idesc, 1u);
+                        mma_tf32_ts(d, ah + j * 8, dbh, idesc, (i | j) ? 1u : 0u);
+                        mma_tf32_ts(d, ah + j * 8, dbl, idesc, 1u);
+                        mma_tf32_ts(d, al + j * 8, dbh, idesc, 1u);
                     }
+                    mma_commit(&raw_empty[s]);
+                    mma_commit(&op_empty[o]);
                 }
-                mma_commit(&empty[s]);
+                mma_commit(&acc_full[acc]);
             }
-            mma_commit(done);
         }
-    } else {  // ---------------------------- warps 2..5: split, then epilogue
-        const int t = threadIdx.x - 64;  // 0..127 = tile row (output pixel)
-        const uint32_t atom = (uint32_t)(t / OWT);
-        const int px = t % OWT;
-        const int kw_pad = (KW > 1) ? g.pad : 0;
-        for (int i = 0; i < nstages; ++i) {
-            const int s = i % S;
-            const uint32_t ph = (uint32_t)(i / S) & 1u;
-            mbar_wait(&full[s], ph);
-            const uint8_t *raw = sRaw(s);
+    } else if (warp < 6) {  // ----------------------------- warps 2..5: split -> TMEM
+        const int quarter = warp & 3;
+        const int row = 32 * quarter + lane;          // this thread's TMEM lane = pixel
+        const uint32_t atom = (uint32_t)(row / OWT);
+        const uint32_t px = (uint32_t)(row % OWT);
+        const uint32_t lane_base = tmem + ((uint32_t)(32 * quarter) << 16);
+        int gi = 0;
+        for (int T = blockIdx.x; T < total; T += gridDim.x) {
+            for (int i = 0; i < nst; ++i, ++gi) {
+                const int s = gi % R, o = gi % OP;
+                mbar_wait(&raw_full[s], (uint32_t)(gi / R) & 1u);
+                mbar_wait(&op_empty[o], ((uint32_t)(gi / OP) & 1u) ^ 1u);
+                tc_fence_after();
+                const uint8_t *raw = sRaw(s);
 #pragma unroll
-            for (int v = 0; v < KW; ++v) {
-                // column tap v reads pixel px + v - pad of the same image row
-                const int sx = px + v - kw_pad;
-                const bool inb = sx >= 0 && sx < OWT;
-                uint8_t *ah = sAh(s, v), *al = sAl(s, v);
+                for (int cg = 0; cg < KC; cg += 16) {
+                    uint32_t hi[16], lo[16];
 #pragma unroll
-                for (int q = 0; q < KC / 4; ++q) {
-                    float xv[4];
-#pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint32_t c = 4 * q + j;
-                        const uint32_t off = (atom * KC + c) * (OWT * 4) + (uint32_t)sx * 4;
-                        xv[j] = inb ? *reinterpret_cast<const float *>(raw + swz_off<C::A_SW>(off))
-                                    : 0.f;
+                    for (int j = 0; j < 16; ++j) {
+                        const uint32_t off = (atom * KC + cg + j) * (OWT * 4) + px * 4;
+                        const float x = *reinterpret_cast<const float *>(raw + swz_off<C::A_SW>(off));
+                        float h, l;
+                        split_tf32(x, h, l);
+                        hi[j] = __float_as_uint(h);
+                        lo[j] = __float_as_uint(l);
                     }
-                    float4 hi, lo;
-                    split_tf32(xv[0], hi.x, lo.x);
-                    split_tf32(xv[1], hi.y, lo.y);
-                    split_tf32(xv[2], hi.z, lo.z);
-                    split_tf32(xv[3], hi.w, lo.w);
-                    const uint32_t koff = swz_off<C::K_SW>((uint32_t)(t / 8) * (8 * KC * 4) +
-                                                           (uint32_t)(t % 8) * (KC * 4) + q * 16);
-                    *reinterpret_cast<float4 *>(ah + koff) = hi;
-                    *reinterpret_cast<float4 *>(al + koff) = lo;
+                    tmem_st16(lane_base + a_col(o) + cg, hi);
+                    tmem_st16(lane_base + a_col(o) + KC + cg, lo);
                 }
+                tmem_wait_st();
+                tc_fence_before();
+                mbar_arrive(&op_full[o]);
             }
-            fence_async_smem();
-            mbar_arrive(&ready[s]);
         }
-        // epilogue: this warp owns TMEM lanes 32*(warp%4) .. +31 = tile rows
-        mbar_wait(done, 0);
-        tc_fence_after();
-        const int row = 32 * (warp & 3) + lane;
+    } else {  // ------------------------------------------ warps 6..9: epilogue
+        const int quarter = warp & 3;
+        const int row = 32 * quarter + lane;
         const int ratom = row / OWT, wcol = row % OWT;
         const int img = ratom / g.rows, rr = ratom % g.rows;
-        const int nn = n0 + img, y = h0 + rr;
-        const uint32_t tbase = tmem + ((uint32_t)(32 * (warp & 3)) << 16);
-        // staging index of (channel j, this pixel): [img][BN][rows][OWT]
-        float *so = s_out + ((size_t)img * BN * g.rows + rr) * OWT + wcol;
         const size_t cstride = (size_t)g.rows * OWT;
-        if (ep.res_tma) mbar_wait(resbar, 0);
+        const bool leader = (warp == 6 && lane == 0);
         const bool res_ldg = ep.res && !ep.res_tma;
+        const int kw_pad = (KW > 1) ? g.pad : 0;
+        if (leader && ep.res_tma && (int)blockIdx.x < total) {  // prefetch the first shortcut tile
+            int n0, h0, co0;
+            tile_coords(blockIdx.x, n0, h0, co0);
+            mbar_expect_tx(&res_full[0], C::OUT_BYTES);
+            tma_load_4d(out_base, &tmRes, &res_full[0], 0, h0, co0, n0);
+        }
+        int lt = 0;
+        for (int T = blockIdx.x; T < total; T += gridDim.x, ++lt) {
+            int n0, h0, co0;
+            tile_coords(T, n0, h0, co0);
+            const int acc = lt & 1, ob = (NOUT > 1) ? (lt & 1) : 0;
+            float *s_out = out_base + (size_t)ob * (C::OUT_BYTES / 4);
+            asm volatile("bar.sync 1, 128;" ::: "memory");   // staging buffer free (see below)
+            mbar_wait(&acc_full[acc], (uint32_t)(lt >> 1) & 1u);
+            tc_fence_after();
+            if (ep.res_tma) mbar_wait(&res_full[ob], (uint32_t)((NOUT > 1 ? lt >> 1 : lt)) & 1u);
+            const int nn = n0 + img, y = h0 + rr;
+            const uint32_t tbase = tmem + ((uint32_t)(32 * quarter) << 16) + (uint32_t)(acc * C::NM);
+            float *so = s_out + ((size_t)img * BN * g.rows + rr) * OWT + wcol;
+            const int64_t hr = (int64_t)g.oh * ep.sr, wr = (int64_t)g.ow * ep.sr;
 #pragma unroll 1
-        for (int cb = 0; cb < BN; cb += 16) {
-            float rv[16];
-            if (res_ldg) {  // strided shortcut (sr > 1): gather, all loads in flight
-                const int64_t hr = (int64_t)g.oh * ep.sr, wr = (int64_t)g.ow * ep.sr;
+            for (int cb = 0; cb < BN; cb += 16) {
+                float rv[16];
+                if (res_ldg) {  // strided shortcut (sr > 1): gather, 16 loads in flight
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const int co = co0 + cb + j;
+                        rv[j] = co < ep.cr ? __ldg(ep.res + (((int64_t)nn * ep.cr + co) * hr +
+                                                             (int64_t)y * ep.sr) * wr +
+                                                    (int64_t)wcol * ep.sr)
+                                           : 0.f;
+                    }
+                }
+                uint32_t r[KW][16];
+#pragma unroll
+                for (int v = 0; v < KW; ++v) tmem_ld16(tbase + v * BN + cb, r[v]);
+                tmem_wait_ld();
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
-                    const int co = co0 + cb + j;
-                    rv[j] = co < ep.cr ? __ldg(ep.res + (((int64_t)nn * ep.cr + co) * hr +
-                                                         (int64_t)y * ep.sr) * wr +
-                                                (int64_t)wcol * ep.sr)
-                                       : 0.f;
-                }
-            }
-            uint32_t r[16];
-            tmem_ld16(tbase + cb, r);
-            tmem_wait_ld();
+                    float v;
+                    if (KW == 1) {
+                        v = __uint_as_float(r[0][j]);
+                    } else {
+                        // out[x] = sum_v D_v[x + v - pad]  (zero outside the image row)
+                        v = 0.f;
 #pragma unroll
-            for (int j = 0; j < 16; ++j) {
-                float v = __uint_as_float(r[j]);
-                float *dst = so + (size_t)(cb + j) * cstride;
-                // out = fp32(conv); cur += shortcut(res)  (engine.py:262-269)
-                if (ep.res_tma) {
-                    if (co0 + cb + j < ep.cr) v = __fadd_rn(v, *dst);
-                } else if (res_ldg && co0 + cb + j < ep.cr) {
-                    v = __fadd_rn(v, rv[j]);
+                        for (int t = 0; t < KW; ++t) {
+                            const int dx = t - kw_pad;
+                            const float d = __uint_as_float(r[t][j]);
+                            const float nb = dx == 0 ? d
+                                             : __shfl_sync(0xffffffffu, d, (lane + dx) & 31);
+                            const int xs = wcol + dx;
+                            v = __fadd_rn(v, (xs >= 0 && xs < OWT) ? nb : 0.f);
+                        }
+                    }
+                    float *dst = so + (size_t)(cb + j) * cstride;
+                    // out = fp32(conv); cur += shortcut(res)  (engine.py:262-269)
+                    if (ep.res_tma) {
+                        if (co0 + cb + j < ep.cr) v = __fadd_rn(v, *dst);
+                    } else if (res_ldg && co0 + cb + j < ep.cr) {
+                        v = __fadd_rn(v, rv[j]);
+                    }
+                    *dst = v;
                 }
-                *dst = v;
+            }
+            tc_fence_before();
+            mbar_arrive(&acc_empty[acc]);            // TMEM buffer free for tile lt+2
+            fence_async_smem();
+            asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (leader) {
+                tma_store_4d(&tmOut, s_out, 0, h0, co0, n0);
+                bulk_commit();
+                // the next tile's staging buffer must have been read by its previous store;
+                // then prefetch the next shortcut tile into it
+                if (NOUT > 1) bulk_wait_read1(); else bulk_wait_read0();
+                const int Tn = T + gridDim.x;
+                if (ep.res_tma && Tn < total) {
+                    int n1, h1, c1;
+                    tile_coords(Tn, n1, h1, c1);
+                    const int ob1 = (NOUT > 1) ? ((lt + 1) & 1) : 0;
+                    mbar_expect_tx(&res_full[ob1], C::OUT_BYTES);
+                    tma_load_4d(out_base + (size_t)ob1 * (C::OUT_BYTES / 4), &tmRes, &res_full[ob1],
+                                0, h1, c1, n1);
+                }
             }
         }
-        fence_async_smem();
-        asm volatile("bar.sync 1, 128;" ::: "memory");   // the 4 epilogue warps
-        if (threadIdx.x == 64) {
-            tma_store_4d(&tmOut, s_out, 0, h0, co0, n0);
-            bulk_commit();
-            bulk_wait_read0();
-        }
+        if (leader) bulk_wait_read0();
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<C::TMEM_COLS>(tmem);
+        tmem_dealloc<512>(tmem);
     }
 }
 
@@ -289,9 +344,11 @@ __global__ void weight_prep_kernel(const float *w, int co_n, int ci_n, int kh, i
     const int64_t total = (int64_t)co_n * kk * ci_n;
     for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
          idx += (int64_t)gridDim.x * blockDim.x) {
+        // layout [uv][co'][ci'] (uv = u*kw + v): the TMA box (KC, BN, KW) at
+        // (c0, co0, u*kw) is the stacked column-tap B tile of kernel row u
         const int c = (int)(idx % ci_n);
-        const int uv = (int)((idx / ci_n) % kk);
-        const int o = (int)(idx / ((int64_t)ci_n * kk));
+        const int o = (int)((idx / ci_n) % co_n);
+        const int uv = (int)(idx / ((int64_t)ci_n * co_n));
         const int u = uv / kw, v = uv % kw;
         float x;
         if (!flip)
@@ -339,14 +396,16 @@ static bool make_map_act(CUtensorMap *m, const float *x, const FwdGeo &g, int ow
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static bool make_map_w(CUtensorMap *m, const float *b, int rows, int kdim, int bn, int kc) {
+// prepared weights [kh*kw][co][ci] as 3D (ci, co, uv); box = KC x BN x KW
+static bool make_map_w(CUtensorMap *m, const float *b, int co, int ci, int kk, int bn, int kc,
+                       int kw) {
     auto enc = encode_fn();
     if (!enc) return false;
-    cuuint64_t dims[2] = {(cuuint64_t)kdim, (cuuint64_t)rows};
-    cuuint64_t strides[1] = {(cuuint64_t)kdim * 4};
-    cuuint32_t box[2] = {(cuuint32_t)kc, (cuuint32_t)bn};
-    cuuint32_t es[2] = {1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void *)b, dims, strides, box, es,
+    cuuint64_t dims[3] = {(cuuint64_t)ci, (cuuint64_t)co, (cuuint64_t)kk};
+    cuuint64_t strides[2] = {(cuuint64_t)ci * 4, (cuuint64_t)co * ci * 4};
+    cuuint32_t box[3] = {(cuuint32_t)kc, (cuuint32_t)bn, (cuuint32_t)kw};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)b, dims, strides, box, es,
                CU_TENSOR_MAP_INTERLEAVE_NONE, swz(kc * 4), CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
                CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -354,6 +413,17 @@ static bool make_map_w(CUtensorMap *m, const float *b, int rows, int kdim, int b
 struct Maps {
     CUtensorMap a, bh, bl, out, res;
 };
+
+static int num_sms() {
+    static int n = 0;
+    if (!n) {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    }
+    return n;
+}
 
 template <int BN, int OWT, int KC, int KW>
 static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, int tiles, int ntiles,
@@ -365,15 +435,23 @@ static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, int t
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    // ring depth: no deeper than the K loop, and small enough that 2+ CTAs
-    // share an SM (one CTA's epilogue / prologue overlaps another's mainloop)
     FwdGeo gg = g;
-    const int nst = g.kh * (g.ci / KC);
-    int S = std::min(nst, C::S_MAX);
-    while (S > 1 && C::smem_bytes(S) > 112 * 1024) --S;
-    gg.stages = S;
-    kern<<<dim3(tiles, ntiles), kTcThreads, C::smem_bytes(S), st>>>(m.a, m.bh, m.bl, m.out, m.res,
-                                                                   gg, ep);
+    gg.mtiles = tiles;
+    gg.ntiles = ntiles;
+    // smem plan: output staging x2 when it fits, raw ring >= 2 (up to 8)
+    const int budget = 227 * 1024 - 1024 - 512;
+    int nout = 2;
+    auto raw_fit = [&](int no) { return (budget - no * C::OUT_BYTES) / C::RAW_BYTES; };
+    if (raw_fit(nout) < 2) nout = 1;
+    int r = raw_fit(nout);
+    if (r < 2) return QT_EUNSUPPORTED;
+    r = std::min(r, 8);
+    gg.R = r;
+    gg.NOUT = nout;
+    const int smem = r * C::RAW_BYTES + nout * C::OUT_BYTES + 1024 + 512;
+    const int total = tiles * ntiles;
+    const int grid = std::min(total, num_sms());
+    kern<<<grid, kFwdThreads, smem, st>>>(m.a, m.bh, m.bl, m.out, m.res, gg, ep);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -385,7 +463,9 @@ static int dispatch_bn(int bn, const Maps &m, const FwdGeo &g, const EpiParams &
         case 16: return launch_fwd<16, OWT, KC, KW>(m, g, ep, tiles, ntiles, st);
         case 32: return launch_fwd<32, OWT, KC, KW>(m, g, ep, tiles, ntiles, st);
         case 64: return launch_fwd<64, OWT, KC, KW>(m, g, ep, tiles, ntiles, st);
-        case 128: return launch_fwd<128, OWT, KC, KW>(m, g, ep, tiles, ntiles, st);
+        case 128:
+            if constexpr (KW == 1) return launch_fwd<128, OWT, KC, KW>(m, g, ep, tiles, ntiles, st);
+            return QT_EUNSUPPORTED;
         default: return QT_EUNSUPPORTED;
     }
 }
@@ -395,15 +475,11 @@ static int dispatch_kc(int kc, int kw, int bn, const Maps &m, const FwdGeo &g,
                        const EpiParams &ep, int tiles, int ntiles, cudaStream_t st) {
     if (kw == 1) {
         switch (kc) {
-            case 8: return dispatch_bn<OWT, 8, 1>(bn, m, g, ep, tiles, ntiles, st);
             case 16: return dispatch_bn<OWT, 16, 1>(bn, m, g, ep, tiles, ntiles, st);
             case 32: return dispatch_bn<OWT, 32, 1>(bn, m, g, ep, tiles, ntiles, st);
         }
     } else if (kw == 3) {
-        switch (kc) {
-            case 8: return dispatch_bn<OWT, 8, 3>(bn, m, g, ep, tiles, ntiles, st);
-            case 16: return dispatch_bn<OWT, 16, 3>(bn, m, g, ep, tiles, ntiles, st);
-        }
+        if (kc == 16) return dispatch_bn<OWT, 16, 3>(bn, m, g, ep, tiles, ntiles, st);
     }
     return QT_EUNSUPPORTED;
 }
@@ -428,7 +504,7 @@ static bool tc_shape_ok(int n, int ci, int h, int wd, int co, int kh, int kw, in
     if (kw != 1 && kw != 3) return false;
     if (kw == 1 && pad != 0) return false;
     if (ow != 8 && ow != 16 && ow != 32) return false;
-    if (ow != wd || ci % 8 || co % 16 || ci < 8) return false;
+    if (ow != wd || ci % 16 || co % 16) return false;
     const int per = 128 / ow;
     if (oh >= per) return oh % per == 0;
     return per % oh == 0 && n % (per / oh) == 0;
@@ -452,10 +528,14 @@ static int tc_conv_s1(const float *x, const float *w, float *out, int n, int ci,
         if (per % g.oh || n % (per / g.oh)) return QT_EUNSUPPORTED;
         g.rows = g.oh; g.nimg = per / g.oh; g.tiles_per_img = 1;
     }
-    const int kcmax = kw == 1 ? 32 : 16;
-    const int kc = ci % kcmax == 0 ? kcmax : (ci % 16 == 0 ? 16 : 8);
+    const int kc = (kw == 1 && ci % 32 == 0) ? 32 : 16;
     int bn = co <= 16 ? 16 : (co <= 32 ? 32 : (co <= 64 ? 64 : 128));
+    if (kw == 3 && bn > 64) bn = 64;         // stacked taps: KW * BN <= 256 (UMMA N)
     if (co % bn) return QT_EUNSUPPORTED;
+    {   // split the channels further while there are fewer tiles than SMs
+        const int mt = (n / g.nimg) * g.tiles_per_img;
+        while (bn > 16 && (int64_t)mt * (co / bn) < num_sms() && co % (bn / 2) == 0) bn /= 2;
+    }
     const int kdim = kh * kw * ci;
     float *bhi = (float *)ws;
     float *blo = bhi + (int64_t)co * kdim;
@@ -464,17 +544,17 @@ static int tc_conv_s1(const float *x, const float *w, float *out, int n, int ci,
                          st>>>(w, co, ci, kh, kw, flip, bhi, blo);
     QT_CHECK_LAUNCH();
     Maps mp;
-    if (!make_map_act(&mp.a, x, g, g.ow, kc) || !make_map_w(&mp.bh, bhi, co, kdim, bn, kc) ||
-        !make_map_w(&mp.bl, blo, co, kdim, bn, kc) ||
+    if (!make_map_act(&mp.a, x, g, g.ow, kc) ||
+        !make_map_w(&mp.bh, bhi, co, ci, kh * kw, bn, kc, kw) ||
+        !make_map_w(&mp.bl, blo, co, ci, kh * kw, bn, kc, kw) ||
         !make_map_nchw(&mp.out, out, n, co, g.oh, g.ow, g.rows, bn, g.nimg))
         return QT_EUNSUPPORTED;
     EpiParams ep{out, res, cr, sr, 0};
-    if (res && sr == 1) {  // same-resolution shortcut: one TMA box per tile (OOB channels -> 0)
+    mp.res = mp.out;
+    if (res && sr == 1) {  // same-resolution shortcut: one TMA box per tile (channels >= cr -> 0)
         if (!make_map_nchw(&mp.res, res, n, cr, g.oh, g.ow, g.rows, bn, g.nimg))
             return QT_EUNSUPPORTED;
         ep.res_tma = 1;
-    } else {
-        mp.res = mp.out;   // unused
     }
     const int tiles = (n / g.nimg) * g.tiles_per_img;
     const int ntiles = co / bn;

@@ -198,16 +198,28 @@ def test_zero_gradient():
     (4, 16, 16, 32, 3, 1, 4, "approx"), (8, 64, 16, 8, 1, 0, 4, "approx"),
     (4, 16, 64, 16, 1, 0, 8, "approx"), (2, 32, 32, 16, 3, 1, 2, "approx"),
     (4, 16, 16, 32, 3, 1, 4, "exact"), (4, 32, 128, 8, 1, 0, 1, "approx"),
+    # 4-bit offsets beyond the bf16 fast path (2^K-1+2*offset > 127): whole
+    # launch generic, and one wide channel making one row group generic
+    (4, 16, 16, 32, 3, 1, 4, "approx", "wide"), (2, 32, 32, 16, 3, 1, 4, "approx", "mixed"),
+    (4, 64, 256, 8, 1, 0, 4, "approx", "mixed"), (4, 16, 64, 16, 1, 0, 4, "approx", "dead"),
 ])
 def test_backward_given_device_tape(cfg):
     """Backward parity with the oracle fed OUR tape (codes, step, offset,
     sigma2, frozen gamma/beta): isolates the backward kernels (TC wgrad with
     fused decode, TC dgrad, BN/ReLU backward) from forward-moment ulps."""
-    n, ci, co, hw, k, pad, bits, mode = cfg
+    n, ci, co, hw, k, pad, bits, mode = cfg[:8]
+    regime = cfg[8] if len(cfg) > 8 else "narrow"
     rng = np.random.default_rng(sum(cfg[:7]))
     w = (rng.standard_normal((co, ci, k, k)) * 0.3).astype(np.float32)
     gamma = rng.uniform(0.5, 1.5, ci).astype(np.float32)
     beta = rng.uniform(-0.3, 0.3, ci).astype(np.float32)
+    if regime == "wide":      # offset = floor(beta * 2^K / (6 |gamma|)) ~ 60..200
+        gamma = rng.uniform(0.05, 0.1, ci).astype(np.float32)
+        beta = rng.uniform(1.5, 3.0, ci).astype(np.float32)
+    elif regime == "mixed":   # the last channel alone is wide
+        gamma[-1], beta[-1] = 0.05, 2.5
+    elif regime == "dead":    # strongly negative offsets: all-zero ReLU channels
+        beta[: ci // 2] = -40.0
     x = (rng.standard_normal((n, ci, hw, hw)) * 2 + 0.5).astype(np.float32)
     p = L.LayerParams(kind="conv", weight=dev(w), stride=1, pad=pad, gamma=dev(gamma),
                       beta=dev(beta))
