@@ -165,6 +165,23 @@ int qt_conv_dgrad(const float *g, const float *w, float *gx,
                   int64_t kh, int64_t kw, int64_t stride, int64_t pad, void *ws,
                   qt_stream_t stream);
 
+/* Prepared weight operands.  On the tensor-core path qt_conv_forward /
+ * qt_conv_dgrad first re-lay the kernel into (hi, lo) TF32 halves in `ws`
+ * ([kh*kw][rows][cols] each; rows = co, cols = ci for the forward, rows = ci,
+ * cols = co of the 180-degree-flipped kernel for the data gradient).  Passing
+ * w == NULL means `ws` already holds that operand -- prepared for many layers
+ * at once by qt_conv_prepare_weights (one launch per optimizer step instead
+ * of one per conv call).  `descs` is a DEVICE array of `count` descriptors;
+ * max_elems = max over descriptors of rows*cols*kh*kw.  w == NULL is an error
+ * for shapes that run on the CUDA cores. */
+typedef struct {
+    const float *w;   /* original (co, ci, kh, kw) kernel */
+    float *out;       /* 2 * rows * cols * kh * kw floats: hi then lo */
+    int32_t rows, cols, kh, kw, flip, pad_;
+} qt_wprep_t;
+int qt_conv_prepare_weights(const qt_wprep_t *descs, int64_t count, int64_t max_elems,
+                            qt_stream_t stream);
+
 /* Scratch for qt_conv_forward / qt_conv_dgrad: the tensor-core path keeps the
  * (hi, lo) TF32 split of the re-laid-out kernel there (2*ci*co*kh*kw floats).
  * The tensor-core path serves stride-1 convs whose output rows are 8, 16 or

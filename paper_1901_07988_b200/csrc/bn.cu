@@ -4,12 +4,14 @@
 // Reductions are deterministic: a fixed element->thread->block partition,
 // float64 partials, and a last-block-per-channel finalize that reads the
 // partials in block order (no float atomics anywhere).
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace qt {
 
 constexpr int kRThreads = 256;
-constexpr int64_t kTargetPerBlock = 4096;
+constexpr int64_t kTargetPerBlock = 8192;
 // Workspace layout of every reduction: [kCounterBytes of per-channel
 // completion counters (always left at zero)][float64 partials].  Keeping the
 // counters at a fixed offset lets differently-shaped launches share one
@@ -23,12 +25,12 @@ struct Part {
 };
 
 static Part partition(int64_t n, int64_t c, int64_t hw) {
-    // ~4 blocks per SM overall, at least kTargetPerBlock/2 elements per block
+    // ~2 blocks per SM overall, at least kTargetPerBlock elements per block
     Part p;
-    const int64_t want_nb = std::max<int64_t>(1, (4 * 148 + c - 1) / c);
+    const int64_t want_nb = std::max<int64_t>(1, (2 * 148) / c);
     p.planes_per_block = std::max<int64_t>(1, qt_cdiv(n, want_nb));
     p.planes_per_block = std::max<int64_t>(p.planes_per_block,
-                                           std::max<int64_t>(1, kTargetPerBlock / 2 / hw));
+                                           std::max<int64_t>(1, kTargetPerBlock / hw));
     if (p.planes_per_block > n) p.planes_per_block = n;
     p.blocks = qt_cdiv(n, p.planes_per_block);
     return p;
@@ -86,6 +88,7 @@ struct StatsArgs {
     double *step;
     int64_t *offset;
     int64_t *clip;
+    FastDiv hw8d;       // hw / 8 (vectorized stats loop)
 };
 
 __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
@@ -96,12 +99,24 @@ __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
     const double shift = (double)a.x[ch * a.hw];  // x[0, c, 0]: shifted sums
     double v[2] = {0.0, 0.0};
     const int64_t cnt = (p1 - p0) * a.hw;
-    if ((a.hw & 7) == 0) {
-        const int64_t hw8 = a.hw >> 3;
-        for (int64_t e = threadIdx.x; e < cnt / 8; e += kRThreads) {
-            int64_t pl = e / hw8, off = e - pl * hw8;
+    if ((a.hw & 7) == 0 && cnt / 8 < (1ll << 31)) {
+        const uint32_t hw8 = (uint32_t)(a.hw >> 3), n8 = (uint32_t)(cnt / 8);
+        constexpr int U = 4;   // groups in flight per thread
+        for (uint32_t e0 = threadIdx.x; e0 < n8; e0 += U * kRThreads) {
+          float4 qq[U], rr[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const uint32_t e = e0 + u * kRThreads;
+            if (e >= n8) break;
+            const uint32_t pl = fast_div(e, a.hw8d), off = e - pl * hw8;
             const float4 *src = reinterpret_cast<const float4 *>(a.x + ((p0 + pl) * a.c + ch) * a.hw) + 2 * off;
-            const float4 q = __ldg(src), r = __ldg(src + 1);
+            qq[u] = __ldg(src);
+            rr[u] = __ldg(src + 1);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            if (e0 + u * kRThreads >= n8) break;
+            const float4 q = qq[u], r = rr[u];
             double d0 = (double)q.x - shift, d1 = (double)q.y - shift;
             double d2 = (double)q.z - shift, d3 = (double)q.w - shift;
             double d4 = (double)r.x - shift, d5 = (double)r.y - shift;
@@ -109,6 +124,7 @@ __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
             v[0] += ((d0 + d1) + (d2 + d3)) + ((d4 + d5) + (d6 + d7));
             v[1] += ((d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3)) +
                     ((d4 * d4 + d5 * d5) + (d6 * d6 + d7 * d7));
+          }
         }
     } else if ((a.hw & 3) == 0) {
         const int64_t hw4 = a.hw >> 2;
@@ -135,14 +151,19 @@ __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
         pp[1] = v[1];
     }
     if (!last_block(a.counter + ch, (unsigned)a.nb)) return;
-    if (threadIdx.x == 0) {
-        __threadfence();
-        double s1 = 0.0, s2 = 0.0;
-        const volatile double *pp = a.part + ch * a.nb * 2;
-        for (int64_t b = 0; b < a.nb; ++b) {
-            s1 += pp[2 * b];
-            s2 += pp[2 * b + 1];
+    // last block: all threads combine the partials (fixed strided order + tree)
+    __threadfence();
+    double fin[2] = {0.0, 0.0};
+    {
+        const double *pp = a.part + ch * a.nb * 2;
+        for (int64_t b = threadIdx.x; b < a.nb; b += kRThreads) {
+            fin[0] += __ldcg(pp + 2 * b);
+            fin[1] += __ldcg(pp + 2 * b + 1);
         }
+    }
+    block_sum<2>(fin, red);
+    if (threadIdx.x == 0) {
+        const double s1 = fin[0], s2 = fin[1];
         const double cntd = (double)(a.n * a.hw);
         const double dm = s1 / cntd;
         double var = (s2 - s1 * dm) / cntd;
@@ -184,13 +205,11 @@ __global__ void __launch_bounds__(kRThreads) chan_sum_kernel(StatsArgs a) {
     block_sum<1>(v, red);
     if (threadIdx.x == 0) a.part[ch * a.nb + blockIdx.x] = v[0];
     if (!last_block(a.counter + ch, (unsigned)a.nb)) return;
-    if (threadIdx.x == 0) {
-        __threadfence();
-        double s1 = 0.0;
-        const volatile double *pp = a.part + ch * a.nb;
-        for (int64_t b = 0; b < a.nb; ++b) s1 += pp[b];
-        a.mean[ch] = s1;
-    }
+    __threadfence();
+    double fin[1] = {0.0};
+    for (int64_t b = threadIdx.x; b < a.nb; b += kRThreads) fin[0] += __ldcg(a.part + ch * a.nb + b);
+    block_sum<1>(fin, red);
+    if (threadIdx.x == 0) a.mean[ch] = fin[0];
 }
 
 // ------------------------------------------------------- reconstruct ---
@@ -298,6 +317,7 @@ extern "C" int qt_bn_stats(const float *x, int64_t n, int64_t c, int64_t hw, dou
     StatsArgs a{x, n, c, hw, p.planes_per_block, p.blocks, mean, var, running_mean, running_var,
                 (double *)((char *)ws + kCounterBytes), (unsigned *)ws,
                 nullptr, nullptr, 0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+    a.hw8d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 3));
     dim3 grid((unsigned)p.blocks, (unsigned)c);
     bn_stats_kernel<<<grid, kRThreads, 0, qt_s(stream)>>>(a);
     QT_CHECK_LAUNCH();
@@ -318,6 +338,7 @@ extern "C" int qt_bn_stats_prep(const float *x, int64_t n, int64_t c, int64_t hw
                 (double *)((char *)ws + kCounterBytes), (unsigned *)ws,
                 gamma, beta, bits, eps, (BnConst *)consts, gamma_copy, beta_copy, step, offset,
                 clip_count};
+    a.hw8d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 3));
     dim3 grid((unsigned)p.blocks, (unsigned)c);
     bn_stats_kernel<<<grid, kRThreads, 0, qt_s(stream)>>>(a);
     QT_CHECK_LAUNCH();

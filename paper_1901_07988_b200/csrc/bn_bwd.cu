@@ -32,10 +32,13 @@ struct BwdPart {
 // channel (enough work per thread that the block's deterministic
 // last-block-finalize tail is amortised)
 static BwdPart bwd_partition(int64_t n, int64_t c, int64_t hw) {
+    // ~2 blocks per SM in total, each with >= 8192 elements (>= 4 groups of
+    // 8 per thread) so the per-block table build and the deterministic
+    // last-block combine are amortised
     BwdPart p;
-    const int64_t want_nb = std::max<int64_t>(1, (4 * 148 + c - 1) / c);
+    const int64_t want_nb = std::max<int64_t>(1, (2 * 148) / c);
     p.ppb = std::max<int64_t>(1, qt_cdiv(n, want_nb));
-    p.ppb = std::max<int64_t>(p.ppb, std::max<int64_t>(1, 2048 / hw));
+    p.ppb = std::max<int64_t>(p.ppb, std::max<int64_t>(1, 8192 / hw));
     if (p.ppb > n) p.ppb = n;
     p.nb = qt_cdiv(n, p.ppb);
     return p;
@@ -60,6 +63,7 @@ struct BwdArgs {
     double *part;
     unsigned *counter;
     float *lut;      // [C][2][256]: mask, a1 per code
+    FastDiv gppd;    // hw / 8
 };
 
 // mask (1/0) and a1 for one code of channel ch (layer.py:354-366)
@@ -83,99 +87,116 @@ __device__ __forceinline__ uint64_t load_code_word(const uint8_t *codes, int64_t
 template <bool CODES, bool VA1>
 __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
     __shared__ float s_m[kMaxLut], s_a1[kMaxLut];
-    __shared__ double red[4][kBT / 32];
+    __shared__ double s_a1d[kMaxLut];
+    __shared__ double red[3][kBT / 32];
     __shared__ bool s_last;
     const int ch = blockIdx.y;
     const float gam = a.gamma[ch], bet = a.beta[ch], sg = safe_gamma(gam);
     const int ncode = CODES ? (1 << a.tape.bits) : 0;
     if (CODES) {
-        for (int code = threadIdx.x; code < ncode; code += kBT)
+        for (int code = threadIdx.x; code < ncode; code += kBT) {
             lut_entry(a.tape, ch, code, bet, sg, s_m[code], s_a1[code]);
+            s_a1d[code] = (double)s_a1[code];
+        }
         __syncthreads();
     }
     const int64_t p0 = (int64_t)blockIdx.x * a.ppb;
     const int64_t p1 = min(p0 + a.ppb, a.n);
-    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;
+    // float64 accumulators: S0 = sum g3m, S1 = sum a1*g3m, S3' = sum a1v*g3m
+    // (g3m = g3*mask is exact in fp32; S2 = gamma*S0 and S3 = gamma*S3' are
+    // formed once per channel).  One float->double conversion per element.
+    double v0 = 0.0, v1 = 0.0, v3 = 0.0;
     const uint32_t cmask = (1u << a.tape.bits) - 1u;
     // The summation order depends only on the shape (never on the tape
     // type), so an exact tape and a K-bit tape with variance_a1 substituted
     // produce bit-identical sums (reference test_layer.py:173-202).
-    if ((a.hw & 7) == 0) {
-        const int64_t groups = (p1 - p0) * (a.hw >> 3);
-        const int64_t gpp = a.hw >> 3;
-#pragma unroll 2
-        for (int64_t gi = threadIdx.x; gi < groups; gi += kBT) {
-            const int64_t pl = gi / gpp, off = (gi - pl * gpp) << 3;
-            const int64_t i0 = ((p0 + pl) * a.c + ch) * a.hw + off;
-            const float4 ga = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0));
-            const float4 gb = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0) + 1);
-            const uint64_t word0 = CODES ? load_code_word(a.tape.codes, i0, a.tape.bits) : 0;
-            const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
-            float mv[8], av[8];
-            if (CODES) {
-                const uint64_t word = word0;
+    const int64_t cnt8 = ((p1 - p0) * a.hw) >> 3;
+    if ((a.hw & 7) == 0 && cnt8 < (1ll << 31)) {
+        const uint32_t groups = (uint32_t)cnt8;
+        const uint32_t gpp = (uint32_t)(a.hw >> 3);
+        constexpr int U = 4;                     // groups in flight per thread
+        for (uint32_t g0 = threadIdx.x; g0 < groups; g0 += U * kBT) {
+            float4 ga[U], gb[U], xa[U], xb[U];
+            uint64_t word[U];
+            int64_t i0[U];
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint32_t code = (uint32_t)(word >> (j * a.tape.bits)) & cmask;
-                    mv[j] = s_m[code];
-                    av[j] = s_a1[code];
-                }
-            } else {
-                const float4 xa = __ldg(reinterpret_cast<const float4 *>(a.tape.a2 + i0));
-                const float4 xb = __ldg(reinterpret_cast<const float4 *>(a.tape.a2 + i0) + 1);
-                const float xv[8] = {xa.x, xa.y, xa.z, xa.w, xb.x, xb.y, xb.z, xb.w};
-#pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    mv[j] = xv[j] > 0.f ? 1.f : 0.f;
-                    av[j] = __fdiv_rn(__fsub_rn(xv[j], bet), sg);
+            for (int u = 0; u < U; ++u) {
+                const uint32_t gi = g0 + u * kBT;
+                if (gi >= groups) break;
+                const uint32_t pl = fast_div(gi, a.gppd), off = (gi - pl * gpp) << 3;
+                i0[u] = ((p0 + pl) * a.c + ch) * a.hw + off;
+                ga[u] = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0[u]));
+                gb[u] = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0[u]) + 1);
+                if (CODES) {
+                    word[u] = load_code_word(a.tape.codes, i0[u], a.tape.bits);
+                } else {
+                    xa[u] = __ldg(reinterpret_cast<const float4 *>(a.tape.a2 + i0[u]));
+                    xb[u] = __ldg(reinterpret_cast<const float4 *>(a.tape.a2 + i0[u]) + 1);
                 }
             }
-            double d0 = 0.0, d1 = 0.0, d2 = 0.0, d3 = 0.0;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float g3m = __fmul_rn(gv[j], mv[j]);
-                const float g1 = __fmul_rn(g3m, gam);
-                const float a1v = VA1 ? a.va1[i0 + j] : av[j];
-                d0 += (double)g3m;
-                d1 += (double)__fmul_rn(av[j], g3m);
-                d2 += (double)g1;
-                d3 += (double)__fmul_rn(a1v, g1);
+            for (int u = 0; u < U; ++u) {
+                if (g0 + u * kBT >= groups) break;
+                const float gv[8] = {ga[u].x, ga[u].y, ga[u].z, ga[u].w,
+                                     gb[u].x, gb[u].y, gb[u].z, gb[u].w};
+                float xv[8];
+                if (!CODES) {
+                    xv[0] = xa[u].x; xv[1] = xa[u].y; xv[2] = xa[u].z; xv[3] = xa[u].w;
+                    xv[4] = xb[u].x; xv[5] = xb[u].y; xv[6] = xb[u].z; xv[7] = xb[u].w;
+                }
+                double d0 = 0.0, d1 = 0.0, d3 = 0.0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    float m;
+                    double a1d;
+                    if (CODES) {
+                        const uint32_t code = (uint32_t)(word[u] >> (j * a.tape.bits)) & cmask;
+                        m = s_m[code];
+                        a1d = s_a1d[code];
+                    } else {
+                        m = xv[j] > 0.f ? 1.f : 0.f;
+                        a1d = (double)__fdiv_rn(__fsub_rn(xv[j], bet), sg);
+                    }
+                    const double gm = (double)__fmul_rn(gv[j], m);
+                    d0 += gm;
+                    d1 = fma(a1d, gm, d1);
+                    if (VA1) d3 = fma((double)a.va1[i0[u] + j], gm, d3);
+                }
+                v0 += d0; v1 += d1; v3 += d3;
             }
-            v0 += d0; v1 += d1; v2 += d2; v3 += d3;
         }
     } else {
         const int64_t cnt = (p1 - p0) * a.hw;
         for (int64_t e = threadIdx.x; e < cnt; e += kBT) {
             const int64_t pl = e / a.hw, off = e - pl * a.hw;
             const int64_t i = ((p0 + pl) * a.c + ch) * a.hw + off;
-            float m, a1;
+            float m;
+            double a1d;
             if (CODES) {
                 const uint32_t code = get_code(a.tape.codes, i, a.tape.bits);
                 m = s_m[code];
-                a1 = s_a1[code];
+                a1d = s_a1d[code];
             } else {
                 const float a2 = a.tape.a2[i];
                 m = a2 > 0.f ? 1.f : 0.f;
-                a1 = __fdiv_rn(__fsub_rn(a2, bet), sg);
+                a1d = (double)__fdiv_rn(__fsub_rn(a2, bet), sg);
             }
-            const float g3m = __fmul_rn(a.g3[i], m);
-            const float g1 = __fmul_rn(g3m, gam);
-            const float a1v = VA1 ? a.va1[i] : a1;
-            v0 += (double)g3m;
-            v1 += (double)__fmul_rn(a1, g3m);
-            v2 += (double)g1;
-            v3 += (double)__fmul_rn(a1v, g1);
+            const double gm = (double)__fmul_rn(a.g3[i], m);
+            v0 += gm;
+            v1 = fma(a1d, gm, v1);
+            if (VA1) v3 = fma((double)a.va1[i], gm, v3);
         }
     }
-    v0 = warp_sum(v0); v1 = warp_sum(v1); v2 = warp_sum(v2); v3 = warp_sum(v3);
+    if (!VA1) v3 = v1;
+    v0 = warp_sum(v0); v1 = warp_sum(v1); v3 = warp_sum(v3);
     const int w = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {
-        red[0][w] = v0; red[1][w] = v1; red[2][w] = v2; red[3][w] = v3;
+        red[0][w] = v0; red[1][w] = v1; red[2][w] = v3;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
         double *pp = a.part + (ch * a.nb + blockIdx.x) * 4;
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < 3; ++j) {
             double t = 0.0;
             for (int q = 0; q < kBT / 32; ++q) t += red[j][q];
             pp[j] = t;
@@ -195,17 +216,31 @@ __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
             lut[kMaxLut + code] = s_a1[code];
         }
     }
+    // combine the partials: fixed strided order, then a fixed tree
+    __threadfence();
+    double f[3] = {0.0, 0.0, 0.0};
+    {
+        const double *pp = a.part + ch * a.nb * 4;
+        for (int64_t b = threadIdx.x; b < a.nb; b += kBT)
+            for (int j = 0; j < 3; ++j) f[j] += __ldcg(pp + 4 * b + j);
+    }
+#pragma unroll
+    for (int j = 0; j < 3; ++j) f[j] = warp_sum(f[j]);
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) {
+        red[0][w] = f[0]; red[1][w] = f[1]; red[2][w] = f[2];
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
-        __threadfence();
-        double s[4] = {0.0, 0.0, 0.0, 0.0};
-        const volatile double *pp = a.part + ch * a.nb * 4;
-        for (int64_t b = 0; b < a.nb; ++b)
-            for (int j = 0; j < 4; ++j) s[j] += pp[4 * b + j];
+        double s[3] = {0.0, 0.0, 0.0};
+        for (int j = 0; j < 3; ++j)
+            for (int q = 0; q < kBT / 32; ++q) s[j] += red[j][q];
+        const double g64 = (double)gam;
         const double cntd = (double)(a.n * a.hw);
         if (a.grad_beta) a.grad_beta[ch] = __double2float_rn((double)a.grad_beta[ch] + s[0]);
         if (a.grad_gamma) a.grad_gamma[ch] = __double2float_rn((double)a.grad_gamma[ch] + s[1]);
-        a.stats[ch] = __double2float_rn(s[2] / cntd);                         // t2
-        a.stats[a.c + ch] = __double2float_rn(s[3] / cntd);                   // t3
+        a.stats[ch] = __double2float_rn(g64 * s[0] / cntd);                   // t2 = mean g1
+        a.stats[a.c + ch] = __double2float_rn(g64 * s[2] / cntd);             // t3 = mean a1v*g1
         a.stats[2 * a.c + ch] =
             __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(a.sigma2[ch], a.eps))));  // inv
     }
@@ -219,6 +254,7 @@ struct ApplyArgs {
     const float *lut;
     int64_t cr, sc;
     float *g_in;
+    FastDiv gppd, cd;   // hw / 8, c
 };
 
 __device__ __forceinline__ float res_value(const ApplyArgs &a, int64_t i, int64_t pl, int ch,
@@ -237,13 +273,12 @@ __global__ void __launch_bounds__(kBT) bn_bwd_apply_kernel(ApplyArgs a) {
     const int64_t hw = a.h * a.w;
     const int64_t numel = a.n * a.c * hw;
     const uint32_t cmask = (1u << a.tape.bits) - 1u;
-    if (CODES && (hw & 7) == 0) {
-        const int64_t groups = numel >> 3;
-        for (int64_t gi = (int64_t)blockIdx.x * kBT + threadIdx.x; gi < groups;
-             gi += (int64_t)gridDim.x * kBT) {
-            const int64_t i0 = gi << 3;
-            const int64_t pl = i0 / hw;
-            const int ch = (int)(pl % a.c);
+    if (CODES && (hw & 7) == 0 && (numel >> 3) < (1ll << 31)) {
+        const uint32_t groups = (uint32_t)(numel >> 3);
+        for (uint32_t gi = blockIdx.x * kBT + threadIdx.x; gi < groups; gi += gridDim.x * kBT) {
+            const int64_t i0 = (int64_t)gi << 3;
+            const uint32_t pl = fast_div(gi, a.gppd);
+            const int ch = (int)(pl - fast_div(pl, a.cd) * (uint32_t)a.c);
             const float gam = __ldg(a.gamma + ch);
             const float t2 = __ldg(a.stats + ch), t3 = __ldg(a.stats + a.c + ch);
             const float inv = __ldg(a.stats + 2 * a.c + ch);
@@ -331,6 +366,7 @@ extern "C" int qt_bn_backward_reduce(const float *g3, qt_tape_t tape, int64_t n,
     if (!codes) tape.bits = 1;
     BwdArgs a{g3, tape, n, c, hw, gamma_tape, beta_tape, sigma2, eps, variance_a1, grad_gamma,
               grad_beta, stats, p.ppb, p.nb, part_base(ws, c), (unsigned *)ws, lut_base(ws)};
+    a.gppd = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 3));
     dim3 grid((unsigned)p.nb, (unsigned)c);
     cudaStream_t s = qt_s(stream);
     if (codes)
@@ -356,6 +392,8 @@ extern "C" int qt_bn_backward_apply(const float *g3, qt_tape_t tape, int64_t n, 
     if (!codes) tape.bits = 1;
     ApplyArgs a{g3, tape, n, c, h, w, gamma_tape, beta_tape, variance_a1, stats, res_g,
                 lut_base((void *)ws), cr, sc, g_in};
+    a.gppd = make_fastdiv((uint32_t)std::max<int64_t>(1, (h * w) >> 3));
+    a.cd = make_fastdiv((uint32_t)c);
     const int64_t work = codes && ((h * w) & 7) == 0 ? (n * c * h * w) >> 3 : n * c * h * w;
     int64_t blocks = std::min<int64_t>(qt_cdiv(work, kBT), 148 * 16);
     blocks = std::max<int64_t>(blocks, 1);

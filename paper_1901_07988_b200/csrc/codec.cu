@@ -45,6 +45,7 @@ struct FwdArgs {
     int64_t *offset;
     unsigned long long *clip_count;
     const BnConst *consts;   // optional: per-channel constants from qt_bn_stats_prep
+    FastDiv hw8d, cd;        // stream kernel: group -> plane -> channel (32-bit)
 };
 
 __device__ __forceinline__ PlaneConst make_plane(const FwdArgs &a, int64_t ch, bool apply_bn) {
@@ -314,10 +315,51 @@ __global__ void unpack_kernel(const uint8_t *packed, int64_t count, int bits, ui
 // qt_bn_stats_prep, hw % 8 == 0): grid-stride over 8-element groups, two
 // groups per iteration with all four 128-bit loads issued before any math,
 // constants through the read-only cache -- no block prologue, no smem.
+// Codes of 8 consecutive A2 values of one channel (approx / naive modes).
+// Common path in fp32/int32 (see code_fast in common.cuh for the error
+// analysis): a*scale = p + e + a*s2, floor taken from f + floor(fr) when the
+// fraction fr is more than 2^-20 from an integer and |p| < 2^20; elements
+// failing that (non-finite, huge, near-integer products) and channels whose
+// offset is outside +-2^30 are recomputed with the exact float64 recipe.
+template <int BITS>
+__device__ __forceinline__ void quant8(const float (&v)[8], const BnConst &k, uint32_t (&code)[8],
+                                       uint32_t &clipmask) {
+    constexpr int top = (1 << BITS) - 1;
+    const bool chan_ok = k.off > -(1ll << 30) && k.off < (1ll << 30);
+    // u_bits = float bits of (floor(a*scale) + 1.5*2^23); raw = u_bits + bias
+    const int bias = (1 << (BITS - 1)) - (int)(chan_ok ? k.off : 0) - 0x4B400000;
+    uint32_t slow = chan_ok ? 0u : 0xFFu;
+    clipmask = 0u;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const float p = __fmul_rn(v[j], k.s1);
+        const float e = __fmaf_rn(v[j], k.s1, -p);
+        const float corr = __fmaf_rn(v[j], k.s2, e);
+        const float f = floorf(p);
+        const float fr = __fadd_rn(__fsub_rn(p, f), corr);
+        const float dist = fabsf(__fsub_rn(fr, rintf(fr)));
+        if (!(fabsf(p) < 1048576.f && dist > 9.5367431640625e-07f)) slow |= 1u << j;
+        const float u = __fadd_rn(__fadd_rn(f, floorf(fr)), 12582912.f);
+        const int raw = __float_as_int(u) + bias;
+        const int c = min(max(raw, 0), top);
+        code[j] = (uint32_t)c;
+        clipmask |= (raw != c) ? (1u << j) : 0u;
+    }
+    if (slow) {
+#pragma unroll 1
+        for (int j = 0; j < 8; ++j) {
+            if (!((slow >> j) & 1u)) continue;
+            const int64_t raw = raw_code(v[j], k.scale, k.off, BITS);
+            const bool cl = raw < 0 || raw > top;
+            code[j] = (uint32_t)(raw < 0 ? 0 : (raw > top ? top : raw));
+            clipmask = (clipmask & ~(1u << j)) | (cl ? (1u << j) : 0u);
+        }
+    }
+}
+
 template <int BITS, int MODE, bool A2, bool CLIP>
 __global__ void __launch_bounds__(kThreads) bn_relu_quant_stream(FwdArgs a) {
     const int64_t ngroups = a.numel >> 3;
-    const int64_t hw8 = a.hw >> 3;
     const int64_t stride = (int64_t)gridDim.x * kThreads;
     unsigned long long clip = 0;
     for (int64_t g0 = (int64_t)blockIdx.x * kThreads + threadIdx.x; g0 < ngroups; g0 += 2 * stride) {
@@ -335,7 +377,8 @@ __global__ void __launch_bounds__(kThreads) bn_relu_quant_stream(FwdArgs a) {
         for (int u = 0; u < 2; ++u) {
             const int64_t gg = gs[u];
             if (gg >= ngroups) break;
-            const int64_t ch = (gg / hw8) % a.c;
+            const uint32_t plane = fast_div((uint32_t)gg, a.hw8d);
+            const uint32_t ch = plane - fast_div(plane, a.cd) * (uint32_t)a.c;
             const BnConst k = a.consts[ch];
             const float xv[8] = {xa[u].x, xa[u].y, xa[u].z, xa[u].w, xb[u].x, xb[u].y, xb[u].z, xb[u].w};
             float a2v[8], a3v[8];
@@ -345,18 +388,27 @@ __global__ void __launch_bounds__(kThreads) bn_relu_quant_stream(FwdArgs a) {
                 float v = __fsub_rn(xv[j], k.m32);       // layer.py:246-249
                 v = __fmul_rn(v, k.inv32);
                 v = __fmul_rn(v, k.g);
-                v = __fadd_rn(v, k.b);
-                a2v[j] = v;
-                float pre = v;
-                if (BITS) {
-                    const int64_t raw = raw_code(v, k.scale, k.off, BITS);
-                    constexpr int64_t top = (1ll << BITS) - 1;
-                    if (CLIP) clip += (raw < 0 || raw > top);
-                    const uint32_t code = (uint32_t)(raw < 0 ? 0 : (raw > top ? top : raw));
-                    word |= (uint64_t)code << (j * BITS);
-                    if (MODE == MODE_NAIVE) pre = decode(code, k.step, k.off, BITS);
+                a2v[j] = __fadd_rn(v, k.b);
+            }
+            if (BITS) {
+                uint32_t code[8], clipmask;
+                quant8<BITS>(a2v, k, code, clipmask);
+                if (CLIP) clip += __popc(clipmask);
+                if (BITS * 8 <= 32) {
+                    uint32_t w32 = 0;
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) w32 |= code[j] << (j * BITS);
+                    word = w32;
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) word |= (uint64_t)code[j] << (j * BITS);
                 }
-                a3v[j] = relu_np(pre);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    a3v[j] = relu_np(MODE == MODE_NAIVE ? decode(code[j], k.step, k.off, BITS) : a2v[j]);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) a3v[j] = relu_np(a2v[j]);
             }
             float4 *d3 = reinterpret_cast<float4 *>(a.a3_out) + 2 * gg;
             d3[0] = make_float4(a3v[0], a3v[1], a3v[2], a3v[3]);
@@ -400,11 +452,16 @@ static void launch_stream(const FwdArgs &a, unsigned blocks, cudaStream_t s) {
     }
 }
 
-static int launch_fwd(const FwdArgs &a, bool apply_bn, cudaStream_t s) {
-    if (a.numel == 0) return QT_OK;
+static int launch_fwd(const FwdArgs &a0, bool apply_bn, cudaStream_t s) {
+    if (a0.numel == 0) return QT_OK;
+    FwdArgs a = a0;
+    if ((a.hw & 7) == 0 && a.hw < (1ll << 31) && a.c < (1ll << 31)) {
+        a.hw8d = make_fastdiv((uint32_t)(a.hw >> 3));
+        a.cd = make_fastdiv((uint32_t)a.c);
+    }
     const bool aligned = ((((uintptr_t)a.x) | ((uintptr_t)a.a3_out) | ((uintptr_t)a.a2_tape)) & 15) == 0;
     if (apply_bn && a.consts && a.a3_out && (a.hw & 7) == 0 && aligned &&
-        (a.bits == 0 || a.codes)) {
+        (a.bits == 0 || a.codes) && (a.numel >> 3) < (1ll << 31)) {
         const int64_t ngroups = a.numel >> 3;
         int64_t blocks = std::min<int64_t>(qt_cdiv(ngroups, 2 * kThreads), 148 * 8);
         blocks = std::max<int64_t>(blocks, 1);

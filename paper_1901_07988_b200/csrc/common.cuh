@@ -61,7 +61,7 @@ struct BnConst {
     double scale;             // 2^K / (6 g)       (codec.py:101-104)
     double step;              // 6 g 2^-K
     int64_t off;              // floor(beta * scale) via x86 cast
-    int64_t pad_;
+    float s1, s2;             // scale = s1 + s2 (+ < 2^-48 rel): code_fast
 };
 
 __device__ __forceinline__ BnConst bn_const(double mean, double var, double eps, float gamma,
@@ -75,12 +75,14 @@ __device__ __forceinline__ BnConst bn_const(double mean, double var, double eps,
     k.scale = 0.0;
     k.step = 0.0;
     k.off = 0;
-    k.pad_ = 0;
+    k.s1 = k.s2 = 0.f;
     if (bits) {
         ChanCode cc = chan_code(gamma, beta, bits);
         k.scale = cc.scale;
         k.step = cc.step;
         k.off = cc.off;
+        k.s1 = __double2float_rn(cc.scale);
+        k.s2 = __double2float_rn(cc.scale - (double)k.s1);
     }
     return k;
 }
@@ -90,6 +92,37 @@ __device__ __forceinline__ int64_t raw_code(float a, double scale, int64_t off, 
     int64_t u = x86_f64_to_i64(floor(__dmul_rn((double)a, scale)));
     uint64_t r = (uint64_t)u + (uint64_t)(1ll << (bits - 1)) - (uint64_t)off;
     return (int64_t)r;
+}
+
+// Same code (clamped to [0, 2^K-1]) and clip flag as raw_code, without
+// float64 arithmetic on the common path: a*scale is evaluated as
+// p + e + a*s2 (p = fl32(a*s1), e its exact FMA error, s1 + s2 = scale), and
+// floor() is taken from the fp32 value when the fraction is more than 2^-20
+// away from an integer (the float64 product's floor is then the same);
+// non-finite / large values, huge offsets and near-integer products take the
+// exact float64 path.  Returns the clamped code, sets *clipped.
+__device__ __forceinline__ uint32_t code_fast(float a, float s1, float s2, double scale, int64_t off,
+                                              int bits, bool *clipped) {
+    const float p = __fmul_rn(a, s1);
+    const float e = __fmaf_rn(a, s1, -p);
+    const float corr = __fmaf_rn(a, s2, e);
+    const float f = floorf(p);
+    const float fr = __fadd_rn(__fsub_rn(p, f), corr);   // p - f exact
+    const int64_t top = (1ll << bits) - 1;
+    const float margin = 9.5367431640625e-07f;            // 2^-20
+    const bool fast = fabsf(p) < 1048576.f && off > -(1ll << 30) && off < (1ll << 30) &&
+                      fabsf(fr) > margin && fabsf(fr - 1.f) > margin && fr > -1.f && fr < 2.f;
+    int64_t raw;
+    if (fast) {
+        // integer value of f (|f| < 2^20) without a conversion instruction
+        const int u = (__float_as_int(__fadd_rn(f, 12582912.f)) - 0x4B400000) +
+                      (fr < 0.f ? -1 : (fr >= 1.f ? 1 : 0));
+        raw = (int64_t)u + (1ll << (bits - 1)) - off;
+    } else {
+        raw = raw_code(a, scale, off, bits);
+    }
+    *clipped = raw < 0 || raw > top;
+    return (uint32_t)(raw < 0 ? 0 : (raw > top ? top : raw));
 }
 
 // Interval-median decode (codec.py:149-154), rounded to the tape dtype.
@@ -117,6 +150,23 @@ __device__ __forceinline__ float safe_gamma(float g) {
     mag = mag > kGammaFloorF ? mag : kGammaFloorF;
     if (isnan(g)) mag = g;
     return g < 0.f ? -mag : mag;
+}
+
+// Division by a launch-invariant divisor for numerators below 2^31
+// (Granlund-Montgomery: q = (umulhi(x, m) + x) >> s), prepared on the host.
+struct FastDiv {
+    uint32_t d, m, s;
+};
+static inline FastDiv make_fastdiv(uint32_t d) {
+    FastDiv f;
+    f.d = d;
+    f.s = 0;
+    while ((1ull << f.s) < d) ++f.s;
+    f.m = (uint32_t)(((((uint64_t)1) << 32) * ((((uint64_t)1) << f.s) - d)) / d + 1);
+    return f;
+}
+__device__ __forceinline__ uint32_t fast_div(uint32_t x, const FastDiv &f) {
+    return (__umulhi(x, f.m) + x) >> f.s;
 }
 
 template <typename T>

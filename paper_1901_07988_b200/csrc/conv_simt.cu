@@ -317,10 +317,11 @@ extern "C" int qt_conv_forward(const float *x, const float *w, float *out, int64
                                int64_t stride, int64_t pad, const float *res, int64_t cr,
                                int64_t sr, void *ws, qt_stream_t stream) {
     ConvGeo g = make_geo(n, ci, h, wd, co, kh, kw, stride, pad);
-    QT_REQUIRE(x && w && out && geo_ok(g));
+    QT_REQUIRE(x && out && geo_ok(g));
     QT_REQUIRE(!res || (cr > 0 && cr <= co && sr >= 1));
     int rc = qt_tc_conv_forward(x, w, out, g, res, cr, sr, ws, qt_s(stream));
     if (rc != QT_EUNSUPPORTED) return rc;
+    QT_REQUIRE(w);   // NULL (prepared operand in ws) is only valid on the tensor-core path
     FwdA la{x, g};
     FwdB lb{w, ci * kh * kw};
     StoreNCHW ep{out, g.oh * g.ow, co, g.ow, res, cr, sr};
@@ -332,9 +333,10 @@ extern "C" int qt_conv_dgrad(const float *gr, const float *w, float *gx, int64_t
                              int64_t h, int64_t wd, int64_t co, int64_t kh, int64_t kw,
                              int64_t stride, int64_t pad, void *ws, qt_stream_t stream) {
     ConvGeo g = make_geo(n, ci, h, wd, co, kh, kw, stride, pad);
-    QT_REQUIRE(gr && w && gx && geo_ok(g));
+    QT_REQUIRE(gr && gx && geo_ok(g));
     int rc = qt_tc_conv_dgrad(gr, w, gx, g, ws, qt_s(stream));
     if (rc != QT_EUNSUPPORTED) return rc;
+    QT_REQUIRE(w);
     DgradA la{gr, g};
     DgradB lb{w, g};
     StoreNCHW ep{gx, h * wd, ci, wd, nullptr, 0, 1};

@@ -362,6 +362,30 @@ __global__ void weight_prep_kernel(const float *w, int co_n, int ci_n, int kh, i
     }
 }
 
+// Many layers' preparations in one launch: blockIdx.y selects the descriptor.
+__global__ void weight_prep_batch_kernel(const qt_wprep_t *descs) {
+    const qt_wprep_t d = descs[blockIdx.y];
+    const int kk = d.kh * d.kw;
+    const int64_t total = (int64_t)d.rows * kk * d.cols;
+    float *bhi = d.out, *blo = d.out + total;
+    for (int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+         idx += (int64_t)gridDim.x * blockDim.x) {
+        const int c = (int)(idx % d.cols);
+        const int o = (int)((idx / d.cols) % d.rows);
+        const int uv = (int)(idx / ((int64_t)d.cols * d.rows));
+        const int u = uv / d.kw, v = uv % d.kw;
+        float x;
+        if (!d.flip)
+            x = d.w[(((int64_t)o * d.cols + c) * d.kh + u) * d.kw + v];
+        else
+            x = d.w[(((int64_t)c * d.rows + o) * d.kh + (d.kh - 1 - u)) * d.kw + (d.kw - 1 - v)];
+        float hi, lo;
+        split_tf32(x, hi, lo);
+        bhi[idx] = hi;
+        blo[idx] = lo;
+    }
+}
+
 // --------------------------------------------------------------- host side
 
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -540,9 +564,11 @@ static int tc_conv_s1(const float *x, const float *w, float *out, int n, int ci,
     float *bhi = (float *)ws;
     float *blo = bhi + (int64_t)co * kdim;
     if (!ws) return QT_EINVAL;
-    weight_prep_kernel<<<(unsigned)std::min<int64_t>(qt_cdiv((int64_t)co * kdim, 256), 1024), 256, 0,
-                         st>>>(w, co, ci, kh, kw, flip, bhi, blo);
-    QT_CHECK_LAUNCH();
+    if (w) {   // w == NULL: ws already holds the prepared operand (qt_conv_prepare_weights)
+        weight_prep_kernel<<<(unsigned)std::min<int64_t>(qt_cdiv((int64_t)co * kdim, 256), 1024), 256,
+                             0, st>>>(w, co, ci, kh, kw, flip, bhi, blo);
+        QT_CHECK_LAUNCH();
+    }
     Maps mp;
     if (!make_map_act(&mp.a, x, g, g.ow, kc) ||
         !make_map_w(&mp.bh, bhi, co, ci, kh * kw, bn, kc, kw) ||
@@ -588,6 +614,16 @@ extern "C" int qt_conv_uses_tc(int64_t n, int64_t ci, int64_t h, int64_t wd, int
     const int64_t oh = h + 2 * pad - kh + 1, ow = wd + 2 * pad - kw + 1;
     return tc_shape_ok((int)n, (int)co, (int)oh, (int)ow, (int)ci, (int)kh, (int)kw,
                        (int)(kh - 1 - pad)) ? 1 : 0;
+}
+
+extern "C" int qt_conv_prepare_weights(const qt_wprep_t *descs, int64_t count, int64_t max_elems,
+                                       qt_stream_t stream) {
+    QT_REQUIRE(descs && count >= 0 && count <= 65535 && max_elems >= 0);
+    if (count == 0) return QT_OK;
+    const unsigned bx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(qt_cdiv(max_elems, 256), 64));
+    weight_prep_batch_kernel<<<dim3(bx, (unsigned)count), 256, 0, qt_s(stream)>>>(descs);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
 }
 
 extern "C" int64_t qt_conv_workspace(int64_t ci, int64_t co, int64_t kh, int64_t kw) {

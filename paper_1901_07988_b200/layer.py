@@ -64,6 +64,10 @@ class LayerParams:
     vel_beta: Optional[torch.Tensor] = None
     running_mean: Optional[torch.Tensor] = None
     running_var: Optional[torch.Tensor] = None
+    # engine hook: tensor-core weight operands prepared once per step
+    # (qt_conv_prepare_weights); None -> prepared inside each conv call
+    prep_fwd: Optional[torch.Tensor] = None
+    prep_dgrad: Optional[torch.Tensor] = None
 
     def __post_init__(self):
         _dev_f32(self.weight, "weight")
@@ -203,7 +207,7 @@ def _linear_forward(a3, p: LayerParams, out, residual=None, ws=None):
     """layer.py:138-151; ``residual`` fuses the block-end shortcut add."""
     if p.kind == "conv":
         return ops.conv2d_forward(a3, p.weight, p.stride, p.pad, out=out, residual=residual,
-                                  ws=None if ws is None else ws.conv)
+                                  ws=None if ws is None else ws.conv, prepared=p.prep_fwd)
     if p.kind == "dense":
         src = a3
     elif p.kind == "gap_dense":
@@ -361,7 +365,7 @@ def layer_backward(g_out: torch.Tensor, tape: LayerTape, p: LayerParams,
                 return None
             g_in = out if out is not None else torch.empty_like(a_in)
             ops.conv2d_dgrad(g_out, p.weight, tuple(a_in.shape), p.stride, p.pad, g_in,
-                             ws=None if ws is None else ws.conv)
+                             ws=None if ws is None else ws.conv, prepared=p.prep_dgrad)
         if residual_grad is not None:
             _apply_adjoint(g_in, residual_grad)
         return g_in
@@ -380,7 +384,7 @@ def layer_backward(g_out: torch.Tensor, tape: LayerTape, p: LayerParams,
         ops.conv2d_wgrad(g_out, tuple(p.weight.shape), p.stride, p.pad, p.grad_weight,
                          tape=nt, in_shape=in_shape, ws=None if ws is None else ws.wgrad)
         ops.conv2d_dgrad(g_out, p.weight, in_shape, p.stride, p.pad, g3,
-                         ws=None if ws is None else ws.conv)
+                         ws=None if ws is None else ws.conv, prepared=p.prep_dgrad)
     else:
         _, _, a3 = reconstruct_from_tape(tape)
         if p.kind == "dense":

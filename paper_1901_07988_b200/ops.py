@@ -116,11 +116,12 @@ def _conv_ws(k, ws):
 
 def conv2d_forward(x: torch.Tensor, k: torch.Tensor, stride: int = 1, pad: int = 0,
                    out: Optional[torch.Tensor] = None, residual: Optional[torch.Tensor] = None,
-                   ws=None) -> torch.Tensor:
+                   ws=None, prepared=None) -> torch.Tensor:
     """Cross-correlation with zero padding (ops.py:106-138).
 
     ``residual`` (engine use) fuses the parameter-free shortcut add of
-    engine.py:262-269 into the epilogue."""
+    engine.py:262-269 into the epilogue; ``prepared`` (engine use) is the
+    tensor-core weight operand already laid out by qt_conv_prepare_weights."""
     if x.dim() != 4 or k.dim() != 4:
         raise ShapeError("conv2d expects rank-4 input and kernel")
     x, k = _dense(x, "x"), _dense(k, "k")
@@ -134,8 +135,9 @@ def conv2d_forward(x: torch.Tensor, k: torch.Tensor, stride: int = 1, pad: int =
     if residual is not None:
         cr = residual.shape[1]
         sr = residual.shape[2] // oh
-    N.call("qt_conv_forward", N.ptr(x), N.ptr(k), N.ptr(out), n, ci, x.shape[2], x.shape[3], co,
-           kh, kw, stride, pad, N.ptr(residual), cr, sr, N.ptr(_conv_ws(k, ws)))
+    wp, wsp = (None, prepared) if prepared is not None else (k, _conv_ws(k, ws))
+    N.call("qt_conv_forward", N.ptr(x), N.ptr(wp), N.ptr(out), n, ci, x.shape[2], x.shape[3], co,
+           kh, kw, stride, pad, N.ptr(residual), cr, sr, N.ptr(wsp))
     _check_finite(out)
     return out
 
@@ -168,11 +170,12 @@ def conv2d_wgrad(g_out, k_shape, stride, pad, grad_w, x_plain=None, tape=None, i
            kw, stride, pad, N.ptr(ws))
 
 
-def conv2d_dgrad(g_out, k, in_shape, stride, pad, g_x_out, ws=None):
+def conv2d_dgrad(g_out, k, in_shape, stride, pad, g_x_out, ws=None, prepared=None):
     n, ci, h, w = in_shape
     co, _, kh, kw = k.shape
-    N.call("qt_conv_dgrad", N.ptr(g_out), N.ptr(k), N.ptr(g_x_out), n, ci, h, w, co, kh, kw,
-           stride, pad, N.ptr(_conv_ws(k, ws)))
+    wp, wsp = (None, prepared) if prepared is not None else (k, _conv_ws(k, ws))
+    N.call("qt_conv_dgrad", N.ptr(g_out), N.ptr(wp), N.ptr(g_x_out), n, ci, h, w, co, kh, kw,
+           stride, pad, N.ptr(wsp))
 
 
 def conv2d_backward(x: torch.Tensor, k: torch.Tensor, g_out: torch.Tensor, stride: int = 1,

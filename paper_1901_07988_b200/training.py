@@ -228,10 +228,49 @@ class Trainer:
         self.graph = None
         self.use_graph = use_graph
         self.tapes = None
+        self._build_weight_prep()
 
     # one iteration of training.py:192-199 on the static buffers, in two
     # parts so the (optional) gradient all-reduce sits between them
+    def _build_weight_prep(self):
+        """Tensor-core conv layers get persistent prepared weight operands,
+        refreshed by ONE qt_conv_prepare_weights launch at the start of every
+        step (instead of one re-layout per conv call)."""
+        descs = []
+        self._prep_max = 0
+        for li, (p, (ins, _)) in enumerate(zip(self.params, self.spec.layer_shapes(self.n))):
+            p.prep_fwd = p.prep_dgrad = None
+            if p.kind != "conv":
+                continue
+            n, ci, h, w = ins
+            co, _, kh, kw = p.weight.shape
+            elems = co * ci * kh * kw
+            for dgrad in (0, 1):
+                if not N.query("qt_conv_uses_tc", n, ci, h, w, co, kh, kw, p.stride, p.pad, dgrad):
+                    continue
+                if dgrad and li == 0:
+                    continue          # the stem needs no input gradient
+                buf = torch.empty(2 * elems, dtype=torch.float32, device=self.device)
+                rows, cols = (ci, co) if dgrad else (co, ci)
+                descs.append((p.weight.data_ptr(), buf.data_ptr(), rows, cols, kh, kw, dgrad, 0))
+                if dgrad:
+                    p.prep_dgrad = buf
+                else:
+                    p.prep_fwd = buf
+                self._prep_max = max(self._prep_max, elems)
+        dt = np.dtype([("w", "<u8"), ("out", "<u8"), ("rows", "<i4"), ("cols", "<i4"),
+                       ("kh", "<i4"), ("kw", "<i4"), ("flip", "<i4"), ("pad", "<i4")])
+        arr = np.array(descs, dtype=dt)
+        self._prep_descs = torch.from_numpy(arr.view(np.uint8).copy()).to(self.device)
+        self._prep_count = len(descs)
+
+    def _prepare_weights(self):
+        if self._prep_count:
+            N.call("qt_conv_prepare_weights", N.ptr(self._prep_descs), self._prep_count,
+                   self._prep_max)
+
     def _fwd_bwd(self):
+        self._prepare_weights()
         logits, tapes = network_forward(self.spec, self.params, self.x, mode=self.mode,
                                         bits=self.bits, pool=self.pool, arena=self.arena)
         _, g = softmax_xent(logits, self.labels, loss_buf=self.loss_buf, check=False)

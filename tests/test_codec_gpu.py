@@ -144,3 +144,56 @@ def test_large_tensor_roundtrip_property():
         sg = (a >= 0) == (d >= 0)
         assert bool((sg | ~unclipped).all())
         assert t.clip_count == int((~unclipped).sum())
+
+
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+def test_stream_kernel_codes_at_interval_boundaries(bits):
+    """The fused BN-apply + quantize stream kernel (per-channel constant table,
+    fp32 fast path for floor(a*scale) with a float64 fallback near integers)
+    against the oracle at exact code boundaries k*step, their fp32
+    neighbours, huge / non-finite / subnormal values and tiny gammas."""
+    from paper_1901_07988_b200 import _native as N
+    rng = np.random.default_rng(bits)
+    n, c, hw = 3, 6, 64
+    gamma = np.array([1.0, 0.37, -2.5, 1e-9, 0.0, 3.0], np.float32)
+    beta = np.array([0.0, 0.11, -0.7, 0.2, 1e-3, 25.0], np.float32)
+    scale, step, off = O.code_constants(gamma, beta, bits)
+    x = np.empty((n, c, hw), np.float32)
+    for ch in range(c):
+        k = rng.integers(-(1 << bits) - 4, (1 << bits) + 4, n * hw).astype(np.float64)
+        base = ((k + off[ch] - (1 << (bits - 1))) / scale[ch]).astype(np.float32)   # a*scale ~ k
+        jitter = rng.integers(-2, 3, n * hw)
+        vals = np.nextafter(base, np.where(jitter > 0, np.inf, -np.inf).astype(np.float32))
+        vals = np.where(jitter == 0, base, vals)
+        vals[:12] = [np.nan, np.inf, -np.inf, 1e30, -1e30, 1.4e-45, -1.4e-45, 0.0, -0.0,
+                     5e18, -5e18, 3.4e38]
+        x[:, ch, :] = vals.reshape(n, hw)
+    # constants with mean 0, inv 1: A2 = x*gamma + beta in fp32 (layer.py:246-249)
+    ct = np.zeros(c, dtype=[("m32", "<f4"), ("inv32", "<f4"), ("g", "<f4"), ("b", "<f4"),
+                            ("scale", "<f8"), ("step", "<f8"), ("off", "<i8"), ("s1", "<f4"),
+                            ("s2", "<f4")])
+    ct["inv32"], ct["g"], ct["b"] = 1.0, gamma, beta
+    ct["scale"], ct["step"], ct["off"] = scale, step, off
+    ct["s1"] = scale.astype(np.float32)
+    ct["s2"] = (scale - ct["s1"].astype(np.float64)).astype(np.float32)
+    assert ct.dtype.itemsize == 48
+    with np.errstate(invalid="ignore", over="ignore"):
+        a2 = (((x - np.float32(0)) * np.float32(1)) * gamma[None, :, None]) + beta[None, :, None]
+        raw = O.raw_codes(a2, gamma, beta, bits)
+    codes_ref = O.pack(np.clip(raw, 0, (1 << bits) - 1), bits)
+    clips_ref = int(((raw < 0) | (raw > (1 << bits) - 1)).sum())
+    xd, consts = dev(x), torch.from_numpy(ct.view(np.uint8).copy()).cuda()
+    a3 = torch.empty_like(xd)
+    codes = torch.empty((bits * x.size + 7) // 8, dtype=torch.uint8, device="cuda")
+    stp = torch.empty(c, dtype=torch.float64, device="cuda")
+    offd = torch.empty(c, dtype=torch.int64, device="cuda")
+    clip = torch.zeros(1, dtype=torch.int64, device="cuda")
+    dummy = torch.zeros(c, dtype=torch.float64, device="cuda")
+    gd, bd = dev(gamma), dev(beta)
+    N.call("qt_bn_relu_forward", N.ptr(xd), n, c, hw, N.ptr(dummy), N.ptr(dummy), 1e-5,
+           N.ptr(gd), N.ptr(bd), 1, bits, N.ptr(a3), None, N.ptr(codes), N.ptr(stp), N.ptr(offd),
+           N.ptr(clip), N.ptr(consts))
+    assert np.array_equal(host(codes), codes_ref)
+    assert int(clip.item()) == clips_ref
+    with np.errstate(invalid="ignore"):
+        assert np.array_equal(host(a3), np.maximum(a2, np.float32(0)), equal_nan=True)

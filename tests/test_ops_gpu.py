@@ -124,3 +124,34 @@ def test_moments_constant_and_two_point():
     x = dev(np.array([[1.0], [3.0]], np.float32))
     m, v = ops.channel_moments(x)
     assert host(m)[0] == 2.0 and host(v)[0] == 1.0
+
+
+def test_prepared_weights_match_per_call_preparation():
+    """qt_conv_prepare_weights (one launch for many layers) + w == NULL gives
+    the same bits as the per-call re-layout, forward and data gradient."""
+    from paper_1901_07988_b200 import _native as N
+    rng = np.random.default_rng(3)
+    cases = [(2, 16, 32, 16, 3, 1), (2, 64, 8, 256, 1, 0), (2, 32, 16, 32, 3, 1)]
+    descs, keep = [], []
+    for n, ci, h, co, k, p in cases:
+        w = dev((rng.standard_normal((co, ci, k, k)) * 0.2).astype(np.float32))
+        pf = torch.empty(2 * w.numel(), dtype=torch.float32, device="cuda")
+        pd = torch.empty(2 * w.numel(), dtype=torch.float32, device="cuda")
+        descs += [(w.data_ptr(), pf.data_ptr(), co, ci, k, k, 0, 0),
+                  (w.data_ptr(), pd.data_ptr(), ci, co, k, k, 1, 0)]
+        keep.append((w, pf, pd))
+    dt = np.dtype([("w", "<u8"), ("out", "<u8"), ("rows", "<i4"), ("cols", "<i4"),
+                   ("kh", "<i4"), ("kw", "<i4"), ("flip", "<i4"), ("pad", "<i4")])
+    assert dt.itemsize == 40
+    d = torch.from_numpy(np.array(descs, dtype=dt).view(np.uint8).copy()).cuda()
+    N.call("qt_conv_prepare_weights", N.ptr(d), len(descs), max(w.numel() for w, _, _ in keep))
+    for (n, ci, h, co, k, p), (w, pf, pd) in zip(cases, keep):
+        x = dev(rng.standard_normal((n, ci, h, h)).astype(np.float32))
+        a = ops.conv2d_forward(x, w, 1, p)
+        b = ops.conv2d_forward(x, w, 1, p, prepared=pf)
+        assert torch.equal(a, b)
+        g = dev(rng.standard_normal(tuple(a.shape)).astype(np.float32))
+        ga, gb = torch.empty_like(x), torch.empty_like(x)
+        ops.conv2d_dgrad(g, w, tuple(x.shape), 1, p, ga)
+        ops.conv2d_dgrad(g, w, tuple(x.shape), 1, p, gb, prepared=pd)
+        assert torch.equal(ga, gb)
