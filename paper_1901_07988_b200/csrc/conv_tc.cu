@@ -46,7 +46,6 @@ struct FwdCfg {
     static constexpr int OUT_BYTES = BM * BN * 4;                    // output staging tile
     static constexpr int ACC_COLS = 2 * NM;                          // double-buffered accumulator
     static constexpr int OP_COLS = 2 * KC;                           // one A operand stage (hi, lo)
-    static constexpr int OP = (512 - ACC_COLS) / OP_COLS >= 2 ? 2 : 1;
     static_assert(NM <= 256 && NM % 16 == 0, "UMMA N");
     static_assert(ACC_COLS + OP_COLS <= 512, "TMEM budget");
     static constexpr int A_SW = OWT * 4;     // swizzle bytes of the raw activation box
@@ -58,6 +57,10 @@ struct FwdGeo {
     int rows, nimg, tiles_per_img;  // tile = nimg images x rows x OW pixels
     int mtiles, ntiles;             // output tiles along pixels / channels
     int R, NOUT;                    // raw ring and output staging depths
+    int G;                          // split warpgroups = operand ring depth (1, 2, 4)
+    int wres;                       // 1: the CTA's weight tiles stay resident in smem
+    int slot;                       // raw ring slot bytes (A box [+ B tiles])
+    FastDiv ntd, tpid;              // / ntiles, / tiles_per_img (no runtime IDIV)
 };
 
 struct EpiParams {
@@ -67,7 +70,24 @@ struct EpiParams {
     int res_tma;   // 1: shortcut tile TMA-loaded into the output staging buffer
 };
 
-constexpr int kFwdThreads = 320;   // w0 TMA, w1 TMEM+MMA, w2-5 split, w6-9 epilogue
+// w0 TMA, w1 TMEM + MMA, w2..w17 up to 4 split warpgroups, w18..w21 epilogue.
+// Split group g owns operand stage g and every G-th (u, chunk) stage, so G
+// stages are transformed concurrently and every mbarrier has one waiter
+// group that consumes its phases in order (R is a multiple of G).
+constexpr int kFwdGroups = 2;
+
+// debug timeline (qt_debug_conv_trace): clock64 stamps of CTA trace_cta.
+// Per stage gi < 64: [8*gi + 0] producer issue, +1 split raw_full ok, +2 split
+// op_empty ok, +3 split done, +4 MMA op_full ok, +5 MMA committed;
+// per tile lt < 32: [600 + 4*lt + 0] epi acc_full ok, +1 epi stored.
+__device__ long long *g_cv_trace = nullptr;
+__device__ int g_cv_trace_cta = 0;
+#define CV_TRACE(idx)                  \
+    do {                               \
+        if (tr_) tr_[idx] = clock64(); \
+    } while (0)
+constexpr int kFwdThreads = 64 + 128 * kFwdGroups + 128;
+constexpr int kFwdEpiWarp = 2 + 4 * kFwdGroups;
 
 // Persistent implicit-GEMM conv: each CTA walks output tiles (128 pixels x BN
 // channels) with a grid-stride loop.
@@ -96,32 +116,39 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                        const __grid_constant__ CUtensorMap tmOut,
                        const __grid_constant__ CUtensorMap tmRes, FwdGeo g, EpiParams ep) {
     using C = FwdCfg<BN, OWT, KC, KW>;
-    constexpr int OP = C::OP;
-    const int R = g.R, NOUT = g.NOUT;
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    const int R = g.R, NOUT = g.NOUT, G = g.G;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1 KiB alignment by pointer arithmetic on the __shared__ array (an
+    // integer round trip would turn every access into a generic LD/ST)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t *raw_base = smem;
-    float *out_base = (float *)(raw_base + R * C::RAW_BYTES);
-    uint64_t *bars = (uint64_t *)((uint8_t *)out_base + NOUT * C::OUT_BYTES);
+    float *out_base = (float *)(raw_base + R * g.slot);
+    // resident weights (wres): every stage's (hi, lo) tile, loaded once per CTA
+    uint8_t *wres_base = (uint8_t *)out_base + NOUT * C::OUT_BYTES;
+    uint64_t *bars = (uint64_t *)(wres_base + (g.wres ? g.kh * (g.ci / KC) * 2 * C::B_SLOT : 0));
     uint64_t *raw_full = bars, *raw_empty = bars + R;
-    uint64_t *op_full = bars + 2 * R, *op_empty = op_full + OP;
-    uint64_t *acc_full = op_empty + OP, *acc_empty = acc_full + 2;
+    uint64_t *op_full = bars + 2 * R, *op_empty = op_full + kFwdGroups;
+    uint64_t *acc_full = op_empty + kFwdGroups, *acc_empty = acc_full + 2;
     uint64_t *res_full = acc_empty + 2;
-    uint32_t *tmem_slot = (uint32_t *)(res_full + 2);
+    uint64_t *w_full = res_full + 2;
+    uint32_t *tmem_slot = (uint32_t *)(w_full + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    long long *const tr_ = (g_cv_trace && blockIdx.x == (unsigned)g_cv_trace_cta) ? g_cv_trace : nullptr;
+    if (threadIdx.x == 0) CV_TRACE(1000);
     const int kchunks = g.ci / KC;
     const int nst = g.kh * kchunks;             // (u, channel chunk) stages per tile
     const int total = g.mtiles * g.ntiles;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < R; ++s) { mbar_init(&raw_full[s], 1); mbar_init(&raw_empty[s], 1); }
-        for (int s = 0; s < OP; ++s) { mbar_init(&op_full[s], 128); mbar_init(&op_empty[s], 1); }
+        for (int s = 0; s < G; ++s) { mbar_init(&op_full[s], 128); mbar_init(&op_empty[s], 1); }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&acc_full[a], 1);
             mbar_init(&acc_empty[a], 128);
             mbar_init(&res_full[a], 1);
         }
+        mbar_init(w_full, 1);
         fence_barrier_init();
     }
     if (warp == 1) tmem_alloc<512>(tmem_slot);
@@ -138,50 +165,77 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const uint32_t tmem = *tmem_slot;
 
     auto tile_coords = [&](int T, int &n0, int &h0, int &co0) {
-        const int mt = T / g.ntiles;
+        const int mt = (int)fast_div((uint32_t)T, g.ntd);
         co0 = (T - mt * g.ntiles) * BN;
-        n0 = (g.nimg > 1) ? mt * g.nimg : mt / g.tiles_per_img;
-        h0 = (g.nimg > 1) ? 0 : (mt % g.tiles_per_img) * g.rows;
+        const int im = (int)fast_div((uint32_t)mt, g.tpid);
+        n0 = (g.nimg > 1) ? mt * g.nimg : im;
+        h0 = (g.nimg > 1) ? 0 : (mt - im * g.tiles_per_img) * g.rows;
     };
-    auto sRaw = [&](int s) { return raw_base + s * C::RAW_BYTES; };
-    auto sBh = [&](int s) { return raw_base + s * C::RAW_BYTES + C::A_BYTES; };
-    auto sBl = [&](int s) { return raw_base + s * C::RAW_BYTES + C::A_BYTES + C::B_SLOT; };
+    auto sRaw = [&](int s) { return raw_base + s * g.slot; };
+    // B tiles of ring slot s / stage i: in the slot, or resident
+    auto sBh = [&](int s, int i) {
+        return g.wres ? wres_base + (2 * i) * C::B_SLOT : raw_base + s * g.slot + C::A_BYTES;
+    };
+    auto sBl = [&](int s, int i) {
+        return g.wres ? wres_base + (2 * i + 1) * C::B_SLOT
+                      : raw_base + s * g.slot + C::A_BYTES + C::B_SLOT;
+    };
     auto a_col = [&](int o) { return (uint32_t)(C::ACC_COLS + o * C::OP_COLS); };
 
     if (warp == 0) {
         if (lane == 0) {  // ---------------------------------------- TMA producer
-            int gi = 0;
+            if (g.wres && (int)blockIdx.x < total) {   // this CTA's co tile is fixed
+                int n0, h0, co0;
+                tile_coords(blockIdx.x, n0, h0, co0);
+                mbar_expect_tx(w_full, nst * 2 * C::B_BYTES);
+                for (int i = 0; i < nst; ++i) {
+                    const int u = i / kchunks, c0 = (i % kchunks) * KC;
+                    tma_load_3d(sBh(0, i), &tmBh, w_full, c0, co0, u * KW);
+                    tma_load_3d(sBl(0, i), &tmBl, w_full, c0, co0, u * KW);
+                }
+            }
+            int gi = 0, s = 0;
+            uint32_t phe = 0;
             for (int T = blockIdx.x; T < total; T += gridDim.x) {
                 int n0, h0, co0;
                 tile_coords(T, n0, h0, co0);
-                for (int i = 0; i < nst; ++i, ++gi) {
-                    const int s = gi % R;
-                    mbar_wait(&raw_empty[s], ((uint32_t)(gi / R) & 1u) ^ 1u);
-                    const int u = i / kchunks, c0 = (i % kchunks) * KC;
-                    mbar_expect_tx(&raw_full[s], C::A_BYTES + 2 * C::B_BYTES);
-                    tma_load_4d(sRaw(s), &tmA, &raw_full[s], 0, c0, h0 + u - g.pad, n0);
-                    tma_load_3d(sBh(s), &tmBh, &raw_full[s], c0, co0, u * KW);
-                    tma_load_3d(sBl(s), &tmBl, &raw_full[s], c0, co0, u * KW);
+                for (int i = 0, u = 0, c0 = 0; i < nst; ++i, ++gi) {
+                    mbar_wait(&raw_empty[s], phe ^ 1u);
+                    if (gi < 64) CV_TRACE(8 * gi);
+                    mbar_expect_tx(&raw_full[s], C::A_BYTES + (g.wres ? 0 : 2 * C::B_BYTES));
+                    // flattened (h*w) plane: the tile's rows shifted by u - pad are one
+                    // contiguous pixel run (rows above / below the image are OOB -> 0)
+                    tma_load_3d(sRaw(s), &tmA, &raw_full[s], (h0 + u - g.pad) * g.w, c0, n0);
+                    if (!g.wres) {
+                        tma_load_3d(sBh(s, i), &tmBh, &raw_full[s], c0, co0, u * KW);
+                        tma_load_3d(sBl(s, i), &tmBl, &raw_full[s], c0, co0, u * KW);
+                    }
+                    if (++s == R) { s = 0; phe ^= 1u; }
+                    c0 += KC;
+                    if (c0 == g.ci) { c0 = 0; ++u; }
                 }
             }
         }
-    } else if (warp == 1) {
-        if (lane == 0) {  // ----------------------------------------- MMA issuer
-            constexpr uint32_t idesc = instr_desc(128, C::NM, 2, 0, 0);  // A (TMEM) x B (K-major)
-            constexpr uint32_t k_sbo = 8 * KC * 4;        // stride between 8-row groups
-            constexpr uint32_t lay = swizzle_layout(C::K_SW);
-            int gi = 0, lt = 0;
-            for (int T = blockIdx.x; T < total; T += gridDim.x, ++lt) {
-                const int acc = lt & 1;
-                mbar_wait(&acc_empty[acc], ((uint32_t)(lt >> 1) & 1u) ^ 1u);
+    } else if (warp == 1) {  // ------------------ MMA issuer (whole warp, one lane issues)
+        constexpr uint32_t idesc = instr_desc(128, C::NM, 2, 0, 0);  // A (TMEM) x B (K-major)
+        constexpr uint32_t k_sbo = 8 * KC * 4;        // stride between 8-row groups
+        constexpr uint32_t lay = swizzle_layout(C::K_SW);
+        int s = 0, o = 0, lt = 0;
+        uint32_t phs = 0, pho = 0;
+        if (g.wres && (int)blockIdx.x < total) mbar_wait(w_full, 0);
+        for (int T = blockIdx.x; T < total; T += gridDim.x, ++lt) {
+            const int acc = lt & 1;
+            mbar_wait(&acc_empty[acc], ((uint32_t)(lt >> 1) & 1u) ^ 1u);
+            tc_fence_after();
+            const uint32_t d = tmem + (uint32_t)(acc * C::NM);
+            for (int i = 0; i < nst; ++i) {
+                mbar_wait(&op_full[o], pho);
+                const int gi_ = lt * nst + i;
+                if (lane == 0 && gi_ < 64) CV_TRACE(8 * gi_ + 4);
                 tc_fence_after();
-                const uint32_t d = tmem + (uint32_t)(acc * C::NM);
-                for (int i = 0; i < nst; ++i, ++gi) {
-                    const int s = gi % R, o = gi % OP;
-                    mbar_wait(&op_full[o], (uint32_t)(gi / OP) & 1u);
-                    tc_fence_after();
+                if (elect_one()) {
                     const uint32_t ah = tmem + a_col(o), al = ah + KC;
-                    const uint32_t bh = smem_u32(sBh(s)), bl = smem_u32(sBl(s));
+                    const uint32_t bh = smem_u32(sBh(s, i)), bl = smem_u32(sBl(s, i));
 #pragma unroll
                     for (int j = 0; j < KC / 8; ++j) {
                         const uint64_t dbh = smem_desc(bh + j * 32, 16, k_sbo, lay);
@@ -192,51 +246,66 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     }
                     mma_commit(&raw_empty[s]);
                     mma_commit(&op_empty[o]);
+                    if (i == nst - 1) mma_commit(&acc_full[acc]);
                 }
-                mma_commit(&acc_full[acc]);
+                __syncwarp();
+                if (lane == 0 && gi_ < 64) CV_TRACE(8 * gi_ + 5);
+                if (++s == R) { s = 0; phs ^= 1u; }
+                if (++o == G) { o = 0; pho ^= 1u; }
             }
         }
-    } else if (warp < 6) {  // ----------------------------- warps 2..5: split -> TMEM
+    } else if (warp < kFwdEpiWarp) {  // ------------ split warpgroups -> TMEM (A operand)
+        const int grp = (warp - 2) >> 2;
         const int quarter = warp & 3;
         const int row = 32 * quarter + lane;          // this thread's TMEM lane = pixel
-        const uint32_t atom = (uint32_t)(row / OWT);
-        const uint32_t px = (uint32_t)(row % OWT);
+        // raw A box: [img][channel][tile pixels of that image], unswizzled
+        const uint32_t tpx = (uint32_t)(g.rows * OWT);
+        const uint32_t aimg = (uint32_t)row / tpx, apx = (uint32_t)row % tpx;
         const uint32_t lane_base = tmem + ((uint32_t)(32 * quarter) << 16);
-        int gi = 0;
-        for (int T = blockIdx.x; T < total; T += gridDim.x) {
-            for (int i = 0; i < nst; ++i, ++gi) {
-                const int s = gi % R, o = gi % OP;
-                mbar_wait(&raw_full[s], (uint32_t)(gi / R) & 1u);
-                mbar_wait(&op_empty[o], ((uint32_t)(gi / OP) & 1u) ^ 1u);
-                tc_fence_after();
-                const uint8_t *raw = sRaw(s);
+        // stages of this CTA: (its tiles) x nst, in MMA order
+        const int my_tiles = (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+        const int nstages = my_tiles * nst;
+        const int o = grp;
+        int gi = grp < G ? grp : nstages;
+        int s = gi % R;
+        uint32_t phr = (uint32_t)(gi / R) & 1u, pho = (uint32_t)(gi / G) & 1u;
+        for (; gi < nstages; gi += G) {
+            mbar_wait(&raw_full[s], phr);
+            if (quarter == 2 && lane == 0 && gi < 64) CV_TRACE(8 * gi + 1);
+            mbar_wait(&op_empty[o], pho ^ 1u);
+            if (quarter == 2 && lane == 0 && gi < 64) CV_TRACE(8 * gi + 2);
+            tc_fence_after();
+            const uint8_t *raw = sRaw(s);
 #pragma unroll
-                for (int cg = 0; cg < KC; cg += 16) {
-                    uint32_t hi[16], lo[16];
+            for (int cg = 0; cg < KC; cg += 16) {
+                uint32_t hi[16], lo[16];
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
-                        const uint32_t off = (atom * KC + cg + j) * (OWT * 4) + px * 4;
-                        const float x = *reinterpret_cast<const float *>(raw + swz_off<C::A_SW>(off));
-                        float h, l;
-                        split_tf32(x, h, l);
-                        hi[j] = __float_as_uint(h);
-                        lo[j] = __float_as_uint(l);
-                    }
-                    tmem_st16(lane_base + a_col(o) + cg, hi);
-                    tmem_st16(lane_base + a_col(o) + KC + cg, lo);
+                for (int j = 0; j < 16; ++j) {
+                    const uint32_t off = ((aimg * KC + cg + j) * tpx + apx) * 4;
+                    const float x = *reinterpret_cast<const float *>(raw + off);
+                    float h, l;
+                    split_tf32(x, h, l);
+                    hi[j] = __float_as_uint(h);
+                    lo[j] = __float_as_uint(l);
                 }
-                tmem_wait_st();
-                tc_fence_before();
-                mbar_arrive(&op_full[o]);
+                tmem_st16(lane_base + a_col(o) + cg, hi);
+                tmem_st16(lane_base + a_col(o) + KC + cg, lo);
             }
+            tmem_wait_st();
+            tc_fence_before();
+            if (quarter == 2 && lane == 0 && gi < 64) CV_TRACE(8 * gi + 3);
+            mbar_arrive(&op_full[o]);
+            s += G;
+            if (s >= R) { s -= R; phr ^= 1u; }    // R is a multiple of G
+            pho ^= 1u;
         }
-    } else {  // ------------------------------------------ warps 6..9: epilogue
+    } else {  // ------------------------------------------------ epilogue warpgroup
         const int quarter = warp & 3;
         const int row = 32 * quarter + lane;
         const int ratom = row / OWT, wcol = row % OWT;
         const int img = ratom / g.rows, rr = ratom % g.rows;
         const size_t cstride = (size_t)g.rows * OWT;
-        const bool leader = (warp == 6 && lane == 0);
+        const bool leader = (warp == kFwdEpiWarp && lane == 0);
         const bool res_ldg = ep.res && !ep.res_tma;
         const int kw_pad = (KW > 1) ? g.pad : 0;
         if (leader && ep.res_tma && (int)blockIdx.x < total) {  // prefetch the first shortcut tile
@@ -253,11 +322,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             float *s_out = out_base + (size_t)ob * (C::OUT_BYTES / 4);
             asm volatile("bar.sync 1, 128;" ::: "memory");   // staging buffer free (see below)
             mbar_wait(&acc_full[acc], (uint32_t)(lt >> 1) & 1u);
+            if (leader && lt < 32) CV_TRACE(600 + 4 * lt);
             tc_fence_after();
             if (ep.res_tma) mbar_wait(&res_full[ob], (uint32_t)((NOUT > 1 ? lt >> 1 : lt)) & 1u);
             const int nn = n0 + img, y = h0 + rr;
             const uint32_t tbase = tmem + ((uint32_t)(32 * quarter) << 16) + (uint32_t)(acc * C::NM);
-            float *so = s_out + ((size_t)img * BN * g.rows + rr) * OWT + wcol;
+            float *so = s_out + (img * BN * g.rows + rr) * OWT + wcol;
             const int64_t hr = (int64_t)g.oh * ep.sr, wr = (int64_t)g.ow * ep.sr;
 #pragma unroll 1
             for (int cb = 0; cb < BN; cb += 16) {
@@ -273,9 +343,20 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     }
                 }
                 uint32_t r[KW][16];
+                // per column tap: source lane and zero-padding mask (branch-free
+                // so the 16 channels' shuffle chains interleave)
+                int src[KW];
+                bool okt[KW];
+#pragma unroll
+                for (int t = 0; t < KW; ++t) {
+                    const int dx = t - kw_pad;
+                    src[t] = (lane + dx) & 31;
+                    okt[t] = (wcol + dx >= 0) && (wcol + dx < OWT);
+                }
 #pragma unroll
                 for (int v = 0; v < KW; ++v) tmem_ld16(tbase + v * BN + cb, r[v]);
                 tmem_wait_ld();
+                if (leader && lt < 32 && cb == 0) CV_TRACE(600 + 4 * lt + 2);
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     float v;
@@ -286,15 +367,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                         v = 0.f;
 #pragma unroll
                         for (int t = 0; t < KW; ++t) {
-                            const int dx = t - kw_pad;
-                            const float d = __uint_as_float(r[t][j]);
-                            const float nb = dx == 0 ? d
-                                             : __shfl_sync(0xffffffffu, d, (lane + dx) & 31);
-                            const int xs = wcol + dx;
-                            v = __fadd_rn(v, (xs >= 0 && xs < OWT) ? nb : 0.f);
+                            const float nb = __shfl_sync(0xffffffffu, __uint_as_float(r[t][j]), src[t]);
+                            v = __fadd_rn(v, okt[t] ? nb : 0.f);
                         }
                     }
-                    float *dst = so + (size_t)(cb + j) * cstride;
+                    float *dst = so + (cb + j) * (int)cstride;
                     // out = fp32(conv); cur += shortcut(res)  (engine.py:262-269)
                     if (ep.res_tma) {
                         if (co0 + cb + j < ep.cr) v = __fadd_rn(v, *dst);
@@ -304,10 +381,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     *dst = v;
                 }
             }
+            if (leader && lt < 32) CV_TRACE(600 + 4 * lt + 3);
             tc_fence_before();
             mbar_arrive(&acc_empty[acc]);            // TMEM buffer free for tile lt+2
             fence_async_smem();
             asm volatile("bar.sync 1, 128;" ::: "memory");
+            if (leader && lt < 32) CV_TRACE(600 + 4 * lt + 1);
             if (leader) {
                 tma_store_4d(&tmOut, s_out, 0, h0, co0, n0);
                 bulk_commit();
@@ -329,6 +408,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     }
     tc_fence_before();
     __syncthreads();
+    if (threadIdx.x == 0) CV_TRACE(1001);
     if (warp == 1) {
         tc_fence_after();
         tmem_dealloc<512>(tmem);
@@ -407,17 +487,20 @@ static CUtensorMapSwizzle swz(int bytes) {
                         : (bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
 }
 
+// activations (n, c, h*w) as 3D (pixel, c, n), box = the tile's pixels of
+// each image (rows*ow <= 128, one contiguous run per channel) x KC x nimg;
+// no swizzle (the split warps read it pixel-per-lane, conflict-free), so
+// a stage is KC*nimg TMA rows of up to 512 B instead of KC*rows 128-B rows
 static bool make_map_act(CUtensorMap *m, const float *x, const FwdGeo &g, int owt, int kc) {
     auto enc = encode_fn();
     if (!enc) return false;
-    cuuint64_t dims[4] = {(cuuint64_t)g.w, (cuuint64_t)g.ci, (cuuint64_t)g.h, (cuuint64_t)g.n};
-    cuuint64_t strides[3] = {(cuuint64_t)g.h * g.w * 4, (cuuint64_t)g.w * 4,
-                             (cuuint64_t)g.ci * g.h * g.w * 4};
-    cuuint32_t box[4] = {(cuuint32_t)owt, (cuuint32_t)kc, (cuuint32_t)g.rows, (cuuint32_t)g.nimg};
-    cuuint32_t es[4] = {1, 1, 1, 1};
-    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void *)x, dims, strides, box, es,
-               CU_TENSOR_MAP_INTERLEAVE_NONE, swz(owt * 4), CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+    cuuint64_t dims[3] = {(cuuint64_t)g.h * g.w, (cuuint64_t)g.ci, (cuuint64_t)g.n};
+    cuuint64_t strides[2] = {(cuuint64_t)g.h * g.w * 4, (cuuint64_t)g.ci * g.h * g.w * 4};
+    cuuint32_t box[3] = {(cuuint32_t)(g.rows * owt), (cuuint32_t)kc, (cuuint32_t)g.nimg};
+    cuuint32_t es[3] = {1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)x, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 // prepared weights [kh*kw][co][ci] as 3D (ci, co, uv); box = KC x BN x KW
@@ -462,19 +545,37 @@ static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, int t
     FwdGeo gg = g;
     gg.mtiles = tiles;
     gg.ntiles = ntiles;
-    // smem plan: output staging x2 when it fits, raw ring >= 2 (up to 8)
-    const int budget = 227 * 1024 - 1024 - 512;
+    // split groups G (operand ring depth) limited by TMEM; smem: output
+    // staging x2 when it fits, raw ring a multiple of G (>= G, up to 8)
+    int G = kFwdGroups;
+    while (G > 1 && C::ACC_COLS + G * C::OP_COLS > 512) G /= 2;
+    if (C::ACC_COLS + G * C::OP_COLS > 512) return QT_EUNSUPPORTED;
+    const int total = tiles * ntiles;
+    // resident weights: every CTA keeps one co tile (grid a multiple of
+    // ntiles) and its nst stages' (hi, lo) tiles fit next to the rings
+    const int nst = g.kh * (g.ci / KC);
+    const int wbytes = nst * 2 * C::B_SLOT;
+    int grid = std::min(total, num_sms());
+    gg.wres = 0;
+    if (ntiles <= num_sms() && wbytes <= 96 * 1024) {
+        gg.wres = 1;
+        grid = std::max(ntiles, std::min(total, num_sms()) / ntiles * ntiles);
+    }
+    gg.slot = gg.wres ? (C::A_BYTES + 1023) / 1024 * 1024 : C::RAW_BYTES;
+    gg.ntd = make_fastdiv((uint32_t)ntiles);
+    gg.tpid = make_fastdiv((uint32_t)std::max(1, g.tiles_per_img));
+    const int budget = 227 * 1024 - 1024 - 512 - (gg.wres ? wbytes : 0);
+    auto raw_fit = [&](int no) { return (budget - no * C::OUT_BYTES) / gg.slot; };
     int nout = 2;
-    auto raw_fit = [&](int no) { return (budget - no * C::OUT_BYTES) / C::RAW_BYTES; };
-    if (raw_fit(nout) < 2) nout = 1;
+    while (G > 1 && raw_fit(1) < G) G /= 2;
+    if (raw_fit(nout) < G) nout = 1;
     int r = raw_fit(nout);
-    if (r < 2) return QT_EUNSUPPORTED;
-    r = std::min(r, 8);
+    if (r < G || r < 1) return QT_EUNSUPPORTED;
+    r = std::min(r, 8) / G * G;
     gg.R = r;
     gg.NOUT = nout;
-    const int smem = r * C::RAW_BYTES + nout * C::OUT_BYTES + 1024 + 512;
-    const int total = tiles * ntiles;
-    const int grid = std::min(total, num_sms());
+    gg.G = G;
+    const int smem = r * gg.slot + nout * C::OUT_BYTES + (gg.wres ? wbytes : 0) + 1024 + 512;
     kern<<<grid, kFwdThreads, smem, st>>>(m.a, m.bh, m.bl, m.out, m.res, gg, ep);
     QT_CHECK_LAUNCH();
     return QT_OK;
@@ -614,6 +715,14 @@ extern "C" int qt_conv_uses_tc(int64_t n, int64_t ci, int64_t h, int64_t wd, int
     const int64_t oh = h + 2 * pad - kh + 1, ow = wd + 2 * pad - kw + 1;
     return tc_shape_ok((int)n, (int)co, (int)oh, (int)ow, (int)ci, (int)kh, (int)kw,
                        (int)(kh - 1 - pad)) ? 1 : 0;
+}
+
+// debug hook (not part of the public ABI): buf = 1002 int64 stamps or NULL
+extern "C" int qt_debug_conv_trace(void *buf, int cta) {
+    long long *b = (long long *)buf;
+    if (cudaMemcpyToSymbol(g_cv_trace, &b, sizeof(b)) != cudaSuccess) return QT_EINVAL;
+    if (cudaMemcpyToSymbol(g_cv_trace_cta, &cta, sizeof(cta)) != cudaSuccess) return QT_EINVAL;
+    return QT_OK;
 }
 
 extern "C" int qt_conv_prepare_weights(const qt_wprep_t *descs, int64_t count, int64_t max_elems,
