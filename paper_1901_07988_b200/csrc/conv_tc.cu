@@ -235,14 +235,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 tc_fence_after();
                 if (elect_one()) {
                     const uint32_t ah = tmem + a_col(o), al = ah + KC;
-                    const uint32_t bh = smem_u32(sBh(s, i)), bl = smem_u32(sBl(s, i));
+                    // descriptor = base + (byte offset >> 4) (tiles below 256 KiB)
+                    const uint64_t dbh = smem_desc(smem_u32(sBh(s, i)), 16, k_sbo, lay);
+                    const uint64_t dbl = smem_desc(smem_u32(sBl(s, i)), 16, k_sbo, lay);
 #pragma unroll
                     for (int j = 0; j < KC / 8; ++j) {
-                        const uint64_t dbh = smem_desc(bh + j * 32, 16, k_sbo, lay);
-                        const uint64_t dbl = smem_desc(bl + j * 32, 16, k_sbo, lay);
-                        mma_tf32_ts(d, ah + j * 8, dbh, idesc, (i | j) ? 1u : 0u);
-                        mma_tf32_ts(d, ah + j * 8, dbl, idesc, 1u);
-                        mma_tf32_ts(d, al + j * 8, dbh, idesc, 1u);
+                        mma_tf32_ts(d, ah + j * 8, dbh + j * 2, idesc, (i | j) ? 1u : 0u);
+                        mma_tf32_ts(d, ah + j * 8, dbl + j * 2, idesc, 1u);
+                        mma_tf32_ts(d, al + j * 8, dbh + j * 2, idesc, 1u);
                     }
                     mma_commit(&raw_empty[s]);
                     mma_commit(&op_empty[o]);

@@ -80,6 +80,7 @@ struct WgParams {
     int cbytes;              // code box bytes per stage (cb x channels)
     int rb;                  // packed bytes per input row (ow*bits/8)
     int dbg_nocodes;         // debug timing experiment: skip the code box loads
+    FastDiv cpid;            // / chunks_per_img
 };
 
 // value of act at (nn, c, y, x) for fp32 sources (zero padding outside)
@@ -141,11 +142,15 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     constexpr bool STACK = 3 * BN <= 192;                   // one N = 3*BN MMA per K step
     constexpr int FACC = STACK ? 3 * BN : BN;               // FAST accumulator columns per tile
     constexpr int SUB = kWgSub;                             // 32-px chunks per pipeline stage
-    extern __shared__ uint8_t smem_raw[];
-    uint8_t *smem = (uint8_t *)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // 1 KiB alignment by pointer arithmetic on the __shared__ array (keeps
+    // every access in the shared window: LDS/STS, not generic LD/ST)
+    uint8_t *smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int RG = p.RG;
-    uint8_t *graw = smem;                                   // RG x SUB x slot (g tile, code box)
-    uint8_t *gop = graw + RG * SUB * p.slot;                // OPS x SUB x 2*G_BYTES operands
+    // raw ring stage: g box [co][sub][32 px] (SW128 rows of 128 B), then the
+    // code box [channel][cb bytes] covering the stage's SUB chunks
+    uint8_t *graw = smem;                                   // RG x slot
+    uint8_t *gop = graw + RG * p.slot;                      // OPS x SUB x 2*G_BYTES operands
     float *s_lut = (float *)(gop + p.OPS * SUB * 2 * G_BYTES);   // GENERIC code table (hi, lo)
     uint32_t *s_bc = (uint32_t *)(s_lut + p.lut_floats);    // FAST: 0x4300 + b per channel
     uint64_t *bars = (uint64_t *)(s_bc + kWgMaxCh);
@@ -225,44 +230,53 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 
     if (warp == 0) {
         if (lane == 0) {  // ----------------------------- TMA producer (g_out + codes)
+            // one g box and one code box per stage: its SUB chunks are
+            // consecutive pixel runs of one image (cps, cpi multiples of SUB)
             int nn = k0 / p.chunks_per_img, yc = k0 % p.chunks_per_img;
             int s = 0;
             uint32_t ph = 0;
             for (int st = 0; st < nst; ++st) {
                 mbar_wait(&raw_empty[s], ph ^ 1u);
                 if (st < 64) WG_TRACE(2 + 5 * st);
-                const int nsub = min(SUB, nk - st * SUB);
-                mbar_expect_tx(&raw_full[s], nsub * (G_BYTES + (p.dbg_nocodes ? 0 : p.cbytes)));
-                if (st < 64) WG_TRACE(334 + 3 * st);
-                for (int sub = 0; sub < nsub; ++sub) {
-                    const int y0 = yc * p.rows_per_chunk;
-                    uint8_t *slot = graw + (s * SUB + sub) * p.slot;
-                    tma_load_3d(slot, &tmG, &raw_full[s], y0 * p.ow, 0, nn);
-                    if (st < 64 && sub == 0) WG_TRACE(335 + 3 * st);
-                    if (p.lut && !p.dbg_nocodes)   // 16-byte aligned window of input rows y0-pad ..
-                        tma_load_3d(slot + G_BYTES, &tmC, &raw_full[s], ((y0 - p.pad) * p.rb) & ~15,
-                                    c_begin, nn);
-                    if (++yc == p.chunks_per_img) { yc = 0; ++nn; }
-                }
+                const int y0 = yc * p.rows_per_chunk;
+                uint8_t *slot = graw + s * p.slot;
+                mbar_expect_tx(&raw_full[s], SUB * G_BYTES + (p.dbg_nocodes ? 0 : p.cbytes));
+                tma_load_4d(slot, &tmG, &raw_full[s], 0, yc, 0, nn);
+                if (p.lut && !p.dbg_nocodes)   // 16-byte aligned window of input rows y0-pad ..
+                    tma_load_3d(slot + SUB * G_BYTES, &tmC, &raw_full[s],
+                                ((y0 - p.pad) * p.rb) & ~15, c_begin, nn);
+                yc += SUB;
+                if (yc >= p.chunks_per_img) { yc -= p.chunks_per_img; ++nn; }
                 if (st < 64) WG_TRACE(336 + 3 * st);
                 if (++s == RG) { s = 0; ph ^= 1u; }
             }
         }
     } else if (warp == 1) {  // ---------------- MMA issuer (whole warp, one lane issues)
+        // descriptors are a fixed base plus (byte offset >> 4) in the start
+        // address field (all operand tiles lie below 256 KiB); the loops are
+        // unrolled over the compile-time maxima with predicates, so an MMA
+        // costs a couple of uniform adds
         int o = 0;
         uint32_t ph = 0;
         const uint32_t gop_base = smem_u32(gop);
+        const uint64_t dfast = smem_desc(gop_base, 16, 512, 4);    // bf16 SW64 K-major
+        const uint64_t dgen = smem_desc(gop_base, 16, 1024, 2);    // tf32 SW128 K-major
+        const uint32_t mtg = (uint32_t)p.mtg;
         for (int st = 0; st < nst; ++st) {
             mbar_wait(&op_full[o], ph);
             if (lane == 0 && st < 64) WG_TRACE(6 + 5 * st);
             tc_fence_after();
             const int nsub = min(SUB, nk - st * SUB);
             if (elect_one()) {
-                for (int t = 0; t < mt_here; ++t) {
-                    for (int sub = 0; sub < nsub; ++sub) {
-                        const uint32_t gb = gop_base + (uint32_t)((o * SUB + sub) * 2 * G_BYTES);
+#pragma unroll
+                for (int t = 0; t < 2; ++t) {
+                    if (t >= mt_here) break;
+#pragma unroll
+                    for (int sub = 0; sub < SUB; ++sub) {
+                        if (sub >= nsub) break;
+                        const uint32_t off16 = (uint32_t)(((o * SUB + sub) * 2 * G_BYTES) >> 4);
                         const uint32_t a =
-                            tmem + acc_cols + (uint32_t)((o * p.mtg + t) * SUB + sub) * acols;
+                            tmem + acc_cols + (((uint32_t)o * mtg + t) * SUB + sub) * acols;
                         const uint32_t first = (st | sub) ? 1u : 0u;   // 0: zero-init D
                         if (fast) {
                             constexpr uint32_t idesc = instr_desc(128, FACC, 1, 0, 0);
@@ -270,13 +284,13 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 #pragma unroll
                             for (int j = 0; j < 2; ++j) {
                                 if (STACK) {
-                                    mma_bf16_ts(d, a + j * 8, smem_desc(gb + j * 32, 16, 512, 4),
-                                                idesc, (first | j) ? 1u : 0u);
+                                    mma_bf16_ts(d, a + j * 8, dfast + off16 + j * 2, idesc,
+                                                (first | j) ? 1u : 0u);
                                 } else {
 #pragma unroll
                                     for (int pc = 0; pc < 3; ++pc)
                                         mma_bf16_ts(d, a + j * 8,
-                                                    smem_desc(gb + pc * BN * 64 + j * 32, 16, 512, 4),
+                                                    dfast + off16 + ((pc * BN * 64) >> 4) + j * 2,
                                                     idesc, (first | j | pc) ? 1u : 0u);
                                 }
                             }
@@ -285,8 +299,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                             const uint32_t d = tmem + (uint32_t)(t * BN);
 #pragma unroll
                             for (int j = 0; j < 4; ++j) {
-                                const uint64_t dgh = smem_desc(gb + j * 32, 16, 1024, 2);
-                                const uint64_t dgl = smem_desc(gb + G_BYTES + j * 32, 16, 1024, 2);
+                                const uint64_t dgh = dgen + off16 + j * 2;
+                                const uint64_t dgl = dgh + (G_BYTES >> 4);
                                 mma_tf32_ts(d, a + j * 8, dgh, idesc, (first | j) ? 1u : 0u);
                                 mma_tf32_ts(d, a + j * 8, dgl, idesc, 1u);
                                 mma_tf32_ts(d, a + 32 + j * 8, dgh, idesc, 1u);
@@ -332,23 +346,25 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             if (tg == 0 && st < 64) WG_TRACE(4 + 5 * st);
             tc_fence_after();
             const int nsub = min(SUB, nk - st * SUB);
+            const int kc0 = k0 + st * SUB;                            // first chunk of the stage
+            const int nn = (int)fast_div((uint32_t)kc0, p.cpid);
+            const int ys = (kc0 - nn * p.chunks_per_img) * p.rows_per_chunk;
+            const uint8_t *graws = graw + s * p.slot;
+            const uint8_t *cst = graws + SUB * G_BYTES;               // code box
+            const int wbase = ((ys - p.pad) * p.rb) & ~15;            // its first byte
             for (int sub = 0; sub < nsub; ++sub) {
-            const int kc = k0 + st * SUB + sub;
-            const int nn = kc / p.chunks_per_img;
-            const int y0 = (kc - nn * p.chunks_per_img) * p.rows_per_chunk;
-            const uint8_t *raw = graw + (s * SUB + sub) * p.slot;
+            const int y0 = ys + sub * p.rows_per_chunk;
             uint8_t *opb = gop + (o * SUB + sub) * 2 * G_BYTES;
-            const uint8_t *cst = raw + G_BYTES;                       // code box
-            const int wbase = ((y0 - p.pad) * p.rb) & ~15;            // its first byte
             if (fast) {
                 // g -> bf16 (hi, mid, lo), K-major SW64, 8-pixel groups
                 // permuted (pair word k = pixels k and k+4)
                 for (int q = tg; q < BN * 4; q += 128) {
                     const int co = q >> 2, qq = q & 3;
+                    const uint32_t rrow = (uint32_t)((co * SUB + sub) * 128);
                     const float4 x0 = *reinterpret_cast<const float4 *>(
-                        raw + swz_off<128>((uint32_t)(co * 128 + qq * 32)));
+                        graws + swz_off<128>(rrow + qq * 32));
                     const float4 x1 = *reinterpret_cast<const float4 *>(
-                        raw + swz_off<128>((uint32_t)(co * 128 + qq * 32 + 16)));
+                        graws + swz_off<128>(rrow + qq * 32 + 16));
                     const float xa[4] = {x0.x, x0.y, x0.z, x0.w}, xb[4] = {x1.x, x1.y, x1.z, x1.w};
                     uint32_t H[4], M[4], L[4];
 #pragma unroll
@@ -364,19 +380,21 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     *reinterpret_cast<uint4 *>(opb + BN * 64 + off) = make_uint4(M[0], M[1], M[2], M[3]);
                     *reinterpret_cast<uint4 *>(opb + 2 * BN * 64 + off) = make_uint4(L[0], L[1], L[2], L[3]);
                 }
-            } else {   // g tile: TF32 (hi, lo) split (layout preserving SW128)
-                const float4 *src = reinterpret_cast<const float4 *>(raw);
-                float4 *gh = reinterpret_cast<float4 *>(opb);
-                float4 *gl = gh + G_BYTES / 16;
+                if (tg == 0 && st < 64) WG_TRACE(3700 + 4 * st + 2 * sub);
+            } else {   // g tile: TF32 (hi, lo) split into a K-major SW128 tile
                 for (int q = tg; q < G_BYTES / 16; q += 128) {
-                    const float4 x = src[q];
+                    const int co = q >> 3, ch16 = q & 7;
+                    const float4 x = *reinterpret_cast<const float4 *>(
+                        graws + swz_off<128>((uint32_t)((co * SUB + sub) * 128 + ch16 * 16)));
+                    float4 *gh = reinterpret_cast<float4 *>(opb + swz_off<128>((uint32_t)(co * 128 + ch16 * 16)));
+                    float4 *gl = reinterpret_cast<float4 *>(reinterpret_cast<uint8_t *>(gh) + G_BYTES);
                     float4 hi, lo;
                     split_tf32(x.x, hi.x, lo.x);
                     split_tf32(x.y, hi.y, lo.y);
                     split_tf32(x.z, hi.z, lo.z);
                     split_tf32(x.w, hi.w, lo.w);
-                    gh[q] = hi;
-                    gl[q] = lo;
+                    *gh = hi;
+                    *gl = lo;
                 }
             }
 #pragma unroll
@@ -417,6 +435,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                             if (sh > 0) av[seg * (OW / 2) + OW / 2 - 1] &= 0x0000FFFFu;  // x = OW-1
                         }
                     }
+                    if (tg == 0 && st < 64 && t == 0) WG_TRACE(3701 + 4 * st + 2 * sub);
                     tmem_st16(lane_base + acol, av);
                 } else {
                     const float *lut = s_lut + (size_t)(c - c_begin) * lut_stride;
@@ -553,6 +572,7 @@ static WgPlan wg_plan(const ConvGeo &g, int bits) {
     if (ow != 8 && ow != 16 && ow != 32) return pl;
     if (g.w != ow) return pl;                    // same-width rows (stride 1, "same" padding)
     if ((oh * ow) % 32 || oh % (32 / ow)) return pl;
+    if ((oh * ow / 32) % kWgSub) return pl;           // SUB chunks per stage within one image
     if (g.co % 16 || g.co > 256 || !(g.kw == 1 || g.kw == 3) || g.pad > 1) return pl;
     if (g.kw == 1 && g.pad != 0) return pl;
     if (g.kh != g.kw) return pl;
@@ -582,17 +602,17 @@ static WgPlan wg_plan(const ConvGeo &g, int bits) {
         const int kk = (int)(g.kh * g.kw);
         pl.nch = (int)std::min<int64_t>(g.ci, (mtg * 128 + kk - 1) / kk + (kk > 1 ? 1 : 0));
         pl.rb = (int)(ow * bits / 8);
-        pl.cb = (((int)(32 / ow) + 2 * (int)g.pad) * pl.rb + 15 + 15) & ~15;
+        pl.cb = (((int)(32 / ow) * SUB + 2 * (int)g.pad) * pl.rb + 15 + 15) & ~15;
         if (pl.cb > 256 || pl.nch > kWgMaxCh) return WgPlan{};
         if (pl.nch * (1 << bits) > kWgLutEntries) return WgPlan{};
         pl.cbytes = pl.cb * pl.nch;
         pl.lut_floats = 2 * pl.nch * (1 << bits);
-        gbytes = (gbytes0 + pl.cbytes + 1023) & ~1023;
     }
+    gbytes = (SUB * gbytes0 + pl.cbytes + 1023) & ~1023;    // one raw stage
     pl.slot = gbytes;
     const int fixed = pl.lut_floats * 4 + kWgMaxCh * 4 + 1024 + 512;
     const int budget = 227 * 1024 - fixed;
-    const int sraw = SUB * gbytes, sop = SUB * 2 * gbytes0;   // bytes per raw / operand stage
+    const int sraw = gbytes, sop = SUB * 2 * gbytes0;         // bytes per raw / operand stage
     while (pl.ops > 1 && pl.ops * (sraw + sop) > budget) pl.ops /= 2;
     if (pl.ops * (sraw + sop) > budget) return WgPlan{};
     pl.ops_g = pl.ops;
@@ -609,6 +629,7 @@ static WgPlan wg_plan(const ConvGeo &g, int bits) {
     want = std::min(want, std::max(1, pl.total / (kWgGroups * SUB)));
     want = std::min(want, std::max(1, (int)(16.0 * pl.total / (double)R)));
     pl.cps = std::max(1, (pl.total + want - 1) / want);
+    pl.cps = (pl.cps + SUB - 1) / SUB * SUB;          // stages never straddle splits or images
     pl.splits = (pl.total + pl.cps - 1) / pl.cps;
     pl.ok = true;
     return pl;
@@ -698,11 +719,12 @@ int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float
     // swizzle span is padded per row by TMA, so rows of 8/16 px cannot be
     // stacked into one swizzle row.)
     CUtensorMap m;
-    cuuint64_t dims[3] = {(cuuint64_t)(g.oh * g.ow), (cuuint64_t)g.co, (cuuint64_t)g.n};
-    cuuint64_t strides[2] = {(cuuint64_t)g.oh * g.ow * 4, (cuuint64_t)g.co * g.oh * g.ow * 4};
-    cuuint32_t box[3] = {32, (cuuint32_t)pl.bn, 1};
-    cuuint32_t es[3] = {1, 1, 1};
-    if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)gr, dims, strides, box, es,
+    // 4D (32 px, chunk, c, n): one box = SUB consecutive chunks x BN channels
+    cuuint64_t dims[4] = {32, (cuuint64_t)(g.oh * g.ow / 32), (cuuint64_t)g.co, (cuuint64_t)g.n};
+    cuuint64_t strides[3] = {128, (cuuint64_t)g.oh * g.ow * 4, (cuuint64_t)g.co * g.oh * g.ow * 4};
+    cuuint32_t box[4] = {32, (cuuint32_t)kWgSub, (cuuint32_t)pl.bn, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void *)gr, dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return QT_EUNSUPPORTED;
@@ -712,7 +734,7 @@ int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float
         cuuint64_t cd[3] = {(cuuint64_t)plane, (cuuint64_t)g.ci, (cuuint64_t)g.n};
         cuuint64_t cs[2] = {(cuuint64_t)plane, (cuuint64_t)(plane * g.ci)};
         cuuint32_t cbx[3] = {(cuuint32_t)pl.cb, (cuuint32_t)pl.nch, 1};
-        if (enc(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void *)act.codes, cd, cs, cbx, es,
+        if (enc(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void *)act.codes, cd, cs, cbx, es + 1,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return QT_EUNSUPPORTED;
@@ -727,6 +749,7 @@ int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float
     p.mtg = pl.mtg;
     p.rows_per_chunk = (int)(32 / g.ow);
     p.chunks_per_img = (int)(g.oh * g.ow / 32);
+    p.cpid = make_fastdiv((uint32_t)p.chunks_per_img);
     p.total_chunks = pl.total;
     p.chunks_per_split = pl.cps;
     p.splits = pl.splits;

@@ -22,7 +22,7 @@ run = lambda: ops.conv2d_wgrad(gout, (co, ci, k, k), 1, pad, gw, tape=tape, in_s
 run()
 torch.cuda.synchronize()
 for cta in (0,):
-    buf = torch.zeros(600 + 3 * 1024, dtype=torch.int64, device=dev)
+    buf = torch.zeros(4000, dtype=torch.int64, device=dev)
     fn(buf.data_ptr(), cta)
     run()
     torch.cuda.synchronize()
@@ -31,12 +31,12 @@ for cta in (0,):
     t0 = b[0]
     print(f"CTA {cta}: globaltimer start {b[332]} end {b[333]} dur {(b[333]-b[332])/1e3:.2f} us;"
           f" fast {b[525]} setup {b[1]-t0} cyc, epi start {b[330]-t0}, end {b[331]-t0}")
-    print("  i  prod  opraw  opempty  p_exptx  p_tma0  p_end  opdone  mma  lastwarp_done  mma_committed")
+    print("  i  prod  opraw  opempty  split0  dec0  split1  dec1  opdone  mma  lastwarp_done  mma_committed")
     for i in range(64):
         r = b[2 + 5 * i: 7 + 5 * i]
         if not any(r):
             break
-        r = r[:3] + b[334 + 3 * i: 337 + 3 * i] + r[3:] + b[400 + 2 * i: 402 + 2 * i]
+        r = r[:3] + b[3700 + 4 * i: 3704 + 4 * i] + r[3:] + b[400 + 2 * i: 402 + 2 * i]
         print(f"{i:3d} " + " ".join(f"{(v - t0) if v else -1:7d}" for v in r))
 
     import collections
