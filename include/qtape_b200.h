@@ -182,13 +182,21 @@ typedef struct {
 int qt_conv_prepare_weights(const qt_wprep_t *descs, int64_t count, int64_t max_elems,
                             qt_stream_t stream);
 
-/* Scratch for qt_conv_forward / qt_conv_dgrad: the tensor-core path keeps the
+/* Scratch for qt_conv_forward / qt_conv_dgrad: size it with
+ * qt_conv_workspace_ex (below), which covers every path; qt_conv_workspace
+ * alone covers the weight operand only.  The tensor-core path keeps the
  * (hi, lo) TF32 split of the re-laid-out kernel there (2*ci*co*kh*kw floats).
  * The tensor-core path serves stride-1 convs whose output rows are 8, 16 or
  * 32 pixels wide with ci % 8 == 0 and co % 16 == 0 (every CIFAR ResNet conv
  * except the stem and the 2x2/s2 transitions); other shapes run on the
  * CUDA-core implicit GEMM.  QTAPE_NO_TC=1 forces the CUDA-core path. */
 int64_t qt_conv_workspace(int64_t ci, int64_t co, int64_t kh, int64_t kw);
+/* Full scratch for qt_conv_forward / qt_conv_dgrad of one shape (>= the
+ * above): non-overlapping convs (kernel == stride, pad 0, e.g. the 2x2/s2
+ * transitions) run as tensor-core 1x1 convs of the space-to-depth tensor,
+ * which lives in this workspace after the weight operand. */
+int64_t qt_conv_workspace_ex(int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co,
+                             int64_t kh, int64_t kw, int64_t stride, int64_t pad);
 /* 1 if qt_conv_forward (dgrad = 0) / qt_conv_dgrad (dgrad = 1) of this shape
  * runs on the tensor cores, 0 if on the CUDA cores (host-side query). */
 int qt_conv_uses_tc(int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co, int64_t kh,

@@ -58,6 +58,7 @@ SIGNATURES = {
                               P, I64, I64, P, P]),
     "qt_conv_dgrad": (I32, [P, P, P, I64, I64, I64, I64, I64, I64, I64, I64, I64, P, P]),
     "qt_conv_workspace": (I64, [I64, I64, I64, I64]),
+    "qt_conv_workspace_ex": (I64, [I64] * 9),
     "qt_conv_prepare_weights": (I32, [P, I64, I64, P]),
     "qt_conv_uses_tc": (I32, [I64] * 9 + [I32]),
     "qt_conv_wgrad_workspace": (I64, [I64] * 9),

@@ -309,8 +309,25 @@ int qt_tc_conv_dgrad(const float *gr, const float *w, float *gx, const qt::ConvG
 int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
                      const qt::ConvGeo &g, void *ws, cudaStream_t st);
 int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g);
+int64_t qt_tc_s2d_workspace(const qt::ConvGeo &g);
+int qt_tc_conv_s2d_forward(const float *x, const float *w, float *out, const qt::ConvGeo &g,
+                           const float *res, int64_t cr, int64_t sr, void *ws, cudaStream_t s);
+int qt_tc_conv_s2d_dgrad(const float *gr, const float *w, float *gx, const qt::ConvGeo &g,
+                         void *ws, cudaStream_t s);
 int qt_tc_wgrad_reduce(const float *partial, int64_t splits, int64_t count, float *grad_w,
                        cudaStream_t st);
+
+static inline bool ws_bytes_ok(void *ws) { return ws != nullptr; }
+
+// Full scratch need of qt_conv_forward / qt_conv_dgrad for this shape: the
+// prepared weight operand, plus the space-to-depth buffer for kernel == stride
+extern "C" int64_t qt_conv_workspace_ex(int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co,
+                                        int64_t kh, int64_t kw, int64_t stride, int64_t pad) {
+    ConvGeo g = make_geo(n, ci, h, wd, co, kh, kw, stride, pad);
+    int64_t need = qt_conv_workspace(ci, co, kh, kw);
+    if (geo_ok(g)) need = std::max(need, qt_tc_s2d_workspace(g));
+    return need;
+}
 
 extern "C" int qt_conv_forward(const float *x, const float *w, float *out, int64_t n, int64_t ci,
                                int64_t h, int64_t wd, int64_t co, int64_t kh, int64_t kw,
@@ -321,7 +338,11 @@ extern "C" int qt_conv_forward(const float *x, const float *w, float *out, int64
     QT_REQUIRE(!res || (cr > 0 && cr <= co && sr >= 1));
     int rc = qt_tc_conv_forward(x, w, out, g, res, cr, sr, ws, qt_s(stream));
     if (rc != QT_EUNSUPPORTED) return rc;
-    QT_REQUIRE(w);   // NULL (prepared operand in ws) is only valid on the tensor-core path
+    QT_REQUIRE(w);
+    if (ws_bytes_ok(ws)) {   // kernel == stride: space-to-depth + tensor-core 1x1
+        rc = qt_tc_conv_s2d_forward(x, w, out, g, res, cr, sr, ws, qt_s(stream));
+        if (rc != QT_EUNSUPPORTED) return rc;
+    }   // NULL (prepared operand in ws) is only valid on the tensor-core path
     FwdA la{x, g};
     FwdB lb{w, ci * kh * kw};
     StoreNCHW ep{out, g.oh * g.ow, co, g.ow, res, cr, sr};
@@ -337,6 +358,10 @@ extern "C" int qt_conv_dgrad(const float *gr, const float *w, float *gx, int64_t
     int rc = qt_tc_conv_dgrad(gr, w, gx, g, ws, qt_s(stream));
     if (rc != QT_EUNSUPPORTED) return rc;
     QT_REQUIRE(w);
+    if (ws_bytes_ok(ws)) {
+        rc = qt_tc_conv_s2d_dgrad(gr, w, gx, g, ws, qt_s(stream));
+        if (rc != QT_EUNSUPPORTED) return rc;
+    }
     DgradA la{gr, g};
     DgradB lb{w, g};
     StoreNCHW ep{gx, h * wd, ci, wd, nullptr, 0, 1};

@@ -757,3 +757,85 @@ int qt_tc_conv_dgrad(const float *gr, const float *w, float *gx, const qt::ConvG
     return tc_conv_s1(gr, w, gx, (int)g.n, (int)g.co, (int)g.oh, (int)g.ow, (int)g.ci, (int)g.kh,
                       (int)g.kw, pad2, 1, nullptr, 0, 1, ws, s);
 }
+
+// ---------------------------------------------------------------------------
+// Non-overlapping convs (kernel == stride, no padding: the 2x2/s2 transition
+// convs of SURVEY.md Appendix C) are 1x1 convs of the space-to-depth input:
+//   x'[n][(c*s + u)*s + v][y][x] = x[n][c][y*s + u][x*s + v]
+// with the kernel viewed as (co, ci*s*s) -- the same memory.  Forward: s2d
+// into the workspace, then the tensor-core 1x1 path; data gradient: the 1x1
+// data gradient into the workspace, then depth-to-space.
+namespace qt {
+
+template <bool TO_DEPTH>
+__global__ void space_depth_kernel(const float *src, float *dst, int64_t n, int64_t c, int64_t h,
+                                   int64_t w, int s) {
+    // iterate over the full-resolution tensor in memory order (coalesced side)
+    const int64_t total = n * c * h * w;
+    const int64_t hs = h / s, ws = w / s;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < total;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t xx = i % w, t1 = i / w, yy = t1 % h, t2 = t1 / h, cc = t2 % c, nn = t2 / c;
+        const int64_t u = yy % s, v = xx % s;
+        const int64_t j = (((nn * c + cc) * s + u) * s + v) * hs * ws + (yy / s) * ws + xx / s;
+        if (TO_DEPTH)
+            dst[j] = src[i];
+        else
+            dst[i] = src[j];
+    }
+}
+
+static int space_depth(const float *src, float *dst, int64_t n, int64_t c, int64_t h, int64_t w,
+                       int s, bool to_depth, cudaStream_t st) {
+    const int64_t total = n * c * h * w;
+    const unsigned blocks = (unsigned)std::min<int64_t>(qt_cdiv(total, 256), 148 * 16);
+    if (to_depth)
+        space_depth_kernel<true><<<blocks, 256, 0, st>>>(src, dst, n, c, h, w, s);
+    else
+        space_depth_kernel<false><<<blocks, 256, 0, st>>>(src, dst, n, c, h, w, s);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+static bool s2d_shape(const ConvGeo &g) {
+    return g.s > 1 && g.kh == g.s && g.kw == g.s && g.pad == 0 && g.h % g.s == 0 && g.w % g.s == 0;
+}
+
+}  // namespace qt
+
+static int64_t s2d_weights_bytes(const qt::ConvGeo &g) {
+    return (qt_conv_workspace(g.ci * g.kh * g.kw, g.co, 1, 1) + 255) / 256 * 256;
+}
+
+int64_t qt_tc_s2d_workspace(const qt::ConvGeo &g) {
+    if (!s2d_shape(g)) return 0;
+    return s2d_weights_bytes(g) + g.n * g.ci * g.h * g.w * (int64_t)sizeof(float);
+}
+
+// 1 if the s2d form of this non-overlapping conv runs on the tensor cores
+int qt_tc_s2d_ok(const qt::ConvGeo &g, int dgrad) {
+    if (tc_disabled() || !s2d_shape(g)) return 0;
+    const int64_t c4 = g.ci * g.kh * g.kw, h2 = g.h / g.s, w2 = g.w / g.s;
+    if (!dgrad) return tc_shape_ok((int)g.n, (int)c4, (int)h2, (int)w2, (int)g.co, 1, 1, 0) ? 1 : 0;
+    return tc_shape_ok((int)g.n, (int)g.co, (int)h2, (int)w2, (int)c4, 1, 1, 0) ? 1 : 0;
+}
+
+int qt_tc_conv_s2d_forward(const float *x, const float *w, float *out, const qt::ConvGeo &g,
+                           const float *res, int64_t cr, int64_t sr, void *ws, cudaStream_t s) {
+    if (!ws || !w || !qt_tc_s2d_ok(g, 0)) return QT_EUNSUPPORTED;
+    float *xd = (float *)((char *)ws + s2d_weights_bytes(g));
+    int rc = space_depth(x, xd, g.n, g.ci, g.h, g.w, (int)g.s, true, s);
+    if (rc) return rc;
+    return tc_conv_s1(xd, w, out, (int)g.n, (int)(g.ci * g.kh * g.kw), (int)g.oh, (int)g.ow,
+                      (int)g.co, 1, 1, 0, 0, res, (int)cr, (int)sr, ws, s);
+}
+
+int qt_tc_conv_s2d_dgrad(const float *gr, const float *w, float *gx, const qt::ConvGeo &g,
+                         void *ws, cudaStream_t s) {
+    if (!ws || !w || !qt_tc_s2d_ok(g, 1)) return QT_EUNSUPPORTED;
+    float *gd = (float *)((char *)ws + s2d_weights_bytes(g));
+    int rc = tc_conv_s1(gr, w, gd, (int)g.n, (int)g.co, (int)g.oh, (int)g.ow,
+                        (int)(g.ci * g.kh * g.kw), 1, 1, 0, 1, nullptr, 0, 1, ws, s);
+    if (rc) return rc;
+    return space_depth(gd, gx, g.n, g.ci, g.h, g.w, (int)g.s, false, s);
+}

@@ -106,9 +106,13 @@ def conv2d_out_shape(in_shape: tuple, k_shape: tuple, stride: int, pad: int) -> 
     return n, co, oh, ow
 
 
-def _conv_ws(k, ws):
+def _conv_ws(k, ws, in_shape=None, stride=1, pad=0):
     co, ci, kh, kw = k.shape
-    need = N.query("qt_conv_workspace", ci, co, kh, kw)
+    if in_shape is not None:
+        n, _, h, w = in_shape
+        need = N.query("qt_conv_workspace_ex", n, ci, h, w, co, kh, kw, stride, pad)
+    else:
+        need = N.query("qt_conv_workspace", ci, co, kh, kw)
     if ws is None or ws.numel() < need:
         ws = workspace(need, k.device, "conv")
     return ws
@@ -135,7 +139,8 @@ def conv2d_forward(x: torch.Tensor, k: torch.Tensor, stride: int = 1, pad: int =
     if residual is not None:
         cr = residual.shape[1]
         sr = residual.shape[2] // oh
-    wp, wsp = (None, prepared) if prepared is not None else (k, _conv_ws(k, ws))
+    wp, wsp = (None, prepared) if prepared is not None else \
+        (k, _conv_ws(k, ws, tuple(x.shape), stride, pad))
     N.call("qt_conv_forward", N.ptr(x), N.ptr(wp), N.ptr(out), n, ci, x.shape[2], x.shape[3], co,
            kh, kw, stride, pad, N.ptr(residual), cr, sr, N.ptr(wsp))
     _check_finite(out)
@@ -173,7 +178,8 @@ def conv2d_wgrad(g_out, k_shape, stride, pad, grad_w, x_plain=None, tape=None, i
 def conv2d_dgrad(g_out, k, in_shape, stride, pad, g_x_out, ws=None, prepared=None):
     n, ci, h, w = in_shape
     co, _, kh, kw = k.shape
-    wp, wsp = (None, prepared) if prepared is not None else (k, _conv_ws(k, ws))
+    wp, wsp = (None, prepared) if prepared is not None else \
+        (k, _conv_ws(k, ws, tuple(in_shape), stride, pad))
     N.call("qt_conv_dgrad", N.ptr(g_out), N.ptr(wp), N.ptr(g_x_out), n, ci, h, w, co, kh, kw,
            stride, pad, N.ptr(wsp))
 

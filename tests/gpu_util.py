@@ -8,9 +8,12 @@ import torch
 #   conv forward & data/weight gradients (fp32-faithful GEMMs vs the
 #   reference's float64 accumulation): normwise relative error <= CONV_TOL
 #   one full training step (logits, loss, every gradient): normwise <= STEP_TOL
+#   ... when some K-bit code landed in the neighbouring interval (a forward
+#   value within an ulp of a boundary): gradients normwise <= FLIP_TOL
 CONV_TOL = 1e-5
 LAYER_TOL = 1e-5
 STEP_TOL = 1e-4
+FLIP_TOL = 2e-3
 MOMENT_TOL = 1e-12
 
 

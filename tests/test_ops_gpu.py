@@ -20,6 +20,8 @@ GEOS = [  # (n, ci, h, co, k, s, p)
     (4, 16, 32, 16, 3, 1, 1), (2, 32, 32, 64, 1, 1, 0), (2, 64, 8, 256, 1, 1, 0),
     (4, 256, 8, 64, 1, 1, 0), (2, 64, 8, 64, 3, 1, 1), (2, 128, 16, 32, 1, 1, 0),
     (2, 32, 16, 32, 3, 1, 1), (2, 16, 32, 64, 1, 1, 0), (6, 8, 8, 16, 3, 1, 1),
+    # kernel == stride transitions: space-to-depth + tensor-core 1x1
+    (2, 32, 32, 32, 2, 2, 0), (4, 64, 16, 64, 2, 2, 0),
 ]
 
 
