@@ -62,7 +62,7 @@ def _geo(args, off):
 
 def algo_cost(name, a):
     """(algorithmic HBM bytes, useful FLOPs) of one qt_* call."""
-    if name == "qt_bn_stats":
+    if name in ("qt_bn_stats", "qt_bn_stats_prep"):
         return 4 * a[1] * a[2] * a[3], 0
     if name == "qt_bn_relu_forward":
         numel = a[1] * a[2] * a[3]
@@ -101,36 +101,52 @@ def algo_cost(name, a):
     return 0, 0
 
 
-class KernelTimer:
-    """_native hook: CUDA events around every qt_* launch on the launching
-    (current) stream."""
+class CallRecorder:
+    """_native hook: records every qt_* call (name, ctypes args) of one step."""
 
-    def __init__(self, torch):
-        self.torch = torch
-        self.rec = []
+    def __init__(self):
+        self.calls = []
 
     def before(self, name, args):
-        e = self.torch.cuda.Event(enable_timing=True)
-        e.record()
-        self._cur = (name, args, e)
+        pass
 
     def after(self, name, args):
-        e = self.torch.cuda.Event(enable_timing=True)
-        e.record()
-        self.rec.append((self._cur[0], self._cur[1], self._cur[2], e))
+        self.calls.append((name, args))
 
-    def summary(self):
-        self.torch.cuda.synchronize()
-        agg = {}
-        for name, args, e0, e1 in self.rec:
-            ms = e0.elapsed_time(e1)
-            b, f = algo_cost(name, args)
-            d = agg.setdefault(name, {"ms": 0.0, "launches": 0, "bytes": 0, "flops": 0})
-            d["ms"] += ms
-            d["launches"] += 1
-            d["bytes"] += b
-            d["flops"] += f
-        return agg
+
+def family_times(torch, N, calls, reps=5):
+    """Per-entry-point device time of one step, measured live: all of a
+    step's calls of one qt_* entry point are captured (same arguments, same
+    order) into a CUDA graph and replayed on the launching stream between
+    CUDA events, so the time is kernel time, not host launch overhead."""
+    agg = {}
+    for name, args in calls:
+        d = agg.setdefault(name, {"ms": 0.0, "launches": 0, "bytes": 0, "flops": 0, "calls": []})
+        b, f = algo_cost(name, args)
+        d["launches"] += 1
+        d["bytes"] += b
+        d["flops"] += f
+        d["calls"].append(args)
+    s = torch.cuda.Stream()
+    for name, d in agg.items():
+        fn = getattr(N.lib(), name)
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.stream(s):
+            with torch.cuda.graph(g, stream=s):
+                for args in d["calls"]:
+                    fn(*args, N.stream())
+        g.replay()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with torch.cuda.stream(s):
+            e0.record(s)
+            for _ in range(reps):
+                g.replay()
+            e1.record(s)
+        torch.cuda.synchronize()
+        d["ms"] = e0.elapsed_time(e1) / reps
+        del d["calls"]
+    return agg
 
 
 class ClockSampler:
@@ -334,13 +350,25 @@ def main():
     e2e_s = D.max_over_ranks(e2e_s, group, dev)
     clk = clocks.stop()
 
-    # per-kernel timing of one instrumented eager step (CUDA events on the
-    # launching stream) -> dominant kernel and its roofline
-    timer = KernelTimer(torch)
-    N.hook = timer
-    tr._body()
+    # per-entry-point device time (graph replay of each entry point's calls
+    # of one step, CUDA events on the launching stream) -> dominant kernel
+    # and its roofline; done last because replaying one family alone
+    # disturbs the model state
+    # (the calls are recorded while capturing one more graph of the step, so
+    # every temporary they point at lives in that graph's memory pool for
+    # as long as `hold` exists)
+    rec = CallRecorder()
+    hold = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    cs.wait_stream(torch.cuda.current_stream())
+    N.hook = rec
+    with torch.cuda.stream(cs):
+        with torch.cuda.graph(hold, stream=cs):
+            tr._body()
     N.hook = None
-    agg = timer.summary()
+    torch.cuda.synchronize()
+    agg = family_times(torch, N, rec.calls)
+    del hold
     hbm, tc, peak_kind = _peaks()
     total_ms = sum(d["ms"] for d in agg.values())
     top = max(agg.items(), key=lambda kv: kv[1]["ms"])

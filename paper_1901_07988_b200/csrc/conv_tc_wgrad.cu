@@ -622,12 +622,15 @@ static WgPlan wg_plan(const ConvGeo &g, int bits) {
     if (pl.rg < pl.ops) return WgPlan{};
     pl.smem = pl.rg * sraw + pl.ops * sop + fixed;
     pl.total = (int)(g.n * oh * ow / 32);
-    // split-K count: two CTAs per SM, at least one chunk per warpgroup, and
-    // the fp32 partials (splits x R x co x 4 B, written + read back) at most
-    // half the g_out bytes the launch streams (total x 128 x co B)
+    // split-K count: about two CTAs per SM in total (one is resident per
+    // SM), at least one pipeline stage (SUB chunks) per CTA, and the fp32
+    // partials (splits x R x co x 4 B, written once and read back by the
+    // fixed-order reduction) at most max(4x the g_out bytes, 32 MiB)
     int want = std::max(1, (2 * 148) / pl.mgroups);
-    want = std::min(want, std::max(1, pl.total / (kWgGroups * SUB)));
-    want = std::min(want, std::max(1, (int)(16.0 * pl.total / (double)R)));
+    want = std::min(want, std::max(1, pl.total / SUB));
+    const double gbytes_all = 128.0 * g.co * pl.total;
+    const double part_cap = std::max(4.0 * gbytes_all, 32.0 * 1024 * 1024);
+    want = std::min(want, std::max(1, (int)(part_cap / (4.0 * (double)R * g.co))));
     pl.cps = std::max(1, (pl.total + want - 1) / want);
     pl.cps = (pl.cps + SUB - 1) / SUB * SUB;          // stages never straddle splits or images
     pl.splits = (pl.total + pl.cps - 1) / pl.cps;
