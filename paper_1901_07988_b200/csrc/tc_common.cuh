@@ -27,15 +27,12 @@ __device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
     uint32_t done = 0;
     while (!done) {
-        // suspend-time hint: the waiting thread sleeps in the barrier unit
-        // instead of re-issuing try_wait (spinning warps steal issue slots
-        // from the producer / MMA threads on the same scheduler)
         asm volatile(
             "{\n\t.reg .pred p;\n\t"
-            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2, %3;\n\t"
+            "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
             "selp.u32 %0, 1, 0, p;\n\t}"
             : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(parity), "r"(0x989680u)
+            : "r"(smem_u32(bar)), "r"(parity)
             : "memory");
     }
 }
