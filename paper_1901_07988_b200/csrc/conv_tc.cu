@@ -86,7 +86,8 @@ __device__ int g_cv_trace_cta = 0;
     do {                               \
         if (tr_) tr_[idx] = clock64(); \
     } while (0)
-constexpr int kFwdThreads = 64 + 128 * kFwdGroups + 128;
+constexpr int kFwdEpiWarps = 8;   // two warps per TMEM lane quarter, alternate 16-channel blocks
+constexpr int kFwdThreads = 64 + 128 * kFwdGroups + 32 * kFwdEpiWarps;
 constexpr int kFwdEpiWarp = 2 + 4 * kFwdGroups;
 
 // Persistent implicit-GEMM conv: each CTA walks output tiles (128 pixels x BN
@@ -145,7 +146,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int s = 0; s < G; ++s) { mbar_init(&op_full[s], 128); mbar_init(&op_empty[s], 1); }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&acc_full[a], 1);
-            mbar_init(&acc_empty[a], 128);
+            mbar_init(&acc_empty[a], 32 * kFwdEpiWarps);
             mbar_init(&res_full[a], 1);
         }
         mbar_init(w_full, 1);
@@ -299,8 +300,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             if (s >= R) { s -= R; phr ^= 1u; }    // R is a multiple of G
             pho ^= 1u;
         }
-    } else {  // ------------------------------------------------ epilogue warpgroup
+    } else {  // ------------------------------------------------ epilogue warps
         const int quarter = warp & 3;
+        const int ehalf = (warp - kFwdEpiWarp) >> 2;  // which alternate 16-channel blocks
         const int row = 32 * quarter + lane;
         const int ratom = row / OWT, wcol = row % OWT;
         const int img = ratom / g.rows, rr = ratom % g.rows;
@@ -320,7 +322,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             tile_coords(T, n0, h0, co0);
             const int acc = lt & 1, ob = (NOUT > 1) ? (lt & 1) : 0;
             float *s_out = out_base + (size_t)ob * (C::OUT_BYTES / 4);
-            asm volatile("bar.sync 1, 128;" ::: "memory");   // staging buffer free (see below)
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kFwdEpiWarps) : "memory");   // staging free
             mbar_wait(&acc_full[acc], (uint32_t)(lt >> 1) & 1u);
             if (leader && lt < 32) CV_TRACE(600 + 4 * lt);
             tc_fence_after();
@@ -330,7 +332,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             float *so = s_out + (img * BN * g.rows + rr) * OWT + wcol;
             const int64_t hr = (int64_t)g.oh * ep.sr, wr = (int64_t)g.ow * ep.sr;
 #pragma unroll 1
-            for (int cb = 0; cb < BN; cb += 16) {
+            for (int cb = 16 * ehalf; cb < BN; cb += 32) {
                 float rv[16];
                 if (res_ldg) {  // strided shortcut (sr > 1): gather, 16 loads in flight
 #pragma unroll
@@ -385,7 +387,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             tc_fence_before();
             mbar_arrive(&acc_empty[acc]);            // TMEM buffer free for tile lt+2
             fence_async_smem();
-            asm volatile("bar.sync 1, 128;" ::: "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * kFwdEpiWarps) : "memory");
             if (leader && lt < 32) CV_TRACE(600 + 4 * lt + 1);
             if (leader) {
                 tma_store_4d(&tmOut, s_out, 0, h0, co0, n0);
