@@ -25,12 +25,12 @@ struct Part {
 };
 
 static Part partition(int64_t n, int64_t c, int64_t hw) {
-    // ~2 blocks per SM overall, at least kTargetPerBlock elements per block
+    // blocks of ~kTargetPerBlock elements (every load of a thread in flight
+    // at once); large layers get several waves of blocks, small ones one
+    // block per channel
+    (void)c;
     Part p;
-    const int64_t want_nb = std::max<int64_t>(1, (2 * 148) / c);
-    p.planes_per_block = std::max<int64_t>(1, qt_cdiv(n, want_nb));
-    p.planes_per_block = std::max<int64_t>(p.planes_per_block,
-                                           std::max<int64_t>(1, kTargetPerBlock / hw));
+    p.planes_per_block = std::max<int64_t>(1, kTargetPerBlock / hw);
     if (p.planes_per_block > n) p.planes_per_block = n;
     p.blocks = qt_cdiv(n, p.planes_per_block);
     return p;

@@ -32,13 +32,12 @@ struct BwdPart {
 // channel (enough work per thread that the block's deterministic
 // last-block-finalize tail is amortised)
 static BwdPart bwd_partition(int64_t n, int64_t c, int64_t hw) {
-    // ~2 blocks per SM in total, each with >= 8192 elements (>= 4 groups of
-    // 8 per thread) so the per-block table build and the deterministic
-    // last-block combine are amortised
+    // blocks of ~8192 elements (4 groups of 8 per thread, all loads in
+    // flight at once): enough blocks to fill the SMs several times over for
+    // the large layers, one block per channel for the small ones
+    (void)c;
     BwdPart p;
-    const int64_t want_nb = std::max<int64_t>(1, (2 * 148) / c);
-    p.ppb = std::max<int64_t>(1, qt_cdiv(n, want_nb));
-    p.ppb = std::max<int64_t>(p.ppb, std::max<int64_t>(1, 8192 / hw));
+    p.ppb = std::max<int64_t>(1, 8192 / hw);
     if (p.ppb > n) p.ppb = n;
     p.nb = qt_cdiv(n, p.ppb);
     return p;

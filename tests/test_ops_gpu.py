@@ -157,3 +157,37 @@ def test_prepared_weights_match_per_call_preparation():
         ops.conv2d_dgrad(g, w, tuple(x.shape), 1, p, ga)
         ops.conv2d_dgrad(g, w, tuple(x.shape), 1, p, gb, prepared=pd)
         assert torch.equal(ga, gb)
+
+
+def test_wgrad_column_tap_form_matches(tmp_path):
+    """The opt-in 3x3 wgrad with the column taps in N (QTAPE_WG_TAP=1, read
+    once per process) against a float64 reference, FAST and GENERIC CTAs."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import torch
+from paper_1901_07988_b200 import codec, ops
+torch.manual_seed(0)
+for regime in ("narrow", "wide"):
+    for n, ci, hw, co in ((2, 16, 32, 16), (2, 32, 16, 32)):
+        x = torch.randn(n, ci, hw, hw, device="cuda")
+        if regime == "narrow":
+            gamma, beta = torch.rand(ci, device="cuda") + 0.5, torch.randn(ci, device="cuda") * 0.1
+        else:
+            gamma, beta = torch.rand(ci, device="cuda") * 0.05 + 0.05, torch.rand(ci, device="cuda") + 1.5
+        t = codec.quantize(x, gamma, beta, 4)
+        act = codec.dequantize(t, relu=True)
+        g = torch.randn(n, co, hw, hw, device="cuda")
+        gw = torch.zeros(co, ci, 3, 3, device="cuda")
+        ops.conv2d_wgrad(g, (co, ci, 3, 3), 1, 1, gw, tape=t.as_native(), in_shape=(n, ci, hw, hw))
+        ref = torch.nn.grad.conv2d_weight(act.double(), (co, ci, 3, 3), g.double(), padding=1)
+        err = ((gw.double() - ref).norm() / ref.norm()).item()
+        assert err < 1e-5, (regime, ci, err)
+print("ok")
+'''
+    env = dict(os.environ, QTAPE_WG_TAP="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
