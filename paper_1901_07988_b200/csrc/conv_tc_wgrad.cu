@@ -124,11 +124,12 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false) {
     if (pl.rg < pl.ops) return WgPlan{};
     pl.smem = pl.rg * sraw + pl.ops * sop + fixed;
     pl.total = (int)(g.n * oh * ow / 32);
-    // split-K count: about two CTAs per SM in total (one is resident per
-    // SM), at least one pipeline stage (SUB chunks) per CTA, and the fp32
+    // split-K count: one CTA per SM (one is resident per SM: a second wave
+    // would pay setup, pipeline fill and epilogue again), at least one
+    // pipeline stage (SUB chunks) per CTA, and the fp32
     // partials (splits x R x co x 4 B, written once and read back by the
     // fixed-order reduction) at most max(4x the g_out bytes, 32 MiB)
-    int want = std::max(1, (2 * 148) / pl.mgroups);
+    int want = std::max(1, 148 / pl.mgroups);      // one wave: fixed costs paid once per SM
     want = std::min(want, std::max(1, pl.total / SUB));
     const double gbytes_all = 128.0 * g.co * pl.total;
     const double part_cap = std::max(4.0 * gbytes_all, 32.0 * 1024 * 1024);

@@ -210,18 +210,20 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     // per-CTA code tables: the reference's fp32 relu(decode(code)) split
     // (hi, lo) for GENERIC, and the FAST lane constant 0x4300 + b with
     // b = 1 - 2^K + 2*offset (clamped below at -64: all-zero channel)
-    int narrow = 1;
-    if (p.lut && threadIdx.x >= 64) {
-        const int nc = c_end - c_begin, bits = p.tape.bits, ncode = 1 << bits;
-        const int nthr = kWgThreads - 64;
-        for (int e = threadIdx.x - 64; e < nc * ncode; e += nthr) {
-            const int cc = c_begin + e / ncode, code = e % ncode;
-            float a = decode((uint32_t)code, p.tape.step[cc], p.tape.offset[cc], bits);
-            a = (a >= 0.f || isnan(a)) ? a : 0.f;
-            split_tf32(a, s_lut[2 * e], s_lut[2 * e + 1]);
-        }
-        if (FAST_OK) {
-            for (int e = threadIdx.x - 64; e < nc; e += nthr) {
+    // The producer starts streaming right after this barrier; the other warps
+    // build the per-CTA tables meanwhile (named barriers among warps 1..17).
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    int fast = 0;
+    if (warp != 0) {
+        constexpr int kRest = kWgThreads - 32;     // warps 1..17
+        int narrow = 1;
+        const int nc = c_end - c_begin;
+        if (FAST_OK && p.lut && threadIdx.x >= 64) {
+            const int bits = p.tape.bits;
+            for (int e = threadIdx.x - 64; e < nc; e += kWgThreads - 64) {
                 const int64_t off = p.tape.offset[c_begin + e];
                 const int64_t top = (1 << bits) - 1;            // m at the largest code
                 if (off > (127 - top) / 2) narrow = 0;          // m could reach 128
@@ -229,11 +231,29 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 s_bc[e] = (uint32_t)(0x4300 + max(b, (int64_t)-64)) * 0x10001u;
             }
         }
+        uint32_t all;
+        asm volatile(
+            "{\n\t.reg .pred p, q;\n\t"
+            "setp.ne.u32 q, %1, 0;\n\t"
+            "bar.red.and.pred p, 1, %2, q;\n\t"
+            "selp.u32 %0, 1, 0, p;\n\t}"
+            : "=r"(all)
+            : "r"((uint32_t)narrow), "n"(kRest)
+            : "memory");
+        fast = (all != 0) && FAST_OK && p.lut;
+        // the GENERIC table only when this CTA takes the GENERIC path
+        if (!fast && p.lut && threadIdx.x >= 64) {
+            const int bits = p.tape.bits, ncode = 1 << bits;
+            for (int e = threadIdx.x - 64; e < nc * ncode; e += kWgThreads - 64) {
+                const int cc = c_begin + e / ncode, code = e % ncode;
+                float a = decode((uint32_t)code, p.tape.step[cc], p.tape.offset[cc], bits);
+                a = (a >= 0.f || isnan(a)) ? a : 0.f;
+                split_tf32(a, s_lut[2 * e], s_lut[2 * e + 1]);
+            }
+        }
+        if (threadIdx.x >= 64)   // operand warps: tables complete before use
+            asm volatile("bar.sync 2, %0;" ::"n"(kWgThreads - 64) : "memory");
     }
-    tc_fence_before();
-    const int fast = __syncthreads_and(narrow) && FAST_OK && p.lut;
-    tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
     if (threadIdx.x == 0) WG_TRACE(1);
     if (threadIdx.x == 0 && tr_)
         tr_[525] = fast;
