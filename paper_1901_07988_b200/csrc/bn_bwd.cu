@@ -86,6 +86,7 @@ __device__ __forceinline__ uint64_t load_code_word(const uint8_t *codes, int64_t
 template <bool CODES, bool VA1>
 __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
     __shared__ float s_m[kMaxLut], s_a1[kMaxLut];
+    __shared__ float2 s_ma[kMaxLut];      // (mask, a1) per code: one 8-byte lookup
     __shared__ double s_a1d[kMaxLut];
     __shared__ double red[3][kBT / 32];
     __shared__ bool s_last;
@@ -96,6 +97,7 @@ __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
         for (int code = threadIdx.x; code < ncode; code += kBT) {
             lut_entry(a.tape, ch, code, bet, sg, s_m[code], s_a1[code]);
             s_a1d[code] = (double)s_a1[code];
+            s_ma[code] = make_float2(s_m[code], s_a1[code]);
         }
         __syncthreads();
     }
@@ -143,25 +145,28 @@ __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
                     xv[0] = xa[u].x; xv[1] = xa[u].y; xv[2] = xa[u].z; xv[3] = xa[u].w;
                     xv[4] = xb[u].x; xv[5] = xb[u].y; xv[6] = xb[u].z; xv[7] = xb[u].w;
                 }
-                double d0 = 0.0, d1 = 0.0, d3 = 0.0;
+                // the 8 elements of a group are combined in fp32 (fixed order,
+                // fused multiply-add for the a1 products), the group sums in
+                // float64: one float->double conversion per sum per group
+                float f0 = 0.f, f1 = 0.f, f3 = 0.f;
 #pragma unroll
                 for (int j = 0; j < 8; ++j) {
-                    float m;
-                    double a1d;
+                    float m, a1;
                     if (CODES) {
                         const uint32_t code = (uint32_t)(word[u] >> (j * a.tape.bits)) & cmask;
-                        m = s_m[code];
-                        a1d = s_a1d[code];
+                        const float2 ma = s_ma[code];
+                        m = ma.x;
+                        a1 = ma.y;
                     } else {
                         m = xv[j] > 0.f ? 1.f : 0.f;
-                        a1d = (double)__fdiv_rn(__fsub_rn(xv[j], bet), sg);
+                        a1 = __fdiv_rn(__fsub_rn(xv[j], bet), sg);
                     }
-                    const double gm = (double)__fmul_rn(gv[j], m);
-                    d0 += gm;
-                    d1 = fma(a1d, gm, d1);
-                    if (VA1) d3 = fma((double)a.va1[i0[u] + j], gm, d3);
+                    const float gm = __fmul_rn(gv[j], m);
+                    f0 = __fadd_rn(f0, gm);
+                    f1 = __fmaf_rn(a1, gm, f1);
+                    if (VA1) f3 = __fmaf_rn(a.va1[i0[u] + j], gm, f3);
                 }
-                v0 += d0; v1 += d1; v3 += d3;
+                v0 += (double)f0; v1 += (double)f1; v3 += (double)f3;
             }
         }
     } else {
