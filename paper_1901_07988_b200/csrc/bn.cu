@@ -92,6 +92,7 @@ struct StatsArgs {
 };
 
 __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
+    pdl_enter();
     __shared__ double red[2][kRThreads / 32];
     const int64_t ch = blockIdx.y;
     const int64_t p0 = (int64_t)blockIdx.x * a.ppb;
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
 
 // Plain per-channel float64 sum (ops.channel_sum, ops.py:199-201).
 __global__ void __launch_bounds__(kRThreads) chan_sum_kernel(StatsArgs a) {
+    pdl_enter();
     __shared__ double red[1][kRThreads / 32];
     const int64_t ch = blockIdx.y;
     const int64_t p0 = (int64_t)blockIdx.x * a.ppb;
@@ -217,6 +219,7 @@ __global__ void __launch_bounds__(kRThreads) chan_sum_kernel(StatsArgs a) {
 __global__ void reconstruct_kernel(qt_tape_t t, int64_t numel, int64_t c, int64_t hw,
                                    const float *gamma, const float *beta, float *a1, float *a2,
                                    float *a3) {
+    pdl_enter();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < numel;
          i += (int64_t)gridDim.x * blockDim.x) {
         const int ch = (int)((i / hw) % c);
@@ -230,6 +233,7 @@ __global__ void reconstruct_kernel(qt_tape_t t, int64_t numel, int64_t c, int64_
 // -------------------------------------------------------------- GAP ---
 
 __global__ void gap_kernel(const float *x, int64_t planes, int64_t hw, float *out) {
+    pdl_enter();
     const int64_t pl = (int64_t)blockIdx.x * (blockDim.x / 32) + (threadIdx.x >> 5);
     if (pl >= planes) return;
     const int lane = threadIdx.x & 31;
@@ -240,6 +244,7 @@ __global__ void gap_kernel(const float *x, int64_t planes, int64_t hw, float *ou
 }
 
 __global__ void gap_bwd_kernel(const float *g, int64_t planes, int64_t hw, float *out) {
+    pdl_enter();
     const int64_t numel = planes * hw;
     const float fhw = (float)hw;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < numel;
@@ -250,12 +255,14 @@ __global__ void gap_bwd_kernel(const float *g, int64_t planes, int64_t hw, float
 // --------------------------------------------------------- shortcut ---
 
 __global__ void copy_kernel(const float4 *src, float4 *dst, int64_t n4) {
+    pdl_enter();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
          i += (int64_t)gridDim.x * blockDim.x)
         dst[i] = src[i];
 }
 
 __global__ void copy1_kernel(const float *src, float *dst, int64_t n) {
+    pdl_enter();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x)
         dst[i] = src[i];
@@ -264,6 +271,7 @@ __global__ void copy1_kernel(const float *src, float *dst, int64_t n) {
 // cur (N,C,H,W) += res (N,CR,H*sr,W*sr) on channels < CR (engine.py:262-269)
 __global__ void shortcut_add_kernel(float *cur, const float *res, int64_t n, int64_t c, int64_t h,
                                     int64_t w, int64_t cr, int64_t sr) {
+    pdl_enter();
     const int64_t numel = n * c * h * w;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < numel;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -280,6 +288,7 @@ __global__ void shortcut_add_kernel(float *cur, const float *res, int64_t n, int
 // g_in (N,C,H,W)[:, :, ::s, ::s] += g_res (N,CRES,H/s,W/s)[:, :C] (engine.py:272-279)
 __global__ void shortcut_adj_kernel(float *g_in, const float *g_res, int64_t n, int64_t c,
                                     int64_t h, int64_t w, int64_t cres, int64_t sr) {
+    pdl_enter();
     const int64_t hr = h / sr, wr = w / sr;
     const int64_t numel = n * c * hr * wr;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < numel;
@@ -319,7 +328,7 @@ extern "C" int qt_bn_stats(const float *x, int64_t n, int64_t c, int64_t hw, dou
                 nullptr, nullptr, 0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     a.hw8d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 3));
     dim3 grid((unsigned)p.blocks, (unsigned)c);
-    bn_stats_kernel<<<grid, kRThreads, 0, qt_s(stream)>>>(a);
+    launch_pdl(bn_stats_kernel, grid, kRThreads, 0, qt_s(stream), a);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -340,7 +349,7 @@ extern "C" int qt_bn_stats_prep(const float *x, int64_t n, int64_t c, int64_t hw
                 clip_count};
     a.hw8d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 3));
     dim3 grid((unsigned)p.blocks, (unsigned)c);
-    bn_stats_kernel<<<grid, kRThreads, 0, qt_s(stream)>>>(a);
+    launch_pdl(bn_stats_kernel, grid, kRThreads, 0, qt_s(stream), a);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -353,7 +362,7 @@ extern "C" int qt_channel_sum(const float *x, int64_t n, int64_t c, int64_t hw, 
                 (double *)((char *)ws + kCounterBytes), (unsigned *)ws,
                 nullptr, nullptr, 0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     dim3 grid((unsigned)p.blocks, (unsigned)c);
-    chan_sum_kernel<<<grid, kRThreads, 0, qt_s(stream)>>>(a);
+    launch_pdl(chan_sum_kernel, grid, kRThreads, 0, qt_s(stream), a);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -364,7 +373,7 @@ extern "C" int qt_reconstruct(qt_tape_t tape, int64_t n, int64_t c, int64_t hw,
     QT_REQUIRE(n > 0 && c > 0 && hw > 0 && gamma_tape && beta_tape);
     QT_REQUIRE(tape.a2 || (tape.codes && tape.step && tape.offset && qt_bits_ok(tape.bits)));
     int64_t numel = n * c * hw;
-    reconstruct_kernel<<<grid_for(numel, 256), 256, 0, qt_s(stream)>>>(tape, numel, c, hw, gamma_tape,
+    launch_pdl(reconstruct_kernel, grid_for(numel, 256), 256, 0, qt_s(stream), tape, numel, c, hw, gamma_tape,
                                                                     beta_tape, a1, a2, a3);
     QT_CHECK_LAUNCH();
     return QT_OK;
@@ -374,7 +383,7 @@ extern "C" int qt_gap(const float *x, int64_t n, int64_t c, int64_t hw, float *o
                       qt_stream_t stream) {
     QT_REQUIRE(x && out && n > 0 && c > 0 && hw > 0);
     int64_t planes = n * c;
-    gap_kernel<<<(unsigned)qt_cdiv(planes, 8), 256, 0, qt_s(stream)>>>(x, planes, hw, out);
+    launch_pdl(gap_kernel, (unsigned)qt_cdiv(planes, 8), 256, 0, qt_s(stream), x, planes, hw, out);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -382,7 +391,7 @@ extern "C" int qt_gap(const float *x, int64_t n, int64_t c, int64_t hw, float *o
 extern "C" int qt_gap_backward(const float *g, int64_t n, int64_t c, int64_t hw, float *out,
                                qt_stream_t stream) {
     QT_REQUIRE(g && out && n > 0 && c > 0 && hw > 0);
-    gap_bwd_kernel<<<grid_for(n * c * hw, 256), 256, 0, qt_s(stream)>>>(g, n * c, hw, out);
+    launch_pdl(gap_bwd_kernel, grid_for(n * c * hw, 256), 256, 0, qt_s(stream), g, n * c, hw, out);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -391,10 +400,10 @@ extern "C" int qt_copy(const float *src, float *dst, int64_t count, qt_stream_t 
     QT_REQUIRE(count >= 0 && (count == 0 || (src && dst)));
     if (count == 0) return QT_OK;
     if ((count & 3) == 0 && (((uintptr_t)src | (uintptr_t)dst) & 15) == 0)
-        copy_kernel<<<grid_for(count / 4, 256), 256, 0, qt_s(stream)>>>(
+        launch_pdl(copy_kernel, grid_for(count / 4, 256), 256, 0, qt_s(stream), 
             (const float4 *)src, (float4 *)dst, count / 4);
     else
-        copy1_kernel<<<grid_for(count, 256), 256, 0, qt_s(stream)>>>(src, dst, count);
+        launch_pdl(copy1_kernel, grid_for(count, 256), 256, 0, qt_s(stream), src, dst, count);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -402,7 +411,7 @@ extern "C" int qt_copy(const float *src, float *dst, int64_t count, qt_stream_t 
 extern "C" int qt_shortcut_add(float *cur, const float *res, int64_t n, int64_t c, int64_t h,
                                int64_t w, int64_t cr, int64_t sr, qt_stream_t stream) {
     QT_REQUIRE(cur && res && n > 0 && c > 0 && h > 0 && w > 0 && cr > 0 && cr <= c && sr >= 1);
-    shortcut_add_kernel<<<grid_for(n * c * h * w, 256), 256, 0, qt_s(stream)>>>(cur, res, n, c, h, w,
+    launch_pdl(shortcut_add_kernel, grid_for(n * c * h * w, 256), 256, 0, qt_s(stream), cur, res, n, c, h, w,
                                                                              cr, sr);
     QT_CHECK_LAUNCH();
     return QT_OK;
@@ -412,7 +421,7 @@ extern "C" int qt_shortcut_adjoint(float *g_in, const float *g_res, int64_t n, i
                                    int64_t w, int64_t cres, int64_t sr, qt_stream_t stream) {
     QT_REQUIRE(g_in && g_res && n > 0 && c > 0 && h > 0 && w > 0 && cres >= c && sr >= 1);
     QT_REQUIRE(h % sr == 0 && w % sr == 0);
-    shortcut_adj_kernel<<<grid_for(n * c * (h / sr) * (w / sr), 256), 256, 0, qt_s(stream)>>>(
+    launch_pdl(shortcut_adj_kernel, grid_for(n * c * (h / sr) * (w / sr), 256), 256, 0, qt_s(stream), 
         g_in, g_res, n, c, h, w, cres, sr);
     QT_CHECK_LAUNCH();
     return QT_OK;

@@ -85,6 +85,7 @@ __device__ __forceinline__ uint64_t load_code_word(const uint8_t *codes, int64_t
 
 template <bool CODES, bool VA1>
 __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
+    pdl_enter();
     __shared__ float s_m[kMaxLut], s_a1[kMaxLut];
     __shared__ float2 s_ma[kMaxLut];      // (mask, a1) per code: one 8-byte lookup
     __shared__ double s_a1d[kMaxLut];
@@ -274,6 +275,7 @@ __device__ __forceinline__ float res_value(const ApplyArgs &a, int64_t i, int64_
 
 template <bool CODES, bool VA1>
 __global__ void __launch_bounds__(kBT) bn_bwd_apply_kernel(ApplyArgs a) {
+    pdl_enter();
     const int64_t hw = a.h * a.w;
     const int64_t numel = a.n * a.c * hw;
     const uint32_t cmask = (1u << a.tape.bits) - 1u;
@@ -374,11 +376,11 @@ extern "C" int qt_bn_backward_reduce(const float *g3, qt_tape_t tape, int64_t n,
     dim3 grid((unsigned)p.nb, (unsigned)c);
     cudaStream_t s = qt_s(stream);
     if (codes)
-        variance_a1 ? bn_bwd_reduce_kernel<true, true><<<grid, kBT, 0, s>>>(a)
-                    : bn_bwd_reduce_kernel<true, false><<<grid, kBT, 0, s>>>(a);
+        variance_a1 ? launch_pdl(bn_bwd_reduce_kernel<true, true>, grid, kBT, 0, s, a)
+                    : launch_pdl(bn_bwd_reduce_kernel<true, false>, grid, kBT, 0, s, a);
     else
-        variance_a1 ? bn_bwd_reduce_kernel<false, true><<<grid, kBT, 0, s>>>(a)
-                    : bn_bwd_reduce_kernel<false, false><<<grid, kBT, 0, s>>>(a);
+        variance_a1 ? launch_pdl(bn_bwd_reduce_kernel<false, true>, grid, kBT, 0, s, a)
+                    : launch_pdl(bn_bwd_reduce_kernel<false, false>, grid, kBT, 0, s, a);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -403,11 +405,11 @@ extern "C" int qt_bn_backward_apply(const float *g3, qt_tape_t tape, int64_t n, 
     blocks = std::max<int64_t>(blocks, 1);
     cudaStream_t s = qt_s(stream);
     if (codes)
-        variance_a1 ? bn_bwd_apply_kernel<true, true><<<(unsigned)blocks, kBT, 0, s>>>(a)
-                    : bn_bwd_apply_kernel<true, false><<<(unsigned)blocks, kBT, 0, s>>>(a);
+        variance_a1 ? launch_pdl(bn_bwd_apply_kernel<true, true>, (unsigned)blocks, kBT, 0, s, a)
+                    : launch_pdl(bn_bwd_apply_kernel<true, false>, (unsigned)blocks, kBT, 0, s, a);
     else
-        variance_a1 ? bn_bwd_apply_kernel<false, true><<<(unsigned)blocks, kBT, 0, s>>>(a)
-                    : bn_bwd_apply_kernel<false, false><<<(unsigned)blocks, kBT, 0, s>>>(a);
+        variance_a1 ? launch_pdl(bn_bwd_apply_kernel<false, true>, (unsigned)blocks, kBT, 0, s, a)
+                    : launch_pdl(bn_bwd_apply_kernel<false, false>, (unsigned)blocks, kBT, 0, s, a);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }

@@ -87,6 +87,7 @@ __device__ __forceinline__ float relu_np(float v) {
 
 template <bool APPLY_BN>
 __global__ void __launch_bounds__(kThreads) bn_relu_quant_kernel(FwdArgs a) {
+    pdl_enter();
     __shared__ PlaneConst sp[kMaxPlanes];
     __shared__ unsigned long long s_clip[kThreads / 32];
 
@@ -218,6 +219,7 @@ struct DecArgs {
 };
 
 __global__ void __launch_bounds__(kThreads) unpack_dequant_kernel(DecArgs a) {
+    pdl_enter();
     __shared__ double s_step[kMaxPlanes];
     __shared__ int64_t s_off[kMaxPlanes];
     const int64_t blk0 = (int64_t)blockIdx.x * kBlockElems;
@@ -279,6 +281,7 @@ __global__ void __launch_bounds__(kThreads) unpack_dequant_kernel(DecArgs a) {
 
 __global__ void codec_constants_kernel(const float *gamma, const float *beta, int64_t c,
                                        int bits, double *step, int64_t *offset) {
+    pdl_enter();
     int64_t ch = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (ch >= c) return;
     ChanCode cc = chan_code(gamma[ch], beta[ch], bits);
@@ -288,6 +291,7 @@ __global__ void codec_constants_kernel(const float *gamma, const float *beta, in
 
 __global__ void pack_kernel(const uint8_t *codes, int64_t count, int bits, uint8_t *packed,
                             int64_t nbytes, int32_t *bad) {
+    pdl_enter();
     int64_t b = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (b >= nbytes) return;
     const int per = 8 / bits;
@@ -306,6 +310,7 @@ __global__ void pack_kernel(const uint8_t *codes, int64_t count, int bits, uint8
 }
 
 __global__ void unpack_kernel(const uint8_t *packed, int64_t count, int bits, uint8_t *codes) {
+    pdl_enter();
     int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= count) return;
     codes[i] = (uint8_t)get_code(packed, i, bits);
@@ -359,6 +364,7 @@ __device__ __forceinline__ void quant8(const float (&v)[8], const BnConst &k, ui
 
 template <int BITS, int MODE, bool A2, bool CLIP>
 __global__ void __launch_bounds__(kThreads) bn_relu_quant_stream(FwdArgs a) {
+    pdl_enter();
     const int64_t ngroups = a.numel >> 3;
     const int64_t stride = (int64_t)gridDim.x * kThreads;
     unsigned long long clip = 0;
@@ -444,11 +450,11 @@ template <int BITS>
 static void launch_stream(const FwdArgs &a, unsigned blocks, cudaStream_t s) {
     const bool clip = a.clip_count != nullptr;
     if (a.mode == MODE_NAIVE) {
-        if (clip) bn_relu_quant_stream<BITS, MODE_NAIVE, false, true><<<blocks, kThreads, 0, s>>>(a);
-        else bn_relu_quant_stream<BITS, MODE_NAIVE, false, false><<<blocks, kThreads, 0, s>>>(a);
+        if (clip) launch_pdl(bn_relu_quant_stream<BITS, MODE_NAIVE, false, true>, blocks, kThreads, 0, s, a);
+        else launch_pdl(bn_relu_quant_stream<BITS, MODE_NAIVE, false, false>, blocks, kThreads, 0, s, a);
     } else {
-        if (clip) bn_relu_quant_stream<BITS, MODE_APPROX, false, true><<<blocks, kThreads, 0, s>>>(a);
-        else bn_relu_quant_stream<BITS, MODE_APPROX, false, false><<<blocks, kThreads, 0, s>>>(a);
+        if (clip) launch_pdl(bn_relu_quant_stream<BITS, MODE_APPROX, false, true>, blocks, kThreads, 0, s, a);
+        else launch_pdl(bn_relu_quant_stream<BITS, MODE_APPROX, false, false>, blocks, kThreads, 0, s, a);
     }
 }
 
@@ -468,8 +474,8 @@ static int launch_fwd(const FwdArgs &a0, bool apply_bn, cudaStream_t s) {
         const unsigned b = (unsigned)blocks;
         switch (a.bits) {
             case 0:
-                if (a.a2_tape) bn_relu_quant_stream<0, MODE_EXACT, true, false><<<b, kThreads, 0, s>>>(a);
-                else bn_relu_quant_stream<0, MODE_EXACT, false, false><<<b, kThreads, 0, s>>>(a);
+                if (a.a2_tape) launch_pdl(bn_relu_quant_stream<0, MODE_EXACT, true, false>, b, kThreads, 0, s, a);
+                else launch_pdl(bn_relu_quant_stream<0, MODE_EXACT, false, false>, b, kThreads, 0, s, a);
                 break;
             case 1: launch_stream<1>(a, b, s); break;
             case 2: launch_stream<2>(a, b, s); break;
@@ -482,9 +488,9 @@ static int launch_fwd(const FwdArgs &a0, bool apply_bn, cudaStream_t s) {
     int64_t blocks = qt_cdiv(a.numel, kBlockElems);
     if (blocks > 0x7fffffff) return QT_EUNSUPPORTED;
     if (apply_bn)
-        bn_relu_quant_kernel<true><<<(unsigned)blocks, kThreads, 0, s>>>(a);
+        launch_pdl(bn_relu_quant_kernel<true>, (unsigned)blocks, kThreads, 0, s, a);
     else
-        bn_relu_quant_kernel<false><<<(unsigned)blocks, kThreads, 0, s>>>(a);
+        launch_pdl(bn_relu_quant_kernel<false>, (unsigned)blocks, kThreads, 0, s, a);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -497,7 +503,7 @@ extern "C" int qt_codec_constants(const float *gamma, const float *beta, int64_t
                                   double *step, int64_t *offset, qt_stream_t stream) {
     QT_REQUIRE(qt_bits_ok(bits) && c >= 0 && gamma && beta && step && offset);
     if (c == 0) return QT_OK;
-    codec_constants_kernel<<<(unsigned)qt_cdiv(c, 256), 256, 0, qt_s(stream)>>>(gamma, beta, c, bits,
+    launch_pdl(codec_constants_kernel, (unsigned)qt_cdiv(c, 256), 256, 0, qt_s(stream), gamma, beta, c, bits,
                                                                               step, offset);
     QT_CHECK_LAUNCH();
     return QT_OK;
@@ -563,7 +569,7 @@ extern "C" int qt_unpack_dequant(const uint8_t *codes, int64_t n, int64_t c, int
     DecArgs d{codes, n * c * hw, c, hw, bits, step, offset, relu, out};
     if (d.numel == 0) return QT_OK;
     int64_t blocks = qt_cdiv(d.numel, kBlockElems);
-    unpack_dequant_kernel<<<(unsigned)blocks, kThreads, 0, qt_s(stream)>>>(d);
+    launch_pdl(unpack_dequant_kernel, (unsigned)blocks, kThreads, 0, qt_s(stream), d);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -573,7 +579,7 @@ extern "C" int qt_pack_codes(const uint8_t *codes, int64_t count, int bits, uint
     QT_REQUIRE(qt_bits_ok(bits) && count >= 0 && (count == 0 || (codes && packed)));
     int64_t nbytes = (count * bits + 7) / 8;
     if (nbytes == 0) return QT_OK;
-    pack_kernel<<<(unsigned)qt_cdiv(nbytes, 256), 256, 0, qt_s(stream)>>>(codes, count, bits, packed,
+    launch_pdl(pack_kernel, (unsigned)qt_cdiv(nbytes, 256), 256, 0, qt_s(stream), codes, count, bits, packed,
                                                                         nbytes, bad);
     QT_CHECK_LAUNCH();
     return QT_OK;
@@ -583,7 +589,7 @@ extern "C" int qt_unpack_codes(const uint8_t *packed, int64_t count, int bits, u
                                qt_stream_t stream) {
     QT_REQUIRE(qt_bits_ok(bits) && count >= 0 && (count == 0 || (codes && packed)));
     if (count == 0) return QT_OK;
-    unpack_kernel<<<(unsigned)qt_cdiv(count, 256), 256, 0, qt_s(stream)>>>(packed, count, bits, codes);
+    launch_pdl(unpack_kernel, (unsigned)qt_cdiv(count, 256), 256, 0, qt_s(stream), packed, count, bits, codes);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }

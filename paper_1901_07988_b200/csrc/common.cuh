@@ -4,6 +4,9 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <cstdlib>
+#include <utility>
+
 #include "../../include/qtape_b200.h"
 
 #define QT_CHECK_LAUNCH()                              \
@@ -23,7 +26,47 @@ static inline bool qt_bits_ok(int b) { return b == 1 || b == 2 || b == 4 || b ==
 
 static inline int64_t qt_cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// Programmatic dependent launch: every kernel is launched with programmatic
+// stream serialization, triggers its dependents as soon as it starts and
+// waits (griddepcontrol.wait) for its predecessor before touching global
+// memory, so a kernel's launch and prologue (barrier init, TMEM allocation,
+// tensor-map prefetch) overlap the previous kernel's tail.  QTAPE_NO_PDL=1
+// launches without the attribute (the wait then returns immediately).
+static inline bool qt_pdl_enabled() {
+    static int v = -1;
+    if (v < 0) {
+        const char *e = getenv("QTAPE_NO_PDL");
+        v = (e && *e && *e != '0') ? 0 : 1;
+    }
+    return v == 1;
+}
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                                     cudaStream_t st, Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = qt_pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 namespace qt {
+
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+// elementwise / reduction kernels: no prologue worth overlapping
+__device__ __forceinline__ void pdl_enter() {
+    pdl_wait();
+    pdl_trigger();
+}
 
 constexpr double kGammaFloor = 1e-8;   // codec.py:24
 constexpr float kGammaFloorF = 1e-8f;  // layer.py:134 (dtype.type(GAMMA_FLOOR))

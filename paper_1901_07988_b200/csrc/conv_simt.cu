@@ -153,6 +153,7 @@ struct StorePartial {
 template <int BM, int BN, int TM, int TN, bool A_KFAST, bool B_KFAST, class LA, class LB, class EP>
 __global__ void __launch_bounds__(kCT) simt_gemm(LA la, LB lb, EP ep, int64_t M, int64_t N,
                                                  int64_t K, int64_t k_per_split) {
+    pdl_enter();
     static_assert((BM / TM) * (BN / TN) == kCT, "thread layout");
     constexpr int RA = BM * kBK / kCT;
     constexpr int RB = BN * kBK / kCT;
@@ -258,13 +259,13 @@ static int run_gemm(LA la, LB lb, EP ep, int64_t M, int64_t N, int64_t K, int64_
     const int64_t splits = std::max<int64_t>(1, qt_cdiv(K, kps));
     if (N <= 16) {
         dim3 grid((unsigned)qt_cdiv(M, 256), (unsigned)qt_cdiv(N, 16), (unsigned)splits);
-        simt_gemm<256, 16, 4, 4, A_KFAST, B_KFAST><<<grid, kCT, 0, s>>>(la, lb, ep, M, N, K, kps);
+        launch_pdl(simt_gemm<256, 16, 4, 4, A_KFAST, B_KFAST, LA, LB, EP>, grid, kCT, 0, s, la, lb, ep, M, N, K, kps);
     } else if (N <= 32) {
         dim3 grid((unsigned)qt_cdiv(M, 128), (unsigned)qt_cdiv(N, 32), (unsigned)splits);
-        simt_gemm<128, 32, 4, 4, A_KFAST, B_KFAST><<<grid, kCT, 0, s>>>(la, lb, ep, M, N, K, kps);
+        launch_pdl(simt_gemm<128, 32, 4, 4, A_KFAST, B_KFAST, LA, LB, EP>, grid, kCT, 0, s, la, lb, ep, M, N, K, kps);
     } else {
         dim3 grid((unsigned)qt_cdiv(M, 128), (unsigned)qt_cdiv(N, 64), (unsigned)splits);
-        simt_gemm<128, 64, 8, 4, A_KFAST, B_KFAST><<<grid, kCT, 0, s>>>(la, lb, ep, M, N, K, kps);
+        launch_pdl(simt_gemm<128, 64, 8, 4, A_KFAST, B_KFAST, LA, LB, EP>, grid, kCT, 0, s, la, lb, ep, M, N, K, kps);
     }
     QT_CHECK_LAUNCH();
     return QT_OK;

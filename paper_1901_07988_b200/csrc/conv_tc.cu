@@ -116,6 +116,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                        const __grid_constant__ CUtensorMap tmBl,
                        const __grid_constant__ CUtensorMap tmOut,
                        const __grid_constant__ CUtensorMap tmRes, FwdGeo g, EpiParams ep) {
+    pdl_enter();
     using C = FwdCfg<BN, OWT, KC, KW>;
     const int R = g.R, NOUT = g.NOUT, G = g.G;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -164,6 +165,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // setup above touched only smem / TMEM / the tensor maps: overlap it with
+    // the previous kernel, then wait for that kernel's results
+    pdl_wait();
+    pdl_trigger();
 
     auto tile_coords = [&](int T, int &n0, int &h0, int &co0) {
         const int mt = (int)fast_div((uint32_t)T, g.ntd);
@@ -421,6 +426,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
 // W[c][co'][kh-1-u][kw-1-v] (data gradient: transposed + flipped kernel).
 __global__ void weight_prep_kernel(const float *w, int co_n, int ci_n, int kh, int kw, int flip,
                                    float *bhi, float *blo) {
+    pdl_enter();
     // output rows co' (co_n of them), K' = kh*kw*ci_n
     const int kk = kh * kw;
     const int64_t total = (int64_t)co_n * kk * ci_n;
@@ -446,6 +452,7 @@ __global__ void weight_prep_kernel(const float *w, int co_n, int ci_n, int kh, i
 
 // Many layers' preparations in one launch: blockIdx.y selects the descriptor.
 __global__ void weight_prep_batch_kernel(const qt_wprep_t *descs) {
+    pdl_enter();
     const qt_wprep_t d = descs[blockIdx.y];
     const int kk = d.kh * d.kw;
     const int64_t total = (int64_t)d.rows * kk * d.cols;
@@ -578,7 +585,7 @@ static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, int t
     gg.NOUT = nout;
     gg.G = G;
     const int smem = r * gg.slot + nout * C::OUT_BYTES + (gg.wres ? wbytes : 0) + 1024 + 512;
-    kern<<<grid, kFwdThreads, smem, st>>>(m.a, m.bh, m.bl, m.out, m.res, gg, ep);
+    launch_pdl(kern, grid, kFwdThreads, smem, st, m.a, m.bh, m.bl, m.out, m.res, gg, ep);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -668,8 +675,7 @@ static int tc_conv_s1(const float *x, const float *w, float *out, int n, int ci,
     float *blo = bhi + (int64_t)co * kdim;
     if (!ws) return QT_EINVAL;
     if (w) {   // w == NULL: ws already holds the prepared operand (qt_conv_prepare_weights)
-        weight_prep_kernel<<<(unsigned)std::min<int64_t>(qt_cdiv((int64_t)co * kdim, 256), 1024), 256,
-                             0, st>>>(w, co, ci, kh, kw, flip, bhi, blo);
+        launch_pdl(weight_prep_kernel, (unsigned)std::min<int64_t>(qt_cdiv((int64_t)co * kdim, 256), 1024), 256, 0, st, w, co, ci, kh, kw, flip, bhi, blo);
         QT_CHECK_LAUNCH();
     }
     Maps mp;
@@ -732,7 +738,7 @@ extern "C" int qt_conv_prepare_weights(const qt_wprep_t *descs, int64_t count, i
     QT_REQUIRE(descs && count >= 0 && count <= 65535 && max_elems >= 0);
     if (count == 0) return QT_OK;
     const unsigned bx = (unsigned)std::max<int64_t>(1, std::min<int64_t>(qt_cdiv(max_elems, 256), 64));
-    weight_prep_batch_kernel<<<dim3(bx, (unsigned)count), 256, 0, qt_s(stream)>>>(descs);
+    launch_pdl(weight_prep_batch_kernel, dim3(bx, (unsigned)count), 256, 0, qt_s(stream), descs);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -772,6 +778,7 @@ namespace qt {
 template <bool TO_DEPTH>
 __global__ void space_depth_kernel(const float *src, float *dst, int64_t n, int64_t c, int64_t h,
                                    int64_t w, int s) {
+    pdl_enter();
     // iterate over the full-resolution tensor in memory order (coalesced side)
     const int64_t total = n * c * h * w;
     const int64_t hs = h / s, ws = w / s;
@@ -792,9 +799,9 @@ static int space_depth(const float *src, float *dst, int64_t n, int64_t c, int64
     const int64_t total = n * c * h * w;
     const unsigned blocks = (unsigned)std::min<int64_t>(qt_cdiv(total, 256), 148 * 16);
     if (to_depth)
-        space_depth_kernel<true><<<blocks, 256, 0, st>>>(src, dst, n, c, h, w, s);
+        launch_pdl(space_depth_kernel<true>, blocks, 256, 0, st, src, dst, n, c, h, w, s);
     else
-        space_depth_kernel<false><<<blocks, 256, 0, st>>>(src, dst, n, c, h, w, s);
+        launch_pdl(space_depth_kernel<false>, blocks, 256, 0, st, src, dst, n, c, h, w, s);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }

@@ -18,6 +18,7 @@ int wg_launch_bn256(const CUtensorMap &, const CUtensorMap &, const WgParams &, 
 // combine in warp order: fixed order, deterministic (layer.py:167).
 __global__ void __launch_bounds__(1024) wgrad_reduce_kernel(const float *partial, int64_t splits,
                                                            int64_t count, float *grad_w) {
+    pdl_enter();
     __shared__ double red[32][33];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t i = (int64_t)blockIdx.x * 32 + lane;
@@ -168,7 +169,7 @@ extern "C" int qt_debug_wgrad_trace(void *buf, int cta) {
 
 int qt_tc_wgrad_reduce(const float *partial, int64_t splits, int64_t count, float *grad_w,
                        cudaStream_t st) {
-    wgrad_reduce_kernel<<<(unsigned)qt_cdiv(count, 32), 1024, 0, st>>>(partial, splits, count,
+    launch_pdl(wgrad_reduce_kernel, (unsigned)qt_cdiv(count, 32), 1024, 0, st, partial, splits, count,
                                                                       grad_w);
     QT_CHECK_LAUNCH();
     return QT_OK;

@@ -144,6 +144,7 @@ template <int BN, int OW, int BITS, bool TAP>
 __global__ void __launch_bounds__(kWgThreads, 1)
     conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmG,
                          const __grid_constant__ CUtensorMap tmC, WgParams p) {
+    pdl_enter();
     constexpr int ROWS = 32 / OW;                           // image rows per 32-pixel chunk
     constexpr int G_BYTES = BN * 128;                       // raw g tile: BN rows x 32 px fp32
     constexpr bool FAST_OK = (BITS == 4);
@@ -216,6 +217,10 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // setup above touched only smem / TMEM / the tensor maps: overlap it with
+    // the previous kernel, then wait for that kernel's results
+    pdl_wait();
+    pdl_trigger();
     int fast = 0;
     if (warp != 0) {
         constexpr int kRest = kWgThreads - 32;     // warps 1..17
@@ -637,7 +642,7 @@ static int launch_wg2(const CUtensorMap &m, const CUtensorMap &mc, const WgParam
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    kern<<<dim3(pl.splits, pl.mgroups), kWgThreads, pl.smem, st>>>(m, mc, p);
+    launch_pdl(kern, dim3(pl.splits, pl.mgroups), kWgThreads, pl.smem, st, m, mc, p);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }

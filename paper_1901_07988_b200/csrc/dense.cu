@@ -10,6 +10,7 @@ namespace qt {
 // rounded multiply and add: bit-identical to ops.matmul (ops.py:54-77).
 __global__ void matmul_f64_kernel(const float *a, const float *b, float *c, int64_t M, int64_t K,
                                   int64_t N, int ta, int tb, int accumulate) {
+    pdl_enter();
     const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (idx >= M * N) return;
     const int64_t m = idx / N, n = idx - m * N;
@@ -27,6 +28,7 @@ __global__ void matmul_f64_kernel(const float *a, const float *b, float *c, int6
 // sequential sum of the per-row nll in row order).  training.py:120-134.
 __global__ void xent_kernel(const float *logits, const int64_t *labels, int64_t n, int64_t c,
                             double *loss, float *grad, double *nll_scratch, int32_t *bad) {
+    pdl_enter();
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nw = blockDim.x >> 5;
     for (int64_t r = warp; r < n; r += nw) {
@@ -59,6 +61,7 @@ __global__ void xent_kernel(const float *logits, const int64_t *labels, int64_t 
 
 __global__ void sgd_kernel(float *w, float *g, float *v, int64_t count, float lr,
                            const float *lr_dev, float mom, float wd) {
+    pdl_enter();
     const float l = lr_dev ? *lr_dev : lr;
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
          i += (int64_t)gridDim.x * blockDim.x) {
@@ -97,7 +100,7 @@ extern "C" int qt_matmul(const float *a, const float *b, float *c, int64_t m, in
                          int ta, int tb, int accumulate, qt_stream_t stream) {
     QT_REQUIRE(a && b && c && m >= 0 && k >= 0 && nn >= 0);
     if (m * nn == 0) return QT_OK;
-    matmul_f64_kernel<<<(unsigned)qt_cdiv(m * nn, 128), 128, 0, qt_s(stream)>>>(a, b, c, m, k, nn, ta,
+    launch_pdl(matmul_f64_kernel, (unsigned)qt_cdiv(m * nn, 128), 128, 0, qt_s(stream), a, b, c, m, k, nn, ta,
                                                                               tb, accumulate);
     QT_CHECK_LAUNCH();
     return QT_OK;
@@ -107,7 +110,7 @@ extern "C" int qt_softmax_xent(const float *logits, const int64_t *labels, int64
                                double *loss, float *grad, int32_t *bad_label, qt_stream_t stream) {
     QT_REQUIRE(logits && labels && loss && grad && n > 0 && c > 0);
     // nll scratch lives past the loss slot: caller passes loss with room for 1 + n doubles
-    xent_kernel<<<1, 1024, 0, qt_s(stream)>>>(logits, labels, n, c, loss, grad, loss + 1, bad_label);
+    launch_pdl(xent_kernel, 1, 1024, 0, qt_s(stream), logits, labels, n, c, loss, grad, loss + 1, bad_label);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -118,7 +121,7 @@ extern "C" int qt_sgd(float *value, float *grad, float *vel, int64_t count, floa
     if (count == 0) return QT_OK;
     int64_t blocks = qt_cdiv(count, 256);
     if (blocks > 148 * 16) blocks = 148 * 16;
-    sgd_kernel<<<(unsigned)blocks, 256, 0, qt_s(stream)>>>(value, grad, vel, count, lr, lr_dev, momentum,
+    launch_pdl(sgd_kernel, (unsigned)blocks, 256, 0, qt_s(stream), value, grad, vel, count, lr, lr_dev, momentum,
                                                         weight_decay);
     QT_CHECK_LAUNCH();
     return QT_OK;
