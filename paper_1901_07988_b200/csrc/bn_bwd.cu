@@ -260,6 +260,7 @@ struct ApplyArgs {
     int64_t cr, sc;
     float *g_in;
     FastDiv gppd, cd;   // hw / 8, c
+    FastDiv wd;         // w
 };
 
 __device__ __forceinline__ float res_value(const ApplyArgs &a, int64_t i, int64_t pl, int ch,
@@ -311,10 +312,20 @@ __global__ void __launch_bounds__(kBT) bn_bwd_apply_kernel(ApplyArgs a) {
                     const float rv[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
 #pragma unroll
                     for (int j = 0; j < 8; ++j) o[j] = __fadd_rn(o[j], rv[j]);
-                } else {
+                } else if (ch < a.cr) {
+                    // shortcut adjoint at a lower resolution (engine.py:270-279):
+                    // the group's 8 pixels share one row y of the plane
+                    const uint32_t off = (uint32_t)(i0 - (int64_t)pl * hw);
+                    const uint32_t y = fast_div(off, a.wd), x0 = off - y * (uint32_t)a.w;
+                    const uint32_t sc = (uint32_t)a.sc;
+                    if (y % sc == 0) {
+                        const uint32_t nn = fast_div(pl, a.cd);
+                        const int64_t hr = a.h / a.sc, wr = a.w / a.sc;
+                        const float *rrow = a.res + (((int64_t)nn * a.cr + ch) * hr + y / sc) * wr;
 #pragma unroll
-                    for (int j = 0; j < 8; ++j)
-                        o[j] = __fadd_rn(o[j], res_value(a, i0 + j, pl, ch, hw));
+                        for (int j = 0; j < 8; ++j)
+                            if ((x0 + j) % sc == 0) o[j] = __fadd_rn(o[j], __ldg(rrow + (x0 + j) / sc));
+                    }
                 }
             }
             float4 *dst = reinterpret_cast<float4 *>(a.g_in + i0);
@@ -400,6 +411,7 @@ extern "C" int qt_bn_backward_apply(const float *g3, qt_tape_t tape, int64_t n, 
                 lut_base((void *)ws), cr, sc, g_in};
     a.gppd = make_fastdiv((uint32_t)std::max<int64_t>(1, (h * w) >> 3));
     a.cd = make_fastdiv((uint32_t)c);
+    a.wd = make_fastdiv((uint32_t)w);
     const int64_t work = codes && ((h * w) & 7) == 0 ? (n * c * h * w) >> 3 : n * c * h * w;
     int64_t blocks = std::min<int64_t>(qt_cdiv(work, kBT), 148 * 16);
     blocks = std::max<int64_t>(blocks, 1);
