@@ -89,7 +89,12 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false) {
     // TMEM (512 columns): FAST needs mtg*facc + ops*mtg*SUB*16, GENERIC
     // mtg*BN + ops_g*mtg*SUB*64; ring depths are powers of two (see kWgGroups)
     constexpr int SUB = kWgSub;
+    // two m-tiles per CTA share one g split, but only pay when the pair
+    // still leaves four operand stages in TMEM and the tiles are not one of
+    // three or more (measured: mtg 1 wins for mt >= 3 and for ops < 4)
     int mtg = (int)std::min<int64_t>(mt, 2);
+    if (mtg == 2 && (mt >= 3 || 2 * facc + 4 * 2 * SUB * 16 > 512)) mtg = 1;
+    if (const char *e = getenv("QTAPE_WG_MTG")) mtg = std::max(1, std::min(mtg, atoi(e)));   // tuning
     while (mtg > 1 && (mtg * gacc + mtg * SUB * 64 > 512 || mtg * facc + 2 * mtg * SUB * 16 > 512))
         --mtg;
     if (mtg * gacc + mtg * SUB * 64 > 512 || mtg * facc + 2 * mtg * SUB * 16 > 512) return WgPlan{};
@@ -130,7 +135,11 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false) {
     // pipeline stage (SUB chunks) per CTA, and the fp32
     // partials (splits x R x co x 4 B, written once and read back by the
     // fixed-order reduction) at most max(4x the g_out bytes, 32 MiB)
-    int want = std::max(1, 148 / pl.mgroups);      // one wave: fixed costs paid once per SM
+    static const int ctas = [] {
+        const char *e = getenv("QTAPE_WG_CTAS");
+        return e && atoi(e) > 0 ? atoi(e) : 148;
+    }();
+    int want = std::max(1, ctas / pl.mgroups);     // one wave: fixed costs paid once per SM
     want = std::min(want, std::max(1, pl.total / SUB));
     const double gbytes_all = 128.0 * g.co * pl.total;
     const double part_cap = std::max(4.0 * gbytes_all, 32.0 * 1024 * 1024);

@@ -570,43 +570,51 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             if (s >= RG) { s -= RG; phr ^= 1u; }   // RG is a multiple of ops
             pho ^= 1u;                          // same stage (o == grp), next round
         }
-        // epilogue: group t reads tile t (lane = act row); FAST sums the three
-        // g pieces and scales by step/2
+        // epilogue: all four groups drain TMEM -- items (tile, tap, 16-column
+        // chunk) dealt round-robin over the groups, each warp its lane
+        // quarter (lane = act row); FAST sums the three g pieces and scales
+        // by step/2.  Warps whose 32 rows are all past the tile skip.
         mbar_wait(done, 0);
         if (tg == 0 && grp == 0) WG_TRACE(330);
         tc_fence_after();
-        if (grp < mt_here) {
-            const int t = grp;
+        constexpr int kChunks = NT * (BN / 16);              // items per tile
+        const int items = mt_here * kChunks;
+        double scale[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+            const int rl = t * 128 + 32 * quarter + lane;
+            scale[t] = (fast && rl < nrows) ? 0.5 * p.tape.step[(row0 + rl) / kk] : 1.0;
+        }
+#pragma unroll 1
+        for (int it = grp; it < items; it += kWgGroups) {
+            const int t = it >= kChunks ? 1 : 0;
+            const int ic = it - t * kChunks;
+            const int v = ic / (BN / 16), cb = (ic - v * (BN / 16)) * 16;
+            if (t * 128 + 32 * quarter >= nrows) continue;   // warp-uniform
             const int rl = t * 128 + 32 * quarter + lane;
             const bool ok = rl < nrows;
             const int r = row0 + rl;
-            const double scale = (fast && ok) ? 0.5 * p.tape.step[r / kk] : 1.0;
+            const int rout = TAP ? r * 3 + v : r;            // dW row (ci, u, v); TAP rows (ci, u)
             const uint32_t tbase = lane_base + (uint32_t)t * (fast ? FACC : GACC);
-#pragma unroll 1
-            for (int v = 0; v < NT; ++v) {
-                // output row of dW: (ci, u, v) -- TAP rows are (ci, u)
-                const int rout = TAP ? r * 3 + v : r;
-                for (int cb = 0; cb < BN; cb += 16) {
-                    uint32_t r0[16], r1[16], r2[16];
-                    if (fast && STACK) {
-                        tmem_ld16(tbase + (0 * NT + v) * BN + cb, r0);
-                        tmem_ld16(tbase + (1 * NT + v) * BN + cb, r1);
-                        tmem_ld16(tbase + (2 * NT + v) * BN + cb, r2);
-                    } else {
-                        tmem_ld16(tbase + v * BN + cb, r0);
-                    }
-                    tmem_wait_ld();
-                    if (ok) {
+            uint32_t r0[16], r1[16], r2[16];
+            if (fast && STACK) {
+                tmem_ld16(tbase + (0 * NT + v) * BN + cb, r0);
+                tmem_ld16(tbase + (1 * NT + v) * BN + cb, r1);
+                tmem_ld16(tbase + (2 * NT + v) * BN + cb, r2);
+            } else {
+                tmem_ld16(tbase + v * BN + cb, r0);
+            }
+            tmem_wait_ld();
+            if (ok) {
+                const double sc = t ? scale[1] : scale[0];
+                float *dst = p.partial + ((int64_t)split * p.co + cb) * p.Rout + rout;
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) {
-                            const int co = cb + j;
-                            double acc = (double)__uint_as_float(r0[j]);
-                            if (fast && STACK)
-                                acc = acc + (double)__uint_as_float(r1[j]) + (double)__uint_as_float(r2[j]);
-                            const float val = fast ? (float)(acc * scale) : __uint_as_float(r0[j]);
-                            if (co < p.co) p.partial[((int64_t)split * p.co + co) * p.Rout + rout] = val;
-                        }
-                    }
+                for (int j = 0; j < 16; ++j) {
+                    double acc = (double)__uint_as_float(r0[j]);
+                    if (fast && STACK)
+                        acc = acc + (double)__uint_as_float(r1[j]) + (double)__uint_as_float(r2[j]);
+                    const float val = fast ? (float)(acc * sc) : __uint_as_float(r0[j]);
+                    if (cb + j < p.co) dst[(int64_t)j * p.Rout] = val;
                 }
             }
         }

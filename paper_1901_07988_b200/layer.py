@@ -337,6 +337,23 @@ def _apply_adjoint(g_in, res_g):
            h // res_g.shape[2])
 
 
+def _on_side(ws, fn) -> None:
+    """Run a weight-gradient launch on the engine's side stream when it has
+    one: it forks after everything queued so far on the current stream and
+    leaves its completion event in ``ws.wgrad_done`` (the engine fences the
+    g_out buffer with it and joins before SGD)."""
+    side = getattr(ws, "side", None)
+    if side is None:
+        fn()
+        return
+    side.wait_stream(torch.cuda.current_stream())
+    with torch.cuda.stream(side):
+        fn()
+    ev = torch.cuda.Event()
+    ev.record(side)
+    ws.wgrad_done = ev
+
+
 def layer_backward(g_out: torch.Tensor, tape: LayerTape, p: LayerParams,
                    out: Optional[torch.Tensor] = None, need_input_grad: bool = True,
                    variance_a1: Optional[torch.Tensor] = None,
@@ -359,8 +376,10 @@ def layer_backward(g_out: torch.Tensor, tape: LayerTape, p: LayerParams,
                 return None
             g_in = ops.matmul(g_out, p.weight, out=out, tb=True)
         else:
-            ops.conv2d_wgrad(g_out, tuple(p.weight.shape), p.stride, p.pad, p.grad_weight,
-                             x_plain=a_in.contiguous(), ws=None if ws is None else ws.wgrad)
+            x_plain = a_in.contiguous()
+            _on_side(ws, lambda: ops.conv2d_wgrad(g_out, tuple(p.weight.shape), p.stride, p.pad,
+                                                  p.grad_weight, x_plain=x_plain,
+                                                  ws=None if ws is None else ws.wgrad))
             if not need_input_grad:
                 return None
             g_in = out if out is not None else torch.empty_like(a_in)
@@ -381,8 +400,9 @@ def layer_backward(g_out: torch.Tensor, tape: LayerTape, p: LayerParams,
 
     # linear transform backward (layer.py:353-362)
     if p.kind == "conv":
-        ops.conv2d_wgrad(g_out, tuple(p.weight.shape), p.stride, p.pad, p.grad_weight,
-                         tape=nt, in_shape=in_shape, ws=None if ws is None else ws.wgrad)
+        _on_side(ws, lambda: ops.conv2d_wgrad(g_out, tuple(p.weight.shape), p.stride, p.pad,
+                                              p.grad_weight, tape=nt, in_shape=in_shape,
+                                              ws=None if ws is None else ws.wgrad))
         ops.conv2d_dgrad(g_out, p.weight, in_shape, p.stride, p.pad, g3,
                          ws=None if ws is None else ws.conv, prepared=p.prep_dgrad)
     else:
