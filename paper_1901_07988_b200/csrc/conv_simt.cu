@@ -310,6 +310,8 @@ int qt_tc_conv_dgrad(const float *gr, const float *w, float *gx, const qt::ConvG
 int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
                      const qt::ConvGeo &g, void *ws, cudaStream_t st);
 int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g);
+int qt_tc_conv_wgrad_s2d(const float *gr, qt_tape_t act, float *grad_w, const qt::ConvGeo &g,
+                         void *ws, cudaStream_t st);
 int64_t qt_tc_s2d_workspace(const qt::ConvGeo &g);
 int qt_tc_conv_s2d_forward(const float *x, const float *w, float *out, const qt::ConvGeo &g,
                            const float *res, int64_t cr, int64_t sr, void *ws, cudaStream_t s);
@@ -389,6 +391,10 @@ extern "C" int qt_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plai
     QT_REQUIRE(x_plain || act.a2 || (act.codes && act.step && act.offset && qt_bits_ok(act.bits)));
     int rc0 = qt_tc_conv_wgrad(gr, act, x_plain, grad_w, g, ws, qt_s(stream));
     if (rc0 != QT_EUNSUPPORTED) return rc0;
+    if (!x_plain) {   // 2x2/s2 on codes: 1x1 of the rearranged (space-to-depth) tape
+        rc0 = qt_tc_conv_wgrad_s2d(gr, act, grad_w, g, ws, qt_s(stream));
+        if (rc0 != QT_EUNSUPPORTED) return rc0;
+    }
     const int64_t M = co, N = ci * kh * kw, K = n * g.oh * g.ow;
     int64_t kps, splits;
     wgrad_plan(g, kps, splits);

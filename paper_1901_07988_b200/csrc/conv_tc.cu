@@ -794,9 +794,52 @@ __global__ void space_depth_kernel(const float *src, float *dst, int64_t n, int6
     }
 }
 
+// s == 2 with w % 4 == 0: a thread moves a 2-row x 4-column patch -- two
+// float4 on the full-resolution side, four float2 (one per (u, v) plane) on
+// the depth side; 32-bit indices through FastDiv
+template <bool TO_DEPTH>
+__global__ void space_depth2_kernel(const float *src, float *dst, uint32_t total, uint32_t h,
+                                    uint32_t w, FastDiv qd, FastDiv yd) {
+    pdl_enter();
+    const uint32_t w4 = w >> 2, h2 = h >> 1, w2 = w >> 1, plane2 = h2 * w2;
+    for (uint32_t t = blockIdx.x * blockDim.x + threadIdx.x; t < total; t += gridDim.x * blockDim.x) {
+        const uint32_t r = fast_div(t, qd), q = t - r * w4;       // r = plane * h2 + Y
+        const uint32_t pl = fast_div(r, yd), Y = r - pl * h2;
+        const size_t full = ((size_t)pl * h + 2 * Y) * w + 4 * q;
+        const size_t dep = (size_t)pl * 4 * plane2 + (size_t)Y * w2 + 2 * q;
+        float4 *f0 = const_cast<float4 *>(reinterpret_cast<const float4 *>((TO_DEPTH ? src : dst) + full));
+        float4 *f1 = const_cast<float4 *>(reinterpret_cast<const float4 *>((TO_DEPTH ? src : dst) + full + w));
+        float2 *d = const_cast<float2 *>(reinterpret_cast<const float2 *>((TO_DEPTH ? dst : src) + dep));
+        if (TO_DEPTH) {
+            const float4 a = __ldg(f0), b = __ldg(f1);
+            d[0] = make_float2(a.x, a.z);                   // (u, v) = (0, 0)
+            d[plane2 / 2] = make_float2(a.y, a.w);          // (0, 1)
+            d[plane2] = make_float2(b.x, b.z);              // (1, 0)
+            d[3 * plane2 / 2] = make_float2(b.y, b.w);      // (1, 1)
+        } else {
+            const float2 p00 = d[0], p01 = d[plane2 / 2], p10 = d[plane2], p11 = d[3 * plane2 / 2];
+            *f0 = make_float4(p00.x, p01.x, p00.y, p01.y);
+            *f1 = make_float4(p10.x, p11.x, p10.y, p11.y);
+        }
+    }
+}
+
 static int space_depth(const float *src, float *dst, int64_t n, int64_t c, int64_t h, int64_t w,
                        int s, bool to_depth, cudaStream_t st) {
     const int64_t total = n * c * h * w;
+    if (s == 2 && w % 4 == 0 && h % 2 == 0 && (h / 2) * (w / 2) % 2 == 0 && total / 8 < (1ll << 31)) {
+        const uint32_t t8 = (uint32_t)(total / 8);
+        const unsigned blocks = (unsigned)std::min<int64_t>(qt_cdiv(t8, 256), 148 * 8);
+        const FastDiv qd = make_fastdiv((uint32_t)(w / 4)), yd = make_fastdiv((uint32_t)(h / 2));
+        if (to_depth)
+            launch_pdl(space_depth2_kernel<true>, blocks, 256, 0, st, src, dst, t8, (uint32_t)h,
+                       (uint32_t)w, qd, yd);
+        else
+            launch_pdl(space_depth2_kernel<false>, blocks, 256, 0, st, src, dst, t8, (uint32_t)h,
+                       (uint32_t)w, qd, yd);
+        QT_CHECK_LAUNCH();
+        return QT_OK;
+    }
     const unsigned blocks = (unsigned)std::min<int64_t>(qt_cdiv(total, 256), 148 * 16);
     if (to_depth)
         launch_pdl(space_depth_kernel<true>, blocks, 256, 0, st, src, dst, n, c, h, w, s);

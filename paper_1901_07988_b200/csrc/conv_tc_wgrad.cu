@@ -141,6 +141,11 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false) {
     }();
     int want = std::max(1, ctas / pl.mgroups);     // one wave: fixed costs paid once per SM
     want = std::min(want, std::max(1, pl.total / SUB));
+    // a CTA's stages run concurrently on its operand groups, so give each
+    // CTA at least one stage per group: the kernel takes about as long on
+    // fewer SMs (latency-bound), leaves the rest to the input-gradient chain
+    // running beside it, and writes fewer partials
+    want = std::min(want, std::max(1, pl.total / (SUB * pl.ops)));
     const double gbytes_all = 128.0 * g.co * pl.total;
     const double part_cap = std::max(4.0 * gbytes_all, 32.0 * 1024 * 1024);
     want = std::min(want, std::max(1, (int)(part_cap / (4.0 * (double)Rout * g.co))));
@@ -160,7 +165,76 @@ static bool tcw_disabled() {
     return e && *e && *e != '0';
 }
 
+// ------------------------------------------------------------------------
+// Kernel == stride 2 (the 2x2/s2 transitions) on a packed code tape: the
+// weight gradient is the 1x1 weight gradient of the space-to-depth input
+//   x'[n][(c*2 + u)*2 + v][y][x] = x[n][c][2y + u][2x + v]
+// with dW viewed as (co, 4 ci) -- the same memory.  Codes move, not values:
+// one 32-bit word of x' codes takes every other code of two words of an input
+// row, and step'/offset' repeat each channel's constants 4x.  The tensor-core
+// path then runs its FAST / GENERIC modes on the rearranged tape unchanged.
+namespace qt {
+
+__global__ void codes_s2d_kernel(const uint8_t *codes, uint32_t *out, uint32_t words,
+                                 uint32_t h, uint32_t w, int bits, FastDiv wrd, FastDiv hd,
+                                 const double *step, const int64_t *offset, double *step4,
+                                 int64_t *offset4, uint32_t c4) {
+    pdl_enter();
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid < c4) {
+        step4[tid] = step[tid >> 2];
+        offset4[tid] = offset[tid >> 2];
+    }
+    const uint32_t per = 32u / (uint32_t)bits;           // codes per output word
+    const uint32_t wr = (w / 2) / per;                   // output words per x' row
+    const uint32_t h2 = h >> 1;
+    const uint32_t mask = (1u << bits) - 1u;
+    const uint32_t rowb = w * (uint32_t)bits / 8;        // bytes per input row
+    for (uint32_t o = tid; o < words; o += gridDim.x * blockDim.x) {
+        const uint32_t r = fast_div(o, wrd), wi = o - r * wr;   // r = dplane * h2 + y
+        const uint32_t dp = fast_div(r, hd), y = r - dp * h2;    // dp = plane * 4 + u * 2 + v
+        const uint32_t pl = dp >> 2, u = (dp >> 1) & 1u, v = dp & 1u;
+        const uint32_t *src = reinterpret_cast<const uint32_t *>(
+            codes + ((size_t)pl * h + 2 * y + u) * rowb) + 2 * wi;
+        const uint64_t both = (uint64_t)__ldg(src) | ((uint64_t)__ldg(src + 1) << 32);
+        uint32_t acc = 0;
+        for (uint32_t k = 0; k < per; ++k)
+            acc |= ((uint32_t)(both >> ((2 * k + v) * (uint32_t)bits)) & mask) << (k * (uint32_t)bits);
+        out[o] = acc;
+    }
+}
+
+static bool wg_s2d_shape(const ConvGeo &g, int bits) {
+    if (g.s != 2 || g.kh != 2 || g.kw != 2 || g.pad != 0 || g.h % 2 || g.w % 2) return false;
+    if (bits != 1 && bits != 2 && bits != 4 && bits != 8) return false;
+    if ((g.w / 2) * bits % 32 || (g.w * bits) % 8) return false;   // whole words per x' row
+    return g.n * g.ci * g.h * g.w * bits / 32 < (1ll << 31);
+}
+
+static ConvGeo wg_s2d_geo(const ConvGeo &g) {
+    ConvGeo d = g;
+    d.ci = g.ci * 4;
+    d.h = g.h / 2;
+    d.w = g.w / 2;
+    d.kh = d.kw = 1;
+    d.s = 1;
+    d.pad = 0;
+    d.oh = d.h;
+    d.ow = d.w;
+    return d;
+}
+
+static int64_t wg_s2d_bytes(const ConvGeo &g, int bits) {   // codes' + step' + offset'
+    return (g.n * g.ci * g.h * g.w * bits / 8 + 255) / 256 * 256 + g.ci * 4 * 16 + 256;
+}
+
+}  // namespace qt
+
 int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g) {
+    if (wg_s2d_shape(g, 8)) {   // the 2x2/s2 rearranged-codes path (widest code width)
+        const ConvGeo d = wg_s2d_geo(g);
+        return wg_s2d_bytes(g, 8) + qt_tc_wgrad_workspace(d);
+    }
     WgPlan a = wg_plan(g, 4), b = wg_plan(g, 0), c = wg_plan(g, 4, true);
     int64_t sp = std::max(a.ok ? a.splits : 0, b.ok ? b.splits : 0);
     sp = std::max(sp, (int64_t)(c.ok ? c.splits : 0));
@@ -267,4 +341,32 @@ int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float
     }
     if (rc) return rc;
     return qt_tc_wgrad_reduce((const float *)ws, pl.splits, g.co * p.Rout, grad_w, st);
+}
+
+// 2x2/s2 weight gradient from a packed code tape through the rearranged tape
+int qt_tc_conv_wgrad_s2d(const float *gr, qt_tape_t act, float *grad_w, const qt::ConvGeo &g,
+                         void *ws, cudaStream_t st) {
+    if (tcw_disabled() || !act.codes || act.a2 || !wg_s2d_shape(g, act.bits)) return QT_EUNSUPPORTED;
+    const ConvGeo d = wg_s2d_geo(g);
+    if (!wg_plan(d, act.bits).ok) return QT_EUNSUPPORTED;
+    if (((uintptr_t)act.codes & 3) || ((uintptr_t)ws & 255)) return QT_EUNSUPPORTED;
+    uint8_t *base = (uint8_t *)ws;
+    const int64_t cbytes = (g.n * g.ci * g.h * g.w * act.bits / 8 + 255) / 256 * 256;
+    uint32_t *codes4 = (uint32_t *)base;
+    double *step4 = (double *)(base + cbytes);
+    int64_t *offset4 = (int64_t *)(base + cbytes + g.ci * 4 * 8);
+    const uint32_t words = (uint32_t)(g.n * g.ci * g.h * g.w * act.bits / 32);
+    const uint32_t per = 32u / (uint32_t)act.bits;
+    const FastDiv wrd = make_fastdiv((uint32_t)(g.w / 2) / per), hd = make_fastdiv((uint32_t)(g.h / 2));
+    const uint32_t c4 = (uint32_t)(g.ci * 4);
+    const uint32_t need = std::max(words, c4);
+    const unsigned blocks = (unsigned)std::min<int64_t>(qt_cdiv(need, 256), 148 * 8);
+    launch_pdl(codes_s2d_kernel, blocks, 256, 0, st, act.codes, codes4, words, (uint32_t)g.h,
+               (uint32_t)g.w, act.bits, wrd, hd, act.step, act.offset, step4, offset4, c4);
+    QT_CHECK_LAUNCH();
+    qt_tape_t t4 = act;
+    t4.codes = (const uint8_t *)codes4;
+    t4.step = step4;
+    t4.offset = offset4;
+    return qt_tc_conv_wgrad(gr, t4, nullptr, grad_w, d, base + wg_s2d_bytes(g, act.bits), st);
 }

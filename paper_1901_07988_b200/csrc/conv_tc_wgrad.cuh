@@ -579,11 +579,13 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         tc_fence_after();
         constexpr int kChunks = NT * (BN / 16);              // items per tile
         const int items = mt_here * kChunks;
-        double scale[2];
+        // fp32 throughout: the pieces sum to within an ulp and fp64 converts
+        // (16/clk/SM) would pace the drain
+        float scale[2];
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
             const int rl = t * 128 + 32 * quarter + lane;
-            scale[t] = (fast && rl < nrows) ? 0.5 * p.tape.step[(row0 + rl) / kk] : 1.0;
+            scale[t] = (fast && rl < nrows) ? (float)(0.5 * p.tape.step[(row0 + rl) / kk]) : 1.f;
         }
 #pragma unroll 1
         for (int it = grp; it < items; it += kWgGroups) {
@@ -606,14 +608,14 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             }
             tmem_wait_ld();
             if (ok) {
-                const double sc = t ? scale[1] : scale[0];
+                const float sc = t ? scale[1] : scale[0];
                 float *dst = p.partial + ((int64_t)split * p.co + cb) * p.Rout + rout;
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
-                    double acc = (double)__uint_as_float(r0[j]);
-                    if (fast && STACK)
-                        acc = acc + (double)__uint_as_float(r1[j]) + (double)__uint_as_float(r2[j]);
-                    const float val = fast ? (float)(acc * sc) : __uint_as_float(r0[j]);
+                    float acc = __uint_as_float(r0[j]);
+                    if (fast && STACK)   // hi + (mid + lo): the small pieces first
+                        acc = __fadd_rn(acc, __fadd_rn(__uint_as_float(r1[j]), __uint_as_float(r2[j])));
+                    const float val = fast ? __fmul_rn(acc, sc) : acc;
                     if (cb + j < p.co) dst[(int64_t)j * p.Rout] = val;
                 }
             }

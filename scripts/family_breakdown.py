@@ -51,7 +51,7 @@ print(f"{fam}: {len(calls)} calls, total {sum(ts):.1f} us")
 from collections import defaultdict
 by = defaultdict(list)
 for a, t in zip(calls, ts):
-    key = tuple(x for x in a if isinstance(x, int) and not isinstance(x, bool))[:6]
+    key = tuple(x for x in a if isinstance(x, int) and not isinstance(x, bool) and x < 1 << 32)[:6]
     by[key].append(t)
 for k, v in sorted(by.items(), key=lambda kv: -sum(kv[1])):
     print(f"  {str(k):40s} n={len(v):3d} avg {sum(v)/len(v):7.2f} us  total {sum(v):8.1f}")

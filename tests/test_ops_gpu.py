@@ -191,3 +191,28 @@ print("ok")
     r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
                        text=True, timeout=300)
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+@pytest.mark.parametrize("shape", [(2, 32, 32, 32), (4, 64, 16, 64), (2, 16, 8, 16)])
+def test_transition_wgrad_from_codes(shape, bits):
+    """2x2/s2 weight gradient from a packed tape (rearranged space-to-depth
+    codes + the 1x1 tensor-core path where eligible, else the SIMT GEMM)
+    against a float64 reference on the dequantized activation."""
+    from paper_1901_07988_b200 import codec
+    n, ci, hw, co = shape
+    torch.manual_seed(bits + ci)
+    for regime in ("narrow", "wide"):
+        x = torch.randn(n, ci, hw, hw, device="cuda")
+        if regime == "narrow":
+            gamma, beta = torch.rand(ci, device="cuda") + 0.5, torch.randn(ci, device="cuda") * 0.1
+        else:
+            gamma, beta = torch.rand(ci, device="cuda") * 0.05 + 0.05, torch.rand(ci, device="cuda") + 1.5
+        t = codec.quantize(x, gamma, beta, bits)
+        act = codec.dequantize(t, relu=True)
+        g = torch.randn(n, co, hw // 2, hw // 2, device="cuda")
+        gw = torch.full((co, ci, 2, 2), 0.25, device="cuda")    # accumulates into gw
+        ops.conv2d_wgrad(g, (co, ci, 2, 2), 2, 0, gw, tape=t.as_native(), in_shape=(n, ci, hw, hw))
+        ref = torch.nn.grad.conv2d_weight(act.double(), (co, ci, 2, 2), g.double(), stride=2) + 0.25
+        err = ((gw.double() - ref).norm() / ref.norm()).item()
+        assert err < CONV_TOL, (regime, err)
