@@ -31,6 +31,10 @@ static Part partition(int64_t n, int64_t c, int64_t hw) {
     (void)c;
     Part p;
     p.planes_per_block = std::max<int64_t>(1, kTargetPerBlock / hw);
+    // at least ~2 blocks per SM: a small layer's single pass is one load
+    // round per block, so spread it rather than lengthen it
+    p.planes_per_block = std::min<int64_t>(p.planes_per_block,
+                                           std::max<int64_t>(1, n * c / (2 * 148)));
     if (p.planes_per_block > n) p.planes_per_block = n;
     p.blocks = qt_cdiv(n, p.planes_per_block);
     return p;

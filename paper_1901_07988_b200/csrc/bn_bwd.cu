@@ -38,6 +38,7 @@ static BwdPart bwd_partition(int64_t n, int64_t c, int64_t hw) {
     (void)c;
     BwdPart p;
     p.ppb = std::max<int64_t>(1, 8192 / hw);
+    p.ppb = std::min<int64_t>(p.ppb, std::max<int64_t>(1, n * c / (2 * 148)));   // >= ~2 blocks / SM
     if (p.ppb > n) p.ppb = n;
     p.nb = qt_cdiv(n, p.ppb);
     return p;

@@ -60,7 +60,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn_wg() {
 
 // bits > 0: the activation is a packed code tape of that width; tap: 3x3
 // with the column taps moved into N (4-bit codes, BN <= 32)
-static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false) {
+static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = false) {
     WgPlan pl;
     if (g.s != 1) return pl;
     const int64_t ow = g.ow, oh = g.oh;
@@ -114,7 +114,15 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false) {
         if (pl.cb > 256 || pl.nch > kWgMaxCh) return WgPlan{};
         if (pl.nch * (1 << bits) > kWgLutEntries) return WgPlan{};
         pl.cbytes = pl.cb * pl.nch;
-        pl.lut_floats = 2 * pl.nch * (1 << bits);
+        pl.lut_floats = pl.nch * ((2 << bits) + 2);      // padded channel stride
+    } else if (fbox) {   // fp32 box per stage: the chunk rows plus the pad rows of each channel
+        const int kk = pl.rpc;
+        pl.nch = (int)std::min<int64_t>(g.ci, (mtg * 128 + kk - 1) / kk + (kk > 1 ? 1 : 0));
+        pl.rb = (int)(ow * 4);
+        pl.cb = ((int)(32 / ow) * SUB + 2 * (int)g.pad) * pl.rb;
+        if (pl.cb / 4 > 256 || pl.nch > kWgMaxCh) return WgPlan{};
+        pl.cbytes = pl.cb * pl.nch;
+        pl.fbox = 1;
     }
     gbytes = (SUB * gbytes0 + pl.cbytes + 1023) & ~1023;    // one raw stage
     pl.slot = gbytes;
@@ -235,9 +243,14 @@ int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g) {
         const ConvGeo d = wg_s2d_geo(g);
         return wg_s2d_bytes(g, 8) + qt_tc_wgrad_workspace(d);
     }
-    WgPlan a = wg_plan(g, 4), b = wg_plan(g, 0), c = wg_plan(g, 4, true);
+    WgPlan a = wg_plan(g, 4), b = wg_plan(g, 0), c = wg_plan(g, 4, true), e = wg_plan(g, 0, false, true);
     int64_t sp = std::max(a.ok ? a.splits : 0, b.ok ? b.splits : 0);
     sp = std::max(sp, (int64_t)(c.ok ? c.splits : 0));
+    sp = std::max(sp, (int64_t)(e.ok ? e.splits : 0));
+    for (int bits : {1, 2, 8}) {   // other code widths plan their own splits
+        WgPlan q = wg_plan(g, bits);
+        sp = std::max(sp, (int64_t)(q.ok ? q.splits : 0));
+    }
     return sp * g.co * g.ci * g.kh * g.kw * (int64_t)sizeof(float);
 }
 
@@ -271,6 +284,7 @@ int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float
     }();
     WgPlan pl{};
     if (codes && use_tap) pl = wg_plan(g, act.bits, true);
+    if (!pl.ok && !codes) pl = wg_plan(g, 0, false, true);   // fp32 rows staged by TMA
     if (!pl.ok) pl = wg_plan(g, codes ? act.bits : 0);
     if (!pl.ok) return QT_EUNSUPPORTED;
     if (codes && ((uintptr_t)act.codes & 15)) return QT_EUNSUPPORTED;
@@ -298,6 +312,18 @@ int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float
         cuuint64_t cs[2] = {(cuuint64_t)plane, (cuuint64_t)(plane * g.ci)};
         cuuint32_t cbx[3] = {(cuuint32_t)pl.cb, (cuuint32_t)pl.nch, 1};
         if (enc(&mc, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void *)act.codes, cd, cs, cbx, es + 1,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return QT_EUNSUPPORTED;
+    } else if (pl.fbox) {   // fp32 source (n, ci, h*w) as 3D (pixel, c, n)
+        const float *src = x_plain ? x_plain : act.a2;
+        if ((uintptr_t)src & 15) return QT_EUNSUPPORTED;
+        const int64_t plane = g.h * g.w;
+        cuuint64_t cd[3] = {(cuuint64_t)plane, (cuuint64_t)g.ci, (cuuint64_t)g.n};
+        cuuint64_t cs[2] = {(cuuint64_t)plane * 4, (cuuint64_t)(plane * g.ci * 4)};
+        cuuint32_t cbx[3] = {(cuuint32_t)(pl.cb / 4), (cuuint32_t)pl.nch, 1};
+        if (plane * 4 % 16 ||
+            enc(&mc, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)src, cd, cs, cbx, es + 1,
                 CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
                 CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
             return QT_EUNSUPPORTED;
@@ -329,6 +355,7 @@ int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float
     p.cbytes = pl.cbytes;
     p.rb = pl.rb;
     p.lut = codes ? 1 : 0;
+    p.fbox = pl.fbox;
     p.dbg_nocodes = getenv("QTAPE_WG_NOCODES") ? 1 : 0;
     int rc;
     switch (pl.bn) {

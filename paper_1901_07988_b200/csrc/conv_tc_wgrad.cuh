@@ -75,6 +75,7 @@ struct WgParams {
     int total_chunks, chunks_per_split, splits;
     int RG, OPS, OPS_G;      // raw ring, operand ring (FAST), operand ring (GENERIC)
     int lut;                 // codes: smem code table in use
+    int fbox;                // fp32 source (plain input / exact tape) staged per stage by TMA
     int lut_floats;          // smem table size (floats)
     int slot;                // raw ring slot stride: g tile + code box (bytes)
     int cb;                  // code box bytes per channel (16-byte multiple)
@@ -100,32 +101,35 @@ __device__ __forceinline__ float act_f32(const WgParams &p, int nn, int c, int y
 // GENERIC operand: 16 consecutive chunk pixels [P0, P0+16) of act row
 // (c, u, v) as TF32 (hi, lo) -- the reference's fp32 relu(decode) from the
 // smem code box through the per-channel table, or the fp32 source value.
-template <int OW, int P0>
-__device__ __forceinline__ void generic_half(const WgParams &p, const uint8_t *cst, int cbox,
-                                             int wbase, int nn, int c, int y0, int u, int sh,
-                                             const float *lut, uint32_t (&hv)[16],
-                                             uint32_t (&lv)[16]) {
-    const uint32_t *cw = reinterpret_cast<const uint32_t *>(cst);
-    const int bits = p.tape.bits;
-    const uint32_t cm = (1u << bits) - 1u;
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-        const int seg = (P0 + j) / OW, x = (P0 + j) % OW;
-        const int iy = y0 + seg + u - p.pad, sx = x + sh;
-        float hh = 0.f, ll = 0.f;
-        if (iy >= 0 && iy < p.h && sx >= 0 && sx < OW) {
-            if (p.lut) {
-                const int bp = (cbox + iy * p.rb - wbase) * 8 + sx * bits;
-                const uint32_t code = __funnelshift_r(cw[bp >> 5], cw[(bp >> 5) + 1], bp & 31) & cm;
-                hh = lut[2 * code];
-                ll = lut[2 * code + 1];
-            } else {
-                split_tf32(act_f32(p, nn, c, iy, sx), hh, ll);
-            }
-        }
-        hv[j] = __float_as_uint(hh);
-        lv[j] = __float_as_uint(ll);
+// GENERIC operand: pixel i of the chunk for act row (c, u, v), as TF32 (hi,
+// lo) of the reference's fp32 relu(decode(code)) (smem code box through the
+// per-channel table), of the staged fp32 source, or of a global fp32 read.
+// Branch-free: every smem read stays inside the stage's box (the pad rows are
+// in the box; a column one past either edge reads a neighbouring word of the
+// same stage) and out-of-image pixels are zeroed by a select.
+__device__ __forceinline__ void generic_px(const WgParams &p, const uint8_t *cst, int cbox,
+                                           int wbase, int nn, int c, int iy, int sx, int ow,
+                                           const float *lut, uint32_t &hv, uint32_t &lv) {
+    const bool ok = iy >= 0 && iy < p.h && sx >= 0 && sx < ow;
+    float hh, ll;
+    if (p.lut) {
+        const uint32_t *cw = reinterpret_cast<const uint32_t *>(cst);
+        const int bits = p.tape.bits;
+        const int bp = (cbox + iy * p.rb - wbase) * 8 + sx * bits;
+        const uint32_t code =
+            __funnelshift_r(cw[bp >> 5], cw[(bp >> 5) + 1], bp & 31) & ((1u << bits) - 1u);
+        const float2 e = *reinterpret_cast<const float2 *>(lut + 2 * code);
+        hh = e.x;
+        ll = e.y;
+    } else if (p.fbox) {
+        float a = *reinterpret_cast<const float *>(cst + cbox + iy * p.rb - wbase + sx * 4);
+        if (!p.plain) a = (a >= 0.f || isnan(a)) ? a : 0.f;   // exact tape: ReLU
+        split_tf32(a, hh, ll);
+    } else {
+        split_tf32(act_f32(p, nn, c, iy, sx), hh, ll);
     }
+    hv = ok ? __float_as_uint(hh) : 0u;
+    lv = ok ? __float_as_uint(ll) : 0u;
 }
 
 // Operand warps form up to 4 warpgroups (one warp per TMEM lane quarter).
@@ -206,7 +210,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     if (warp == 1) tmem_alloc<512>(tmem_slot);
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmG);
-        if (p.lut) tma_prefetch(&tmC);
+        if (p.lut || p.fbox) tma_prefetch(&tmC);
     }
     // per-CTA code tables: the reference's fp32 relu(decode(code)) split
     // (hi, lo) for GENERIC, and the FAST lane constant 0x4300 + b with
@@ -253,14 +257,17 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const int cc = c_begin + e / ncode, code = e % ncode;
                 float a = decode((uint32_t)code, p.tape.step[cc], p.tape.offset[cc], bits);
                 a = (a >= 0.f || isnan(a)) ? a : 0.f;
-                split_tf32(a, s_lut[2 * e], s_lut[2 * e + 1]);
+                // channel stride 2^(K+1) + 2 floats: lanes on different
+                // channels reading the same code hit different banks
+                float *q = s_lut + (e / ncode) * ((2 << bits) + 2) + 2 * code;
+                split_tf32(a, q[0], q[1]);
             }
         }
         if (threadIdx.x >= 64)   // operand warps: tables complete before use
             asm volatile("bar.sync 2, %0;" ::"n"(kWgThreads - 64) : "memory");
     }
     if (threadIdx.x == 0) WG_TRACE(1);
-    if (threadIdx.x == 0 && tr_)
+    if (threadIdx.x == 64 && tr_)   // an operand thread (warp 0 does not take part in the vote)
         tr_[525] = fast;
     const int ops = fast ? p.OPS : p.OPS_G;
     const uint32_t acc_cols = (uint32_t)(p.mtg * (fast ? FACC : GACC));
@@ -283,6 +290,9 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 if (p.lut && !p.dbg_nocodes)   // 16-byte aligned window of input rows y0-pad ..
                     tma_load_3d(slot + SUB * G_BYTES, &tmC, &raw_full[s],
                                 ((y0 - p.pad) * p.rb) & ~15, c_begin, nn);
+                else if (p.fbox)               // fp32 rows y0-pad .. (OOB rows zero-filled)
+                    tma_load_3d(slot + SUB * G_BYTES, &tmC, &raw_full[s], (y0 - p.pad) * p.ow,
+                                c_begin, nn);
                 yc += SUB;
                 if (yc >= p.chunks_per_img) { yc -= p.chunks_per_img; ++nn; }
                 if (st < 64) WG_TRACE(336 + 3 * st);
@@ -359,7 +369,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         const int quarter = warp & 3;        // TMEM lanes 32*quarter .. +31
         const int tg = threadIdx.x - 64 - 128 * grp;        // 0..127 within the group
         const uint32_t lane_base = tmem + ((uint32_t)(32 * quarter) << 16);
-        const int lut_stride = p.lut ? (2 << p.tape.bits) : 0;
+        const int lut_stride = p.lut ? (2 << p.tape.bits) + 2 : 0;
         // this thread's act rows: tile t -> local row t*128 + 32*quarter + lane
         int rc[2], ru[2], rsh[2];
         bool rok[2];
@@ -390,7 +400,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             const int ys = (kc0 - nn * p.chunks_per_img) * p.rows_per_chunk;
             const uint8_t *graws = graw + s * p.slot;
             const uint8_t *cst = graws + SUB * G_BYTES;               // code box
-            const int wbase = ((ys - p.pad) * p.rb) & ~15;            // its first byte
+            const int wbase = p.fbox ? (ys - p.pad) * p.rb                // its first byte
+                                     : ((ys - p.pad) * p.rb) & ~15;
             for (int sub = 0; sub < nsub; ++sub) {
             const int y0 = ys + sub * p.rows_per_chunk;
             uint8_t *opb = gop + (o * SUB + sub) * OPB;
@@ -543,19 +554,25 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     if (tg == 0 && st < 64 && t == 0) WG_TRACE(3701 + 4 * st + 2 * sub);
                     tmem_st16(lane_base + acol, av);
                 } else {
+                    // a compact loop of 4-pixel quads (x4 TMEM stores): the
+                    // fully unrolled form overflows the instruction cache
                     const float *lut = s_lut + (size_t)(c - c_begin) * lut_stride;
-                    uint32_t hv[16], lv[16];
-                    if (rok[t]) {
-                        generic_half<OW, 0>(p, cst, cbox, wbase, nn, c, y0, u, sh, lut, hv, lv);
-                    } else {
+                    const bool live = rok[t];
+#pragma unroll 1
+                    for (int q4 = 0; q4 < 8; ++q4) {
+                        uint32_t h[4] = {0u, 0u, 0u, 0u}, l[4] = {0u, 0u, 0u, 0u};
+                        if (live) {
 #pragma unroll
-                        for (int x = 0; x < 16; ++x) hv[x] = lv[x] = 0u;
+                            for (int k = 0; k < 4; ++k) {
+                                const int i = 4 * q4 + k;
+                                const int seg = i / OW, x = i - seg * OW;
+                                generic_px(p, cst, cbox, wbase, nn, c, y0 + seg + u - p.pad, x + sh,
+                                           OW, lut, h[k], l[k]);
+                            }
+                        }
+                        tmem_st4(lane_base + acol + 4 * q4, h[0], h[1], h[2], h[3]);
+                        tmem_st4(lane_base + acol + 32 + 4 * q4, l[0], l[1], l[2], l[3]);
                     }
-                    tmem_st16(lane_base + acol, hv);
-                    tmem_st16(lane_base + acol + 32, lv);
-                    if (rok[t]) generic_half<OW, 16>(p, cst, cbox, wbase, nn, c, y0, u, sh, lut, hv, lv);
-                    tmem_st16(lane_base + acol + 16, hv);
-                    tmem_st16(lane_base + acol + 48, lv);
                 }
             }
             }   // sub
@@ -574,7 +591,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         // chunk) dealt round-robin over the groups, each warp its lane
         // quarter (lane = act row); FAST sums the three g pieces and scales
         // by step/2.  Warps whose 32 rows are all past the tile skip.
-        mbar_wait(done, 0);
+        if (grp < ops) mbar_wait(done, 0);    // groups that ran stages: the tail is short
+        else mbar_wait_idle(done, 0);         // idle groups (ring shallower than 4)
         if (tg == 0 && grp == 0) WG_TRACE(330);
         tc_fence_after();
         constexpr int kChunks = NT * (BN / 16);              // items per tile
@@ -641,6 +659,7 @@ struct WgPlan {
     int nch = 0, rb = 0, cb = 0, cbytes = 0, slot = 0;    // code box (codes tapes)
     int lut_floats = 0;
     int tap = 0, rpc = 0;                                 // column taps in N; A rows per channel
+    int fbox = 0;                                         // fp32 source boxed per stage
 };
 
 template <int BN, int OW, int BITS, bool TAP = false>

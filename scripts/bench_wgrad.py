@@ -29,6 +29,10 @@ ap.add_argument("--bits", type=int, default=4)
 a = ap.parse_args()
 dev = torch.device("cuda:0")
 g = torch.Generator(device=dev).manual_seed(0)
+_w = torch.randn(1 << 26, device=dev)      # ~0.3 s of work: clocks up before the first shape
+for _ in range(200):
+    _w.mul_(1.0)
+torch.cuda.synchronize()
 for i, (n, ci, h, w, co, k, pad) in enumerate(SHAPES):
     if a.only >= 0 and i != a.only:
         continue

@@ -12,13 +12,21 @@ shape = [int(v) for v in (sys.argv[1] if len(sys.argv) > 1 else "128,16,32,32,16
 n, ci, h, w, co, k, pad = shape
 dev = torch.device("cuda:0")
 x = torch.randn(n, ci, h, w, device=dev)
-tape = codec.quantize(x, torch.rand(ci, device=dev) + 0.5, torch.randn(ci, device=dev) * 0.1, 4).as_native()
+if os.environ.get("WIDE"):   # offsets beyond the FAST range: GENERIC CTAs
+    tape = codec.quantize(x, torch.rand(ci, device=dev) * 0.05 + 0.05, torch.rand(ci, device=dev) + 1.5,
+                          4).as_native()
+else:
+    tape = codec.quantize(x, torch.rand(ci, device=dev) + 0.5, torch.randn(ci, device=dev) * 0.1,
+                          4).as_native()
 gout = torch.randn(n, co, h, w, device=dev)
 gw = torch.zeros(co, ci, k, k, device=dev)
 lib = N.lib()
 fn = lib.qt_debug_wgrad_trace
 fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
-run = lambda: ops.conv2d_wgrad(gout, (co, ci, k, k), 1, pad, gw, tape=tape, in_shape=(n, ci, h, w))
+if os.environ.get("PLAIN"):
+    run = lambda: ops.conv2d_wgrad(gout, (co, ci, k, k), 1, pad, gw, x_plain=x)
+else:
+    run = lambda: ops.conv2d_wgrad(gout, (co, ci, k, k), 1, pad, gw, tape=tape, in_shape=(n, ci, h, w))
 run()
 torch.cuda.synchronize()
 for cta in (0,):
