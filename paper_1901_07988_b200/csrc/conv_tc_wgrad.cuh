@@ -384,11 +384,18 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             ru[t] = u;
             rsh[t] = v - p.pad;   // TAP: 0 (the column shift is in B)
         }
-        int st = grp < ops ? grp : nst;      // groups beyond the ring depth idle
+        // FAST: group g owns ring stage g (stages g, g+ops, ...).  GENERIC
+        // (coop): the TF32 A operand limits the ring to 1-2 stages, so all
+        // four groups share every stage -- pixel quads and g items dealt
+        // round-robin -- and meet at a named barrier before group 0 arrives.
+        const bool coop = !fast;
+        const int sstep = coop ? 1 : ops;
+        const int gsplit = coop ? grp : 0, gstride = coop ? kWgGroups : 1;
+        int st = coop ? 0 : (grp < ops ? grp : nst);   // FAST groups beyond the ring idle
         int s = st % RG;
-        const int o = grp;                    // this group's operand stage (st % ops)
-        uint32_t phr = (uint32_t)(st / RG) & 1u, pho = (uint32_t)(st / ops) & 1u;
-        for (; st < nst; st += ops) {
+        int o = coop ? 0 : grp;               // operand ring stage
+        uint32_t phr = (uint32_t)(st / RG) & 1u, pho = 0u;
+        for (; st < nst; st += sstep) {
             mbar_wait(&raw_full[s], phr);
             if (tg == 0 && st < 64) WG_TRACE(3 + 5 * st);
             mbar_wait(&op_empty[o], pho ^ 1u);
@@ -412,7 +419,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 // rows (v, co), natural pixel order
                 // items (v, co, 8-px group): three per (co, group), spread over
                 // all 128 threads of the group
-                for (int q = tg; q < 3 * BN * 4; q += 128) {
+                for (int q = tg + 128 * gsplit; q < 3 * BN * 4; q += 128 * gstride) {
                     const int v = q / (BN * 4), qr = q - v * (BN * 4);
                     const int co = qr >> 2, qq = qr & 3, px0 = 8 * qq;
                     const uint32_t rrow = (uint32_t)((co * SUB + sub) * 128);
@@ -498,7 +505,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 }
                 if (tg == 0 && st < 64) WG_TRACE(3700 + 4 * st + 2 * sub);
             } else {   // g tile: TF32 (hi, lo) split into a K-major SW128 tile
-                for (int q = tg; q < G_BYTES / 16; q += 128) {
+                for (int q = tg + 128 * gsplit; q < G_BYTES / 16; q += 128 * gstride) {
                     const int co = q >> 3, ch16 = q & 7;
                     const float4 x = *reinterpret_cast<const float4 *>(
                         graws + swz_off<128>((uint32_t)((co * SUB + sub) * 128 + ch16 * 16)));
@@ -559,7 +566,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     const float *lut = s_lut + (size_t)(c - c_begin) * lut_stride;
                     const bool live = rok[t];
 #pragma unroll 1
-                    for (int q4 = 0; q4 < 8; ++q4) {
+                    for (int q4 = gsplit; q4 < 8; q4 += gstride) {
                         uint32_t h[4] = {0u, 0u, 0u, 0u}, l[4] = {0u, 0u, 0u, 0u};
                         if (live) {
 #pragma unroll
@@ -577,21 +584,35 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             }
             }   // sub
             tmem_wait_st();
-            mbar_arrive(&raw_empty[s]);      // raw slots (g tiles + codes) free for TMA
-            fence_async_smem();
-            tc_fence_before();
-            if (tg == 0 && st < 64) WG_TRACE(5 + 5 * st);
-            if (tg == 96 && st < 64) WG_TRACE(400 + 2 * st);
-            mbar_arrive(&op_full[o]);
-            s += ops;
+            if (coop) {
+                fence_async_smem();
+                tc_fence_before();
+                asm volatile("bar.sync 3, %0;" ::"n"(kWgThreads - 64) : "memory");
+                if (grp == 0) {
+                    mbar_arrive(&raw_empty[s]);
+                    mbar_arrive(&op_full[o]);
+                }
+            } else {
+                mbar_arrive(&raw_empty[s]);      // raw slots (g tiles + codes) free for TMA
+                fence_async_smem();
+                tc_fence_before();
+                if (tg == 0 && st < 64) WG_TRACE(5 + 5 * st);
+                if (tg == 96 && st < 64) WG_TRACE(400 + 2 * st);
+                mbar_arrive(&op_full[o]);
+            }
+            s += sstep;
             if (s >= RG) { s -= RG; phr ^= 1u; }   // RG is a multiple of ops
-            pho ^= 1u;                          // same stage (o == grp), next round
+            if (coop) {
+                if (++o == ops) { o = 0; pho ^= 1u; }
+            } else {
+                pho ^= 1u;                          // same stage (o == grp), next round
+            }
         }
         // epilogue: all four groups drain TMEM -- items (tile, tap, 16-column
         // chunk) dealt round-robin over the groups, each warp its lane
         // quarter (lane = act row); FAST sums the three g pieces and scales
         // by step/2.  Warps whose 32 rows are all past the tile skip.
-        if (grp < ops) mbar_wait(done, 0);    // groups that ran stages: the tail is short
+        if (coop || grp < ops) mbar_wait(done, 0);   // groups that ran stages: short tail
         else mbar_wait_idle(done, 0);         // idle groups (ring shallower than 4)
         if (tg == 0 && grp == 0) WG_TRACE(330);
         tc_fence_after();
