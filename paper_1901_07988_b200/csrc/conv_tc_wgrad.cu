@@ -68,13 +68,18 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = 
     if (g.w != ow) return pl;                    // same-width rows (stride 1, "same" padding)
     if ((oh * ow) % 32 || oh % (32 / ow)) return pl;
     if ((oh * ow / 32) % kWgSub) return pl;           // SUB chunks per stage within one image
-    if (g.co % 16 || g.co > 256 || !(g.kw == 1 || g.kw == 3) || g.pad > 1) return pl;
+    if (g.co % 16 || (g.co > 256 && g.co % 64) || !(g.kw == 1 || g.kw == 3) || g.pad > 1) return pl;
     if (g.kw == 1 && g.pad != 0) return pl;
     if (g.kh != g.kw) return pl;
     if (g.n * oh * ow / 32 > INT32_MAX) return pl;
-    const int bn = g.co <= 16 ? 16 : g.co <= 32 ? 32 : g.co <= 64 ? 64 : g.co <= 128 ? 128 : 256;
+    int bn = g.co <= 16 ? 16 : g.co <= 32 ? 32 : g.co <= 64 ? 64 : g.co <= 128 ? 128 : 256;
+    // wide outputs in blocks of 64 channels (grid z): three stacked bf16
+    // pieces and a four-deep operand ring fit only up to 64 -- the A decode
+    // is repeated per block, cheap for the narrow-input expand layers
+    if (bn > 64 && g.co % 64 == 0 && !tap) bn = 64;
     if (g.co % bn) return pl;
     pl.bn = bn;
+    pl.nblk = (int)(g.co / bn);
     if (tap && !(g.kh == 3 && g.pad == 1 && bn <= 32 && bits == 4)) return WgPlan{};
     pl.tap = tap ? 1 : 0;
     pl.rpc = (int)(tap ? g.kh : g.kh * g.kw);
@@ -147,7 +152,7 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = 
         const char *e = getenv("QTAPE_WG_CTAS");
         return e && atoi(e) > 0 ? atoi(e) : 148;
     }();
-    int want = std::max(1, ctas / pl.mgroups);     // one wave: fixed costs paid once per SM
+    int want = std::max(1, ctas / (pl.mgroups * pl.nblk));   // one wave: fixed costs once per SM
     want = std::min(want, std::max(1, pl.total / SUB));
     // a CTA's stages run concurrently on its operand groups, so give each
     // CTA at least one stage per group: the kernel takes about as long on

@@ -179,6 +179,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int split = blockIdx.x;
+    const int co0 = blockIdx.z * BN;                        // this CTA's output-channel block
     const int row0 = blockIdx.y * p.mtg * 128;              // first M row of this group
     const int nrows = min(p.mtg * 128, p.R - row0);
     const int mt_here = (nrows + 127) / 128;
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const int y0 = yc * p.rows_per_chunk;
                 uint8_t *slot = graw + s * p.slot;
                 mbar_expect_tx(&raw_full[s], SUB * G_BYTES + (p.dbg_nocodes ? 0 : p.cbytes));
-                tma_load_4d(slot, &tmG, &raw_full[s], 0, yc, 0, nn);
+                tma_load_4d(slot, &tmG, &raw_full[s], 0, yc, co0, nn);
                 if (p.lut && !p.dbg_nocodes)   // 16-byte aligned window of input rows y0-pad ..
                     tma_load_3d(slot + SUB * G_BYTES, &tmC, &raw_full[s],
                                 ((y0 - p.pad) * p.rb) & ~15, c_begin, nn);
@@ -648,14 +649,14 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             tmem_wait_ld();
             if (ok) {
                 const float sc = t ? scale[1] : scale[0];
-                float *dst = p.partial + ((int64_t)split * p.co + cb) * p.Rout + rout;
+                float *dst = p.partial + ((int64_t)split * p.co + co0 + cb) * p.Rout + rout;
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     float acc = __uint_as_float(r0[j]);
                     if (fast && STACK)   // hi + (mid + lo): the small pieces first
                         acc = __fadd_rn(acc, __fadd_rn(__uint_as_float(r1[j]), __uint_as_float(r2[j])));
                     const float val = fast ? __fmul_rn(acc, sc) : acc;
-                    if (cb + j < p.co) dst[(int64_t)j * p.Rout] = val;
+                    if (co0 + cb + j < p.co) dst[(int64_t)j * p.Rout] = val;
                 }
             }
         }
@@ -681,6 +682,7 @@ struct WgPlan {
     int lut_floats = 0;
     int tap = 0, rpc = 0;                                 // column taps in N; A rows per channel
     int fbox = 0;                                         // fp32 source boxed per stage
+    int nblk = 1;                                         // output-channel blocks of BN
 };
 
 template <int BN, int OW, int BITS, bool TAP = false>
@@ -692,7 +694,7 @@ static int launch_wg2(const CUtensorMap &m, const CUtensorMap &mc, const WgParam
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
         attr = true;
     }
-    launch_pdl(kern, dim3(pl.splits, pl.mgroups), kWgThreads, pl.smem, st, m, mc, p);
+    launch_pdl(kern, dim3(pl.splits, pl.mgroups, pl.nblk), kWgThreads, pl.smem, st, m, mc, p);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }

@@ -216,3 +216,27 @@ def test_transition_wgrad_from_codes(shape, bits):
         ref = torch.nn.grad.conv2d_weight(act.double(), (co, ci, 2, 2), g.double(), stride=2) + 0.25
         err = ((gw.double() - ref).norm() / ref.norm()).item()
         assert err < CONV_TOL, (regime, err)
+
+
+@pytest.mark.parametrize("shape", [(2, 64, 8, 256, 1), (2, 32, 16, 512, 1), (2, 16, 32, 128, 3),
+                                   (2, 64, 8, 320, 1)])
+def test_wgrad_from_codes_channel_blocks(shape):
+    """Weight gradient from a 4-bit tape for outputs wider than one 64-channel
+    block (grid z) -- FAST and GENERIC CTAs -- against float64."""
+    from paper_1901_07988_b200 import codec
+    n, ci, hw, co, k = shape
+    torch.manual_seed(co + k)
+    for regime in ("narrow", "wide"):
+        x = torch.randn(n, ci, hw, hw, device="cuda")
+        if regime == "narrow":
+            gamma, beta = torch.rand(ci, device="cuda") + 0.5, torch.randn(ci, device="cuda") * 0.1
+        else:
+            gamma, beta = torch.rand(ci, device="cuda") * 0.05 + 0.05, torch.rand(ci, device="cuda") + 1.5
+        t = codec.quantize(x, gamma, beta, 4)
+        act = codec.dequantize(t, relu=True)
+        g = torch.randn(n, co, hw, hw, device="cuda")
+        gw = torch.zeros(co, ci, k, k, device="cuda")
+        ops.conv2d_wgrad(g, (co, ci, k, k), 1, k // 2, gw, tape=t.as_native(), in_shape=(n, ci, hw, hw))
+        ref = torch.nn.grad.conv2d_weight(act.double(), (co, ci, k, k), g.double(), padding=k // 2)
+        err = ((gw.double() - ref).norm() / ref.norm()).item()
+        assert err < CONV_TOL, (regime, err)
