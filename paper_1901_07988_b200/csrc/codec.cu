@@ -446,6 +446,128 @@ __global__ void __launch_bounds__(kThreads) bn_relu_quant_stream(FwdArgs a) {
     }
 }
 
+// Quantize-pack from A2 (codec.quantize, codec.py:123-143) as a streaming
+// kernel: 8 elements (one channel, hw % 8 == 0) per group, two groups in
+// flight per thread, the per-channel constants recomputed per group (one
+// float64 divide per 8 elements, L1-resident gamma/beta), the fp32 fast floor
+// with the exact float64 fallback (quant8).  Threads below C also write the
+// frozen step / offset.
+template <int BITS, bool CLIP>
+__global__ void __launch_bounds__(kThreads) quant_pack_stream(FwdArgs a) {
+    pdl_enter();
+    const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (tid < a.c && a.step) {
+        const ChanCode cc = chan_code(a.gamma[tid], a.beta[tid], BITS);
+        a.step[tid] = cc.step;
+        a.offset[tid] = cc.off;
+    }
+    const int64_t ngroups = a.numel >> 3;
+    const int64_t stride = (int64_t)gridDim.x * kThreads;
+    unsigned long long clip = 0;
+    for (int64_t g0 = tid; g0 < ngroups; g0 += 2 * stride) {
+        const int64_t gs[2] = {g0, g0 + stride};
+        float4 xa[2], xb[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (gs[u] < ngroups) {
+                const float4 *src = reinterpret_cast<const float4 *>(a.x) + 2 * gs[u];
+                xa[u] = __ldcs(src);
+                xb[u] = __ldcs(src + 1);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t gg = gs[u];
+            if (gg >= ngroups) break;
+            const uint32_t plane = fast_div((uint32_t)gg, a.hw8d);
+            const uint32_t ch = plane - fast_div(plane, a.cd) * (uint32_t)a.c;
+            const ChanCode cc = chan_code(__ldg(a.gamma + ch), __ldg(a.beta + ch), BITS);
+            BnConst k;
+            k.scale = cc.scale;
+            k.step = cc.step;
+            k.off = cc.off;
+            k.s1 = __double2float_rn(cc.scale);
+            k.s2 = __double2float_rn(cc.scale - (double)k.s1);
+            const float xv[8] = {xa[u].x, xa[u].y, xa[u].z, xa[u].w, xb[u].x, xb[u].y, xb[u].z, xb[u].w};
+            uint32_t code[8], clipmask;
+            quant8<BITS>(xv, k, code, clipmask);
+            if (CLIP) clip += __popc(clipmask);
+            uint8_t *dst = a.codes + gg * BITS;
+            if (BITS == 8) {
+                uint64_t word = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) word |= (uint64_t)code[j] << (j * 8);
+                *reinterpret_cast<uint2 *>(dst) = make_uint2((uint32_t)word, (uint32_t)(word >> 32));
+            } else {
+                uint32_t w32 = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) w32 |= code[j] << (j * BITS);
+                if (BITS == 4) *reinterpret_cast<uint32_t *>(dst) = w32;
+                else if (BITS == 2) *reinterpret_cast<uint16_t *>(dst) = (uint16_t)w32;
+                else *dst = (uint8_t)w32;
+            }
+        }
+    }
+    if (CLIP) {
+        __shared__ unsigned long long s_clip[kThreads / 32];
+        clip = warp_sum(clip);
+        if ((threadIdx.x & 31) == 0) s_clip[threadIdx.x >> 5] = clip;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            for (int w = 0; w < kThreads / 32; ++w) t += s_clip[w];
+            if (t) atomicAdd(a.clip_count, t);
+        }
+    }
+}
+
+// Unpack + dequantize (codec.dequantize, codec.py:146-156) as a streaming
+// kernel: 8 codes -> 8 fp32 (two float4 stores) per group; decode in float64
+// exactly as the reference (step * ((code + (0.5 - 2^(K-1))) + offset)).
+template <int BITS>
+__global__ void __launch_bounds__(kThreads) dequant_stream(DecArgs a, FastDiv hw8d, FastDiv cd) {
+    pdl_enter();
+    const int64_t ngroups = a.numel >> 3;
+    const int64_t stride = (int64_t)gridDim.x * kThreads;
+    for (int64_t g0 = (int64_t)blockIdx.x * kThreads + threadIdx.x; g0 < ngroups; g0 += 2 * stride) {
+        const int64_t gs[2] = {g0, g0 + stride};
+        uint64_t words[2] = {0, 0};
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            if (gs[u] >= ngroups) continue;
+            const uint8_t *src = a.codes + gs[u] * BITS;
+            if (BITS == 8) {
+                const uint2 w = __ldcs(reinterpret_cast<const uint2 *>(src));
+                words[u] = w.x | ((uint64_t)w.y << 32);
+            } else if (BITS == 4) {
+                words[u] = __ldcs(reinterpret_cast<const unsigned int *>(src));
+            } else if (BITS == 2) {
+                words[u] = __ldcs(reinterpret_cast<const unsigned short *>(src));
+            } else {
+                words[u] = __ldcs(reinterpret_cast<const unsigned char *>(src));
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+            const int64_t gg = gs[u];
+            if (gg >= ngroups) break;
+            const uint32_t plane = fast_div((uint32_t)gg, hw8d);
+            const uint32_t ch = plane - fast_div(plane, cd) * (uint32_t)a.c;
+            const double st = __ldg(a.step + ch);
+            const int64_t of = __ldg(a.offset + ch);
+            float v[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const float d = decode((uint32_t)(words[u] >> (j * BITS)) & ((1u << BITS) - 1u), st, of, BITS);
+                v[j] = a.relu ? relu_np(d) : d;
+            }
+            float4 *dst = reinterpret_cast<float4 *>(a.out) + 2 * gg;
+            __stcs(dst, make_float4(v[0], v[1], v[2], v[3]));
+            __stcs(dst + 1, make_float4(v[4], v[5], v[6], v[7]));
+        }
+    }
+}
+
 template <int BITS>
 static void launch_stream(const FwdArgs &a, unsigned blocks, cudaStream_t s) {
     const bool clip = a.clip_count != nullptr;
@@ -481,6 +603,27 @@ static int launch_fwd(const FwdArgs &a0, bool apply_bn, cudaStream_t s) {
             case 2: launch_stream<2>(a, b, s); break;
             case 4: launch_stream<4>(a, b, s); break;
             case 8: launch_stream<8>(a, b, s); break;
+        }
+        QT_CHECK_LAUNCH();
+        return QT_OK;
+    }
+    if (!apply_bn && a.codes && (a.hw & 7) == 0 && a.hw < (1ll << 31) && a.c < (1ll << 31) &&
+        (((uintptr_t)a.x) & 15) == 0 &&
+        (a.numel >> 3) < (1ll << 31)) {   // quantize-pack from A2: the streaming form
+        const int64_t ngroups = a.numel >> 3;
+        int64_t blocks = std::min<int64_t>(qt_cdiv(ngroups, 2 * kThreads), 148 * 8);
+        blocks = std::max<int64_t>(blocks, qt_cdiv(a.c, kThreads));   // constants for every channel
+        const unsigned b = (unsigned)std::max<int64_t>(blocks, 1);
+        const bool clip = a.clip_count != nullptr;
+        switch (a.bits) {
+            case 1: clip ? launch_pdl(quant_pack_stream<1, true>, b, kThreads, 0, s, a)
+                         : launch_pdl(quant_pack_stream<1, false>, b, kThreads, 0, s, a); break;
+            case 2: clip ? launch_pdl(quant_pack_stream<2, true>, b, kThreads, 0, s, a)
+                         : launch_pdl(quant_pack_stream<2, false>, b, kThreads, 0, s, a); break;
+            case 4: clip ? launch_pdl(quant_pack_stream<4, true>, b, kThreads, 0, s, a)
+                         : launch_pdl(quant_pack_stream<4, false>, b, kThreads, 0, s, a); break;
+            case 8: clip ? launch_pdl(quant_pack_stream<8, true>, b, kThreads, 0, s, a)
+                         : launch_pdl(quant_pack_stream<8, false>, b, kThreads, 0, s, a); break;
         }
         QT_CHECK_LAUNCH();
         return QT_OK;
@@ -568,6 +711,21 @@ extern "C" int qt_unpack_dequant(const uint8_t *codes, int64_t n, int64_t c, int
     QT_REQUIRE(qt_bits_ok(bits) && n >= 0 && c > 0 && hw > 0 && codes && step && offset && out);
     DecArgs d{codes, n * c * hw, c, hw, bits, step, offset, relu, out};
     if (d.numel == 0) return QT_OK;
+    if ((hw & 7) == 0 && hw < (1ll << 31) && c < (1ll << 31) && (((uintptr_t)out) & 15) == 0 &&
+        (d.numel >> 3) < (1ll << 31)) {   // the streaming form
+        const int64_t ngroups = d.numel >> 3;
+        const unsigned b = (unsigned)std::max<int64_t>(
+            std::min<int64_t>(qt_cdiv(ngroups, 2 * kThreads), 148 * 8), 1);
+        const FastDiv hw8d = make_fastdiv((uint32_t)(hw >> 3)), cd = make_fastdiv((uint32_t)c);
+        switch (bits) {
+            case 1: launch_pdl(dequant_stream<1>, b, kThreads, 0, qt_s(stream), d, hw8d, cd); break;
+            case 2: launch_pdl(dequant_stream<2>, b, kThreads, 0, qt_s(stream), d, hw8d, cd); break;
+            case 4: launch_pdl(dequant_stream<4>, b, kThreads, 0, qt_s(stream), d, hw8d, cd); break;
+            case 8: launch_pdl(dequant_stream<8>, b, kThreads, 0, qt_s(stream), d, hw8d, cd); break;
+        }
+        QT_CHECK_LAUNCH();
+        return QT_OK;
+    }
     int64_t blocks = qt_cdiv(d.numel, kBlockElems);
     launch_pdl(unpack_dequant_kernel, (unsigned)blocks, kThreads, 0, qt_s(stream), d);
     QT_CHECK_LAUNCH();
