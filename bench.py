@@ -51,6 +51,20 @@ def _peaks():
         return 6650.0, 1590.0, "fallback"
 
 
+def _traffic(entry, cfg_name):
+    """DRAM bytes per call of ``entry`` from the committed ncu capture
+    (profiles/r1_wgrad_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum
+    over every kernel the entry point launches in one C2 step), else None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r1_wgrad_traffic.json")) as f:
+            t = json.load(f)
+    except Exception:
+        return None
+    if t.get("entry_point") != entry or cfg_name != "C2":
+        return None
+    return t["dram_bytes_per_call"]
+
+
 # ------------------------------------------------------------ cost model
 
 def _geo(args, off):
@@ -385,7 +399,8 @@ def main():
                 "frac": achieved / hbm}
     roof.update({"kernel": name, "launches_per_step": d["launches"],
                  "share_of_step": d["ms"] / total_ms if total_ms else None,
-                 "traffic": None, "peak_kind": peak_kind})
+                 "traffic": _traffic(name, args.config), "peak_kind": peak_kind,
+                 "algorithmic_bytes_per_launch": d["bytes"] / d["launches"] if d["launches"] else None})
     # step roofline: every launch at its own bound (HBM or tensor), summed
     step_roof_ms = 0.0
     for nm, dd in agg.items():
