@@ -55,6 +55,8 @@ struct FwdCfg {
 struct FwdGeo {
     int n, ci, h, w, co, kh, kw, pad, oh, ow;
     int rows, nimg, tiles_per_img;  // tile = nimg images x rows x OW pixels
+    int hw;                         // true pixels per plane (the activation map's extent)
+    int flat;                       // 1x1 on any plane: 128-pixel runs of the flattened plane
     int mtiles, ntiles;             // output tiles along pixels / channels
     int R, NOUT;                    // raw ring and output staging depths
     int G;                          // split warpgroups = operand ring depth (1, 2, 4)
@@ -319,7 +321,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             int n0, h0, co0;
             tile_coords(blockIdx.x, n0, h0, co0);
             mbar_expect_tx(&res_full[0], C::OUT_BYTES);
-            tma_load_4d(out_base, &tmRes, &res_full[0], 0, h0, co0, n0);
+            tma_load_4d(out_base, &tmRes, &res_full[0], g.flat ? h0 * OWT : 0, g.flat ? 0 : h0,
+                        co0, n0);
         }
         int lt = 0;
         for (int T = blockIdx.x; T < total; T += gridDim.x, ++lt) {
@@ -395,7 +398,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             asm volatile("bar.sync 1, %0;" ::"n"(32 * kFwdEpiWarps) : "memory");
             if (leader && lt < 32) CV_TRACE(600 + 4 * lt + 1);
             if (leader) {
-                tma_store_4d(&tmOut, s_out, 0, h0, co0, n0);
+                tma_store_4d(&tmOut, s_out, g.flat ? h0 * OWT : 0, g.flat ? 0 : h0, co0, n0);
                 bulk_commit();
                 // the next tile's staging buffer must have been read by its previous store;
                 // then prefetch the next shortcut tile into it
@@ -407,7 +410,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     const int ob1 = (NOUT > 1) ? ((lt + 1) & 1) : 0;
                     mbar_expect_tx(&res_full[ob1], C::OUT_BYTES);
                     tma_load_4d(out_base + (size_t)ob1 * (C::OUT_BYTES / 4), &tmRes, &res_full[ob1],
-                                0, h1, c1, n1);
+                                g.flat ? h1 * OWT : 0, g.flat ? 0 : h1, c1, n1);
                 }
             }
         }
@@ -503,8 +506,8 @@ static CUtensorMapSwizzle swz(int bytes) {
 static bool make_map_act(CUtensorMap *m, const float *x, const FwdGeo &g, int owt, int kc) {
     auto enc = encode_fn();
     if (!enc) return false;
-    cuuint64_t dims[3] = {(cuuint64_t)g.h * g.w, (cuuint64_t)g.ci, (cuuint64_t)g.n};
-    cuuint64_t strides[2] = {(cuuint64_t)g.h * g.w * 4, (cuuint64_t)g.ci * g.h * g.w * 4};
+    cuuint64_t dims[3] = {(cuuint64_t)g.hw, (cuuint64_t)g.ci, (cuuint64_t)g.n};
+    cuuint64_t strides[2] = {(cuuint64_t)g.hw * 4, (cuuint64_t)g.ci * g.hw * 4};
     cuuint32_t box[3] = {(cuuint32_t)(g.rows * owt), (cuuint32_t)kc, (cuuint32_t)g.nimg};
     cuuint32_t es[3] = {1, 1, 1};
     return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, (void *)x, dims, strides, box, es,
@@ -632,8 +635,24 @@ static bool make_map_nchw(CUtensorMap *m, const float *t, int n, int c, int h, i
                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// Shape predicate of the tensor-core path (also used by qt_conv_uses_tc).
-static bool tc_shape_ok(int n, int ci, int h, int wd, int co, int kh, int kw, int pad) {
+// (hw, 1, c, n) view of an NCHW fp32 tensor for the flattened 1x1 mode: box =
+// 128 consecutive pixels of one plane x BN channels (the last run of a plane
+// is partial: TMA zero-fills the load and clips the store)
+static bool make_map_flat(CUtensorMap *m, const float *t, int n, int c, int hw, int bn) {
+    auto enc = encode_fn();
+    if (!enc) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)hw, 1, (cuuint64_t)c, (cuuint64_t)n};
+    cuuint64_t strides[3] = {(cuuint64_t)hw * 4, (cuuint64_t)hw * 4, (cuuint64_t)c * hw * 4};
+    cuuint32_t box[4] = {128, 1, (cuuint32_t)bn, 1};
+    cuuint32_t es[4] = {1, 1, 1, 1};
+    return enc(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void *)t, dims, strides, box, es,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// Row-tiled form: output rows of 8/16/32 px, whole rows (or whole images) per
+// 128-pixel tile.
+static bool tc_rows_ok(int n, int ci, int h, int wd, int co, int kh, int kw, int pad) {
     const int oh = h + 2 * pad - kh + 1, ow = wd + 2 * pad - kw + 1;
     if (kw != 1 && kw != 3) return false;
     if (kw == 1 && pad != 0) return false;
@@ -642,6 +661,19 @@ static bool tc_shape_ok(int n, int ci, int h, int wd, int co, int kh, int kw, in
     const int per = 128 / ow;
     if (oh >= per) return oh % per == 0;
     return per % oh == 0 && n % (per / oh) == 0;
+}
+
+// Flattened form: a 1x1 conv is a per-pixel GEMM, so any plane whose byte
+// stride is a 16-byte multiple (TMA) tiles as 128-pixel runs
+static bool tc_flat_ok(int ci, int h, int wd, int co, int kh, int kw, int pad) {
+    if (kh != 1 || kw != 1 || pad != 0 || ci % 16 || co % 16) return false;
+    const int64_t hw = (int64_t)h * wd;
+    return hw % 4 == 0 && hw >= 16 && hw < (1 << 30);
+}
+
+// Shape predicate of the tensor-core path (also used by qt_conv_uses_tc).
+static bool tc_shape_ok(int n, int ci, int h, int wd, int co, int kh, int kw, int pad) {
+    return tc_rows_ok(n, ci, h, wd, co, kh, kw, pad) || tc_flat_ok(ci, h, wd, co, kh, kw, pad);
 }
 
 // Runs out = conv_s1(x, W') with W' the (possibly transposed+flipped) kernel.
@@ -653,14 +685,27 @@ static int tc_conv_s1(const float *x, const float *w, float *out, int n, int ci,
     g.n = n; g.ci = ci; g.h = h; g.w = wd; g.co = co; g.kh = kh; g.kw = kw; g.pad = pad;
     g.oh = h + 2 * pad - kh + 1;
     g.ow = wd + 2 * pad - kw + 1;
-    if (!tc_shape_ok(n, ci, h, wd, co, kh, kw, pad)) return QT_EUNSUPPORTED;
-    const int per = 128 / g.ow;                         // rows per 128-pixel tile
-    if (g.oh >= per) {
-        if (g.oh % per) return QT_EUNSUPPORTED;
-        g.rows = per; g.nimg = 1; g.tiles_per_img = g.oh / per;
+    g.hw = h * wd;
+    if (tc_rows_ok(n, ci, h, wd, co, kh, kw, pad)) {
+        const int per = 128 / g.ow;                     // rows per 128-pixel tile
+        if (g.oh >= per) {
+            g.rows = per; g.nimg = 1; g.tiles_per_img = g.oh / per;
+        } else {
+            g.rows = g.oh; g.nimg = per / g.oh; g.tiles_per_img = 1;
+        }
+    } else if (tc_flat_ok(ci, h, wd, co, kh, kw, pad)) {
+        if (res && sr != 1) {   // strided shortcut: the conv, then the standalone add
+            int rc = tc_conv_s1(x, w, out, n, ci, h, wd, co, kh, kw, pad, flip, nullptr, 0, 1, ws, st);
+            if (rc) return rc;
+            return qt_shortcut_add(out, res, n, co, h, wd, cr, sr, st);
+        }
+        // virtual rows of 32 px: tile t = pixels [128 t, 128 t + 128) of the plane
+        g.flat = 1;
+        g.w = g.ow = 32;
+        g.h = g.oh = (g.hw + 31) / 32;
+        g.rows = 4; g.nimg = 1; g.tiles_per_img = (g.hw + 127) / 128;
     } else {
-        if (per % g.oh || n % (per / g.oh)) return QT_EUNSUPPORTED;
-        g.rows = g.oh; g.nimg = per / g.oh; g.tiles_per_img = 1;
+        return QT_EUNSUPPORTED;
     }
     const int kc = (kw == 1 && ci % 32 == 0) ? 32 : 16;
     int bn = co <= 16 ? 16 : (co <= 32 ? 32 : (co <= 64 ? 64 : 128));
@@ -682,12 +727,14 @@ static int tc_conv_s1(const float *x, const float *w, float *out, int n, int ci,
     if (!make_map_act(&mp.a, x, g, g.ow, kc) ||
         !make_map_w(&mp.bh, bhi, co, ci, kh * kw, bn, kc, kw) ||
         !make_map_w(&mp.bl, blo, co, ci, kh * kw, bn, kc, kw) ||
-        !make_map_nchw(&mp.out, out, n, co, g.oh, g.ow, g.rows, bn, g.nimg))
+        !(g.flat ? make_map_flat(&mp.out, out, n, co, g.hw, bn)
+                 : make_map_nchw(&mp.out, out, n, co, g.oh, g.ow, g.rows, bn, g.nimg)))
         return QT_EUNSUPPORTED;
     EpiParams ep{out, res, cr, sr, 0};
     mp.res = mp.out;
     if (res && sr == 1) {  // same-resolution shortcut: one TMA box per tile (channels >= cr -> 0)
-        if (!make_map_nchw(&mp.res, res, n, cr, g.oh, g.ow, g.rows, bn, g.nimg))
+        if (!(g.flat ? make_map_flat(&mp.res, res, n, cr, g.hw, bn)
+                     : make_map_nchw(&mp.res, res, n, cr, g.oh, g.ow, g.rows, bn, g.nimg)))
             return QT_EUNSUPPORTED;
         ep.res_tma = 1;
     }

@@ -22,6 +22,12 @@ GEOS = [  # (n, ci, h, co, k, s, p)
     (2, 32, 16, 32, 3, 1, 1), (2, 16, 32, 64, 1, 1, 0), (6, 8, 8, 16, 3, 1, 1),
     # kernel == stride transitions: space-to-depth + tensor-core 1x1
     (2, 32, 32, 32, 2, 2, 0), (4, 64, 16, 64, 2, 2, 0),
+    # 1x1 on any plane (flattened 128-pixel runs; last run partial): ImageNet
+    # widths 56/28/14, a 12-wide plane, 7x7 (SIMT: plane not 16-byte aligned),
+    # and the 4x4/s4 stem / 2x2/s2 transitions landing on them via s2d
+    (2, 64, 14, 32, 1, 1, 0), (2, 32, 28, 64, 1, 1, 0), (1, 16, 56, 16, 1, 1, 0),
+    (3, 48, 12, 16, 1, 1, 0), (2, 32, 7, 32, 1, 1, 0), (2, 16, 56, 32, 2, 2, 0),
+    (1, 3, 64, 16, 4, 4, 0),
 ]
 
 
@@ -81,6 +87,22 @@ def test_conv_residual_fused():
     want = y.copy()
     want[:, :4] += res[:, :, ::2, ::2]
     got = host(ops.conv2d_forward(dev(x), dev(w), 2, 0, residual=dev(res)))
+    assert norm_err(got, want) < CONV_TOL
+
+
+@pytest.mark.parametrize("geo", [(2, 16, 28, 32, 1), (2, 32, 14, 64, 2), (2, 16, 56, 32, 2)])
+def test_conv_residual_flat_1x1(geo):
+    """Residual add on the flattened 1x1 path: same-resolution (fused, one TMA
+    box per 128-pixel run) and strided (standalone add after the conv)."""
+    n, ci, h, co, sr = geo
+    rng = np.random.default_rng(sum(geo))
+    x = rng.standard_normal((n, ci, h, h)).astype(np.float32)
+    w = rng.standard_normal((co, ci, 1, 1)).astype(np.float32)
+    cr = co // 2
+    res = rng.standard_normal((n, cr, h * sr, h * sr)).astype(np.float32)
+    want = O.conv_fwd(x, w, 1, 0)
+    want[:, :cr] += res[:, :, ::sr, ::sr]
+    got = host(ops.conv2d_forward(dev(x), dev(w), 1, 0, residual=dev(res)))
     assert norm_err(got, want) < CONV_TOL
 
 
