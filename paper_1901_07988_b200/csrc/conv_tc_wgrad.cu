@@ -224,6 +224,22 @@ static bool wg_s2d_shape(const ConvGeo &g, int bits) {
     return g.n * g.ci * g.h * g.w * bits / 32 < (1ll << 31);
 }
 
+// A 1x1 / stride 1 / pad 0 weight gradient only sees pixels, so a plane of
+// hw % 64 == 0 pixels (e.g. 56x56) can be read as rows of 32 -- the same
+// bytes in memory, codes and g alike -- when its own width is not 8/16/32.
+static bool wg_flat_shape(const ConvGeo &g) {
+    if (g.kh != 1 || g.kw != 1 || g.s != 1 || g.pad != 0) return false;
+    if (g.w == 8 || g.w == 16 || g.w == 32) return false;
+    return (g.h * g.w) % 64 == 0;
+}
+
+static ConvGeo wg_flat_geo(const ConvGeo &g) {
+    ConvGeo d = g;
+    d.w = d.ow = 32;
+    d.h = d.oh = g.h * g.w / 32;
+    return d;
+}
+
 static ConvGeo wg_s2d_geo(const ConvGeo &g) {
     ConvGeo d = g;
     d.ci = g.ci * 4;
@@ -244,6 +260,7 @@ static int64_t wg_s2d_bytes(const ConvGeo &g, int bits) {   // codes' + step' + 
 }  // namespace qt
 
 int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g) {
+    if (wg_flat_shape(g)) return qt_tc_wgrad_workspace(wg_flat_geo(g));
     if (wg_s2d_shape(g, 8)) {   // the 2x2/s2 rearranged-codes path (widest code width)
         const ConvGeo d = wg_s2d_geo(g);
         return wg_s2d_bytes(g, 8) + qt_tc_wgrad_workspace(d);
@@ -277,8 +294,9 @@ int qt_tc_wgrad_reduce(const float *partial, int64_t splits, int64_t count, floa
 }
 
 int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
-                     const qt::ConvGeo &g, void *ws, cudaStream_t st) {
+                     const qt::ConvGeo &g0, void *ws, cudaStream_t st) {
     if (tcw_disabled()) return QT_EUNSUPPORTED;
+    const ConvGeo g = wg_flat_shape(g0) ? wg_flat_geo(g0) : g0;
     const bool codes = !x_plain && !act.a2;
     // 3x3 on 4-bit codes with the column taps in N: correct (tested) but not
     // yet faster than the (ci, u, v)-row form -- its g split triples -- so

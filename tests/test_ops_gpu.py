@@ -241,7 +241,7 @@ def test_transition_wgrad_from_codes(shape, bits):
 
 
 @pytest.mark.parametrize("shape", [(2, 64, 8, 256, 1), (2, 32, 16, 512, 1), (2, 16, 32, 128, 3),
-                                   (2, 64, 8, 320, 1)])
+                                   (2, 64, 8, 320, 1), (2, 16, 56, 32, 1), (1, 64, 24, 64, 1)])
 def test_wgrad_from_codes_channel_blocks(shape):
     """Weight gradient from a 4-bit tape for outputs wider than one 64-channel
     block (grid z) -- FAST and GENERIC CTAs -- against float64."""
