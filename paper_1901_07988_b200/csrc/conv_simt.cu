@@ -317,6 +317,14 @@ int qt_tc_conv_s2d_forward(const float *x, const float *w, float *out, const qt:
                            const float *res, int64_t cr, int64_t sr, void *ws, cudaStream_t s);
 int qt_tc_conv_s2d_dgrad(const float *gr, const float *w, float *gx, const qt::ConvGeo &g,
                          void *ws, cudaStream_t s);
+int64_t qt_tc_seg_workspace(const qt::ConvGeo &g);
+int qt_tc_conv_seg_forward(const float *x, const float *w, float *out, const qt::ConvGeo &g,
+                           const float *res, int64_t cr, int64_t sr, void *ws, cudaStream_t st);
+int qt_tc_conv_seg_dgrad(const float *gr, const float *w, float *gx, const qt::ConvGeo &g,
+                         void *ws, cudaStream_t st);
+int64_t qt_tc_seg_wgrad_workspace(const qt::ConvGeo &g);
+int qt_tc_conv_seg_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
+                         const qt::ConvGeo &g, void *ws, cudaStream_t st);
 int qt_tc_wgrad_reduce(const float *partial, int64_t splits, int64_t count, float *grad_w,
                        cudaStream_t st);
 
@@ -328,7 +336,7 @@ extern "C" int64_t qt_conv_workspace_ex(int64_t n, int64_t ci, int64_t h, int64_
                                         int64_t kh, int64_t kw, int64_t stride, int64_t pad) {
     ConvGeo g = make_geo(n, ci, h, wd, co, kh, kw, stride, pad);
     int64_t need = qt_conv_workspace(ci, co, kh, kw);
-    if (geo_ok(g)) need = std::max(need, qt_tc_s2d_workspace(g));
+    if (geo_ok(g)) need = std::max({need, qt_tc_s2d_workspace(g), qt_tc_seg_workspace(g)});
     return need;
 }
 
@@ -344,6 +352,9 @@ extern "C" int qt_conv_forward(const float *x, const float *w, float *out, int64
     QT_REQUIRE(w);
     if (ws_bytes_ok(ws)) {   // kernel == stride: space-to-depth + tensor-core 1x1
         rc = qt_tc_conv_s2d_forward(x, w, out, g, res, cr, sr, ws, qt_s(stream));
+        if (rc != QT_EUNSUPPORTED) return rc;
+        // other plane widths: segmented copy + tensor-core rows
+        rc = qt_tc_conv_seg_forward(x, w, out, g, res, cr, sr, ws, qt_s(stream));
         if (rc != QT_EUNSUPPORTED) return rc;
     }   // NULL (prepared operand in ws) is only valid on the tensor-core path
     FwdA la{x, g};
@@ -364,6 +375,8 @@ extern "C" int qt_conv_dgrad(const float *gr, const float *w, float *gx, int64_t
     if (ws_bytes_ok(ws)) {
         rc = qt_tc_conv_s2d_dgrad(gr, w, gx, g, ws, qt_s(stream));
         if (rc != QT_EUNSUPPORTED) return rc;
+        rc = qt_tc_conv_seg_dgrad(gr, w, gx, g, ws, qt_s(stream));
+        if (rc != QT_EUNSUPPORTED) return rc;
     }
     DgradA la{gr, g};
     DgradB lb{w, g};
@@ -378,7 +391,8 @@ extern "C" int64_t qt_conv_wgrad_workspace(int64_t n, int64_t ci, int64_t h, int
     if (!geo_ok(g)) return 0;
     int64_t kps, splits;
     wgrad_plan(g, kps, splits);
-    return std::max(splits * co * ci * kh * kw * (int64_t)sizeof(float), qt_tc_wgrad_workspace(g)) +
+    return std::max({splits * co * ci * kh * kw * (int64_t)sizeof(float), qt_tc_wgrad_workspace(g),
+                     qt_tc_seg_wgrad_workspace(g)}) +
            256;
 }
 
@@ -395,6 +409,8 @@ extern "C" int qt_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plai
         rc0 = qt_tc_conv_wgrad_s2d(gr, act, grad_w, g, ws, qt_s(stream));
         if (rc0 != QT_EUNSUPPORTED) return rc0;
     }
+    rc0 = qt_tc_conv_seg_wgrad(gr, act, x_plain, grad_w, g, ws, qt_s(stream));
+    if (rc0 != QT_EUNSUPPORTED) return rc0;
     const int64_t M = co, N = ci * kh * kw, K = n * g.oh * g.ow;
     int64_t kps, splits;
     wgrad_plan(g, kps, splits);

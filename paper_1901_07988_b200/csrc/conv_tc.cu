@@ -938,3 +938,210 @@ int qt_tc_conv_s2d_dgrad(const float *gr, const float *w, float *gx, const qt::C
     if (rc) return rc;
     return space_depth(gd, gx, g.n, g.ci, g.h, g.w, (int)g.s, false, s);
 }
+
+// ---------------------------------------------------------------------------
+// "Same"-padded stride-1 convs whose width is not a tensor-core row width
+// (the ImageNet 56/28/14/7 planes of SURVEY.md Appendix C) run on the
+// row-tiled tensor-core path over a SEGMENTED copy of the plane:
+//   * W <= 32: each row is zero-padded on the right to OWT = 8/16/32 px;
+//   * W > 32: each row is cut into segments of 30 output columns carrying a
+//     one-column halo on both sides (32 px), and segment j of image n becomes
+//     image n * nseg + j of a (N * nseg, C, Hp, 32) tensor.
+// Rows are zero-padded to Hp so tiles hold whole rows (and whole images for
+// small planes).  The kernel's own row-edge mask supplies the left zero
+// column; the padding supplies the right one, so every output column that
+// maps back to the image is exact, and the unsegment pass drops the rest.
+// For the weight gradient the g_out copy is zero outside those columns, so
+// each output pixel contributes exactly once.
+namespace qt {
+
+struct SegGeo {
+    int ok, owt, halo, nseg, step, hp;
+};
+
+constexpr int kWgSubRows = 2;   // = kWgSub (conv_tc_wgrad.cuh): 32-px chunks per wgrad stage
+
+static SegGeo seg_geo(int64_t n, int64_t h, int64_t w, int64_t kh, int64_t kw, int64_t pad) {
+    SegGeo s{};
+    if (kh != 3 || kw != 3 || pad != 1 || h < 1 || w < 1) return s;
+    if (w <= 32) {
+        s.owt = w <= 8 ? 8 : (w <= 16 ? 16 : 32);
+        s.halo = 0; s.nseg = 1; s.step = s.owt;
+    } else {
+        s.owt = 32; s.halo = 1; s.step = 30; s.nseg = (int)((w + 29) / 30);
+    }
+    const int per = 128 / s.owt;
+    auto wg_rows_ok = [&](int hp) {   // weight-gradient row tiling (conv_tc_wgrad.cu:wg_plan)
+        const int chunks = hp * s.owt / 32;
+        return (hp * s.owt) % 32 == 0 && hp % (32 / s.owt) == 0 && chunks % kWgSubRows == 0;
+    };
+    int hp;
+    if (h >= per) {
+        hp = (int)((h + per - 1) / per * per);
+    } else {
+        hp = 1;
+        while (hp < h) hp *= 2;
+        if ((n * s.nseg) % (per / hp) || !wg_rows_ok(hp)) hp = per;
+    }
+    if (!wg_rows_ok(hp)) return s;
+    s.hp = hp;
+    s.ok = 1;
+    return s;
+}
+
+// dst (n*nseg, c, hp, owt) from src (n, c, h, w).  mode 0: fp32 source, copied;
+// 1: g_out, zero outside the segment's own output columns; 2: tape (relu of
+// the decoded pre-activation, layer.py:356) or plain fp32 when src != NULL.
+template <int MODE>
+__global__ void seg_in_kernel(const float *src, qt_tape_t t, float *dst, uint32_t total, int c,
+                              int h, int w, SegGeo s) {
+    pdl_enter();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const uint32_t k = i % (uint32_t)s.owt, r = i / (uint32_t)s.owt;
+        const uint32_t y = r % (uint32_t)s.hp, r2 = r / (uint32_t)s.hp;
+        const uint32_t ch = r2 % (uint32_t)c, m = r2 / (uint32_t)c;
+        const uint32_t nn = m / (uint32_t)s.nseg, j = m - nn * (uint32_t)s.nseg;
+        const int col = (int)(j * s.step + k) - s.halo;
+        bool ok = y < (uint32_t)h && col >= 0 && col < w;
+        if (MODE == 1) ok = ok && (int)k >= s.halo && (int)k < s.halo + s.step;
+        float v = 0.f;
+        if (ok) {
+            const int64_t si = (((int64_t)nn * c + ch) * h + y) * w + col;
+            if (MODE != 2 || src) {
+                v = __ldg(src + si);
+            } else {
+                const float a = tape_value(t, si, (int)ch);
+                v = (a >= 0.f || isnan(a)) ? a : 0.f;
+            }
+        }
+        dst[i] = v;
+    }
+}
+
+// out (n, c, h, w) [+ shortcut res (n, cr, h*sr, w*sr), engine.py:262-269]
+// from the segmented conv result (n*nseg, c, hp, owt)
+__global__ void seg_out_kernel(const float *src, float *out, uint32_t total, int c, int h, int w,
+                               SegGeo s, const float *res, int cr, int sr) {
+    pdl_enter();
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const uint32_t x = i % (uint32_t)w, r = i / (uint32_t)w;
+        const uint32_t y = r % (uint32_t)h, r2 = r / (uint32_t)h;
+        const uint32_t ch = r2 % (uint32_t)c, nn = r2 / (uint32_t)c;
+        const uint32_t j = x / (uint32_t)s.step, k = x - j * s.step + s.halo;
+        const uint32_t m = nn * s.nseg + j;
+        float v = __ldg(src + (((size_t)m * c + ch) * s.hp + y) * s.owt + k);
+        if (res && (int)ch < cr)
+            v = __fadd_rn(v, __ldg(res + (((size_t)nn * cr + ch) * h * sr + (size_t)y * sr) * w * sr +
+                                   (size_t)x * sr));
+        out[i] = v;
+    }
+}
+
+static int64_t seg_elems(const SegGeo &s, int64_t n, int64_t c) {
+    return n * s.nseg * c * s.hp * s.owt;
+}
+
+static unsigned seg_blocks(int64_t total) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(qt_cdiv(total, 256), 148 * 16));
+}
+
+template <int MODE>
+static int seg_in(const float *src, qt_tape_t t, float *dst, int64_t n, int64_t c, int64_t h,
+                  int64_t w, const SegGeo &s, cudaStream_t st) {
+    const int64_t total = seg_elems(s, n, c);
+    launch_pdl(seg_in_kernel<MODE>, seg_blocks(total), 256, 0, st, src, t, dst, (uint32_t)total,
+               (int)c, (int)h, (int)w, s);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+static bool seg_fits(const SegGeo &s, int64_t n, int64_t c, int64_t h, int64_t w) {
+    return s.ok && seg_elems(s, n, c) < (1ll << 31) && n * c * h * w < (1ll << 31);
+}
+
+static int64_t seg_wbytes(int64_t ci, int64_t co) {
+    return (qt_conv_workspace(ci, co, 3, 3) + 255) / 256 * 256;
+}
+
+// stride-1 3x3 "same" conv (forward: flip 0; data gradient: flip 1, ci/co
+// swapped by the caller) through the segmented plane
+static int seg_conv(const float *x, const float *w, float *out, int64_t n, int64_t ci, int64_t h,
+                    int64_t wd, int64_t co, int flip, const float *res, int64_t cr, int64_t sr,
+                    void *ws, cudaStream_t st) {
+    const SegGeo s = seg_geo(n, h, wd, 3, 3, 1);
+    if (!w || !ws || !seg_fits(s, n, ci, h, wd) || !seg_fits(s, n, co, h, wd) || ci % 16 || co % 16)
+        return QT_EUNSUPPORTED;
+    float *xs = (float *)((char *)ws + seg_wbytes(ci, co));
+    float *os = xs + seg_elems(s, n, ci);
+    int rc = seg_in<0>(x, qt_tape_t{}, xs, n, ci, h, wd, s, st);
+    if (rc) return rc;
+    rc = tc_conv_s1(xs, w, os, (int)(n * s.nseg), (int)ci, s.hp, s.owt, (int)co, 3, 3, 1, flip,
+                    nullptr, 0, 1, ws, st);
+    if (rc) return rc;
+    const int64_t total = n * co * h * wd;
+    launch_pdl(seg_out_kernel, seg_blocks(total), 256, 0, st, (const float *)os, out,
+               (uint32_t)total, (int)co, (int)h, (int)wd, s, res, (int)cr, (int)sr);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+}  // namespace qt
+
+// scratch of the segmented forward / data gradient (0: shape not taken)
+int64_t qt_tc_seg_workspace(const qt::ConvGeo &g) {
+    if (g.s != 1) return 0;
+    const SegGeo s = seg_geo(g.n, g.h, g.w, g.kh, g.kw, g.pad);
+    if (!s.ok) return 0;
+    return seg_wbytes(g.ci, g.co) + 4 * seg_elems(s, g.n, g.ci + g.co) + 256;
+}
+
+int qt_tc_conv_seg_forward(const float *x, const float *w, float *out, const qt::ConvGeo &g,
+                           const float *res, int64_t cr, int64_t sr, void *ws, cudaStream_t st) {
+    if (tc_disabled() || g.s != 1 || g.kh != 3 || g.kw != 3 || g.pad != 1) return QT_EUNSUPPORTED;
+    return seg_conv(x, w, out, g.n, g.ci, g.h, g.w, g.co, 0, res, cr, sr, ws, st);
+}
+
+int qt_tc_conv_seg_dgrad(const float *gr, const float *w, float *gx, const qt::ConvGeo &g,
+                         void *ws, cudaStream_t st) {
+    if (tc_disabled() || g.s != 1 || g.kh != 3 || g.kw != 3 || g.pad != 1) return QT_EUNSUPPORTED;
+    return seg_conv(gr, w, gx, g.n, g.co, g.oh, g.ow, g.ci, 1, nullptr, 0, 1, ws, st);
+}
+
+int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
+                     const qt::ConvGeo &g, void *ws, cudaStream_t st);
+int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g);
+
+static qt::ConvGeo seg_wgrad_geo(const qt::ConvGeo &g, const SegGeo &s) {
+    qt::ConvGeo d = g;
+    d.n = g.n * s.nseg;
+    d.h = d.oh = s.hp;
+    d.w = d.ow = s.owt;
+    return d;
+}
+
+int64_t qt_tc_seg_wgrad_workspace(const qt::ConvGeo &g) {
+    if (g.s != 1) return 0;
+    const SegGeo s = seg_geo(g.n, g.h, g.w, g.kh, g.kw, g.pad);
+    if (!s.ok) return 0;
+    const int64_t part = (qt_tc_wgrad_workspace(seg_wgrad_geo(g, s)) + 255) / 256 * 256;
+    return part + 4 * seg_elems(s, g.n, g.ci + g.co) + 256;
+}
+
+// weight gradient: segmented g_out (zero outside each segment's own columns)
+// against the segmented rectified activation, on the fp32-operand path
+int qt_tc_conv_seg_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
+                         const qt::ConvGeo &g, void *ws, cudaStream_t st) {
+    if (tc_disabled() || g.s != 1 || !ws) return QT_EUNSUPPORTED;
+    const SegGeo s = seg_geo(g.n, g.h, g.w, g.kh, g.kw, g.pad);
+    if (!seg_fits(s, g.n, g.ci, g.h, g.w) || !seg_fits(s, g.n, g.co, g.h, g.w)) return QT_EUNSUPPORTED;
+    const qt::ConvGeo d = seg_wgrad_geo(g, s);
+    const int64_t part = (qt_tc_wgrad_workspace(d) + 255) / 256 * 256;
+    if (part <= 0) return QT_EUNSUPPORTED;
+    float *gs = (float *)((char *)ws + part);
+    float *as = gs + seg_elems(s, g.n, g.co);
+    int rc = seg_in<1>(gr, qt_tape_t{}, gs, g.n, g.co, g.h, g.w, s, st);
+    if (rc) return rc;
+    rc = seg_in<2>(x_plain, act, as, g.n, g.ci, g.h, g.w, s, st);
+    if (rc) return rc;
+    return qt_tc_conv_wgrad(gs, qt_tape_t{}, as, grad_w, d, ws, st);
+}

@@ -28,6 +28,12 @@ GEOS = [  # (n, ci, h, co, k, s, p)
     (2, 64, 14, 32, 1, 1, 0), (2, 32, 28, 64, 1, 1, 0), (1, 16, 56, 16, 1, 1, 0),
     (3, 48, 12, 16, 1, 1, 0), (2, 32, 7, 32, 1, 1, 0), (2, 16, 56, 32, 2, 2, 0),
     (1, 3, 64, 16, 4, 4, 0),
+    # 3x3 "same" convs on other plane widths: segmented copy (rows padded to
+    # 8/16/32 px, or 30-column segments with a one-column halo above 32 px)
+    # + tensor-core rows: ImageNet 56/28/14/7, odd widths, an odd batch
+    (2, 16, 56, 16, 3, 1, 1), (2, 32, 28, 32, 3, 1, 1), (2, 64, 14, 32, 3, 1, 1),
+    (2, 64, 7, 64, 3, 1, 1), (3, 16, 7, 16, 3, 1, 1), (1, 16, 40, 32, 3, 1, 1),
+    (2, 16, 3, 16, 3, 1, 1), (1, 32, 61, 16, 3, 1, 1),
 ]
 
 
@@ -92,17 +98,27 @@ def test_conv_residual_fused():
 
 @pytest.mark.parametrize("geo", [(2, 16, 28, 32, 1), (2, 32, 14, 64, 2), (2, 16, 56, 32, 2)])
 def test_conv_residual_flat_1x1(geo):
+    _residual_case(geo, 1)
+
+
+@pytest.mark.parametrize("geo", [(2, 16, 56, 32, 1), (2, 32, 14, 32, 2), (2, 16, 7, 16, 1)])
+def test_conv_residual_segmented_3x3(geo):
+    """Residual add in the unsegment pass of the segmented 3x3 path."""
+    _residual_case(geo, 3)
+
+
+def _residual_case(geo, k):
     """Residual add on the flattened 1x1 path: same-resolution (fused, one TMA
     box per 128-pixel run) and strided (standalone add after the conv)."""
     n, ci, h, co, sr = geo
     rng = np.random.default_rng(sum(geo))
     x = rng.standard_normal((n, ci, h, h)).astype(np.float32)
-    w = rng.standard_normal((co, ci, 1, 1)).astype(np.float32)
+    w = rng.standard_normal((co, ci, k, k)).astype(np.float32)
     cr = co // 2
     res = rng.standard_normal((n, cr, h * sr, h * sr)).astype(np.float32)
-    want = O.conv_fwd(x, w, 1, 0)
+    want = O.conv_fwd(x, w, 1, k // 2)
     want[:, :cr] += res[:, :, ::sr, ::sr]
-    got = host(ops.conv2d_forward(dev(x), dev(w), 1, 0, residual=dev(res)))
+    got = host(ops.conv2d_forward(dev(x), dev(w), 1, k // 2, residual=dev(res)))
     assert norm_err(got, want) < CONV_TOL
 
 
@@ -241,7 +257,9 @@ def test_transition_wgrad_from_codes(shape, bits):
 
 
 @pytest.mark.parametrize("shape", [(2, 64, 8, 256, 1), (2, 32, 16, 512, 1), (2, 16, 32, 128, 3),
-                                   (2, 64, 8, 320, 1), (2, 16, 56, 32, 1), (1, 64, 24, 64, 1)])
+                                   (2, 64, 8, 320, 1), (2, 16, 56, 32, 1), (1, 64, 24, 64, 1),
+                                   (2, 16, 56, 32, 3), (2, 64, 14, 64, 3), (2, 64, 7, 128, 3),
+                                   (2, 32, 28, 32, 3)])
 def test_wgrad_from_codes_channel_blocks(shape):
     """Weight gradient from a 4-bit tape for outputs wider than one 64-channel
     block (grid z) -- FAST and GENERIC CTAs -- against float64."""
