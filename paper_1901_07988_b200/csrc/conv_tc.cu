@@ -957,12 +957,16 @@ namespace qt {
 
 struct SegGeo {
     int ok, owt, halo, nseg, step, hp;
+    int flat;   // weight gradient of a kernel == stride conv (1x1 included): the
+                // (space-to-depth) plane flattened and zero-padded to 64-px multiples
+    int sd;     // flat: the stride (space-to-depth factor of the activation)
 };
 
 constexpr int kWgSubRows = 2;   // = kWgSub (conv_tc_wgrad.cuh): 32-px chunks per wgrad stage
 
 static SegGeo seg_geo(int64_t n, int64_t h, int64_t w, int64_t kh, int64_t kw, int64_t pad) {
     SegGeo s{};
+    s.sd = 1;
     if (kh != 3 || kw != 3 || pad != 1 || h < 1 || w < 1) return s;
     if (w <= 32) {
         s.owt = w <= 8 ? 8 : (w <= 16 ? 16 : 32);
@@ -989,6 +993,22 @@ static SegGeo seg_geo(int64_t n, int64_t h, int64_t w, int64_t kh, int64_t kw, i
     return s;
 }
 
+// Weight gradient of a non-overlapping conv (kernel == stride, no padding; 1x1
+// stride 1 included) whose plane is not a multiple of 64 px: dW is the 1x1
+// weight gradient of the space-to-depth activation (dW viewed as (co, ci s s),
+// the same memory), so both operands are flattened to (n, c, hp * 32) planes,
+// zero-padded to whole 64-pixel pairs of 32-px rows.
+static SegGeo seg_geo_flat(int64_t h, int64_t w, int64_t kh, int64_t kw, int64_t st, int64_t pad) {
+    SegGeo s{};
+    if (kh != kw || kh != st || pad != 0 || h % st || w % st) return s;
+    const int64_t plane = (h / st) * (w / st);
+    s.flat = 1; s.sd = (int)st;
+    s.owt = 32; s.halo = 0; s.nseg = 1; s.step = 32;
+    s.hp = (int)((plane + 63) / 64 * 2);
+    s.ok = 1;
+    return s;
+}
+
 // dst (n*nseg, c, hp, owt) from src (n, c, h, w).  mode 0: fp32 source, copied;
 // 1: g_out, zero outside the segment's own output columns; 2: tape (relu of
 // the decoded pre-activation, layer.py:356) or plain fp32 when src != NULL.
@@ -1004,13 +1024,25 @@ __global__ void seg_in_kernel(const float *src, qt_tape_t t, float *dst, uint32_
         const int col = (int)(j * s.step + k) - s.halo;
         bool ok = y < (uint32_t)h && col >= 0 && col < w;
         if (MODE == 1) ok = ok && (int)k >= s.halo && (int)k < s.halo + s.step;
+        int64_t si = (((int64_t)nn * c + ch) * h + y) * w + col;
+        int tc = (int)ch;
+        if (s.flat) {   // c = source channels x sd^2; (h, w) = source extent
+            const uint32_t p = y * (uint32_t)s.owt + k;
+            const uint32_t wd = (uint32_t)(w / s.sd), sd2 = (uint32_t)(s.sd * s.sd);
+            ok = p < (uint32_t)(h / s.sd) * wd;
+            const uint32_t Y = p / wd, X = p - Y * wd;
+            const uint32_t c0 = ch / sd2, uv = ch - c0 * sd2;
+            const uint32_t u = uv / (uint32_t)s.sd, v = uv - u * (uint32_t)s.sd;
+            const uint32_t cs = (uint32_t)c / sd2;
+            si = (((int64_t)nn * cs + c0) * h + Y * s.sd + u) * w + X * s.sd + v;
+            tc = (int)c0;
+        }
         float v = 0.f;
         if (ok) {
-            const int64_t si = (((int64_t)nn * c + ch) * h + y) * w + col;
             if (MODE != 2 || src) {
                 v = __ldg(src + si);
             } else {
-                const float a = tape_value(t, si, (int)ch);
+                const float a = tape_value(t, si, tc);
                 v = (a >= 0.f || isnan(a)) ? a : 0.f;
             }
         }
@@ -1116,32 +1148,52 @@ static qt::ConvGeo seg_wgrad_geo(const qt::ConvGeo &g, const SegGeo &s) {
     d.n = g.n * s.nseg;
     d.h = d.oh = s.hp;
     d.w = d.ow = s.owt;
+    if (s.flat) {   // 1x1, stride 1 over the (space-to-depth) channels
+        d.ci = g.ci * s.sd * s.sd;
+        d.kh = d.kw = 1;
+        d.s = 1;
+        d.pad = 0;
+    }
     return d;
 }
 
+static SegGeo seg_geo_wgrad(const qt::ConvGeo &g) {
+    const SegGeo f = seg_geo_flat(g.h, g.w, g.kh, g.kw, g.s, g.pad);
+    if (f.ok) return f;
+    return g.s == 1 ? seg_geo(g.n, g.h, g.w, g.kh, g.kw, g.pad) : SegGeo{};
+}
+
 int64_t qt_tc_seg_wgrad_workspace(const qt::ConvGeo &g) {
-    if (g.s != 1) return 0;
-    const SegGeo s = seg_geo(g.n, g.h, g.w, g.kh, g.kw, g.pad);
+    const SegGeo s = seg_geo_wgrad(g);
     if (!s.ok) return 0;
     const int64_t part = (qt_tc_wgrad_workspace(seg_wgrad_geo(g, s)) + 255) / 256 * 256;
-    return part + 4 * seg_elems(s, g.n, g.ci + g.co) + 256;
+    return part + 4 * seg_elems(s, g.n, g.ci * s.sd * s.sd + g.co) + 256;
 }
 
 // weight gradient: segmented g_out (zero outside each segment's own columns)
 // against the segmented rectified activation, on the fp32-operand path
 int qt_tc_conv_seg_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
                          const qt::ConvGeo &g, void *ws, cudaStream_t st) {
-    if (tc_disabled() || g.s != 1 || !ws) return QT_EUNSUPPORTED;
-    const SegGeo s = seg_geo(g.n, g.h, g.w, g.kh, g.kw, g.pad);
-    if (!seg_fits(s, g.n, g.ci, g.h, g.w) || !seg_fits(s, g.n, g.co, g.h, g.w)) return QT_EUNSUPPORTED;
+    if (tc_disabled() || !ws) return QT_EUNSUPPORTED;
+    if (!x_plain && !act.a2 && !act.codes) return QT_EUNSUPPORTED;
+    const SegGeo s = seg_geo_wgrad(g);
+    const int64_t cin = g.ci * (s.flat ? s.sd * s.sd : 1);
+    if (!seg_fits(s, g.n, cin, g.h, g.w) || !seg_fits(s, g.n, g.co, g.h, g.w)) return QT_EUNSUPPORTED;
     const qt::ConvGeo d = seg_wgrad_geo(g, s);
     const int64_t part = (qt_tc_wgrad_workspace(d) + 255) / 256 * 256;
     if (part <= 0) return QT_EUNSUPPORTED;
     float *gs = (float *)((char *)ws + part);
     float *as = gs + seg_elems(s, g.n, g.co);
-    int rc = seg_in<1>(gr, qt_tape_t{}, gs, g.n, g.co, g.h, g.w, s, st);
+    int rc;
+    if (s.flat) {   // g_out is already the flat plane: a 1x1 view of (oh, ow)
+        SegGeo s1 = s;
+        s1.sd = 1;
+        rc = seg_in<1>(gr, qt_tape_t{}, gs, g.n, g.co, g.oh, g.ow, s1, st);
+    } else {
+        rc = seg_in<1>(gr, qt_tape_t{}, gs, g.n, g.co, g.h, g.w, s, st);
+    }
     if (rc) return rc;
-    rc = seg_in<2>(x_plain, act, as, g.n, g.ci, g.h, g.w, s, st);
+    rc = seg_in<2>(x_plain, act, as, g.n, cin, g.h, g.w, s, st);
     if (rc) return rc;
     return qt_tc_conv_wgrad(gs, qt_tape_t{}, as, grad_w, d, ws, st);
 }

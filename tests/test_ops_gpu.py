@@ -232,7 +232,8 @@ print("ok")
 
 
 @pytest.mark.parametrize("bits", [1, 2, 4, 8])
-@pytest.mark.parametrize("shape", [(2, 32, 32, 32), (4, 64, 16, 64), (2, 16, 8, 16)])
+@pytest.mark.parametrize("shape", [(2, 32, 32, 32), (4, 64, 16, 64), (2, 16, 8, 16),
+                                   (2, 32, 56, 64), (2, 64, 14, 32)])
 def test_transition_wgrad_from_codes(shape, bits):
     """2x2/s2 weight gradient from a packed tape (rearranged space-to-depth
     codes + the 1x1 tensor-core path where eligible, else the SIMT GEMM)
@@ -259,7 +260,8 @@ def test_transition_wgrad_from_codes(shape, bits):
 @pytest.mark.parametrize("shape", [(2, 64, 8, 256, 1), (2, 32, 16, 512, 1), (2, 16, 32, 128, 3),
                                    (2, 64, 8, 320, 1), (2, 16, 56, 32, 1), (1, 64, 24, 64, 1),
                                    (2, 16, 56, 32, 3), (2, 64, 14, 64, 3), (2, 64, 7, 128, 3),
-                                   (2, 32, 28, 32, 3)])
+                                   (2, 32, 28, 32, 3), (2, 64, 14, 64, 1), (2, 32, 7, 64, 1),
+                                   (2, 16, 28, 32, 1)])
 def test_wgrad_from_codes_channel_blocks(shape):
     """Weight gradient from a 4-bit tape for outputs wider than one 64-channel
     block (grid z) -- FAST and GENERIC CTAs -- against float64."""
