@@ -1050,6 +1050,41 @@ __global__ void seg_in_kernel(const float *src, qt_tape_t t, float *dst, uint32_
     }
 }
 
+// Flat weight-gradient operand from a packed tape: codes of the (space-to-
+// depth) plane repacked into zero-padded (n, c sd^2, hp * owt) planes in the
+// same K-bit little-endian order (codec.pack_codes, codec.py:59-78), plus the
+// per-channel step / offset repeated sd^2 times.  Padding pixels carry code 0:
+// their g is zero, so any finite decode contributes nothing.
+__global__ void seg_codes_kernel(const uint8_t *codes, uint32_t *dst, uint32_t words, int bits,
+                                 int c4, int h, int w, SegGeo s, const double *step,
+                                 const int64_t *offset, double *step4, int64_t *offset4) {
+    pdl_enter();
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    const uint32_t sd = (uint32_t)s.sd, sd2 = sd * sd;
+    if (tid < (uint32_t)c4) {
+        step4[tid] = step[tid / sd2];
+        offset4[tid] = offset[tid / sd2];
+    }
+    const uint32_t per = 32u / (uint32_t)bits;
+    const uint32_t pw = (uint32_t)(s.hp * s.owt) / per;       // words per padded plane
+    const uint32_t wd = (uint32_t)w / sd, pl = (uint32_t)h / sd * wd;
+    const uint32_t cs = (uint32_t)c4 / sd2;
+    for (uint32_t o = tid; o < words; o += gridDim.x * blockDim.x) {
+        const uint32_t m = o / pw, wi = o - m * pw;
+        const uint32_t nn = m / (uint32_t)c4, ch = m - nn * (uint32_t)c4;
+        const uint32_t c0 = ch / sd2, uv = ch - c0 * sd2, u = uv / sd, v = uv - u * sd;
+        uint32_t acc = 0;
+        for (uint32_t k = 0; k < per; ++k) {
+            const uint32_t p = wi * per + k;
+            if (p >= pl) break;
+            const uint32_t Y = p / wd, X = p - Y * wd;
+            const int64_t si = (((int64_t)nn * cs + c0) * h + Y * sd + u) * w + X * sd + v;
+            acc |= get_code(codes, si, bits) << (k * (uint32_t)bits);
+        }
+        dst[o] = acc;
+    }
+}
+
 // out (n, c, h, w) [+ shortcut res (n, cr, h*sr, w*sr), engine.py:262-269]
 // from the segmented conv result (n*nseg, c, hp, owt)
 __global__ void seg_out_kernel(const float *src, float *out, uint32_t total, int c, int h, int w,
@@ -1059,9 +1094,17 @@ __global__ void seg_out_kernel(const float *src, float *out, uint32_t total, int
         const uint32_t x = i % (uint32_t)w, r = i / (uint32_t)w;
         const uint32_t y = r % (uint32_t)h, r2 = r / (uint32_t)h;
         const uint32_t ch = r2 % (uint32_t)c, nn = r2 / (uint32_t)c;
-        const uint32_t j = x / (uint32_t)s.step, k = x - j * s.step + s.halo;
-        const uint32_t m = nn * s.nseg + j;
-        float v = __ldg(src + (((size_t)m * c + ch) * s.hp + y) * s.owt + k);
+        float v;
+        if (s.flat) {   // src (n, c sd^2, hp * owt): flattened (space-to-depth) plane
+            const uint32_t sd = (uint32_t)s.sd, Y = y / sd, u = y - Y * sd, X = x / sd, vv = x - X * sd;
+            const uint32_t cs = (ch * sd + u) * sd + vv;
+            v = __ldg(src + ((size_t)nn * c * sd * sd + cs) * ((size_t)s.hp * s.owt) +
+                      Y * ((uint32_t)w / sd) + X);
+        } else {
+            const uint32_t j = x / (uint32_t)s.step, k = x - j * s.step + s.halo;
+            const uint32_t m = nn * s.nseg + j;
+            v = __ldg(src + (((size_t)m * c + ch) * s.hp + y) * s.owt + k);
+        }
         if (res && (int)ch < cr)
             v = __fadd_rn(v, __ldg(res + (((size_t)nn * cr + ch) * h * sr + (size_t)y * sr) * w * sr +
                                    (size_t)x * sr));
@@ -1117,10 +1160,55 @@ static int seg_conv(const float *x, const float *w, float *out, int64_t n, int64
     return QT_OK;
 }
 
+// kernel == stride conv (1x1 included) on a plane the flat tensor-core path
+// cannot address (e.g. 7x7 = 49 px: rows not 16-byte aligned): the
+// (space-to-depth) plane zero-padded to 64-px multiples, the tensor-core 1x1,
+// then back.  Forward: x (n, ci, h, w) -> out (n, co, h/sd, w/sd); data
+// gradient (flip 1): g (n, co, h/sd, w/sd) -> gx (n, ci, h, w).
+static int seg_conv_flat(const float *src, const float *w, float *dst, int64_t n, int64_t ci,
+                         int64_t h, int64_t wd, int64_t co, int sd, int flip, const float *res,
+                         int64_t cr, int64_t sr, void *ws, cudaStream_t st) {
+    const SegGeo s = seg_geo_flat(h, wd, sd, sd, sd, 0);
+    const int64_t c4 = ci * sd * sd, oh = h / sd, ow = wd / sd;
+    if (!w || !ws || !s.ok || c4 % 16 || co % 16) return QT_EUNSUPPORTED;
+    if (seg_elems(s, n, c4 + co) >= (1ll << 31) || n * c4 * oh * ow >= (1ll << 31) ||
+        n * co * oh * ow >= (1ll << 31))
+        return QT_EUNSUPPORTED;
+    float *xs = (float *)((char *)ws + (qt_conv_workspace(c4, co, 1, 1) + 255) / 256 * 256);
+    float *os = xs + seg_elems(s, n, flip ? co : c4);
+    SegGeo s1 = s;
+    s1.sd = 1;
+    int rc;
+    if (!flip) {
+        rc = seg_in<0>(src, qt_tape_t{}, xs, n, c4, h, wd, s, st);
+        if (rc) return rc;
+        rc = tc_conv_s1(xs, w, os, (int)n, (int)c4, s.hp, s.owt, (int)co, 1, 1, 0, 0, nullptr, 0, 1, ws, st);
+        if (rc) return rc;
+        const int64_t total = n * co * oh * ow;
+        launch_pdl(seg_out_kernel, seg_blocks(total), 256, 0, st, (const float *)os, dst,
+                   (uint32_t)total, (int)co, (int)oh, (int)ow, s1, res, (int)cr, (int)sr);
+    } else {
+        rc = seg_in<0>(src, qt_tape_t{}, xs, n, co, oh, ow, s1, st);
+        if (rc) return rc;
+        rc = tc_conv_s1(xs, w, os, (int)n, (int)co, s.hp, s.owt, (int)c4, 1, 1, 0, 1, nullptr, 0, 1, ws, st);
+        if (rc) return rc;
+        const int64_t total = n * ci * h * wd;
+        launch_pdl(seg_out_kernel, seg_blocks(total), 256, 0, st, (const float *)os, dst,
+                   (uint32_t)total, (int)ci, (int)h, (int)wd, s, nullptr, 0, 1);
+    }
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
 }  // namespace qt
 
 // scratch of the segmented forward / data gradient (0: shape not taken)
 int64_t qt_tc_seg_workspace(const qt::ConvGeo &g) {
+    const SegGeo f = seg_geo_flat(g.h, g.w, g.kh, g.kw, g.s, g.pad);
+    if (f.ok) {
+        const int64_t c4 = g.ci * g.kh * g.kw;
+        return (qt_conv_workspace(c4, g.co, 1, 1) + 255) / 256 * 256 + 4 * seg_elems(f, g.n, c4 + g.co) + 256;
+    }
     if (g.s != 1) return 0;
     const SegGeo s = seg_geo(g.n, g.h, g.w, g.kh, g.kw, g.pad);
     if (!s.ok) return 0;
@@ -1129,13 +1217,19 @@ int64_t qt_tc_seg_workspace(const qt::ConvGeo &g) {
 
 int qt_tc_conv_seg_forward(const float *x, const float *w, float *out, const qt::ConvGeo &g,
                            const float *res, int64_t cr, int64_t sr, void *ws, cudaStream_t st) {
-    if (tc_disabled() || g.s != 1 || g.kh != 3 || g.kw != 3 || g.pad != 1) return QT_EUNSUPPORTED;
+    if (tc_disabled()) return QT_EUNSUPPORTED;
+    if (seg_geo_flat(g.h, g.w, g.kh, g.kw, g.s, g.pad).ok)
+        return seg_conv_flat(x, w, out, g.n, g.ci, g.h, g.w, g.co, (int)g.s, 0, res, cr, sr, ws, st);
+    if (g.s != 1 || g.kh != 3 || g.kw != 3 || g.pad != 1) return QT_EUNSUPPORTED;
     return seg_conv(x, w, out, g.n, g.ci, g.h, g.w, g.co, 0, res, cr, sr, ws, st);
 }
 
 int qt_tc_conv_seg_dgrad(const float *gr, const float *w, float *gx, const qt::ConvGeo &g,
                          void *ws, cudaStream_t st) {
-    if (tc_disabled() || g.s != 1 || g.kh != 3 || g.kw != 3 || g.pad != 1) return QT_EUNSUPPORTED;
+    if (tc_disabled()) return QT_EUNSUPPORTED;
+    if (seg_geo_flat(g.h, g.w, g.kh, g.kw, g.s, g.pad).ok)
+        return seg_conv_flat(gr, w, gx, g.n, g.ci, g.h, g.w, g.co, (int)g.s, 1, nullptr, 0, 1, ws, st);
+    if (g.s != 1 || g.kh != 3 || g.kw != 3 || g.pad != 1) return QT_EUNSUPPORTED;
     return seg_conv(gr, w, gx, g.n, g.co, g.oh, g.ow, g.ci, 1, nullptr, 0, 1, ws, st);
 }
 
@@ -1167,7 +1261,7 @@ int64_t qt_tc_seg_wgrad_workspace(const qt::ConvGeo &g) {
     const SegGeo s = seg_geo_wgrad(g);
     if (!s.ok) return 0;
     const int64_t part = (qt_tc_wgrad_workspace(seg_wgrad_geo(g, s)) + 255) / 256 * 256;
-    return part + 4 * seg_elems(s, g.n, g.ci * s.sd * s.sd + g.co) + 256;
+    return part + 4 * seg_elems(s, g.n, g.ci * s.sd * s.sd + g.co) + g.ci * s.sd * s.sd * 16 + 1024;
 }
 
 // weight gradient: segmented g_out (zero outside each segment's own columns)
@@ -1193,6 +1287,20 @@ int qt_tc_conv_seg_wgrad(const float *gr, qt_tape_t act, const float *x_plain, f
         rc = seg_in<1>(gr, qt_tape_t{}, gs, g.n, g.co, g.h, g.w, s, st);
     }
     if (rc) return rc;
+    if (s.flat && !x_plain && !act.a2 && act.codes && qt_bits_ok(act.bits)) {
+        // packed operand: the tensor-core path decodes it in its operand staging
+        const int64_t words = seg_elems(s, g.n, cin) * act.bits / 32;
+        uint32_t *cw = (uint32_t *)as;
+        double *step4 = (double *)((char *)as + (words * 4 + 255) / 256 * 256);
+        int64_t *off4 = (int64_t *)(step4 + cin);
+        launch_pdl(seg_codes_kernel, seg_blocks(std::max(words, cin)), 256, 0, st, act.codes, cw,
+                   (uint32_t)words, act.bits, (int)cin, (int)g.h, (int)g.w, s, act.step, act.offset,
+                   step4, off4);
+        QT_CHECK_LAUNCH();
+        qt_tape_t t2{nullptr, (const uint8_t *)cw, step4, off4, act.bits};
+        rc = qt_tc_conv_wgrad(gs, t2, nullptr, grad_w, d, ws, st);
+        if (rc != QT_EUNSUPPORTED) return rc;
+    }
     rc = seg_in<2>(x_plain, act, as, g.n, cin, g.h, g.w, s, st);
     if (rc) return rc;
     return qt_tc_conv_wgrad(gs, qt_tape_t{}, as, grad_w, d, ws, st);

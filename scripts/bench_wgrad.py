@@ -23,10 +23,26 @@ SHAPES = [
 ]
 
 ap = argparse.ArgumentParser()
+ap.add_argument("--config", default="C2", choices=["C2", "C4"])
+ap.add_argument("--op", default="wgrad", choices=["wgrad", "fwd", "dgrad"])
 ap.add_argument("--iters", type=int, default=20)
 ap.add_argument("--only", type=int, default=-1)
 ap.add_argument("--bits", type=int, default=4)
 a = ap.parse_args()
+MULT = [1] * len(SHAPES)
+STRIDE = [1] * len(SHAPES)
+if a.config == "C4":   # distinct conv layers of ResNet-152 224^2 at batch 64, with multiplicity
+    from collections import Counter
+    import paper_1901_07988_b200 as P
+    spec = P.resnet152_spec()
+    cnt = Counter()
+    for l, (ins, _) in zip(spec.layers, spec.layer_shapes(64)):
+        if l.kind == "conv":
+            cnt[(ins[0], ins[1], ins[2], ins[3], l.out_channels, l.kernel, l.pad, l.stride)] += 1
+    SHAPES = [k[:7] for k in cnt]
+    STRIDE = [k[7] for k in cnt]
+    MULT = list(cnt.values())
+total_us = 0.0
 dev = torch.device("cuda:0")
 g = torch.Generator(device=dev).manual_seed(0)
 _w = torch.randn(1 << 26, device=dev)      # ~0.3 s of work: clocks up before the first shape
@@ -39,12 +55,21 @@ for i, (n, ci, h, w, co, k, pad) in enumerate(SHAPES):
     x = torch.randn(n, ci, h, w, device=dev, generator=g)
     gamma = torch.rand(ci, device=dev, generator=g) + 0.5
     beta = torch.randn(ci, device=dev, generator=g) * 0.1
-    tape = codec.quantize(x, gamma, beta, a.bits).as_native()
-    gout = torch.randn(n, co, h, w, device=dev, generator=g)
+    qtape = codec.quantize(x, gamma, beta, a.bits)   # keeps the codes alive
+    tape = qtape.as_native()
+    sd = STRIDE[i]
+    oh, ow = (h + 2 * pad - k) // sd + 1, (w + 2 * pad - k) // sd + 1
+    gout = torch.randn(n, co, oh, ow, device=dev, generator=g)
     gw = torch.zeros(co, ci, k, k, device=dev)
-    ws = None
-    run = lambda: ops.conv2d_wgrad(gout, (co, ci, k, k), 1, pad, gw, tape=tape,
-                                   in_shape=(n, ci, h, w))
+    if a.op == "wgrad":
+        run = lambda: ops.conv2d_wgrad(gout, (co, ci, k, k), sd, pad, gw, tape=tape,
+                                       in_shape=(n, ci, h, w))
+    elif a.op == "fwd":
+        yb = torch.empty(n, co, oh, ow, device=dev)
+        run = lambda: ops.conv2d_forward(x, gw, sd, pad, out=yb)
+    else:
+        gxb = torch.empty(n, ci, h, w, device=dev)
+        run = lambda: ops.conv2d_dgrad(gout, gw, (n, ci, h, w), sd, pad, gxb)
     if a.only >= 0:
         run()
         torch.cuda.synchronize()
@@ -72,4 +97,8 @@ for i, (n, ci, h, w, co, k, pad) in enumerate(SHAPES):
     R = ci * k * k
     mt = (R + 127) // 128
     floor_us = (n * h * w / 32) * mt * 8 * 46 / 148 / 1.965e3   # 2 tf32 passes, 46 clk/MMA
-    print(f"{i}: n={n} ci={ci} {h}x{w} co={co} k={k}: {us:8.2f} us  (MMA floor {floor_us:6.2f} us)")
+    total_us += us * MULT[i]
+    tflops = 2.0 * n * oh * ow * co * ci * k * k / us / 1e6
+    print(f"{i}: n={n} ci={ci} {h}x{w} co={co} k={k}/s{sd} x{MULT[i]}: {us:8.2f} us "
+          f"{tflops:6.1f} TF/s (MMA floor {floor_us:6.2f} us)")
+print(f"total {a.op}: {total_us / 1e3:.2f} ms per step")

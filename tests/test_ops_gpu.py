@@ -34,6 +34,9 @@ GEOS = [  # (n, ci, h, co, k, s, p)
     (2, 16, 56, 16, 3, 1, 1), (2, 32, 28, 32, 3, 1, 1), (2, 64, 14, 32, 3, 1, 1),
     (2, 64, 7, 64, 3, 1, 1), (3, 16, 7, 16, 3, 1, 1), (1, 16, 40, 32, 3, 1, 1),
     (2, 16, 3, 16, 3, 1, 1), (1, 32, 61, 16, 3, 1, 1),
+    # kernel == stride convs whose (space-to-depth) plane is not 16-byte
+    # aligned (7x7 = 49 px): zero-padded flat plane + tensor-core 1x1
+    (2, 64, 7, 32, 1, 1, 0), (2, 32, 14, 64, 2, 2, 0), (3, 16, 5, 48, 1, 1, 0),
 ]
 
 
@@ -233,13 +236,14 @@ print("ok")
 
 @pytest.mark.parametrize("bits", [1, 2, 4, 8])
 @pytest.mark.parametrize("shape", [(2, 32, 32, 32), (4, 64, 16, 64), (2, 16, 8, 16),
-                                   (2, 32, 56, 64), (2, 64, 14, 32)])
+                                   (2, 32, 56, 64), (2, 64, 14, 32), (2, 3, 224, 64, 4),
+                                   (2, 3, 32, 16, 4), (2, 48, 28, 32, 4)])
 def test_transition_wgrad_from_codes(shape, bits):
     """2x2/s2 weight gradient from a packed tape (rearranged space-to-depth
     codes + the 1x1 tensor-core path where eligible, else the SIMT GEMM)
     against a float64 reference on the dequantized activation."""
     from paper_1901_07988_b200 import codec
-    n, ci, hw, co = shape
+    n, ci, hw, co, sd = shape + (2,) if len(shape) == 4 else shape
     torch.manual_seed(bits + ci)
     for regime in ("narrow", "wide"):
         x = torch.randn(n, ci, hw, hw, device="cuda")
@@ -249,10 +253,10 @@ def test_transition_wgrad_from_codes(shape, bits):
             gamma, beta = torch.rand(ci, device="cuda") * 0.05 + 0.05, torch.rand(ci, device="cuda") + 1.5
         t = codec.quantize(x, gamma, beta, bits)
         act = codec.dequantize(t, relu=True)
-        g = torch.randn(n, co, hw // 2, hw // 2, device="cuda")
-        gw = torch.full((co, ci, 2, 2), 0.25, device="cuda")    # accumulates into gw
-        ops.conv2d_wgrad(g, (co, ci, 2, 2), 2, 0, gw, tape=t.as_native(), in_shape=(n, ci, hw, hw))
-        ref = torch.nn.grad.conv2d_weight(act.double(), (co, ci, 2, 2), g.double(), stride=2) + 0.25
+        g = torch.randn(n, co, hw // sd, hw // sd, device="cuda")
+        gw = torch.full((co, ci, sd, sd), 0.25, device="cuda")    # accumulates into gw
+        ops.conv2d_wgrad(g, (co, ci, sd, sd), sd, 0, gw, tape=t.as_native(), in_shape=(n, ci, hw, hw))
+        ref = torch.nn.grad.conv2d_weight(act.double(), (co, ci, sd, sd), g.double(), stride=sd) + 0.25
         err = ((gw.double() - ref).norm() / ref.norm()).item()
         assert err < CONV_TOL, (regime, err)
 
