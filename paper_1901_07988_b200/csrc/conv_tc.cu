@@ -1012,30 +1012,60 @@ static SegGeo seg_geo_flat(int64_t h, int64_t w, int64_t kh, int64_t kw, int64_t
 // dst (n*nseg, c, hp, owt) from src (n, c, h, w).  mode 0: fp32 source, copied;
 // 1: g_out, zero outside the segment's own output columns; 2: tape (relu of
 // the decoded pre-activation, layer.py:356) or plain fp32 when src != NULL.
+// launch-invariant divisors of seg_in_kernel (no runtime IDIV in the loop)
+struct SegDiv {
+    FastDiv hp, c, nseg, plane, wd, sd2, sd;
+    uint32_t owt_log2;
+};
+
+static SegDiv seg_div(const SegGeo &s, int64_t c, int64_t w) {
+    SegDiv d;
+    d.hp = make_fastdiv((uint32_t)s.hp);
+    d.c = make_fastdiv((uint32_t)c);
+    d.nseg = make_fastdiv((uint32_t)s.nseg);
+    d.plane = make_fastdiv((uint32_t)(s.hp * s.owt));
+    const int sd = s.sd > 0 ? s.sd : 1;
+    d.wd = make_fastdiv((uint32_t)std::max<int64_t>(1, w / sd));
+    d.sd2 = make_fastdiv((uint32_t)(sd * sd));
+    d.sd = make_fastdiv((uint32_t)sd);
+    d.owt_log2 = s.owt == 8 ? 3 : (s.owt == 16 ? 4 : 5);
+    return d;
+}
+
 template <int MODE>
 __global__ void seg_in_kernel(const float *src, qt_tape_t t, float *dst, uint32_t total, int c,
-                              int h, int w, SegGeo s) {
+                              int h, int w, SegGeo s, SegDiv dv) {
     pdl_enter();
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-        const uint32_t k = i % (uint32_t)s.owt, r = i / (uint32_t)s.owt;
-        const uint32_t y = r % (uint32_t)s.hp, r2 = r / (uint32_t)s.hp;
-        const uint32_t ch = r2 % (uint32_t)c, m = r2 / (uint32_t)c;
-        const uint32_t nn = m / (uint32_t)s.nseg, j = m - nn * (uint32_t)s.nseg;
-        const int col = (int)(j * s.step + k) - s.halo;
-        bool ok = y < (uint32_t)h && col >= 0 && col < w;
-        if (MODE == 1) ok = ok && (int)k >= s.halo && (int)k < s.halo + s.step;
-        int64_t si = (((int64_t)nn * c + ch) * h + y) * w + col;
-        int tc = (int)ch;
+        bool ok;
+        int64_t si;
+        int tc;
         if (s.flat) {   // c = source channels x sd^2; (h, w) = source extent
-            const uint32_t p = y * (uint32_t)s.owt + k;
-            const uint32_t wd = (uint32_t)(w / s.sd), sd2 = (uint32_t)(s.sd * s.sd);
-            ok = p < (uint32_t)(h / s.sd) * wd;
-            const uint32_t Y = p / wd, X = p - Y * wd;
-            const uint32_t c0 = ch / sd2, uv = ch - c0 * sd2;
-            const uint32_t u = uv / (uint32_t)s.sd, v = uv - u * (uint32_t)s.sd;
-            const uint32_t cs = (uint32_t)c / sd2;
-            si = (((int64_t)nn * cs + c0) * h + Y * s.sd + u) * w + X * s.sd + v;
-            tc = (int)c0;
+            const uint32_t m = fast_div(i, dv.plane), p = i - m * (uint32_t)(s.hp * s.owt);
+            const uint32_t wd = (uint32_t)w / (uint32_t)s.sd;
+            ok = p < (uint32_t)h / (uint32_t)s.sd * wd;
+            if (s.sd == 1) {
+                si = (int64_t)m * (uint32_t)(h * w) + p;
+                tc = (int)(m - fast_div(m, dv.c) * (uint32_t)c);
+            } else {
+                const uint32_t nn = fast_div(m, dv.c), ch = m - nn * (uint32_t)c;
+                const uint32_t Y = fast_div(p, dv.wd), X = p - Y * wd;
+                const uint32_t sd2 = (uint32_t)(s.sd * s.sd), c0 = fast_div(ch, dv.sd2), uv = ch - c0 * sd2;
+                const uint32_t u = fast_div(uv, dv.sd), v = uv - u * (uint32_t)s.sd;
+                const uint32_t cs = (uint32_t)c / sd2;
+                si = (((int64_t)nn * cs + c0) * h + Y * s.sd + u) * w + X * s.sd + v;
+                tc = (int)c0;
+            }
+        } else {
+            const uint32_t k = i & ((uint32_t)s.owt - 1u), r = i >> dv.owt_log2;
+            const uint32_t r2 = fast_div(r, dv.hp), y = r - r2 * (uint32_t)s.hp;
+            const uint32_t m = fast_div(r2, dv.c), ch = r2 - m * (uint32_t)c;
+            const uint32_t nn = fast_div(m, dv.nseg), j = m - nn * (uint32_t)s.nseg;
+            const int col = (int)(j * s.step + k) - s.halo;
+            ok = y < (uint32_t)h && col >= 0 && col < w;
+            if (MODE == 1) ok = ok && (int)k >= s.halo && (int)k < s.halo + s.step;
+            si = (((int64_t)nn * c + ch) * h + y) * w + col;
+            tc = (int)ch;
         }
         float v = 0.f;
         if (ok) {
@@ -1071,17 +1101,86 @@ __global__ void seg_codes_kernel(const uint8_t *codes, uint32_t *dst, uint32_t w
     const uint32_t cs = (uint32_t)c4 / sd2;
     for (uint32_t o = tid; o < words; o += gridDim.x * blockDim.x) {
         const uint32_t m = o / pw, wi = o - m * pw;
-        const uint32_t nn = m / (uint32_t)c4, ch = m - nn * (uint32_t)c4;
-        const uint32_t c0 = ch / sd2, uv = ch - c0 * sd2, u = uv / sd, v = uv - u * sd;
         uint32_t acc = 0;
-        for (uint32_t k = 0; k < per; ++k) {
-            const uint32_t p = wi * per + k;
-            if (p >= pl) break;
-            const uint32_t Y = p / wd, X = p - Y * wd;
-            const int64_t si = (((int64_t)nn * cs + c0) * h + Y * sd + u) * w + X * sd + v;
-            acc |= get_code(codes, si, bits) << (k * (uint32_t)bits);
+        if (s.flat) {
+            const uint32_t nn = m / (uint32_t)c4, ch = m - nn * (uint32_t)c4;
+            const uint32_t c0 = ch / sd2, uv = ch - c0 * sd2, u = uv / sd, v = uv - u * sd;
+            for (uint32_t k = 0; k < per; ++k) {
+                const uint32_t p = wi * per + k;
+                if (p >= pl) break;
+                const uint32_t Y = p / wd, X = p - Y * wd;
+                const int64_t si = (((int64_t)nn * cs + c0) * h + Y * sd + u) * w + X * sd + v;
+                acc |= get_code(codes, si, bits) << (k * (uint32_t)bits);
+            }
+        } else {   // segmented (n*nseg, c, hp, owt) layout of the 3x3 path
+            const uint32_t img = m / (uint32_t)c4, ch = m - img * (uint32_t)c4;
+            const uint32_t nn = img / (uint32_t)s.nseg, j = img - nn * (uint32_t)s.nseg;
+            for (uint32_t k = 0; k < per; ++k) {
+                const uint32_t p = wi * per + k;
+                const uint32_t y = p / (uint32_t)s.owt, kx = p - y * (uint32_t)s.owt;
+                const int col = (int)(j * s.step + kx) - s.halo;
+                if (y < (uint32_t)h && col >= 0 && col < w)
+                    acc |= get_code(codes, (((int64_t)nn * c4 + ch) * h + y) * w + col, bits)
+                           << (k * (uint32_t)bits);
+            }
         }
         dst[o] = acc;
+    }
+}
+
+// Segmented 3x3 weight gradient from codes: the padding pixels inside the
+// segmented planes (right of the image, below it) hold code 0, whose
+// rectified decode z_c = relu(decode(0)) is 0 unless every code of channel c
+// decodes positive.  Remove their contribution exactly:
+//   dW[co][c][u][v] -= z_c * S[co][u][v],
+//   S[co][u][v] = sum over outputs (y, x) whose (u, v) neighbour is such a
+//   padding pixel of g[co][y][x]
+// (only the last row and the first / last column of outputs have one).
+// One block per co.
+__global__ void seg_pad_fix_kernel(const float *g, float *grad_w, int n, int co_n, int ci, int h,
+                                   int w, SegGeo s, const double *step, const int64_t *offset,
+                                   int bits) {
+    pdl_enter();
+    __shared__ double red[9][256];
+    __shared__ double S[9];
+    const int co = blockIdx.x, tid = threadIdx.x;
+    const int L = w + 2 * (h - 1);   // last row, last column above it, first column above it
+    double acc[9];
+#pragma unroll
+    for (int q = 0; q < 9; ++q) acc[q] = 0.0;
+    for (int t = tid; t < n * L; t += blockDim.x) {
+        const int nn = t / L, q = t - nn * L;
+        const int y = q < w ? h - 1 : (q < w + h - 1 ? q - w : q - w - h + 1);
+        const int x = q < w ? q : (q < w + h - 1 ? w - 1 : 0);
+        const double gv = (double)g[(((int64_t)nn * co_n + co) * h + y) * w + x];
+#pragma unroll
+        for (int uv = 0; uv < 9; ++uv) {
+            const int Y = y + uv / 3 - 1, X = x + uv % 3 - 1;
+            // inside the segmented plane (row -1 and, without a halo, column
+            // -1 are the kernel's own zero padding) but not an image pixel;
+            // with a halo, column -1 is segment 0's first column
+            const bool in_plane = Y >= 0 && Y < s.hp && X >= -s.halo && (s.halo || X < s.owt);
+            const bool pad = in_plane && (Y >= h || X >= w || X < 0);
+            if (pad) acc[uv] += gv;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 9; ++q) red[q][tid] = acc[q];
+    __syncthreads();
+    for (int st = blockDim.x / 2; st > 0; st >>= 1) {   // fixed-order tree
+        if (tid < st)
+            for (int q = 0; q < 9; ++q) red[q][tid] += red[q][tid + st];
+        __syncthreads();
+    }
+    if (tid < 9) S[tid] = red[tid][0];
+    __syncthreads();
+    for (int i = tid; i < ci * 9; i += blockDim.x) {
+        const int c = i / 9, uv = i - c * 9;
+        const float z = decode(0u, step[c], offset[c], bits);
+        if (z > 0.f && S[uv] != 0.0) {
+            float *d = grad_w + ((int64_t)co * ci + c) * 9 + uv;
+            *d = __fadd_rn(*d, -(float)((double)z * S[uv]));
+        }
     }
 }
 
@@ -1125,7 +1224,7 @@ static int seg_in(const float *src, qt_tape_t t, float *dst, int64_t n, int64_t 
                   int64_t w, const SegGeo &s, cudaStream_t st) {
     const int64_t total = seg_elems(s, n, c);
     launch_pdl(seg_in_kernel<MODE>, seg_blocks(total), 256, 0, st, src, t, dst, (uint32_t)total,
-               (int)c, (int)h, (int)w, s);
+               (int)c, (int)h, (int)w, s, seg_div(s, c, w));
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -1287,7 +1386,7 @@ int qt_tc_conv_seg_wgrad(const float *gr, qt_tape_t act, const float *x_plain, f
         rc = seg_in<1>(gr, qt_tape_t{}, gs, g.n, g.co, g.h, g.w, s, st);
     }
     if (rc) return rc;
-    if (s.flat && !x_plain && !act.a2 && act.codes && qt_bits_ok(act.bits)) {
+    if (!x_plain && !act.a2 && act.codes && qt_bits_ok(act.bits)) {
         // packed operand: the tensor-core path decodes it in its operand staging
         const int64_t words = seg_elems(s, g.n, cin) * act.bits / 32;
         uint32_t *cw = (uint32_t *)as;
@@ -1299,7 +1398,14 @@ int qt_tc_conv_seg_wgrad(const float *gr, qt_tape_t act, const float *x_plain, f
         QT_CHECK_LAUNCH();
         qt_tape_t t2{nullptr, (const uint8_t *)cw, step4, off4, act.bits};
         rc = qt_tc_conv_wgrad(gs, t2, nullptr, grad_w, d, ws, st);
-        if (rc != QT_EUNSUPPORTED) return rc;
+        if (rc != QT_EUNSUPPORTED) {
+            if (rc || s.flat) return rc;
+            if (s.hp == g.h && !s.halo && s.owt == g.w) return rc;   // no padding pixels
+            launch_pdl(seg_pad_fix_kernel, (unsigned)g.co, 256, 0, st, gr, grad_w, (int)g.n,
+                       (int)g.co, (int)g.ci, (int)g.h, (int)g.w, s, act.step, act.offset, act.bits);
+            QT_CHECK_LAUNCH();
+            return QT_OK;
+        }
     }
     rc = seg_in<2>(x_plain, act, as, g.n, cin, g.h, g.w, s, st);
     if (rc) return rc;

@@ -44,6 +44,19 @@ __global__ void __launch_bounds__(1024) wgrad_reduce_kernel(const float *partial
     }
 }
 
+// Few splits: one thread per output sums its splits in order (z = 0, 1, ...)
+// in float64 -- fixed order, deterministic, coalesced across threads.
+__global__ void __launch_bounds__(256) wgrad_reduce_few_kernel(const float *partial, int splits,
+                                                              int64_t count, float *grad_w) {
+    pdl_enter();
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < count;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        for (int z = 0; z < splits; ++z) s += (double)__ldg(partial + z * count + i);
+        grad_w[i] = __fadd_rn(grad_w[i], __double2float_rn(s));
+    }
+}
+
 static PFN_cuTensorMapEncodeTiled_v12000 encode_fn_wg() {
     static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
     static std::once_flag once;
@@ -287,6 +300,12 @@ extern "C" int qt_debug_wgrad_trace(void *buf, int cta) {
 
 int qt_tc_wgrad_reduce(const float *partial, int64_t splits, int64_t count, float *grad_w,
                        cudaStream_t st) {
+    if (splits <= 48) {
+        launch_pdl(wgrad_reduce_few_kernel, (unsigned)std::min<int64_t>(qt_cdiv(count, 256), 148 * 8),
+                   256, 0, st, partial, (int)splits, count, grad_w);
+        QT_CHECK_LAUNCH();
+        return QT_OK;
+    }
     launch_pdl(wgrad_reduce_kernel, (unsigned)qt_cdiv(count, 32), 1024, 0, st, partial, splits, count,
                                                                       grad_w);
     QT_CHECK_LAUNCH();

@@ -286,3 +286,28 @@ def test_wgrad_from_codes_channel_blocks(shape):
         ref = torch.nn.grad.conv2d_weight(act.double(), (co, ci, k, k), g.double(), padding=k // 2)
         err = ((gw.double() - ref).norm() / ref.norm()).item()
         assert err < CONV_TOL, (regime, err)
+
+
+@pytest.mark.parametrize("bits", [1, 2, 8])
+@pytest.mark.parametrize("shape", [(2, 32, 14, 32), (1, 16, 40, 16), (2, 16, 7, 32)])
+def test_segmented_3x3_wgrad_from_codes(shape, bits):
+    """3x3 weight gradient on planes of other widths from a packed tape:
+    segmented codes (padding pixels = code 0) + the exact padding correction
+    for channels whose every code decodes positive ("wide" regime)."""
+    from paper_1901_07988_b200 import codec
+    n, ci, hw, co = shape
+    torch.manual_seed(bits + hw)
+    for regime in ("narrow", "wide"):
+        x = torch.randn(n, ci, hw, hw, device="cuda")
+        if regime == "narrow":
+            gamma, beta = torch.rand(ci, device="cuda") + 0.5, torch.randn(ci, device="cuda") * 0.1
+        else:
+            gamma, beta = torch.rand(ci, device="cuda") * 0.05 + 0.05, torch.rand(ci, device="cuda") + 1.5
+        t = codec.quantize(x, gamma, beta, bits)
+        act = codec.dequantize(t, relu=True)
+        g = torch.randn(n, co, hw, hw, device="cuda")
+        gw = torch.full((co, ci, 3, 3), -0.5, device="cuda")
+        ops.conv2d_wgrad(g, (co, ci, 3, 3), 1, 1, gw, tape=t.as_native(), in_shape=(n, ci, hw, hw))
+        ref = torch.nn.grad.conv2d_weight(act.double(), (co, ci, 3, 3), g.double(), padding=1) - 0.5
+        err = ((gw.double() - ref).norm() / ref.norm()).item()
+        assert err < CONV_TOL, (regime, err)
