@@ -84,7 +84,27 @@ __device__ __forceinline__ uint64_t load_code_word(const uint8_t *codes, int64_t
     }
 }
 
-template <bool CODES, bool VA1>
+// G consecutive codes starting at element i0 (a multiple of G)
+template <int G>
+__device__ __forceinline__ uint64_t load_code_group(const uint8_t *codes, int64_t i0, int bits) {
+    if (G == 8) return load_code_word(codes, i0, bits);
+    const uint8_t *src = codes + ((i0 * bits) >> 3);
+    switch (bits) {
+        case 8: return *reinterpret_cast<const uint32_t *>(src);
+        case 4: return *reinterpret_cast<const uint16_t *>(src);
+        case 2: return *src;
+        default: return (uint64_t)(*src >> (i0 & 4)) & 0xFu;   // 1-bit: a nibble
+    }
+}
+
+// vector group width for a plane of hw pixels (rows of w): 8, 4 or 0 (scalar)
+static inline int bn_group(int64_t hw, int64_t w) {
+    if (hw % 8 == 0 && w >= 8) return 8;
+    if (hw % 4 == 0 && w >= 4) return 4;
+    return 0;
+}
+
+template <bool CODES, bool VA1, int G>
 __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
     pdl_enter();
     __shared__ float s_m[kMaxLut], s_a1[kMaxLut];
@@ -113,10 +133,10 @@ __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
     // The summation order depends only on the shape (never on the tape
     // type), so an exact tape and a K-bit tape with variance_a1 substituted
     // produce bit-identical sums (reference test_layer.py:173-202).
-    const int64_t cnt8 = ((p1 - p0) * a.hw) >> 3;
-    if ((a.hw & 7) == 0 && cnt8 < (1ll << 31)) {
+    const int64_t cnt8 = ((p1 - p0) * a.hw) / G;
+    if (G > 0 && a.hw % G == 0 && cnt8 < (1ll << 31)) {
         const uint32_t groups = (uint32_t)cnt8;
-        const uint32_t gpp = (uint32_t)(a.hw >> 3);
+        const uint32_t gpp = (uint32_t)(a.hw / G);
         constexpr int U = 4;                     // groups in flight per thread
         for (uint32_t g0 = threadIdx.x; g0 < groups; g0 += U * kBT) {
             float4 ga[U], gb[U], xa[U], xb[U];
@@ -126,33 +146,33 @@ __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
             for (int u = 0; u < U; ++u) {
                 const uint32_t gi = g0 + u * kBT;
                 if (gi >= groups) break;
-                const uint32_t pl = fast_div(gi, a.gppd), off = (gi - pl * gpp) << 3;
+                const uint32_t pl = fast_div(gi, a.gppd), off = (gi - pl * gpp) * G;
                 i0[u] = ((p0 + pl) * a.c + ch) * a.hw + off;
                 ga[u] = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0[u]));
-                gb[u] = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0[u]) + 1);
+                if (G == 8) gb[u] = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0[u]) + 1);
                 if (CODES) {
-                    word[u] = load_code_word(a.tape.codes, i0[u], a.tape.bits);
+                    word[u] = load_code_group<G>(a.tape.codes, i0[u], a.tape.bits);
                 } else {
                     xa[u] = __ldg(reinterpret_cast<const float4 *>(a.tape.a2 + i0[u]));
-                    xb[u] = __ldg(reinterpret_cast<const float4 *>(a.tape.a2 + i0[u]) + 1);
+                    if (G == 8) xb[u] = __ldg(reinterpret_cast<const float4 *>(a.tape.a2 + i0[u]) + 1);
                 }
             }
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (g0 + u * kBT >= groups) break;
-                const float gv[8] = {ga[u].x, ga[u].y, ga[u].z, ga[u].w,
-                                     gb[u].x, gb[u].y, gb[u].z, gb[u].w};
-                float xv[8];
+                float gv[8], xv[8];
+                gv[0] = ga[u].x; gv[1] = ga[u].y; gv[2] = ga[u].z; gv[3] = ga[u].w;
+                if (G == 8) { gv[4] = gb[u].x; gv[5] = gb[u].y; gv[6] = gb[u].z; gv[7] = gb[u].w; }
                 if (!CODES) {
                     xv[0] = xa[u].x; xv[1] = xa[u].y; xv[2] = xa[u].z; xv[3] = xa[u].w;
-                    xv[4] = xb[u].x; xv[5] = xb[u].y; xv[6] = xb[u].z; xv[7] = xb[u].w;
+                    if (G == 8) { xv[4] = xb[u].x; xv[5] = xb[u].y; xv[6] = xb[u].z; xv[7] = xb[u].w; }
                 }
                 // the 8 elements of a group are combined in fp32 (fixed order,
                 // fused multiply-add for the a1 products), the group sums in
                 // float64: one float->double conversion per sum per group
                 float f0 = 0.f, f1 = 0.f, f3 = 0.f;
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
+                for (int j = 0; j < (G > 0 ? G : 1); ++j) {
                     float m, a1;
                     if (CODES) {
                         const uint32_t code = (uint32_t)(word[u] >> (j * a.tape.bits)) & cmask;
@@ -275,16 +295,16 @@ __device__ __forceinline__ float res_value(const ApplyArgs &a, int64_t i, int64_
     return a.res[((nn * a.cr + ch) * hr + y / a.sc) * wr + x / a.sc];
 }
 
-template <bool CODES, bool VA1>
+template <bool CODES, bool VA1, int G>
 __global__ void __launch_bounds__(kBT) bn_bwd_apply_kernel(ApplyArgs a) {
     pdl_enter();
     const int64_t hw = a.h * a.w;
     const int64_t numel = a.n * a.c * hw;
     const uint32_t cmask = (1u << a.tape.bits) - 1u;
-    if (CODES && (hw & 7) == 0 && (numel >> 3) < (1ll << 31)) {
-        const uint32_t groups = (uint32_t)(numel >> 3);
+    if (CODES && G > 0 && hw % G == 0 && numel / G < (1ll << 31)) {
+        const uint32_t groups = (uint32_t)(numel / G);
         for (uint32_t gi = blockIdx.x * kBT + threadIdx.x; gi < groups; gi += gridDim.x * kBT) {
-            const int64_t i0 = (int64_t)gi << 3;
+            const int64_t i0 = (int64_t)gi * G;
             const uint32_t pl = fast_div(gi, a.gppd);
             const int ch = (int)(pl - fast_div(pl, a.cd) * (uint32_t)a.c);
             const float gam = __ldg(a.gamma + ch);
@@ -292,12 +312,16 @@ __global__ void __launch_bounds__(kBT) bn_bwd_apply_kernel(ApplyArgs a) {
             const float inv = __ldg(a.stats + 2 * a.c + ch);
             const float *lm = a.lut + (int64_t)ch * 2 * kMaxLut;
             const float4 ga = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0));
-            const float4 gb = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0) + 1);
-            const float gv[8] = {ga.x, ga.y, ga.z, ga.w, gb.x, gb.y, gb.z, gb.w};
-            const uint64_t word = load_code_word(a.tape.codes, i0, a.tape.bits);
+            float gv[8];
+            gv[0] = ga.x; gv[1] = ga.y; gv[2] = ga.z; gv[3] = ga.w;
+            if (G == 8) {
+                const float4 gb = __ldg(reinterpret_cast<const float4 *>(a.g3 + i0) + 1);
+                gv[4] = gb.x; gv[5] = gb.y; gv[6] = gb.z; gv[7] = gb.w;
+            }
+            const uint64_t word = load_code_group<G>(a.tape.codes, i0, a.tape.bits);
             float o[8];
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
+            for (int j = 0; j < (G > 0 ? G : 1); ++j) {
                 const uint32_t code = (uint32_t)(word >> (j * a.tape.bits)) & cmask;
                 const float m = __ldg(lm + code), a1 = __ldg(lm + kMaxLut + code);
                 const float g1 = __fmul_rn(__fmul_rn(gv[j], m), gam);
@@ -309,29 +333,35 @@ __global__ void __launch_bounds__(kBT) bn_bwd_apply_kernel(ApplyArgs a) {
             if (a.res) {
                 if (a.sc == 1 && a.cr == a.c) {
                     const float4 ra = __ldg(reinterpret_cast<const float4 *>(a.res + i0));
-                    const float4 rb = __ldg(reinterpret_cast<const float4 *>(a.res + i0) + 1);
-                    const float rv[8] = {ra.x, ra.y, ra.z, ra.w, rb.x, rb.y, rb.z, rb.w};
-#pragma unroll
-                    for (int j = 0; j < 8; ++j) o[j] = __fadd_rn(o[j], rv[j]);
+                    o[0] = __fadd_rn(o[0], ra.x); o[1] = __fadd_rn(o[1], ra.y);
+                    o[2] = __fadd_rn(o[2], ra.z); o[3] = __fadd_rn(o[3], ra.w);
+                    if (G == 8) {
+                        const float4 rb = __ldg(reinterpret_cast<const float4 *>(a.res + i0) + 1);
+                        o[4] = __fadd_rn(o[4], rb.x); o[5] = __fadd_rn(o[5], rb.y);
+                        o[6] = __fadd_rn(o[6], rb.z); o[7] = __fadd_rn(o[7], rb.w);
+                    }
                 } else if (ch < a.cr) {
                     // shortcut adjoint at a lower resolution (engine.py:270-279):
-                    // the group's 8 pixels share one row y of the plane
+                    // the group's pixels start in row y and may wrap into row
+                    // y + 1 (w >= G, so at most once)
                     const uint32_t off = (uint32_t)(i0 - (int64_t)pl * hw);
                     const uint32_t y = fast_div(off, a.wd), x0 = off - y * (uint32_t)a.w;
-                    const uint32_t sc = (uint32_t)a.sc;
-                    if (y % sc == 0) {
-                        const uint32_t nn = fast_div(pl, a.cd);
-                        const int64_t hr = a.h / a.sc, wr = a.w / a.sc;
-                        const float *rrow = a.res + (((int64_t)nn * a.cr + ch) * hr + y / sc) * wr;
+                    const uint32_t sc = (uint32_t)a.sc, wv = (uint32_t)a.w;
+                    const uint32_t nn = fast_div(pl, a.cd);
+                    const int64_t hr = a.h / a.sc, wr = a.w / a.sc;
+                    const float *rimg = a.res + ((int64_t)nn * a.cr + ch) * hr * wr;
 #pragma unroll
-                        for (int j = 0; j < 8; ++j)
-                            if ((x0 + j) % sc == 0) o[j] = __fadd_rn(o[j], __ldg(rrow + (x0 + j) / sc));
+                    for (int j = 0; j < G; ++j) {
+                        const uint32_t wrap = x0 + j >= wv ? 1u : 0u;
+                        const uint32_t yy = y + wrap, xx = x0 + j - wrap * wv;
+                        if (yy % sc == 0 && xx % sc == 0)
+                            o[j] = __fadd_rn(o[j], __ldg(rimg + (int64_t)(yy / sc) * wr + xx / sc));
                     }
                 }
             }
             float4 *dst = reinterpret_cast<float4 *>(a.g_in + i0);
             dst[0] = make_float4(o[0], o[1], o[2], o[3]);
-            dst[1] = make_float4(o[4], o[5], o[6], o[7]);
+            if (G == 8) dst[1] = make_float4(o[4], o[5], o[6], o[7]);
         }
         return;
     }
@@ -384,15 +414,21 @@ extern "C" int qt_bn_backward_reduce(const float *g3, qt_tape_t tape, int64_t n,
     if (!codes) tape.bits = 1;
     BwdArgs a{g3, tape, n, c, hw, gamma_tape, beta_tape, sigma2, eps, variance_a1, grad_gamma,
               grad_beta, stats, p.ppb, p.nb, part_base(ws, c), (unsigned *)ws, lut_base(ws)};
-    a.gppd = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 3));
+    // the vector group width (hence the summation order) depends on the shape
+    // and code width only, never on the tape type
+    const int G = bn_group(hw, hw);
+    a.gppd = make_fastdiv((uint32_t)std::max<int64_t>(1, hw / (G > 0 ? G : 8)));
     dim3 grid((unsigned)p.nb, (unsigned)c);
     cudaStream_t s = qt_s(stream);
-    if (codes)
-        variance_a1 ? launch_pdl(bn_bwd_reduce_kernel<true, true>, grid, kBT, 0, s, a)
-                    : launch_pdl(bn_bwd_reduce_kernel<true, false>, grid, kBT, 0, s, a);
-    else
-        variance_a1 ? launch_pdl(bn_bwd_reduce_kernel<false, true>, grid, kBT, 0, s, a)
-                    : launch_pdl(bn_bwd_reduce_kernel<false, false>, grid, kBT, 0, s, a);
+#define QT_RED(GG)                                                                                \
+    (codes ? (variance_a1 ? launch_pdl(bn_bwd_reduce_kernel<true, true, GG>, grid, kBT, 0, s, a)   \
+                          : launch_pdl(bn_bwd_reduce_kernel<true, false, GG>, grid, kBT, 0, s, a)) \
+           : (variance_a1 ? launch_pdl(bn_bwd_reduce_kernel<false, true, GG>, grid, kBT, 0, s, a)  \
+                          : launch_pdl(bn_bwd_reduce_kernel<false, false, GG>, grid, kBT, 0, s, a)))
+    if (G == 8) QT_RED(8);
+    else if (G == 4) QT_RED(4);
+    else QT_RED(0);
+#undef QT_RED
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -410,19 +446,24 @@ extern "C" int qt_bn_backward_apply(const float *g3, qt_tape_t tape, int64_t n, 
     if (!codes) tape.bits = 1;
     ApplyArgs a{g3, tape, n, c, h, w, gamma_tape, beta_tape, variance_a1, stats, res_g,
                 lut_base((void *)ws), cr, sc, g_in};
-    a.gppd = make_fastdiv((uint32_t)std::max<int64_t>(1, (h * w) >> 3));
+    const int G = codes ? bn_group(h * w, w) : 0;
+    a.gppd = make_fastdiv((uint32_t)std::max<int64_t>(1, (h * w) / (G > 0 ? G : 8)));
     a.cd = make_fastdiv((uint32_t)c);
     a.wd = make_fastdiv((uint32_t)w);
-    const int64_t work = codes && ((h * w) & 7) == 0 ? (n * c * h * w) >> 3 : n * c * h * w;
+    const int64_t work = G > 0 ? (n * c * h * w) / G : n * c * h * w;
     int64_t blocks = std::min<int64_t>(qt_cdiv(work, kBT), 148 * 16);
     blocks = std::max<int64_t>(blocks, 1);
     cudaStream_t s = qt_s(stream);
-    if (codes)
-        variance_a1 ? launch_pdl(bn_bwd_apply_kernel<true, true>, (unsigned)blocks, kBT, 0, s, a)
-                    : launch_pdl(bn_bwd_apply_kernel<true, false>, (unsigned)blocks, kBT, 0, s, a);
-    else
-        variance_a1 ? launch_pdl(bn_bwd_apply_kernel<false, true>, (unsigned)blocks, kBT, 0, s, a)
-                    : launch_pdl(bn_bwd_apply_kernel<false, false>, (unsigned)blocks, kBT, 0, s, a);
+    const unsigned nb = (unsigned)blocks;
+#define QT_APP(GG)                                                                                \
+    (codes ? (variance_a1 ? launch_pdl(bn_bwd_apply_kernel<true, true, GG>, nb, kBT, 0, s, a)      \
+                          : launch_pdl(bn_bwd_apply_kernel<true, false, GG>, nb, kBT, 0, s, a))    \
+           : (variance_a1 ? launch_pdl(bn_bwd_apply_kernel<false, true, GG>, nb, kBT, 0, s, a)     \
+                          : launch_pdl(bn_bwd_apply_kernel<false, false, GG>, nb, kBT, 0, s, a)))
+    if (G == 8) QT_APP(8);
+    else if (G == 4) QT_APP(4);
+    else QT_APP(0);
+#undef QT_APP
     QT_CHECK_LAUNCH();
     return QT_OK;
 }

@@ -157,3 +157,40 @@ def test_full_size_c2_step_properties():
     loss, g = P.softmax_xent(la, np.arange(128) % 10)
     E.network_backward(spec, pa, tapes, g, x, mode="approx")
     assert bool(torch.isfinite(pa.grads).all()) and bool(pa.grads.any())
+
+
+def test_imagenet_plane_widths_network_step():
+    """One approx step of a small bottleneck net whose stages sit on the
+    ImageNet plane widths 56 / 28 / 14 / 7 (segmented 3x3 convs with and
+    without a halo, flat zero-padded 1x1 / 2x2-s2 convs, 4-pixel BN-backward
+    groups, the lower-resolution shortcut adjoint on 28-wide rows) against
+    the oracle."""
+    spec = E.make_bottleneck_spec([1, 1, 1, 1], [16, 16, 16, 16], input_shape=(3, 112, 112),
+                                  stem=(2, 2, 0, 16))
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((2, 3, 112, 112)).astype(np.float32)
+    y = rng.integers(0, 10, 2)
+    params = P.init_params(spec, 0)
+    xd = dev(x)
+    logits, tapes = E.network_forward(spec, params, xd, mode="approx", bits=4)
+    loss, lg = P.softmax_xent(logits, y)
+    E.network_backward(spec, params, tapes, lg, xd, mode="approx")
+    sj = spec.to_json()
+    ref = O.init_params(sj, 0)
+    rlog, rtapes = O.net_fwd(sj, ref, x, "approx", 4)
+    rloss, rg = O.softmax_xent(rlog, y)
+    O.net_bwd(sj, ref, rtapes, rg)
+    assert norm_err(host(logits), rlog) < STEP_TOL
+    flips = 0
+    for t, r in zip(tapes, rtapes):
+        if t is not None and t.is_quantized:
+            a = O.unpack(host(t.stored.codes), 4, t.stored.numel)
+            b = O.unpack(r["q"]["codes"], 4, t.stored.numel)
+            assert np.mean(a == b) > 0.995
+            flips += int((a != b).sum())
+    gtol = STEP_TOL if flips == 0 else FLIP_TOL
+    for j, (p, rp) in enumerate(zip(params, ref)):
+        assert norm_err(host(p.grad_weight), rp["grad_weight"]) < gtol, (j, flips)
+        if p.preact:
+            assert norm_err(host(p.grad_gamma), rp["grad_gamma"]) < gtol, (j, flips)
+            assert norm_err(host(p.grad_beta), rp["grad_beta"]) < gtol, (j, flips)

@@ -202,6 +202,11 @@ def test_zero_gradient():
     # launch generic, and one wide channel making one row group generic
     (4, 16, 16, 32, 3, 1, 4, "approx", "wide"), (2, 32, 32, 16, 3, 1, 4, "approx", "mixed"),
     (4, 64, 256, 8, 1, 0, 4, "approx", "mixed"), (4, 16, 64, 16, 1, 0, 4, "approx", "dead"),
+    # ImageNet plane widths: segmented 3x3 (halo above 32 px), flat-padded
+    # 1x1, 4-pixel BN-backward groups (14x14), scalar BN backward (7x7)
+    (2, 32, 32, 14, 3, 1, 4, "approx"), (2, 16, 32, 7, 1, 0, 4, "approx"),
+    (2, 16, 16, 14, 3, 1, 1, "approx"), (2, 16, 16, 28, 3, 1, 2, "approx", "wide"),
+    (2, 32, 16, 14, 1, 0, 8, "exact"), (1, 16, 16, 56, 3, 1, 4, "approx", "mixed"),
 ])
 def test_backward_given_device_tape(cfg):
     """Backward parity with the oracle fed OUR tape (codes, step, offset,
