@@ -46,6 +46,7 @@ struct FwdArgs {
     unsigned long long *clip_count;
     const BnConst *consts;   // optional: per-channel constants from qt_bn_stats_prep
     FastDiv hw8d, cd;        // stream kernel: group -> plane -> channel (32-bit)
+    FastDiv hw4d;            // fused stream kernel: half group -> plane (hw % 4 == 0)
 };
 
 __device__ __forceinline__ PlaneConst make_plane(const FwdArgs &a, int64_t ch, bool apply_bn) {
@@ -383,22 +384,35 @@ __global__ void __launch_bounds__(kThreads) bn_relu_quant_stream(FwdArgs a) {
         for (int u = 0; u < 2; ++u) {
             const int64_t gg = gs[u];
             if (gg >= ngroups) break;
-            const uint32_t plane = fast_div((uint32_t)gg, a.hw8d);
-            const uint32_t ch = plane - fast_div(plane, a.cd) * (uint32_t)a.c;
+            // planes of hw % 8 == 4 pixels: a group may start in one channel
+            // and end in the next (halves 0-3 / 4-7 never straddle)
+            const uint32_t pa = fast_div(2u * (uint32_t)gg, a.hw4d);
+            const uint32_t pb = fast_div(2u * (uint32_t)gg + 1u, a.hw4d);
+            const uint32_t ch = pa - fast_div(pa, a.cd) * (uint32_t)a.c;
             const BnConst k = a.consts[ch];
+            const bool split = pb != pa;
+            const BnConst kb = split ? a.consts[pb - fast_div(pb, a.cd) * (uint32_t)a.c] : k;
             const float xv[8] = {xa[u].x, xa[u].y, xa[u].z, xa[u].w, xb[u].x, xb[u].y, xb[u].z, xb[u].w};
             float a2v[8], a3v[8];
             uint64_t word = 0;
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
-                float v = __fsub_rn(xv[j], k.m32);       // layer.py:246-249
-                v = __fmul_rn(v, k.inv32);
-                v = __fmul_rn(v, k.g);
-                a2v[j] = __fadd_rn(v, k.b);
+                const BnConst &kk = j < 4 ? k : kb;
+                float v = __fsub_rn(xv[j], kk.m32);      // layer.py:246-249
+                v = __fmul_rn(v, kk.inv32);
+                v = __fmul_rn(v, kk.g);
+                a2v[j] = __fadd_rn(v, kk.b);
             }
             if (BITS) {
                 uint32_t code[8], clipmask;
                 quant8<BITS>(a2v, k, code, clipmask);
+                if (split) {   // second half with the next channel's constants
+                    uint32_t code_b[8], clip_b;
+                    quant8<BITS>(a2v, kb, code_b, clip_b);
+#pragma unroll
+                    for (int j = 4; j < 8; ++j) code[j] = code_b[j];
+                    clipmask = (clipmask & 0x0Fu) | (clip_b & 0xF0u);
+                }
                 if (CLIP) clip += __popc(clipmask);
                 if (BITS * 8 <= 32) {
                     uint32_t w32 = 0;
@@ -411,7 +425,9 @@ __global__ void __launch_bounds__(kThreads) bn_relu_quant_stream(FwdArgs a) {
                 }
 #pragma unroll
                 for (int j = 0; j < 8; ++j)
-                    a3v[j] = relu_np(MODE == MODE_NAIVE ? decode(code[j], k.step, k.off, BITS) : a2v[j]);
+                    a3v[j] = relu_np(MODE == MODE_NAIVE ? decode(code[j], j < 4 ? k.step : kb.step,
+                                                                 j < 4 ? k.off : kb.off, BITS)
+                                                        : a2v[j]);
             } else {
 #pragma unroll
                 for (int j = 0; j < 8; ++j) a3v[j] = relu_np(a2v[j]);
@@ -583,13 +599,14 @@ static void launch_stream(const FwdArgs &a, unsigned blocks, cudaStream_t s) {
 static int launch_fwd(const FwdArgs &a0, bool apply_bn, cudaStream_t s) {
     if (a0.numel == 0) return QT_OK;
     FwdArgs a = a0;
-    if ((a.hw & 7) == 0 && a.hw < (1ll << 31) && a.c < (1ll << 31)) {
-        a.hw8d = make_fastdiv((uint32_t)(a.hw >> 3));
+    if ((a.hw & 3) == 0 && a.hw < (1ll << 31) && a.c < (1ll << 31)) {
+        a.hw8d = make_fastdiv((uint32_t)std::max<int64_t>(1, a.hw >> 3));
+        a.hw4d = make_fastdiv((uint32_t)(a.hw >> 2));
         a.cd = make_fastdiv((uint32_t)a.c);
     }
     const bool aligned = ((((uintptr_t)a.x) | ((uintptr_t)a.a3_out) | ((uintptr_t)a.a2_tape)) & 15) == 0;
-    if (apply_bn && a.consts && a.a3_out && (a.hw & 7) == 0 && aligned &&
-        (a.bits == 0 || a.codes) && (a.numel >> 3) < (1ll << 31)) {
+    if (apply_bn && a.consts && a.a3_out && (a.hw & 3) == 0 && aligned &&
+        (a.bits == 0 || a.codes) && (a.numel & 7) == 0 && (a.numel >> 2) < (1ll << 31)) {
         const int64_t ngroups = a.numel >> 3;
         int64_t blocks = std::min<int64_t>(qt_cdiv(ngroups, 2 * kThreads), 148 * 8);
         blocks = std::max<int64_t>(blocks, 1);

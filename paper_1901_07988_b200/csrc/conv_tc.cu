@@ -1099,9 +1099,31 @@ __global__ void seg_codes_kernel(const uint8_t *codes, uint32_t *dst, uint32_t w
     const uint32_t pw = (uint32_t)(s.hp * s.owt) / per;       // words per padded plane
     const uint32_t wd = (uint32_t)w / sd, pl = (uint32_t)h / sd * wd;
     const uint32_t cs = (uint32_t)c4 / sd2;
+    const uint32_t *src32 = reinterpret_cast<const uint32_t *>(codes);   // 16-byte aligned tape
     for (uint32_t o = tid; o < words; o += gridDim.x * blockDim.x) {
         const uint32_t m = o / pw, wi = o - m * pw;
         uint32_t acc = 0;
+        // the word's codes are one contiguous run of the source tape: extract
+        // its 32 bits with a funnel shift across two aligned words
+        int64_t run = -1;
+        if (s.flat && sd == 1) {
+            if ((wi + 1) * per <= pl) run = (int64_t)m * pl + wi * per;
+        } else if (!s.flat && per <= (uint32_t)s.owt) {
+            const uint32_t img = m / (uint32_t)c4, ch = m - img * (uint32_t)c4;
+            const uint32_t nn = img / (uint32_t)s.nseg, j = img - nn * (uint32_t)s.nseg;
+            const uint32_t p0 = wi * per, y = p0 / (uint32_t)s.owt, kx = p0 - y * (uint32_t)s.owt;
+            const int col = (int)(j * s.step + kx) - s.halo;
+            if (y < (uint32_t)h && col >= 0 && col + (int)per <= w)
+                run = (((int64_t)nn * c4 + ch) * h + y) * w + col;
+        }
+        if (run >= 0) {
+            const int64_t bit = run * bits;
+            const int64_t q = bit >> 5;
+            const uint32_t sh = (uint32_t)(bit & 31);
+            const uint32_t lo = __ldg(src32 + q);
+            dst[o] = sh ? __funnelshift_r(lo, __ldg(src32 + q + 1), sh) : lo;
+            continue;
+        }
         if (s.flat) {
             const uint32_t nn = m / (uint32_t)c4, ch = m - nn * (uint32_t)c4;
             const uint32_t c0 = ch / sd2, uv = ch - c0 * sd2, u = uv / sd, v = uv - u * sd;

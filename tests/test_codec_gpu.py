@@ -146,15 +146,17 @@ def test_large_tensor_roundtrip_property():
         assert t.clip_count == int((~unclipped).sum())
 
 
+@pytest.mark.parametrize("hw", [64, 196, 12, 4])
 @pytest.mark.parametrize("bits", [1, 2, 4, 8])
-def test_stream_kernel_codes_at_interval_boundaries(bits):
+def test_stream_kernel_codes_at_interval_boundaries(bits, hw):
     """The fused BN-apply + quantize stream kernel (per-channel constant table,
     fp32 fast path for floor(a*scale) with a float64 fallback near integers)
     against the oracle at exact code boundaries k*step, their fp32
-    neighbours, huge / non-finite / subnormal values and tiny gammas."""
+    neighbours, huge / non-finite / subnormal values and tiny gammas, on
+    planes of hw % 8 == 0 and hw % 8 == 4 pixels."""
     from paper_1901_07988_b200 import _native as N
     rng = np.random.default_rng(bits)
-    n, c, hw = 3, 6, 64
+    n, c = 3, 6   # hw % 8 == 4: 8-element groups straddle two channels
     gamma = np.array([1.0, 0.37, -2.5, 1e-9, 0.0, 3.0], np.float32)
     beta = np.array([0.0, 0.11, -0.7, 0.2, 1e-3, 25.0], np.float32)
     scale, step, off = O.code_constants(gamma, beta, bits)
