@@ -363,7 +363,7 @@ __device__ __forceinline__ void quant8(const float (&v)[8], const BnConst &k, ui
     }
 }
 
-template <int BITS, int MODE, bool A2, bool CLIP>
+template <int BITS, int MODE, bool A2, bool CLIP, bool H4 = false>
 __global__ void __launch_bounds__(kThreads) bn_relu_quant_stream(FwdArgs a) {
     pdl_enter();
     const int64_t ngroups = a.numel >> 3;
@@ -386,11 +386,12 @@ __global__ void __launch_bounds__(kThreads) bn_relu_quant_stream(FwdArgs a) {
             if (gg >= ngroups) break;
             // planes of hw % 8 == 4 pixels: a group may start in one channel
             // and end in the next (halves 0-3 / 4-7 never straddle)
-            const uint32_t pa = fast_div(2u * (uint32_t)gg, a.hw4d);
-            const uint32_t pb = fast_div(2u * (uint32_t)gg + 1u, a.hw4d);
+            // (H4 instantiation only; hw % 8 == 0 keeps the one-channel group)
+            const uint32_t pa = H4 ? fast_div(2u * (uint32_t)gg, a.hw4d) : fast_div((uint32_t)gg, a.hw8d);
+            const uint32_t pb = H4 ? fast_div(2u * (uint32_t)gg + 1u, a.hw4d) : pa;
             const uint32_t ch = pa - fast_div(pa, a.cd) * (uint32_t)a.c;
             const BnConst k = a.consts[ch];
-            const bool split = pb != pa;
+            const bool split = H4 && pb != pa;
             const BnConst kb = split ? a.consts[pb - fast_div(pb, a.cd) * (uint32_t)a.c] : k;
             const float xv[8] = {xa[u].x, xa[u].y, xa[u].z, xa[u].w, xb[u].x, xb[u].y, xb[u].z, xb[u].w};
             float a2v[8], a3v[8];
@@ -587,13 +588,18 @@ __global__ void __launch_bounds__(kThreads) dequant_stream(DecArgs a, FastDiv hw
 template <int BITS>
 static void launch_stream(const FwdArgs &a, unsigned blocks, cudaStream_t s) {
     const bool clip = a.clip_count != nullptr;
+    const bool h4 = (a.hw & 7) != 0;
+#define QT_ST(M, C)                                                                                 \
+    (h4 ? launch_pdl(bn_relu_quant_stream<BITS, M, false, C, true>, blocks, kThreads, 0, s, a)       \
+        : launch_pdl(bn_relu_quant_stream<BITS, M, false, C, false>, blocks, kThreads, 0, s, a))
     if (a.mode == MODE_NAIVE) {
-        if (clip) launch_pdl(bn_relu_quant_stream<BITS, MODE_NAIVE, false, true>, blocks, kThreads, 0, s, a);
-        else launch_pdl(bn_relu_quant_stream<BITS, MODE_NAIVE, false, false>, blocks, kThreads, 0, s, a);
+        if (clip) QT_ST(MODE_NAIVE, true);
+        else QT_ST(MODE_NAIVE, false);
     } else {
-        if (clip) launch_pdl(bn_relu_quant_stream<BITS, MODE_APPROX, false, true>, blocks, kThreads, 0, s, a);
-        else launch_pdl(bn_relu_quant_stream<BITS, MODE_APPROX, false, false>, blocks, kThreads, 0, s, a);
+        if (clip) QT_ST(MODE_APPROX, true);
+        else QT_ST(MODE_APPROX, false);
     }
+#undef QT_ST
 }
 
 static int launch_fwd(const FwdArgs &a0, bool apply_bn, cudaStream_t s) {
@@ -613,8 +619,13 @@ static int launch_fwd(const FwdArgs &a0, bool apply_bn, cudaStream_t s) {
         const unsigned b = (unsigned)blocks;
         switch (a.bits) {
             case 0:
-                if (a.a2_tape) launch_pdl(bn_relu_quant_stream<0, MODE_EXACT, true, false>, b, kThreads, 0, s, a);
-                else launch_pdl(bn_relu_quant_stream<0, MODE_EXACT, false, false>, b, kThreads, 0, s, a);
+                if ((a.hw & 7) != 0) {
+                    if (a.a2_tape) launch_pdl(bn_relu_quant_stream<0, MODE_EXACT, true, false, true>, b, kThreads, 0, s, a);
+                    else launch_pdl(bn_relu_quant_stream<0, MODE_EXACT, false, false, true>, b, kThreads, 0, s, a);
+                } else {
+                    if (a.a2_tape) launch_pdl(bn_relu_quant_stream<0, MODE_EXACT, true, false>, b, kThreads, 0, s, a);
+                    else launch_pdl(bn_relu_quant_stream<0, MODE_EXACT, false, false>, b, kThreads, 0, s, a);
+                }
                 break;
             case 1: launch_stream<1>(a, b, s); break;
             case 2: launch_stream<2>(a, b, s); break;
