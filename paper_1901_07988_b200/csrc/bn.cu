@@ -93,6 +93,7 @@ struct StatsArgs {
     int64_t *offset;
     int64_t *clip;
     FastDiv hw8d;       // hw / 8 (vectorized stats loop)
+    FastDiv hw4d;       // hw / 4 (4-pixel groups, hw % 8 == 4)
 };
 
 __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
@@ -131,15 +132,28 @@ __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
                     ((d4 * d4 + d5 * d5) + (d6 * d6 + d7 * d7));
           }
         }
-    } else if ((a.hw & 3) == 0) {
-        const int64_t hw4 = a.hw >> 2;
-        for (int64_t e = threadIdx.x; e < cnt / 4; e += kRThreads) {
-            int64_t pl = e / hw4, off = e - pl * hw4;
-            float4 q = __ldg(reinterpret_cast<const float4 *>(a.x + ((p0 + pl) * a.c + ch) * a.hw) + off);
-            double d0 = (double)q.x - shift, d1 = (double)q.y - shift;
-            double d2 = (double)q.z - shift, d3 = (double)q.w - shift;
-            v[0] += (d0 + d1) + (d2 + d3);
-            v[1] += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+    } else if ((a.hw & 3) == 0 && cnt / 4 < (1ll << 31)) {
+        // same per-thread order as one group per iteration; U loads in flight
+        const uint32_t hw4 = (uint32_t)(a.hw >> 2), n4 = (uint32_t)(cnt / 4);
+        constexpr int U = 4;
+        for (uint32_t e0 = threadIdx.x; e0 < n4; e0 += U * kRThreads) {
+            float4 qq[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t e = e0 + u * kRThreads;
+                if (e >= n4) break;
+                const uint32_t pl = fast_div(e, a.hw4d), off = e - pl * hw4;
+                qq[u] = __ldg(reinterpret_cast<const float4 *>(a.x + ((p0 + pl) * a.c + ch) * a.hw) + off);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (e0 + u * kRThreads >= n4) break;
+                const float4 q = qq[u];
+                double d0 = (double)q.x - shift, d1 = (double)q.y - shift;
+                double d2 = (double)q.z - shift, d3 = (double)q.w - shift;
+                v[0] += (d0 + d1) + (d2 + d3);
+                v[1] += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+            }
         }
     } else {
         for (int64_t e = threadIdx.x; e < cnt; e += kRThreads) {
@@ -331,6 +345,7 @@ extern "C" int qt_bn_stats(const float *x, int64_t n, int64_t c, int64_t hw, dou
                 (double *)((char *)ws + kCounterBytes), (unsigned *)ws,
                 nullptr, nullptr, 0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     a.hw8d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 3));
+    a.hw4d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 2));
     dim3 grid((unsigned)p.blocks, (unsigned)c);
     launch_pdl(bn_stats_kernel, grid, kRThreads, 0, qt_s(stream), a);
     QT_CHECK_LAUNCH();
@@ -352,6 +367,7 @@ extern "C" int qt_bn_stats_prep(const float *x, int64_t n, int64_t c, int64_t hw
                 gamma, beta, bits, eps, (BnConst *)consts, gamma_copy, beta_copy, step, offset,
                 clip_count};
     a.hw8d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 3));
+    a.hw4d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 2));
     dim3 grid((unsigned)p.blocks, (unsigned)c);
     launch_pdl(bn_stats_kernel, grid, kRThreads, 0, qt_s(stream), a);
     QT_CHECK_LAUNCH();
