@@ -30,13 +30,25 @@ static Part partition(int64_t n, int64_t c, int64_t hw) {
     // block per channel
     (void)c;
     Part p;
-    p.planes_per_block = std::max<int64_t>(1, kTargetPerBlock / hw);
+    p.planes_per_block = std::max<int64_t>(1, qt_red_target() / hw);
     // at least ~2 blocks per SM: a small layer's single pass is one load
     // round per block, so spread it rather than lengthen it
     p.planes_per_block = std::min<int64_t>(p.planes_per_block,
-                                           std::max<int64_t>(1, n * c / (2 * 148)));
+                                           std::max<int64_t>(1, n * c / qt_red_div()));
     if (p.planes_per_block > n) p.planes_per_block = n;
     p.blocks = qt_cdiv(n, p.planes_per_block);
+    return p;
+}
+
+// Clustered BN statistics: at most kStatsCluster blocks per channel (one
+// cluster), each a contiguous run of planes.
+constexpr int64_t kStatsCluster = 8;
+static Part stats_partition(int64_t n, int64_t c, int64_t hw) {
+    Part p = partition(n, c, hw);
+    if (p.blocks > kStatsCluster) {
+        p.planes_per_block = qt_cdiv(n, kStatsCluster);
+        p.blocks = qt_cdiv(n, p.planes_per_block);
+    }
     return p;
 }
 
@@ -102,6 +114,20 @@ __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
     const int64_t ch = blockIdx.y;
     const int64_t p0 = (int64_t)blockIdx.x * a.ppb;
     const int64_t p1 = min(p0 + a.ppb, a.n);
+    // the finalizing thread loads the channel's parameters and evaluates its
+    // code constants now, under the main loop's loads
+    const bool fin = blockIdx.x == 0 && threadIdx.x == 0;
+    float pg = 0.f, pb = 0.f;
+    double prm = 0.0, prv = 0.0;
+    ChanCode pcc{};
+    if (fin) {
+        if (a.rmean) { prm = a.rmean[ch]; prv = a.rvar[ch]; }
+        if (a.consts) {
+            pg = a.gamma[ch];
+            pb = a.beta[ch];
+            if (a.bits) pcc = chan_code(pg, pb, a.bits);
+        }
+    }
     const double shift = (double)a.x[ch * a.hw];  // x[0, c, 0]: shifted sums
     double v[2] = {0.0, 0.0};
     const int64_t cnt = (p1 - p0) * a.hw;
@@ -163,26 +189,25 @@ __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
             v[1] += d * d;
         }
     }
+    // the nb blocks of channel ch form one cluster: each publishes its block
+    // sum in shared memory, rank 0 adds them in rank order (no global
+    // partials, fence or counter)
+    __shared__ double s_part[2];
     block_sum<2>(v, red);
     if (threadIdx.x == 0) {
-        double *pp = a.part + (ch * a.nb + blockIdx.x) * 2;
-        pp[0] = v[0];
-        pp[1] = v[1];
+        s_part[0] = v[0];
+        s_part[1] = v[1];
     }
-    if (!last_block(a.counter + ch, (unsigned)a.nb)) return;
-    // last block: all threads combine the partials (fixed strided order + tree)
-    __threadfence();
-    double fin[2] = {0.0, 0.0};
-    {
-        const double *pp = a.part + ch * a.nb * 2;
-        for (int64_t b = threadIdx.x; b < a.nb; b += kRThreads) {
-            fin[0] += __ldcg(pp + 2 * b);
-            fin[1] += __ldcg(pp + 2 * b + 1);
+    cluster_sync_all();
+    double s1 = 0.0, s2 = 0.0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        for (unsigned r = 0; r < (unsigned)a.nb; ++r) {
+            s1 += ld_dsmem_f64(&s_part[0], r);
+            s2 += ld_dsmem_f64(&s_part[1], r);
         }
     }
-    block_sum<2>(fin, red);
-    if (threadIdx.x == 0) {
-        const double s1 = fin[0], s2 = fin[1];
+    cluster_sync_all();   // remote CTAs keep their shared memory until read
+    if (fin) {
         const double cntd = (double)(a.n * a.hw);
         const double dm = s1 / cntd;
         double var = (s2 - s1 * dm) / cntd;
@@ -192,17 +217,17 @@ __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
         a.var[ch] = var;
         if (a.rmean) {  // layer.py:237-241
             const double m = 0.9;
-            a.rmean[ch] = __dadd_rn(__dmul_rn(a.rmean[ch], m), __dmul_rn(1.0 - m, mean));
-            a.rvar[ch] = __dadd_rn(__dmul_rn(a.rvar[ch], m), __dmul_rn(1.0 - m, var));
+            a.rmean[ch] = __dadd_rn(__dmul_rn(prm, m), __dmul_rn(1.0 - m, mean));
+            a.rvar[ch] = __dadd_rn(__dmul_rn(prv, m), __dmul_rn(1.0 - m, var));
         }
         if (a.consts) {  // per-channel constants of the fused forward (K1)
-            const float g = a.gamma[ch], b = a.beta[ch];
-            a.consts[ch] = bn_const(mean, var, a.eps, g, b, a.bits);
-            a.gcopy[ch] = g;          // frozen tape copies (layer.py:253-255)
-            a.bcopy[ch] = b;
+            const BnConst k = bn_const_cc(mean, var, a.eps, pg, pb, a.bits, pcc);
+            a.consts[ch] = k;
+            a.gcopy[ch] = pg;          // frozen tape copies (layer.py:253-255)
+            a.bcopy[ch] = pb;
             if (a.bits) {
-                a.step[ch] = a.consts[ch].step;
-                a.offset[ch] = a.consts[ch].off;
+                a.step[ch] = k.step;
+                a.offset[ch] = k.off;
             }
             if (ch == 0 && a.clip) *a.clip = 0;
         }
@@ -340,14 +365,14 @@ extern "C" int qt_bn_stats(const float *x, int64_t n, int64_t c, int64_t hw, dou
                            qt_stream_t stream) {
     QT_REQUIRE(x && mean && var && ws && n > 0 && c > 0 && hw > 0 && c <= kMaxChannels);
     QT_REQUIRE((running_mean == nullptr) == (running_var == nullptr));
-    Part p = partition(n, c, hw);
+    Part p = stats_partition(n, c, hw);
     StatsArgs a{x, n, c, hw, p.planes_per_block, p.blocks, mean, var, running_mean, running_var,
                 (double *)((char *)ws + kCounterBytes), (unsigned *)ws,
                 nullptr, nullptr, 0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     a.hw8d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 3));
     a.hw4d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 2));
     dim3 grid((unsigned)p.blocks, (unsigned)c);
-    launch_pdl(bn_stats_kernel, grid, kRThreads, 0, qt_s(stream), a);
+    launch_pdl_cluster(bn_stats_kernel, grid, kRThreads, 0, qt_s(stream), (unsigned)p.blocks, a);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -361,7 +386,7 @@ extern "C" int qt_bn_stats_prep(const float *x, int64_t n, int64_t c, int64_t hw
     QT_REQUIRE(n > 0 && c > 0 && hw > 0 && c <= kMaxChannels);
     QT_REQUIRE(bits == 0 || (qt_bits_ok(bits) && step && offset));
     QT_REQUIRE((running_mean == nullptr) == (running_var == nullptr));
-    Part p = partition(n, c, hw);
+    Part p = stats_partition(n, c, hw);
     StatsArgs a{x, n, c, hw, p.planes_per_block, p.blocks, mean, var, running_mean, running_var,
                 (double *)((char *)ws + kCounterBytes), (unsigned *)ws,
                 gamma, beta, bits, eps, (BnConst *)consts, gamma_copy, beta_copy, step, offset,
@@ -369,7 +394,7 @@ extern "C" int qt_bn_stats_prep(const float *x, int64_t n, int64_t c, int64_t hw
     a.hw8d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 3));
     a.hw4d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 2));
     dim3 grid((unsigned)p.blocks, (unsigned)c);
-    launch_pdl(bn_stats_kernel, grid, kRThreads, 0, qt_s(stream), a);
+    launch_pdl_cluster(bn_stats_kernel, grid, kRThreads, 0, qt_s(stream), (unsigned)p.blocks, a);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }

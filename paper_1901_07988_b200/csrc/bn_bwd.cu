@@ -37,8 +37,8 @@ static BwdPart bwd_partition(int64_t n, int64_t c, int64_t hw) {
     // the large layers, one block per channel for the small ones
     (void)c;
     BwdPart p;
-    p.ppb = std::max<int64_t>(1, 8192 / hw);
-    p.ppb = std::min<int64_t>(p.ppb, std::max<int64_t>(1, n * c / (2 * 148)));   // >= ~2 blocks / SM
+    p.ppb = std::max<int64_t>(1, qt_env_i64("QTAPE_BWD_TGT", qt_red_target()) / hw);
+    p.ppb = std::min<int64_t>(p.ppb, std::max<int64_t>(1, n * c / qt_env_i64("QTAPE_BWD_DIV", qt_red_div())));   // >= ~2 blocks / SM
     if (p.ppb > n) p.ppb = n;
     p.nb = qt_cdiv(n, p.ppb);
     return p;
@@ -64,6 +64,7 @@ struct BwdArgs {
     unsigned *counter;
     float *lut;      // [C][2][256]: mask, a1 per code
     FastDiv gppd;    // hw / 8
+    int dbg_nofin;
 };
 
 // mask (1/0) and a1 for one code of channel ch (layer.py:354-366)
@@ -227,6 +228,7 @@ __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
             for (int q = 0; q < kBT / 32; ++q) t += red[j][q];
             pp[j] = t;
         }
+        if (a.dbg_nofin) return;
         __threadfence();
         const unsigned prev = atomicAdd(a.counter + ch, 1u);
         s_last = prev == (unsigned)a.nb - 1;
@@ -418,6 +420,7 @@ extern "C" int qt_bn_backward_reduce(const float *g3, qt_tape_t tape, int64_t n,
     // and code width only, never on the tape type
     const int G = bn_group(hw, hw);
     a.gppd = make_fastdiv((uint32_t)std::max<int64_t>(1, hw / (G > 0 ? G : 8)));
+    a.dbg_nofin = getenv("QTAPE_DBG_NOFIN") ? 1 : 0;
     dim3 grid((unsigned)p.nb, (unsigned)c);
     cudaStream_t s = qt_s(stream);
 #define QT_RED(GG)                                                                                \

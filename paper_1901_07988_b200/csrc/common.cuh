@@ -40,6 +40,20 @@ static inline bool qt_pdl_enabled() {
     }
     return v == 1;
 }
+// Reduction partition knobs (tuning only): elements per block and the
+// divisor that spreads small layers (blocks per channel >= n*c / div).
+static inline int64_t qt_env_i64(const char *name, int64_t dflt) {
+    const char *e = getenv(name);
+    return (e && *e) ? (int64_t)atoll(e) : dflt;
+}
+static inline int64_t qt_red_target() {
+    static int64_t v = qt_env_i64("QTAPE_RED_TGT", 8192);
+    return v;
+}
+static inline int64_t qt_red_div() {
+    static int64_t v = qt_env_i64("QTAPE_RED_DIV", 2 * 148);
+    return v;
+}
 template <typename... KArgs, typename... Args>
 static inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem,
                                      cudaStream_t st, Args &&...args) {
@@ -56,6 +70,30 @@ static inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 blo
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// Same, with a thread-block cluster of `cx` CTAs along x (the blocks of one
+// channel reduce through distributed shared memory instead of a global
+// counter).
+template <typename... KArgs, typename... Args>
+static inline cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block,
+                                             size_t smem, cudaStream_t st, unsigned cx,
+                                             Args &&...args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = cx;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = qt_pdl_enabled() ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 namespace qt {
 
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
@@ -66,6 +104,20 @@ __device__ __forceinline__ void pdl_trigger() {
 __device__ __forceinline__ void pdl_enter() {
     pdl_wait();
     pdl_trigger();
+}
+
+// Cluster-wide barrier (release/acquire: shared-memory writes before it are
+// visible to every CTA of the cluster after it).
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// Load a double from CTA `rank`'s copy of the shared variable at `p`.
+__device__ __forceinline__ double ld_dsmem_f64(const double *p, unsigned rank) {
+    uint32_t local = (uint32_t)__cvta_generic_to_shared(p), remote;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local), "r"(rank));
+    double v;
+    asm volatile("ld.shared::cluster.f64 %0, [%1];" : "=d"(v) : "r"(remote) : "memory");
+    return v;
 }
 
 constexpr double kGammaFloor = 1e-8;   // codec.py:24
@@ -107,8 +159,10 @@ struct BnConst {
     float s1, s2;             // scale = s1 + s2 (+ < 2^-48 rel): code_fast
 };
 
-__device__ __forceinline__ BnConst bn_const(double mean, double var, double eps, float gamma,
-                                            float beta, int bits) {
+// bn_const with the channel's code constants already computed (they depend
+// on gamma / beta only, so a finalizer can evaluate them off the critical path)
+__device__ __forceinline__ BnConst bn_const_cc(double mean, double var, double eps, float gamma,
+                                               float beta, int bits, const ChanCode &cc) {
     BnConst k;
     const double inv = __ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(var, eps)));   // layer.py:245
     k.m32 = __double2float_rn(mean);
@@ -120,7 +174,6 @@ __device__ __forceinline__ BnConst bn_const(double mean, double var, double eps,
     k.off = 0;
     k.s1 = k.s2 = 0.f;
     if (bits) {
-        ChanCode cc = chan_code(gamma, beta, bits);
         k.scale = cc.scale;
         k.step = cc.step;
         k.off = cc.off;
@@ -128,6 +181,13 @@ __device__ __forceinline__ BnConst bn_const(double mean, double var, double eps,
         k.s2 = __double2float_rn(cc.scale - (double)k.s1);
     }
     return k;
+}
+
+__device__ __forceinline__ BnConst bn_const(double mean, double var, double eps, float gamma,
+                                            float beta, int bits) {
+    ChanCode cc{};
+    if (bits) cc = chan_code(gamma, beta, bits);
+    return bn_const_cc(mean, var, eps, gamma, beta, bits, cc);
 }
 
 // Unclipped code with wrapping int64 arithmetic (codec.py:118-120).
