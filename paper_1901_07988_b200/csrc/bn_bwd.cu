@@ -44,6 +44,17 @@ static BwdPart bwd_partition(int64_t n, int64_t c, int64_t hw) {
     return p;
 }
 
+// The reduce launch: at most kBwdCluster blocks per channel (one cluster).
+constexpr int64_t kBwdCluster = 8;
+static BwdPart reduce_partition(int64_t n, int64_t c, int64_t hw) {
+    BwdPart p = bwd_partition(n, c, hw);
+    if (p.nb > kBwdCluster) {
+        p.ppb = qt_cdiv(n, kBwdCluster);
+        p.nb = qt_cdiv(n, p.ppb);
+    }
+    return p;
+}
+
 // ws layout: [counters 256 KiB][lut: C x 2 x 256 floats][partials C x nb x 4 doubles]
 static inline float *lut_base(void *ws) { return (float *)((char *)ws + kBwdCounterBytes); }
 static inline double *part_base(void *ws, int64_t c) {
@@ -64,7 +75,6 @@ struct BwdArgs {
     unsigned *counter;
     float *lut;      // [C][2][256]: mask, a1 per code
     FastDiv gppd;    // hw / 8
-    int dbg_nofin;
 };
 
 // mask (1/0) and a1 for one code of channel ch (layer.py:354-366)
@@ -112,18 +122,29 @@ __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
     __shared__ float2 s_ma[kMaxLut];      // (mask, a1) per code: one 8-byte lookup
     __shared__ double s_a1d[kMaxLut];
     __shared__ double red[3][kBT / 32];
-    __shared__ bool s_last;
+    __shared__ double s_part[3];          // this block's sums, read by cluster rank 0
     const int ch = blockIdx.y;
+    // the finalizing thread (rank 0, thread 0) loads what the finalize needs now
+    const bool fin = blockIdx.x == 0 && threadIdx.x == 0;
+    double fin_s2 = 0.0;
+    float fin_gb = 0.f, fin_gg = 0.f;
+    if (fin) {
+        fin_s2 = a.sigma2[ch];
+        if (a.grad_beta) fin_gb = a.grad_beta[ch];
+        if (a.grad_gamma) fin_gg = a.grad_gamma[ch];
+    }
     const float gam = a.gamma[ch], bet = a.beta[ch], sg = safe_gamma(gam);
     const int ncode = CODES ? (1 << a.tape.bits) : 0;
-    if (CODES) {
-        for (int code = threadIdx.x; code < ncode; code += kBT) {
-            lut_entry(a.tape, ch, code, bet, sg, s_m[code], s_a1[code]);
-            s_a1d[code] = (double)s_a1[code];
-            s_ma[code] = make_float2(s_m[code], s_a1[code]);
+    auto build_lut = [&]() {
+        if (CODES) {
+            for (int code = threadIdx.x; code < ncode; code += kBT) {
+                lut_entry(a.tape, ch, code, bet, sg, s_m[code], s_a1[code]);
+                s_a1d[code] = (double)s_a1[code];
+                s_ma[code] = make_float2(s_m[code], s_a1[code]);
+            }
+            __syncthreads();
         }
-        __syncthreads();
-    }
+    };
     const int64_t p0 = (int64_t)blockIdx.x * a.ppb;
     const int64_t p1 = min(p0 + a.ppb, a.n);
     // float64 accumulators: S0 = sum g3m, S1 = sum a1*g3m, S3' = sum a1v*g3m
@@ -139,10 +160,10 @@ __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
         const uint32_t groups = (uint32_t)cnt8;
         const uint32_t gpp = (uint32_t)(a.hw / G);
         constexpr int U = 4;                     // groups in flight per thread
-        for (uint32_t g0 = threadIdx.x; g0 < groups; g0 += U * kBT) {
-            float4 ga[U], gb[U], xa[U], xb[U];
-            uint64_t word[U];
-            int64_t i0[U];
+        float4 ga[U], gb[U], xa[U], xb[U];
+        uint64_t word[U];
+        int64_t i0[U];
+        auto load = [&](uint32_t g0) {
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const uint32_t gi = g0 + u * kBT;
@@ -158,6 +179,12 @@ __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
                     if (G == 8) xb[u] = __ldg(reinterpret_cast<const float4 *>(a.tape.a2 + i0[u]) + 1);
                 }
             }
+        };
+        // the first round of loads is in flight while the code table is built
+        load(threadIdx.x);
+        build_lut();
+        for (uint32_t g0 = threadIdx.x; g0 < groups; g0 += U * kBT) {
+            if (g0 != threadIdx.x) load(g0);
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 if (g0 + u * kBT >= groups) break;
@@ -193,6 +220,7 @@ __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
             }
         }
     } else {
+        build_lut();
         const int64_t cnt = (p1 - p0) * a.hw;
         for (int64_t e = threadIdx.x; e < cnt; e += kBT) {
             const int64_t pl = e / a.hw, off = e - pl * a.hw;
@@ -222,21 +250,23 @@ __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        double *pp = a.part + (ch * a.nb + blockIdx.x) * 4;
         for (int j = 0; j < 3; ++j) {
             double t = 0.0;
             for (int q = 0; q < kBT / 32; ++q) t += red[j][q];
-            pp[j] = t;
+            s_part[j] = t;
         }
-        if (a.dbg_nofin) return;
-        __threadfence();
-        const unsigned prev = atomicAdd(a.counter + ch, 1u);
-        s_last = prev == (unsigned)a.nb - 1;
-        if (s_last) a.counter[ch] = 0;
     }
-    __syncthreads();
-    if (!s_last) return;
-    // last block of this channel: publish the code table for the apply pass
+    // the nb blocks of channel ch form one cluster: rank 0 adds the block
+    // sums in rank order through distributed shared memory
+    cluster_sync_all();
+    double s[3] = {0.0, 0.0, 0.0};
+    if (fin) {
+        for (unsigned r = 0; r < (unsigned)a.nb; ++r)
+            for (int j = 0; j < 3; ++j) s[j] += ld_dsmem_f64(&s_part[j], r);
+    }
+    cluster_sync_all();   // remote CTAs keep their shared memory until read
+    if (blockIdx.x != 0) return;
+    // rank 0 publishes the code table for the apply pass
     if (CODES) {
         float *lut = a.lut + (int64_t)ch * 2 * kMaxLut;
         for (int code = threadIdx.x; code < ncode; code += kBT) {
@@ -244,33 +274,15 @@ __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
             lut[kMaxLut + code] = s_a1[code];
         }
     }
-    // combine the partials: fixed strided order, then a fixed tree
-    __threadfence();
-    double f[3] = {0.0, 0.0, 0.0};
-    {
-        const double *pp = a.part + ch * a.nb * 4;
-        for (int64_t b = threadIdx.x; b < a.nb; b += kBT)
-            for (int j = 0; j < 3; ++j) f[j] += __ldcg(pp + 4 * b + j);
-    }
-#pragma unroll
-    for (int j = 0; j < 3; ++j) f[j] = warp_sum(f[j]);
-    __syncthreads();
-    if ((threadIdx.x & 31) == 0) {
-        red[0][w] = f[0]; red[1][w] = f[1]; red[2][w] = f[2];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        double s[3] = {0.0, 0.0, 0.0};
-        for (int j = 0; j < 3; ++j)
-            for (int q = 0; q < kBT / 32; ++q) s[j] += red[j][q];
+    if (fin) {
         const double g64 = (double)gam;
         const double cntd = (double)(a.n * a.hw);
-        if (a.grad_beta) a.grad_beta[ch] = __double2float_rn((double)a.grad_beta[ch] + s[0]);
-        if (a.grad_gamma) a.grad_gamma[ch] = __double2float_rn((double)a.grad_gamma[ch] + s[1]);
+        if (a.grad_beta) a.grad_beta[ch] = __double2float_rn((double)fin_gb + s[0]);
+        if (a.grad_gamma) a.grad_gamma[ch] = __double2float_rn((double)fin_gg + s[1]);
         a.stats[ch] = __double2float_rn(g64 * s[0] / cntd);                   // t2 = mean g1
         a.stats[a.c + ch] = __double2float_rn(g64 * s[2] / cntd);             // t3 = mean a1v*g1
         a.stats[2 * a.c + ch] =
-            __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(a.sigma2[ch], a.eps))));  // inv
+            __double2float_rn(__ddiv_rn(1.0, __dsqrt_rn(__dadd_rn(fin_s2, a.eps))));  // inv
     }
 }
 
@@ -411,7 +423,7 @@ extern "C" int qt_bn_backward_reduce(const float *g3, qt_tape_t tape, int64_t n,
     QT_REQUIRE(g3 && gamma_tape && beta_tape && sigma2 && stats && ws);
     QT_REQUIRE(n > 0 && c > 0 && hw > 0 && c <= 65535);
     QT_REQUIRE(tape.a2 || (tape.codes && tape.step && tape.offset && qt_bits_ok(tape.bits)));
-    BwdPart p = bwd_partition(n, c, hw);
+    BwdPart p = reduce_partition(n, c, hw);
     const bool codes = tape.a2 == nullptr;
     if (!codes) tape.bits = 1;
     BwdArgs a{g3, tape, n, c, hw, gamma_tape, beta_tape, sigma2, eps, variance_a1, grad_gamma,
@@ -420,14 +432,13 @@ extern "C" int qt_bn_backward_reduce(const float *g3, qt_tape_t tape, int64_t n,
     // and code width only, never on the tape type
     const int G = bn_group(hw, hw);
     a.gppd = make_fastdiv((uint32_t)std::max<int64_t>(1, hw / (G > 0 ? G : 8)));
-    a.dbg_nofin = getenv("QTAPE_DBG_NOFIN") ? 1 : 0;
     dim3 grid((unsigned)p.nb, (unsigned)c);
     cudaStream_t s = qt_s(stream);
 #define QT_RED(GG)                                                                                \
-    (codes ? (variance_a1 ? launch_pdl(bn_bwd_reduce_kernel<true, true, GG>, grid, kBT, 0, s, a)   \
-                          : launch_pdl(bn_bwd_reduce_kernel<true, false, GG>, grid, kBT, 0, s, a)) \
-           : (variance_a1 ? launch_pdl(bn_bwd_reduce_kernel<false, true, GG>, grid, kBT, 0, s, a)  \
-                          : launch_pdl(bn_bwd_reduce_kernel<false, false, GG>, grid, kBT, 0, s, a)))
+    (codes ? (variance_a1 ? launch_pdl_cluster(bn_bwd_reduce_kernel<true, true, GG>, grid, kBT, 0, s, (unsigned)p.nb, a)   \
+                          : launch_pdl_cluster(bn_bwd_reduce_kernel<true, false, GG>, grid, kBT, 0, s, (unsigned)p.nb, a)) \
+           : (variance_a1 ? launch_pdl_cluster(bn_bwd_reduce_kernel<false, true, GG>, grid, kBT, 0, s, (unsigned)p.nb, a)  \
+                          : launch_pdl_cluster(bn_bwd_reduce_kernel<false, false, GG>, grid, kBT, 0, s, (unsigned)p.nb, a)))
     if (G == 8) QT_RED(8);
     else if (G == 4) QT_RED(4);
     else QT_RED(0);
