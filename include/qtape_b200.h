@@ -39,6 +39,13 @@ typedef void *qt_stream_t;    /* cudaStream_t */
 int qt_version(void);
 const char *qt_error_string(int status);
 int qt_num_sms(void);
+/* SM partition for a backward pass that runs the data gradients and the
+ * weight gradients concurrently on two streams (the engine's side-stream
+ * weight gradients, engine.py Workspace): when on, layers under 2^30 MACs
+ * launch their data-gradient and weight-gradient GEMMs on half the SMs each,
+ * so the two chains run side by side instead of queueing for every SM.
+ * Off (the default): both use every SM.  Returns the previous setting. */
+int qt_set_concurrent_backward(int on);
 
 /* ---------------------------------------------------------------- codec ---
  * Per-channel codec constants (codec.py:27-29, :101-104, :117):

@@ -36,6 +36,7 @@ SIGNATURES = {
     "qt_version": (I32, []),
     "qt_error_string": (ctypes.c_char_p, [I32]),
     "qt_num_sms": (I32, []),
+    "qt_set_concurrent_backward": (I32, [I32]),
     "qt_codec_constants": (I32, [P, P, I64, I32, P, P, P]),
     "qt_quantize_pack": (I32, [P, I64, I64, I64, P, P, I32, P, P, P, P, P]),
     "qt_unpack_dequant": (I32, [P, I64, I64, I64, I32, P, P, I32, P, P]),

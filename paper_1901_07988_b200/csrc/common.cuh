@@ -96,6 +96,11 @@ static inline cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, 
 
 namespace qt {
 
+// qt_set_concurrent_backward (dense.cu): split the SMs between the data- and
+// weight-gradient GEMMs of small layers
+extern int g_concurrent_bwd;
+constexpr double kSmallLayerMacs = 1073741824.0;   // 2^30
+
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() {
     asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

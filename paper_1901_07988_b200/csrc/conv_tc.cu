@@ -544,6 +544,16 @@ static int num_sms() {
     return n;
 }
 
+// CTA cap of the current launch (0 = every SM); set per call by tc_conv_s1
+static int s_cta_cap = 0;
+static int dgrad_cta_cap() {
+    static const int v = [] {
+        const char *e = getenv("QTAPE_DGRAD_CTAS");
+        return e && atoi(e) > 0 ? atoi(e) : 0;
+    }();
+    return v;
+}
+
 template <int BN, int OWT, int KC, int KW>
 static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, int tiles, int ntiles,
                       cudaStream_t st) {
@@ -567,11 +577,12 @@ static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, int t
     // ntiles) and its nst stages' (hi, lo) tiles fit next to the rings
     const int nst = g.kh * (g.ci / KC);
     const int wbytes = nst * 2 * C::B_SLOT;
-    int grid = std::min(total, num_sms());
+    const int sms = s_cta_cap > 0 ? std::min(num_sms(), s_cta_cap) : num_sms();
+    int grid = std::min(total, sms);
     gg.wres = 0;
-    if (ntiles <= num_sms() && wbytes <= 96 * 1024) {
+    if (ntiles <= sms && wbytes <= 96 * 1024) {
         gg.wres = 1;
-        grid = std::max(ntiles, std::min(total, num_sms()) / ntiles * ntiles);
+        grid = std::max(ntiles, std::min(total, sms) / ntiles * ntiles);
     }
     gg.slot = gg.wres ? (C::A_BYTES + 1023) / 1024 * 1024 : C::RAW_BYTES;
     gg.ntd = make_fastdiv((uint32_t)ntiles);
@@ -682,6 +693,13 @@ static int tc_conv_s1(const float *x, const float *w, float *out, int n, int ci,
                       int co, int kh, int kw, int pad, int flip, const float *res, int cr, int sr,
                       void *ws, cudaStream_t st) {
     FwdGeo g{};
+    {   // data gradient beside the side-stream weight gradients: half the SMs
+        const double macs = (double)n * (h + 2 * pad - kh + 1) * (wd + 2 * pad - kw + 1) *
+                            (double)co * ci * kh * kw;
+        s_cta_cap = !flip ? 0
+                    : dgrad_cta_cap() > 0 ? dgrad_cta_cap()
+                    : (g_concurrent_bwd && macs < kSmallLayerMacs) ? num_sms() / 2 : 0;
+    }
     g.n = n; g.ci = ci; g.h = h; g.w = wd; g.co = co; g.kh = kh; g.kw = kw; g.pad = pad;
     g.oh = h + 2 * pad - kh + 1;
     g.ow = wd + 2 * pad - kw + 1;

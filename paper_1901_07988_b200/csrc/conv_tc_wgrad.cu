@@ -161,17 +161,17 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = 
     // pipeline stage (SUB chunks) per CTA, and the fp32
     // partials (splits x R x co x 4 B, written once and read back by the
     // fixed-order reduction) at most max(4x the g_out bytes, 32 MiB)
-    // Small (CIFAR-sized, < 2^30 MAC) layers are latency-bound: on half the
-    // SMs they take about as long and leave the other half to the
-    // input-gradient chain running beside them on the main stream (measured:
-    // C2 9.72 -> 9.50 ms/step, C3 58.2 -> 57.0; 64 or 96 CTAs are worse).
+    // With the data gradients running beside (qt_set_concurrent_backward),
+    // small (CIFAR-sized, < 2^30 MAC) layers take half the SMs and the data
+    // gradient the other half (measured on C2: wgrad alone on 74 CTAs 9.72 ->
+    // 9.50 ms/step, both halved 8.97; any split summing past 148 is worse).
     // ImageNet-sized layers use every SM (C4 53 ms at 148 CTAs, 62 at 74).
     static const int ctas_env = [] {
         const char *e = getenv("QTAPE_WG_CTAS");
         return e && atoi(e) > 0 ? atoi(e) : 0;
     }();
     const double macs = (double)g.n * (double)oh * (double)ow * (double)g.co * (double)Rout;
-    const int ctas = ctas_env > 0 ? ctas_env : (macs < 1073741824.0 ? 74 : 148);
+    const int ctas = ctas_env > 0 ? ctas_env : ((g_concurrent_bwd && macs < kSmallLayerMacs) ? 74 : 148);
     int want = std::max(1, ctas / (pl.mgroups * pl.nblk));   // one wave: fixed costs once per SM
     want = std::min(want, std::max(1, pl.total / SUB));
     // a CTA's stages run concurrently on its operand groups, so give each

@@ -89,6 +89,16 @@ extern "C" const char *qt_error_string(int status) {
     return "unknown error";
 }
 
+namespace qt {
+int g_concurrent_bwd = 0;
+}
+
+extern "C" int qt_set_concurrent_backward(int on) {
+    const int prev = qt::g_concurrent_bwd;
+    qt::g_concurrent_bwd = on ? 1 : 0;
+    return prev;
+}
+
 extern "C" int qt_num_sms(void) {
     int dev = 0, n = 0;
     if (cudaGetDevice(&dev) != cudaSuccess) return 0;
