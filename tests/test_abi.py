@@ -46,6 +46,18 @@ def test_host_queries_without_gpu():
     assert N.lib().qt_error_string(-1) == b"invalid argument"
 
 
+def test_concurrent_backward_setter_returns_previous():
+    """qt_set_concurrent_backward is a host-side flag (no GPU needed)."""
+    from paper_1901_07988_b200 import _native as N
+    prev = N.query("qt_set_concurrent_backward", 1)
+    try:
+        assert N.query("qt_set_concurrent_backward", 1) == 1
+        assert N.query("qt_set_concurrent_backward", 0) == 1
+        assert N.query("qt_set_concurrent_backward", 0) == 0
+    finally:
+        N.query("qt_set_concurrent_backward", prev)
+
+
 def test_built_for_sm100a():
     import subprocess
     from paper_1901_07988_b200 import _native as N
