@@ -46,7 +46,7 @@ constexpr int64_t kStatsCluster = 8;
 static Part stats_partition(int64_t n, int64_t c, int64_t hw) {
     Part p = partition(n, c, hw);
     // balanced runs: the launch lasts as long as its longest block
-    const int64_t nb = std::min<int64_t>(p.blocks, kStatsCluster);
+    const int64_t nb = std::min<int64_t>(p.blocks, qt_red_cluster());
     p.planes_per_block = qt_cdiv(n, nb);
     p.blocks = qt_cdiv(n, p.planes_per_block);
     return p;

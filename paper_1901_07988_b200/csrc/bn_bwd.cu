@@ -49,7 +49,7 @@ constexpr int64_t kBwdCluster = 8;
 static BwdPart reduce_partition(int64_t n, int64_t c, int64_t hw) {
     BwdPart p = bwd_partition(n, c, hw);
     // balanced runs: the launch lasts as long as its longest block
-    const int64_t nb = std::min<int64_t>(p.nb, kBwdCluster);
+    const int64_t nb = std::min<int64_t>(p.nb, qt_red_cluster());
     p.ppb = qt_cdiv(n, nb);
     p.nb = qt_cdiv(n, p.ppb);
     return p;

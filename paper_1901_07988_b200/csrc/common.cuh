@@ -73,10 +73,17 @@ static inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 blo
 // Same, with a thread-block cluster of `cx` CTAs along x (the blocks of one
 // channel reduce through distributed shared memory instead of a global
 // counter).
+// Blocks per channel (= cluster size) of the clustered reductions; above 8
+// needs the non-portable cluster attribute (set at launch).
+static inline int64_t qt_red_cluster() {
+    static int64_t v = qt_env_i64("QTAPE_RED_CLUSTER", 8);
+    return v;
+}
 template <typename... KArgs, typename... Args>
 static inline cudaError_t launch_pdl_cluster(void (*kern)(KArgs...), dim3 grid, dim3 block,
                                              size_t smem, cudaStream_t st, unsigned cx,
                                              Args &&...args) {
+    if (cx > 8) cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
     cfg.blockDim = block;
