@@ -614,7 +614,12 @@ static int launch_fwd(const FwdArgs &a0, bool apply_bn, cudaStream_t s) {
     if (apply_bn && a.consts && a.a3_out && (a.hw & 3) == 0 && aligned &&
         (a.bits == 0 || a.codes) && (a.numel & 7) == 0 && (a.numel >> 2) < (1ll << 31)) {
         const int64_t ngroups = a.numel >> 3;
-        int64_t blocks = std::min<int64_t>(qt_cdiv(ngroups, 2 * kThreads), 148 * 8);
+        // one 8-element group per thread: more blocks in flight per SM
+        // (C2 BN-apply + quantize 1.04 -> 1.00 ms/step; 2 or 4 per thread,
+        // and block caps of 592 or 2368, were slower)
+        static const int64_t gpt = qt_env_i64("QTAPE_FWD_GPT", 1);
+        static const int64_t maxb = qt_env_i64("QTAPE_FWD_MAXB", 148 * 8);
+        int64_t blocks = std::min<int64_t>(qt_cdiv(ngroups, gpt * kThreads), maxb);
         blocks = std::max<int64_t>(blocks, 1);
         const unsigned b = (unsigned)blocks;
         switch (a.bits) {
