@@ -731,7 +731,8 @@ static int tc_conv_s1(const float *x, const float *w, float *out, int n, int ci,
     if (co % bn) return QT_EUNSUPPORTED;
     {   // split the channels further while there are fewer tiles than SMs
         const int mt = (n / g.nimg) * g.tiles_per_img;
-        while (bn > 16 && (int64_t)mt * (co / bn) < num_sms() && co % (bn / 2) == 0) bn /= 2;
+        const int sm_target = s_cta_cap > 0 ? std::min(num_sms(), s_cta_cap) : num_sms();
+        while (bn > 16 && (int64_t)mt * (co / bn) < sm_target && co % (bn / 2) == 0) bn /= 2;
     }
     const int kdim = kh * kw * ci;
     float *bhi = (float *)ws;
