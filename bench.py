@@ -43,26 +43,52 @@ CONFIGS = {
 
 
 def _peaks():
+    """(HBM GB/s, bf16 dense TF/s sustained, tf32 dense TF/s sustained, kind).
+
+    HBM and bf16 come from the driver-written MEASURED_PEAKS.json; the
+    kind::tf32 rate from profiles/r2_tc_peaks.json, measured on this pool's
+    B200s with the same method (torch.matmul 8192^3 back to back for 4 s,
+    fp32 inputs with TF32 tensor cores: scripts/measure_tc_peaks.py)."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             d = json.load(f)
-        return float(d["hbm_gbs"]), float(d["bf16_tflops_sustained"]), "measured"
+        hbm, bf16, kind = float(d["hbm_gbs"]), float(d["bf16_tflops_sustained"]), "measured"
     except Exception:
-        return 6650.0, 1590.0, "fallback"
+        hbm, bf16, kind = 6650.0, 1590.0, "fallback"
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_tc_peaks.json")) as f:
+            tf32 = float(json.load(f)["tf32_tflops_sustained"])
+    except Exception:
+        tf32, kind = bf16 / 2, kind + " (tf32 = bf16/2 fallback)"
+    return hbm, bf16, tf32, kind
+
+
+# MMA issue model of each conv entry point (DESIGN.md section 3): the
+# forward and data-gradient GEMMs run 3xTF32 (three kind::tf32 passes per
+# useful FLOP); the weight gradient from 4-bit codes runs kind::f16 with g
+# split into three bf16 pieces (three passes), GENERIC tapes 3xTF32.
+TC_PASSES = {"qt_conv_forward": ("tf32", 3), "qt_conv_dgrad": ("tf32", 3),
+             "qt_conv_wgrad": ("bf16", 3)}
 
 
 def _traffic(entry, cfg_name):
-    """DRAM bytes per call of ``entry`` from the committed ncu capture
-    (profiles/r1_wgrad_traffic.json: dram__bytes_read.sum + dram__bytes_write.sum
-    over every kernel the entry point launches in one C2 step), else None."""
+    """DRAM bytes per call of ``entry`` (dram__bytes_read.sum +
+    dram__bytes_write.sum over every kernel launched inside the entry
+    point's NVTX range in one step, scripts/capture_traffic.py under ncu),
+    if the committed capture was taken from the current sources (build
+    digest match); else None."""
     try:
-        with open(os.path.join(ROOT, "profiles", "r1_wgrad_traffic.json")) as f:
+        from paper_1901_07988_b200 import build as B
+        with open(os.path.join(ROOT, "profiles", f"r2_traffic_{cfg_name}.json")) as f:
             t = json.load(f)
     except Exception:
-        return None
-    if t.get("entry_point") != entry or cfg_name != "C2":
-        return None
-    return t["dram_bytes_per_call"]
+        return None, "no capture"
+    fam = t.get("families", {}).get(entry)
+    if fam is None:
+        return None, "entry point not in capture"
+    if t.get("build_digest") != B._digest():
+        return None, f"stale capture (digest {t.get('build_digest')})"
+    return fam["dram_bytes_per_call"], "ncu capture of the current build"
 
 
 # ------------------------------------------------------------ cost model
@@ -163,6 +189,57 @@ def family_times(torch, N, calls, reps=5):
     return agg
 
 
+class _FamilyEvents:
+    """_native hook: external timing events around every call of one entry
+    point, recorded on the stream the call is launched on (inside a CUDA
+    graph capture they become event-record nodes)."""
+
+    def __init__(self, torch, family):
+        self.torch, self.family, self.pairs = torch, family, []
+
+    def before(self, name, args):
+        if name == self.family:
+            ev = self.torch.cuda.Event(enable_timing=True, external=True)
+            ev.record()
+            self.pairs.append([ev, None])
+
+    def after(self, name, args):
+        if name == self.family:
+            ev = self.torch.cuda.Event(enable_timing=True, external=True)
+            ev.record()
+            self.pairs[-1][1] = ev
+
+
+def concurrent_family_ms(torch, N, tr, family, reps=3):
+    """Device time per step of ``family`` inside the real captured step
+    (the weight gradients overlapping the data-gradient chain): one more
+    capture of the step with external events around each of its calls,
+    replayed; the per-launch durations are summed."""
+    try:
+        hook = _FamilyEvents(torch, family)
+        g = torch.cuda.CUDAGraph()
+        cs = torch.cuda.Stream()
+        cs.wait_stream(torch.cuda.current_stream())
+        N.hook = hook
+        try:
+            with torch.cuda.stream(cs):
+                with torch.cuda.graph(g, stream=cs):
+                    tr._body()
+        finally:
+            N.hook = None
+        torch.cuda.synchronize()
+        tot = 0.0
+        for _ in range(reps):
+            g.replay()
+            torch.cuda.synchronize()
+            tot += sum(a.elapsed_time(b) for a, b in hook.pairs)
+        del g
+        return tot / reps
+    except Exception as e:          # measurement aid only; never fails the bench
+        print(f"concurrent timing unavailable: {e}", file=sys.stderr)
+        return None
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons during the timed region."""
 
@@ -260,6 +337,46 @@ def cpu_reference(cfg_name, batch, steps, warmup, procs):
 
 # ------------------------------------------------------------------ main
 
+def _comm_info(torch, tr, group, world):
+    """Data-parallel exchange of this run: backend, rank count (from the
+    process group itself), NCCL version, gradient buckets."""
+    if group is None:
+        return {"backend": None, "nranks": 1, "allreduce": "none (single GPU)"}
+    import torch.distributed as dist
+    ver = torch.cuda.nccl.version()
+    info = {"backend": dist.get_backend(group), "nranks": dist.get_world_size(group),
+            "nranks_ok": dist.get_world_size(group) == world,
+            "nccl_version": ".".join(map(str, ver)) if isinstance(ver, tuple) else str(ver),
+            "grad_bytes": tr.params.grads.numel() * 4}
+    if tr.buckets is not None:
+        info.update(allreduce="bucketed AVG on a comm stream, overlapped with backward, in-graph",
+                    buckets=len(tr.buckets.buckets) + 1,
+                    bucket_bytes=[(b[2] - b[1]) * 4 for b in tr.buckets.buckets])
+    else:
+        info.update(allreduce="one AVG over the whole slab between two graph replays")
+    return info
+
+
+def _spawn_ranks(n):
+    """``bench.py --gpus N`` without a launcher: re-run this command under
+    torch.distributed.run with N ranks on this node (127.0.0.1 rendezvous);
+    NCCL prints its communicator-init lines (NCCL_DEBUG=INFO, INIT subsystem)
+    to stderr so the rank count can be checked.  Exits with the launcher's
+    status."""
+    import socket
+    sock = socket.socket()
+    sock.bind(("127.0.0.1", 0))
+    port = sock.getsockname()[1]
+    sock.close()
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           os.path.abspath(__file__)] + sys.argv[1:]
+    sys.exit(subprocess.call(cmd, env=env))
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -273,8 +390,15 @@ def main():
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     bits = args.bits or cfg["bits"]
+    if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        _spawn_ranks(args.gpus)            # re-exec under torchrun: one rank per GPU
+        return
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        print(json.dumps({"error": f"--gpus {args.gpus} but WORLD_SIZE={world}: launch one "
+                                   f"rank per GPU"}), flush=True)
+        sys.exit(2)
 
     if args.impl == "reference":
         if rank != 0:
@@ -381,32 +505,58 @@ def main():
             tr._body()
     N.hook = None
     torch.cuda.synchronize()
+    # replay each family with the launch shapes of the step (the side-stream
+    # SM partition is scoped to network_backward, so set it here as well)
+    ws = tr.pool.cache[("ws", id(spec), n)]
+    prev = N.query("qt_set_concurrent_backward", int(ws.side is not None))
     agg = family_times(torch, N, rec.calls)
+    N.query("qt_set_concurrent_backward", prev)
     del hold
-    hbm, tc, peak_kind = _peaks()
+    hbm, bf16, tf32, peak_kind = _peaks()
     total_ms = sum(d["ms"] for d in agg.values())
     top = max(agg.items(), key=lambda kv: kv[1]["ms"])
     name, d = top
-    ai = d["flops"] / d["bytes"] if d["bytes"] else float("inf")
-    ridge = tc * 1e12 / (hbm * 1e9)
-    if d["flops"] and ai > ridge:
+    conc_ms = concurrent_family_ms(torch, N, tr, name)
+
+    def tc_time(nm, dd):
+        kind, passes = TC_PASSES.get(nm, ("bf16", 1))
+        return passes * dd["flops"] / ((tf32 if kind == "tf32" else bf16) * 1e12)
+
+    if d["flops"] and tc_time(name, d) > d["bytes"] / (hbm * 1e9):
+        kind, passes = TC_PASSES.get(name, ("bf16", 1))
+        pk = (tf32 if kind == "tf32" else bf16) / passes
         achieved = d["flops"] / (d["ms"] * 1e-3) / 1e12
-        roof = {"bound": "tensor", "achieved": achieved, "peak": tc, "unit": "TFLOP/s",
-                "frac": achieved / tc}
+        roof = {"bound": "tensor", "achieved": achieved, "peak": pk, "unit": "TFLOP/s",
+                "frac": achieved / pk,
+                "peak_note": f"useful FLOP/s: {kind} dense sustained / {passes} split passes"}
     else:
         achieved = d["bytes"] / (d["ms"] * 1e-3) / 1e9
         roof = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": achieved / hbm}
+    traffic, traffic_src = _traffic(name, args.config)
+    per = d["bytes"] / d["launches"] if d["launches"] else None
     roof.update({"kernel": name, "launches_per_step": d["launches"],
+                 "ms_per_step_isolated": d["ms"],
+                 "ms_per_step_concurrent": conc_ms,
+                 "timing": "isolated: the family's calls of one step replayed alone from a CUDA "
+                           "graph (step launch shapes); concurrent: sum of per-launch durations "
+                           "inside the captured step (external CUDA events on the launching "
+                           "stream)",
                  "share_of_step": d["ms"] / total_ms if total_ms else None,
-                 "traffic": _traffic(name, args.config), "peak_kind": peak_kind,
-                 "algorithmic_bytes_per_launch": d["bytes"] / d["launches"] if d["launches"] else None})
+                 "traffic": traffic, "traffic_source": traffic_src,
+                 "traffic_over_algorithmic": traffic / per if (traffic and per) else None,
+                 "peak_kind": peak_kind, "algorithmic_bytes_per_launch": per})
+    if conc_ms:
+        a_c = (d["bytes"] / (conc_ms * 1e-3) / 1e9) if roof["bound"] == "hbm" else \
+            d["flops"] / (conc_ms * 1e-3) / 1e12
+        roof["frac_concurrent"] = a_c / roof["peak"]
     # step roofline: every launch at its own bound (HBM or tensor), summed
     step_roof_ms = 0.0
     for nm, dd in agg.items():
-        step_roof_ms += max(dd["bytes"] / (hbm * 1e9), dd["flops"] / (tc * 1e12)) * 1e3
+        step_roof_ms += max(dd["bytes"] / (hbm * 1e9), tc_time(nm, dd)) * 1e3
     kernels = sorted(({"kernel": k, "ms": v["ms"], "launches": v["launches"],
-                       "GBps": v["bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] else None}
+                       "GBps": v["bytes"] / (v["ms"] * 1e-3) / 1e9 if v["ms"] else None,
+                       "TFps": v["flops"] / (v["ms"] * 1e-3) / 1e12 if v["ms"] and v["flops"] else None}
                       for k, v in agg.items()), key=lambda r: -r["ms"])[:8]
 
     rep = E.memory_report(spec, (n,) + tuple(spec.input_shape), mode="approx", bits=bits)
@@ -428,6 +578,7 @@ def main():
         "e2e": {"value": images / e2e_s, "unit": "images/s",
                 "h2d_bytes_per_step": tr.h2d_bytes, "d2h_bytes_per_step": tr.d2h_bytes},
         "gpu_launches": launches_per_step * args.steps,
+        "comm": _comm_info(torch, tr, group, world),
         "roofline": roof,
         "step_roofline": {"ms": step_roof_ms, "frac": step_roof_ms / ms},
         "kernels": kernels,

@@ -318,8 +318,13 @@ def _lin_bwd(a3, g, p, need_gx=True):
         a3.shape))
 
 
-def layer_fwd(a_in, p, mode="exact", bits=8, training=True):
-    """layer.py:208-266 -> (a_out, tape dict or None)."""
+def layer_fwd(a_in, p, mode="exact", bits=8, training=True, keep_a2=False):
+    """layer.py:208-266 -> (a_out, tape dict or None).
+
+    ``keep_a2`` (test instrumentation, not in the reference) also keeps the
+    pre-ReLU A2 of a quantized tape as ``tape["a2_pre"]`` (and the layer
+    input as ``tape["a_in"]``) so a parity test can locate each code's
+    distance to its quantization boundary."""
     if p["gamma"] is None:
         return _lin_fwd(a_in, p), {"mode": "plain", "input": a_in}
     dt = a_in.dtype
@@ -348,6 +353,9 @@ def layer_fwd(a_in, p, mode="exact", bits=8, training=True):
             tape["a2"] = w.copy()
         else:
             tape["q"] = quantize(w, p["gamma"], p["beta"], bits, sigma2=var)
+            if keep_a2:
+                tape["a2_pre"] = w.copy()
+                tape["a_in"] = a_in
             if mode == "naive":
                 w = dequantize(tape["q"])
     w = np.maximum(w, dt.type(0))
@@ -456,7 +464,7 @@ def _shortcut_adj(g_in, g_res):
     return out
 
 
-def net_fwd(spec, params, batch, mode="exact", bits=8, training=True):
+def net_fwd(spec, params, batch, mode="exact", bits=8, training=True, keep_a2=False):
     """engine.py:282-329 (values only; pool reuse does not change values)."""
     starts, ends = _block_starts_ends(spec)
     head = len(spec["layers"]) - 1
@@ -464,7 +472,7 @@ def net_fwd(spec, params, batch, mode="exact", bits=8, training=True):
     for i, p in enumerate(params):
         if i in starts:
             res = cur.copy()
-        cur, tape = layer_fwd(cur, p, "exact" if i == head else mode, bits, training)
+        cur, tape = layer_fwd(cur, p, "exact" if i == head else mode, bits, training, keep_a2)
         tapes.append(tape)
         if i in ends:
             cur = _shortcut_add(cur, res)

@@ -347,7 +347,7 @@ __global__ void shortcut_adj_kernel(float *g_in, const float *g_res, int64_t n, 
 
 static unsigned grid_for(int64_t n, int threads) {
     int64_t b = qt_cdiv(n, threads);
-    if (b > 148 * 64) b = 148 * 64;
+    if (b > qt_sm_count() * 64) b = qt_sm_count() * 64;
     return (unsigned)std::max<int64_t>(b, 1);
 }
 

@@ -465,7 +465,7 @@ extern "C" int qt_bn_backward_apply(const float *g3, qt_tape_t tape, int64_t n, 
     a.cd = make_fastdiv((uint32_t)c);
     a.wd = make_fastdiv((uint32_t)w);
     const int64_t work = G > 0 ? (n * c * h * w) / G : n * c * h * w;
-    static const int64_t maxb = qt_env_i64("QTAPE_APPLY_MAXB", 148 * 16);
+    static const int64_t maxb = qt_env_i64("QTAPE_APPLY_MAXB", qt_sm_count() * 16);
     static const int64_t gpt = qt_env_i64("QTAPE_APPLY_GPT", 1);
     int64_t blocks = std::min<int64_t>(qt_cdiv(work, gpt * kBT), maxb);
     blocks = std::max<int64_t>(blocks, 1);

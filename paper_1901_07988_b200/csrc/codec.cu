@@ -618,7 +618,7 @@ static int launch_fwd(const FwdArgs &a0, bool apply_bn, cudaStream_t s) {
         // (C2 BN-apply + quantize 1.04 -> 1.00 ms/step; 2 or 4 per thread,
         // and block caps of 592 or 2368, were slower)
         static const int64_t gpt = qt_env_i64("QTAPE_FWD_GPT", 1);
-        static const int64_t maxb = qt_env_i64("QTAPE_FWD_MAXB", 148 * 8);
+        static const int64_t maxb = qt_env_i64("QTAPE_FWD_MAXB", qt_sm_count() * 8);
         int64_t blocks = std::min<int64_t>(qt_cdiv(ngroups, gpt * kThreads), maxb);
         blocks = std::max<int64_t>(blocks, 1);
         const unsigned b = (unsigned)blocks;
@@ -644,7 +644,7 @@ static int launch_fwd(const FwdArgs &a0, bool apply_bn, cudaStream_t s) {
         (((uintptr_t)a.x) & 15) == 0 &&
         (a.numel >> 3) < (1ll << 31)) {   // quantize-pack from A2: the streaming form
         const int64_t ngroups = a.numel >> 3;
-        int64_t blocks = std::min<int64_t>(qt_cdiv(ngroups, 2 * kThreads), 148 * 8);
+        int64_t blocks = std::min<int64_t>(qt_cdiv(ngroups, 2 * kThreads), qt_sm_count() * 8);
         blocks = std::max<int64_t>(blocks, qt_cdiv(a.c, kThreads));   // constants for every channel
         const unsigned b = (unsigned)std::max<int64_t>(blocks, 1);
         const bool clip = a.clip_count != nullptr;
@@ -748,7 +748,7 @@ extern "C" int qt_unpack_dequant(const uint8_t *codes, int64_t n, int64_t c, int
         (d.numel >> 3) < (1ll << 31)) {   // the streaming form
         const int64_t ngroups = d.numel >> 3;
         const unsigned b = (unsigned)std::max<int64_t>(
-            std::min<int64_t>(qt_cdiv(ngroups, 2 * kThreads), 148 * 8), 1);
+            std::min<int64_t>(qt_cdiv(ngroups, 2 * kThreads), qt_sm_count() * 8), 1);
         const FastDiv hw8d = make_fastdiv((uint32_t)(hw >> 3)), cd = make_fastdiv((uint32_t)c);
         switch (bits) {
             case 1: launch_pdl(dequant_stream<1>, b, kThreads, 0, qt_s(stream), d, hw8d, cd); break;

@@ -26,6 +26,20 @@ static inline bool qt_bits_ok(int b) { return b == 1 || b == 2 || b == 4 || b ==
 
 static inline int64_t qt_cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
 
+// SM count of the current device (cached per device ordinal; one process
+// drives one GPU, but a process may switch devices between calls).
+static inline int qt_sm_count() {
+    static int cache[64] = {0};
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) dev = 0;
+    if (!cache[dev]) {
+        int n = 0;
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        cache[dev] = n > 0 ? n : 1;
+    }
+    return cache[dev];
+}
+
 // Programmatic dependent launch: every kernel is launched with programmatic
 // stream serialization, triggers its dependents as soon as it starts and
 // waits (griddepcontrol.wait) for its predecessor before touching global
@@ -51,7 +65,7 @@ static inline int64_t qt_red_target() {
     return v;
 }
 static inline int64_t qt_red_div() {
-    static int64_t v = qt_env_i64("QTAPE_RED_DIV", 2 * 148);
+    static int64_t v = qt_env_i64("QTAPE_RED_DIV", 2 * qt_sm_count());
     return v;
 }
 template <typename... KArgs, typename... Args>

@@ -291,7 +291,7 @@ static bool geo_ok(const ConvGeo &g) {
 static void wgrad_plan(const ConvGeo &g, int64_t &kps, int64_t &splits) {
     const int64_t M = g.co, N = g.ci * g.kh * g.kw, K = g.n * g.oh * g.ow;
     int64_t tiles = qt_cdiv(M, N <= 16 ? 256 : 128) * qt_cdiv(N, N <= 16 ? 16 : (N <= 32 ? 32 : 64));
-    int64_t want = std::max<int64_t>(1, (4 * 148) / std::max<int64_t>(tiles, 1));
+    int64_t want = std::max<int64_t>(1, (4 * qt_sm_count()) / std::max<int64_t>(tiles, 1));
     int64_t maxs = std::max<int64_t>(1, K / (4 * kBK));
     int64_t sp = std::min(want, maxs);
     kps = std::max<int64_t>(kBK, qt_cdiv(qt_cdiv(K, sp), kBK) * kBK);

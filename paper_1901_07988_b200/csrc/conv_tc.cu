@@ -118,7 +118,6 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                        const __grid_constant__ CUtensorMap tmBl,
                        const __grid_constant__ CUtensorMap tmOut,
                        const __grid_constant__ CUtensorMap tmRes, FwdGeo g, EpiParams ep) {
-    pdl_enter();
     using C = FwdCfg<BN, OWT, KC, KW>;
     const int R = g.R, NOUT = g.NOUT, G = g.G;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -533,16 +532,7 @@ struct Maps {
     CUtensorMap a, bh, bl, out, res;
 };
 
-static int num_sms() {
-    static int n = 0;
-    if (!n) {
-        int dev = 0;
-        cudaGetDevice(&dev);
-        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-        if (n <= 0) n = 148;
-    }
-    return n;
-}
+static int num_sms() { return qt_sm_count(); }
 
 // CTA cap of the current launch (0 = every SM); set per call by tc_conv_s1
 static int s_cta_cap = 0;
@@ -728,7 +718,7 @@ static int tc_conv_s1(const float *x, const float *w, float *out, int n, int ci,
     const int kc = (kw == 1 && ci % 32 == 0) ? 32 : 16;
     int bn = co <= 16 ? 16 : (co <= 32 ? 32 : (co <= 64 ? 64 : 128));
     if (kw == 3 && bn > 64) bn = 64;         // stacked taps: KW * BN <= 256 (UMMA N)
-    if (co % bn) return QT_EUNSUPPORTED;
+    while (co % bn) bn /= 2;                 // co % 16 == 0 (tc_shape_ok): 48, 80, 96, 160, 192 ...
     {   // split the channels further while there are fewer tiles than SMs
         const int mt = (n / g.nimg) * g.tiles_per_img;
         const int sm_target = s_cta_cap > 0 ? std::min(num_sms(), s_cta_cap) : num_sms();
@@ -895,7 +885,7 @@ static int space_depth(const float *src, float *dst, int64_t n, int64_t c, int64
     const int64_t total = n * c * h * w;
     if (s == 2 && w % 4 == 0 && h % 2 == 0 && (h / 2) * (w / 2) % 2 == 0 && total / 8 < (1ll << 31)) {
         const uint32_t t8 = (uint32_t)(total / 8);
-        const unsigned blocks = (unsigned)std::min<int64_t>(qt_cdiv(t8, 256), 148 * 8);
+        const unsigned blocks = (unsigned)std::min<int64_t>(qt_cdiv(t8, 256), qt_sm_count() * 8);
         const FastDiv qd = make_fastdiv((uint32_t)(w / 4)), yd = make_fastdiv((uint32_t)(h / 2));
         if (to_depth)
             launch_pdl(space_depth2_kernel<true>, blocks, 256, 0, st, src, dst, t8, (uint32_t)h,
@@ -906,7 +896,7 @@ static int space_depth(const float *src, float *dst, int64_t n, int64_t c, int64
         QT_CHECK_LAUNCH();
         return QT_OK;
     }
-    const unsigned blocks = (unsigned)std::min<int64_t>(qt_cdiv(total, 256), 148 * 16);
+    const unsigned blocks = (unsigned)std::min<int64_t>(qt_cdiv(total, 256), qt_sm_count() * 16);
     if (to_depth)
         launch_pdl(space_depth_kernel<true>, blocks, 256, 0, st, src, dst, n, c, h, w, s);
     else
@@ -1257,7 +1247,7 @@ static int64_t seg_elems(const SegGeo &s, int64_t n, int64_t c) {
 }
 
 static unsigned seg_blocks(int64_t total) {
-    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(qt_cdiv(total, 256), 148 * 16));
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(qt_cdiv(total, 256), qt_sm_count() * 16));
 }
 
 template <int MODE>

@@ -171,7 +171,7 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = 
         return e && atoi(e) > 0 ? atoi(e) : 0;
     }();
     const double macs = (double)g.n * (double)oh * (double)ow * (double)g.co * (double)Rout;
-    const int ctas = ctas_env > 0 ? ctas_env : ((g_concurrent_bwd && macs < kSmallLayerMacs) ? 74 : 148);
+    const int ctas = ctas_env > 0 ? ctas_env : ((g_concurrent_bwd && macs < kSmallLayerMacs) ? qt_sm_count() / 2 : qt_sm_count());
     int want = std::max(1, ctas / (pl.mgroups * pl.nblk));   // one wave: fixed costs once per SM
     want = std::min(want, std::max(1, pl.total / SUB));
     // a CTA's stages run concurrently on its operand groups, so give each
@@ -308,7 +308,7 @@ extern "C" int qt_debug_wgrad_trace(void *buf, int cta) {
 int qt_tc_wgrad_reduce(const float *partial, int64_t splits, int64_t count, float *grad_w,
                        cudaStream_t st) {
     if (splits <= 48) {
-        launch_pdl(wgrad_reduce_few_kernel, (unsigned)std::min<int64_t>(qt_cdiv(count, 256), 148 * 8),
+        launch_pdl(wgrad_reduce_few_kernel, (unsigned)std::min<int64_t>(qt_cdiv(count, 256), qt_sm_count() * 8),
                    256, 0, st, partial, (int)splits, count, grad_w);
         QT_CHECK_LAUNCH();
         return QT_OK;
@@ -436,7 +436,7 @@ int qt_tc_conv_wgrad_s2d(const float *gr, qt_tape_t act, float *grad_w, const qt
     const FastDiv wrd = make_fastdiv((uint32_t)(g.w / 2) / per), hd = make_fastdiv((uint32_t)(g.h / 2));
     const uint32_t c4 = (uint32_t)(g.ci * 4);
     const uint32_t need = std::max(words, c4);
-    const unsigned blocks = (unsigned)std::min<int64_t>(qt_cdiv(need, 256), 148 * 8);
+    const unsigned blocks = (unsigned)std::min<int64_t>(qt_cdiv(need, 256), qt_sm_count() * 8);
     launch_pdl(codes_s2d_kernel, blocks, 256, 0, st, act.codes, codes4, words, (uint32_t)g.h,
                (uint32_t)g.w, act.bits, wrd, hd, act.step, act.offset, step4, offset4, c4);
     QT_CHECK_LAUNCH();

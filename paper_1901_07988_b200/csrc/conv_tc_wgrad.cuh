@@ -148,7 +148,6 @@ template <int BN, int OW, int BITS, bool TAP>
 __global__ void __launch_bounds__(kWgThreads, 1)
     conv_wgrad_tc_kernel(const __grid_constant__ CUtensorMap tmG,
                          const __grid_constant__ CUtensorMap tmC, WgParams p) {
-    pdl_enter();
     constexpr int ROWS = 32 / OW;                           // image rows per 32-pixel chunk
     constexpr int G_BYTES = BN * 128;                       // raw g tile: BN rows x 32 px fp32
     constexpr bool FAST_OK = (BITS == 4);

@@ -130,7 +130,7 @@ extern "C" int qt_sgd(float *value, float *grad, float *vel, int64_t count, floa
     QT_REQUIRE(count >= 0 && (count == 0 || (value && grad && vel)));
     if (count == 0) return QT_OK;
     int64_t blocks = qt_cdiv(count, 256);
-    if (blocks > 148 * 16) blocks = 148 * 16;
+    if (blocks > qt_sm_count() * 16) blocks = qt_sm_count() * 16;
     launch_pdl(sgd_kernel, (unsigned)blocks, 256, 0, qt_s(stream), value, grad, vel, count, lr, lr_dev, momentum,
                                                         weight_decay);
     QT_CHECK_LAUNCH();

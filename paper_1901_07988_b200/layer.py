@@ -64,10 +64,6 @@ class LayerParams:
     vel_beta: Optional[torch.Tensor] = None
     running_mean: Optional[torch.Tensor] = None
     running_var: Optional[torch.Tensor] = None
-    # engine hook: tensor-core weight operands prepared once per step
-    # (qt_conv_prepare_weights); None -> prepared inside each conv call
-    prep_fwd: Optional[torch.Tensor] = None
-    prep_dgrad: Optional[torch.Tensor] = None
 
     def __post_init__(self):
         _dev_f32(self.weight, "weight")
@@ -203,11 +199,24 @@ def _gap(a3: torch.Tensor) -> torch.Tensor:
     return out
 
 
+def _prepared(ws, p: LayerParams, dgrad: int):
+    """Tensor-core weight operand of ``p`` prepared by the Trainer for this
+    step (Workspace.prep, keyed by the LayerParams object), else None: the
+    conv call then lays out the operand from ``p.weight`` itself.  The
+    prepared copies live in the Trainer's workspace only, so eager calls on
+    the same parameters never see a stale (pre-SGD) operand."""
+    prep = getattr(ws, "prep", None)
+    if not prep:
+        return None
+    ent = prep.get(id(p))
+    return None if ent is None else ent[dgrad]
+
+
 def _linear_forward(a3, p: LayerParams, out, residual=None, ws=None):
     """layer.py:138-151; ``residual`` fuses the block-end shortcut add."""
     if p.kind == "conv":
         return ops.conv2d_forward(a3, p.weight, p.stride, p.pad, out=out, residual=residual,
-                                  ws=None if ws is None else ws.conv, prepared=p.prep_fwd)
+                                  ws=None if ws is None else ws.conv, prepared=_prepared(ws, p, 0))
     if p.kind == "dense":
         src = a3
     elif p.kind == "gap_dense":
@@ -384,7 +393,7 @@ def layer_backward(g_out: torch.Tensor, tape: LayerTape, p: LayerParams,
                 return None
             g_in = out if out is not None else torch.empty_like(a_in)
             ops.conv2d_dgrad(g_out, p.weight, tuple(a_in.shape), p.stride, p.pad, g_in,
-                             ws=None if ws is None else ws.conv, prepared=p.prep_dgrad)
+                             ws=None if ws is None else ws.conv, prepared=_prepared(ws, p, 1))
         if residual_grad is not None:
             _apply_adjoint(g_in, residual_grad)
         return g_in
@@ -404,7 +413,7 @@ def layer_backward(g_out: torch.Tensor, tape: LayerTape, p: LayerParams,
                                               p.grad_weight, tape=nt, in_shape=in_shape,
                                               ws=None if ws is None else ws.wgrad))
         ops.conv2d_dgrad(g_out, p.weight, in_shape, p.stride, p.pad, g3,
-                         ws=None if ws is None else ws.conv, prepared=p.prep_dgrad)
+                         ws=None if ws is None else ws.conv, prepared=_prepared(ws, p, 1))
     else:
         _, _, a3 = reconstruct_from_tape(tape)
         if p.kind == "dense":

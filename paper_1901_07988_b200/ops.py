@@ -3,7 +3,8 @@
 Same names/signatures as /root/reference/pkg/src/qtape/ops.py, operating on
 ``torch.cuda`` float32 tensors (rank 2 (N,C) or rank 4 NCHW, contiguous).
 
-Precision contract (stated, and tested in tests/test_parity_gpu.py):
+Precision contract (stated, and tested in tests/test_ops_gpu.py and, at network
+level, tests/test_parity_gpu.py):
   * matmul: float64 ascending-k accumulation -> bit-identical to ops.matmul.
   * conv2d_forward / conv2d_backward: fp32-faithful implicit GEMMs (CUDA-core
     FFMA or tcgen05 split-precision); the reference accumulates in float64,

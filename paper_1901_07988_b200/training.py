@@ -193,6 +193,13 @@ def softmax_xent(logits: torch.Tensor, labels, loss_buf=None, grad_out=None, che
     return loss_buf[:1], grad
 
 
+def _dp_overlap() -> bool:
+    """Bucketed all-reduce overlapped with backward inside the captured step
+    (default); QTAPE_DP_OVERLAP=0 falls back to one all-reduce of the whole
+    slab between two graph replays."""
+    return os.environ.get("QTAPE_DP_OVERLAP", "1") not in ("", "0")
+
+
 def _capture_priority() -> int:
     """Stream priority of the captured step (QTAPE_CAPTURE_PRIORITY, default 0
     = the default priority; torch clamps to the device's range)."""
@@ -237,22 +244,31 @@ class Trainer:
         self.use_graph = use_graph
         self.tapes = None
         self._build_weight_prep()
+        self.buckets = None
+        if process_group is not None and _dp_overlap():
+            from .dist import GradBuckets
+            self.buckets = GradBuckets(self.params, process_group)
 
     # one iteration of training.py:192-199 on the static buffers, in two
     # parts so the (optional) gradient all-reduce sits between them
     def _build_weight_prep(self):
         """Tensor-core conv layers get persistent prepared weight operands,
         refreshed by ONE qt_conv_prepare_weights launch at the start of every
-        step (instead of one re-layout per conv call)."""
+        step (instead of one re-layout per conv call).  They live in this
+        Trainer's workspace (``Workspace.prep``), never on the shared
+        LayerParams, so an eager forward on ``self.params`` after a step
+        lays out the current weights itself."""
         descs = []
         self._prep_max = 0
+        prep = self.pool.cache[("ws", id(self.spec), self.n)].prep
+        prep.clear()
         for li, (p, (ins, _)) in enumerate(zip(self.params, self.spec.layer_shapes(self.n))):
-            p.prep_fwd = p.prep_dgrad = None
             if p.kind != "conv":
                 continue
             n, ci, h, w = ins
             co, _, kh, kw = p.weight.shape
             elems = co * ci * kh * kw
+            ent = [None, None]
             for dgrad in (0, 1):
                 if not N.query("qt_conv_uses_tc", n, ci, h, w, co, kh, kw, p.stride, p.pad, dgrad):
                     continue
@@ -261,11 +277,10 @@ class Trainer:
                 buf = torch.empty(2 * elems, dtype=torch.float32, device=self.device)
                 rows, cols = (ci, co) if dgrad else (co, ci)
                 descs.append((p.weight.data_ptr(), buf.data_ptr(), rows, cols, kh, kw, dgrad, 0))
-                if dgrad:
-                    p.prep_dgrad = buf
-                else:
-                    p.prep_fwd = buf
+                ent[dgrad] = buf
                 self._prep_max = max(self._prep_max, elems)
+            if ent[0] is not None or ent[1] is not None:
+                prep[id(p)] = ent
         dt = np.dtype([("w", "<u8"), ("out", "<u8"), ("rows", "<i4"), ("cols", "<i4"),
                        ("kh", "<i4"), ("kw", "<i4"), ("flip", "<i4"), ("pad", "<i4")])
         arr = np.array(descs, dtype=dt)
@@ -282,14 +297,23 @@ class Trainer:
         logits, tapes = network_forward(self.spec, self.params, self.x, mode=self.mode,
                                         bits=self.bits, pool=self.pool, arena=self.arena)
         _, g = softmax_xent(logits, self.labels, loss_buf=self.loss_buf, check=False)
-        network_backward(self.spec, self.params, tapes, g, self.x, mode=self.mode, pool=self.pool)
+        hook = None
+        if self.buckets is not None:
+            self.buckets.reset()
+            hook = self.buckets.layer_done
+        network_backward(self.spec, self.params, tapes, g, self.x, mode=self.mode, pool=self.pool,
+                         grad_ready=hook)
         self.tapes = tapes
 
     def _update(self):
         sgd_step(self.params, 0.0, self.momentum, self.weight_decay, lr_dev=self.lr)
 
     def _allreduce(self):
-        if self.group is not None:
+        if self.group is None:
+            return
+        if self.buckets is not None:      # buckets already issued during backward
+            self.buckets.finish()
+        else:
             from .dist import allreduce_mean_
             allreduce_mean_(self.params.grads, self.group)
 
@@ -319,7 +343,9 @@ class Trainer:
             # input-gradient chain or the side-stream weight gradients the
             # higher priority costs 0.3 ms/step at C2
             cap = torch.cuda.Stream(device=self.device, priority=_capture_priority())
-            if self.group is None:
+            if self.group is None or self.buckets is not None:
+                # one graph: forward, backward with the bucketed all-reduce
+                # on the communication stream, join, SGD
                 self.graph = torch.cuda.CUDAGraph()
                 with torch.cuda.graph(self.graph, stream=cap):
                     self._body()
@@ -342,7 +368,7 @@ class Trainer:
         """Replay one step on the resident inputs (no host traffic)."""
         if self.graph is None:
             self._body()
-        elif self.group is None:
+        elif self.group is None or self.buckets is not None:
             self.graph.replay()
         else:
             self.graph.replay()

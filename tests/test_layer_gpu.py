@@ -5,7 +5,7 @@ import pytest
 import torch
 
 import oracle as O
-from gpu_util import LAYER_TOL, dev, host, norm_err
+from gpu_util import LAYER_TOL, code_flips, dev, host, norm_err
 
 pytestmark = pytest.mark.gpu
 
@@ -87,9 +87,17 @@ def test_golden_layers(golden_layers):
             assert norm_err(host(tape.sigma2), g[k + "_sigma2"]) < 1e-12, k
             assert norm_err(host(p.running_mean), g[k + "_rmean"]) < 1e-12, k
             if tape.is_quantized:
-                mine = O.unpack(host(tape.stored.codes), bits, tape.stored.numel)
-                ref = O.unpack(g[k + "_codes"], bits, tape.stored.numel)
-                assert np.mean(mine == ref) > 0.999, k      # moments differ in the last ulp
+                # the moments may differ from numpy's pairwise sums in the
+                # last ulp, which moves A2 by an ulp: any differing code must
+                # sit within FLIP_TAU of its boundary (oracle A2, pinned: its
+                # codes == the golden codes)
+                rp = O.new_params(kind=p.kind, weight=g[k + "_w"], stride=int(g[k + "_stride"]),
+                                  pad=int(g[k + "_pad"]), gamma=g[k + "_gamma"],
+                                  beta=g[k + "_beta"])
+                _, rt = O.layer_fwd(g[k + "_x"], rp, mode, bits, keep_a2=True)
+                assert np.array_equal(rt["q"]["codes"], g[k + "_codes"]), k
+                f = code_flips(host(tape.stored.codes), rt, bits)
+                assert f["bad"] == 0 and f["flips"] <= f["near"], (k, f)
                 assert np.array_equal(host(tape.stored.offset), g[k + "_offset"]), k
                 assert np.array_equal(host(tape.stored.step), g[k + "_step"]), k
             else:

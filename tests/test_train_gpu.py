@@ -102,3 +102,51 @@ def test_trainer_c2_runs():
     for _ in range(5):
         l1 = tr.step(x, y)
     assert np.isfinite(l0) and l1 < l0      # overfits one batch
+
+
+def test_eager_forward_after_trainer_sees_current_weights():
+    """The Trainer's prepared tensor-core weight operands live in its own
+    workspace: an eager forward on ``tr.params`` after SGD uses the updated
+    weights (== a forward on a fresh copy of the same values), including a
+    batch shape the Trainer was not built for."""
+    spec = E.make_residual_spec(base_channels=16)
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((8, 3, 32, 32)).astype(np.float32)
+    y = rng.integers(0, 10, 8)
+    tr = P.Trainer(spec, 8, mode="approx", bits=4, lr=0.1)
+    tr.capture()
+    for _ in range(2):
+        tr.step(x, y)
+    for n in (8, 3):
+        xe = dev(rng.standard_normal((n, 3, 32, 32)).astype(np.float32))
+        got, _ = E.network_forward(spec, tr.params, xe, training=False)
+        fresh = P.init_params(spec, 0)
+        fresh.values.copy_(tr.params.values)
+        for a, b in zip(fresh, tr.params):
+            if a.preact:
+                a.running_mean.copy_(b.running_mean)
+                a.running_var.copy_(b.running_var)
+        want, _ = E.network_forward(spec, fresh, xe, training=False)
+        assert torch.equal(got, want), n
+
+
+@pytest.mark.parametrize("co", [48, 80, 96, 192])
+def test_trainer_odd_channel_widths(co):
+    """Output widths that are multiples of 16 but not of the preferred
+    channel tile (48, 80, 96, 192): the tensor-core predicate and launcher
+    agree, the captured step runs and tracks the oracle's first step."""
+    layers = [E.LayerSpec("conv", 32, 3, 1, 1, preact=False),
+              E.LayerSpec("conv", co, 1, 1, 0), E.LayerSpec("conv", co, 3, 1, 1),
+              E.LayerSpec("conv", 32, 1, 1, 0), E.LayerSpec("gap_dense", 10)]
+    spec = E.NetworkSpec((3, 16, 16), 10, layers, [(1, 3)])
+    rng = np.random.default_rng(co)
+    x = rng.standard_normal((8, 3, 16, 16)).astype(np.float32)
+    y = rng.integers(0, 10, 8)
+    tr = P.Trainer(spec, 8, mode="approx", bits=4, lr=0.1)
+    tr.capture()
+    loss = tr.step(x, y)
+    ref = O.init_params(spec.to_json(), 0)
+    lo, _, _ = O.train_step(spec.to_json(), ref, x, y, "approx", 4)
+    assert abs(lo - loss) < STEP_TOL * abs(lo)
+    for p, r in zip(tr.params, ref):
+        assert norm_err(host(p.weight), r["weight"]) < 10 * STEP_TOL
