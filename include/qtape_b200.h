@@ -166,6 +166,54 @@ int qt_conv_forward(const float *x, const float *w, float *out,
                     const float *res, int64_t cr, int64_t sr, void *ws,
                     qt_stream_t stream);
 
+/* Fused forward of one pre-activation layer around the forward GEMM.
+ * Replaces, for shapes qt_conv_fused_support accepts, the reference's
+ * layer_forward sequence channel_moments -> BN apply -> codec.quantize ->
+ * ReLU -> conv2d_forward (layer.py:236-266, codec.py:123-143, ops.py:106-138):
+ *   pro != NULL: x is the layer's PRE-BN input; the operand staging applies
+ *     ((x - mean32) * inv32) * gamma + beta (4 rounded fp32 ops) from the
+ *     layer's BnConst table `consts` (written by qt_bn_stats_prep or by the
+ *     previous conv's statistics epilogue), ReLU, zero padding AFTER the
+ *     apply, and writes the K-bit packed tape of A2 (bit-identical to
+ *     qt_bn_relu_forward's) and ACCUMULATES its clip count.  The rectified
+ *     activation never exists in memory.
+ *   epi != NULL: the output (after the fused shortcut add) gets the NEXT
+ *     layer's batch statistics and all of qt_bn_stats_prep's outputs for it
+ *     (mean, var, running stats, BnConst, frozen gamma/beta, step/offset,
+ *     clip counter zeroed); epi->ws holds qt_conv_stats_workspace(co) bytes,
+ *     zeroed once by the caller (the kernel leaves its counters at zero).
+ * Both NULL: exactly qt_conv_forward. */
+typedef struct {
+    const void *consts;     /* BnConst[ci] (48 B each) of this layer           */
+    uint8_t *codes;         /* packed K-bit tape of this layer (4-byte aligned) */
+    int64_t *clip_count;    /* accumulated                                      */
+    int bits;               /* 1, 2, 4, 8                                       */
+} qt_bn_prologue_t;
+typedef struct {
+    double eps;
+    const float *gamma, *beta;   /* next layer's parameters                    */
+    int bits;                    /* next layer's tape width (0: exact tape)     */
+    double *mean, *var, *running_mean, *running_var;
+    float *gamma_copy, *beta_copy;
+    double *step;
+    int64_t *offset;
+    int64_t *clip_count;
+    void *consts;
+    void *ws;
+} qt_bn_stats_epilogue_t;
+int64_t qt_conv_stats_workspace(int64_t co);
+/* Bit 0: the BN prologue is available for this shape at `bits`; bit 1: the
+ * statistics epilogue is (sr = the fused shortcut's stride, 1 if none). */
+int qt_conv_fused_support(int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co,
+                          int64_t kh, int64_t kw, int64_t stride, int64_t pad, int64_t sr,
+                          int bits);
+int qt_conv_forward_fused(const float *x, const float *w, float *out,
+                          int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co,
+                          int64_t kh, int64_t kw, int64_t stride, int64_t pad,
+                          const float *res, int64_t cr, int64_t sr,
+                          const qt_bn_prologue_t *pro, const qt_bn_stats_epilogue_t *epi,
+                          void *ws, qt_stream_t stream);
+
 /* Data gradient (ops.conv2d_backward g_x path, ops.py:168-183). */
 int qt_conv_dgrad(const float *g, const float *w, float *gx,
                   int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co,

@@ -31,6 +31,19 @@ class Tape(ctypes.Structure):
     _fields_ = [("a2", P), ("codes", P), ("step", P), ("offset", P), ("bits", I32)]
 
 
+class BnPrologue(ctypes.Structure):
+    """qt_bn_prologue_t: BN-apply + ReLU + K-bit tape in the conv operand staging."""
+    _fields_ = [("consts", P), ("codes", P), ("clip_count", P), ("bits", I32)]
+
+
+class BnStatsEpilogue(ctypes.Structure):
+    """qt_bn_stats_epilogue_t: the next layer's BN statistics in the conv epilogue."""
+    _fields_ = [("eps", F64), ("gamma", P), ("beta", P), ("bits", I32), ("mean", P),
+                ("var", P), ("running_mean", P), ("running_var", P), ("gamma_copy", P),
+                ("beta_copy", P), ("step", P), ("offset", P), ("clip_count", P),
+                ("consts", P), ("ws", P)]
+
+
 # name -> (restype, argtypes); keep in sync with include/qtape_b200.h
 SIGNATURES = {
     "qt_version": (I32, []),
@@ -57,6 +70,11 @@ SIGNATURES = {
                                    I64, P, P, P]),
     "qt_conv_forward": (I32, [P, P, P, I64, I64, I64, I64, I64, I64, I64, I64, I64,
                               P, I64, I64, P, P]),
+    "qt_conv_stats_workspace": (I64, [I64]),
+    "qt_conv_fused_support": (I32, [I64] * 10 + [I32]),
+    "qt_conv_forward_fused": (I32, [P, P, P, I64, I64, I64, I64, I64, I64, I64, I64, I64,
+                                    P, I64, I64, ctypes.POINTER(BnPrologue),
+                                    ctypes.POINTER(BnStatsEpilogue), P, P]),
     "qt_conv_dgrad": (I32, [P, P, P, I64, I64, I64, I64, I64, I64, I64, I64, I64, P, P]),
     "qt_conv_workspace": (I64, [I64, I64, I64, I64]),
     "qt_conv_workspace_ex": (I64, [I64] * 9),

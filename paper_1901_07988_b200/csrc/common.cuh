@@ -254,6 +254,36 @@ __device__ __forceinline__ uint32_t code_fast(float a, float s1, float s2, doubl
     return (uint32_t)(raw < 0 ? 0 : (raw > top ? top : raw));
 }
 
+// code_fast split for unrolled callers: the fp32/int32 common path and a
+// flag when the element needs the exact float64 recipe (code_slow, kept out
+// of line so the rare path costs a call, not if-converted float64 work).
+__device__ __forceinline__ uint32_t code_fast_only(float a, float s1, float s2, int64_t off,
+                                                   int bits, bool *clipped, bool *slow) {
+    const float p = __fmul_rn(a, s1);
+    const float e = __fmaf_rn(a, s1, -p);
+    const float corr = __fmaf_rn(a, s2, e);
+    const float f = floorf(p);
+    const float fr = __fadd_rn(__fsub_rn(p, f), corr);   // p - f exact
+    const float dist = fabsf(__fsub_rn(fr, rintf(fr)));
+    const bool off_ok = off > -(1ll << 30) && off < (1ll << 30);
+    *slow = !(fabsf(p) < 1048576.f && dist > 9.5367431640625e-07f && off_ok);
+    // floor(a*scale) = f + floor(fr) (|f| < 2^20): its int value from the float bits
+    const float u = __fadd_rn(__fadd_rn(f, floorf(fr)), 12582912.f);
+    const int raw = __float_as_int(u) - 0x4B400000 + (1 << (bits - 1)) - (int)(off_ok ? off : 0);
+    const int top = (1 << bits) - 1;
+    const int c = min(max(raw, 0), top);
+    *clipped = raw != c;
+    return (uint32_t)c;
+}
+
+static __device__ __noinline__ uint32_t code_slow(float a, double scale, int64_t off, int bits,
+                                           bool *clipped) {
+    const int64_t top = (1ll << bits) - 1;
+    const int64_t raw = raw_code(a, scale, off, bits);
+    *clipped = raw < 0 || raw > top;
+    return (uint32_t)(raw < 0 ? 0 : (raw > top ? top : raw));
+}
+
 // Interval-median decode (codec.py:149-154), rounded to the tape dtype.
 __device__ __forceinline__ float decode(uint32_t code, double step, int64_t off, int bits) {
     double half = (double)(1 << (bits - 1));

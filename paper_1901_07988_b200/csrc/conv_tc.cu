@@ -72,6 +72,51 @@ struct EpiParams {
     int res_tma;   // 1: shortcut tile TMA-loaded into the output staging buffer
 };
 
+// Layer fusion around the forward GEMM (qt_conv_forward_fused).
+//
+// Prologue (bits != 0): the activation boxes hold the layer's PRE-BN input x;
+// the split warps form A3 = relu(((x - mean32) * inv32) * gamma + beta)
+// (layer.py:245-249, 264: four rounded fp32 ops, no FMA) from the channel's
+// BnConst and feed it to the MMA -- the rectified activation never exists in
+// HBM -- and, on the centre-row stage of the CTA's first channel tile, emit
+// the K-bit packed tape of A2 (codec.quantize, codec.py:107-143, bit-exact
+// through code_fast) with the clip count.  Pixels outside the image (the
+// conv's zero padding, the flat path's partial last run) are forced to 0
+// after the BN apply, as the reference pads the rectified activation.
+//
+// Epilogue (stats != 0): the BN statistics of the OUTPUT (the next layer's
+// input, after the fused shortcut add) -- the next layer's
+// channel_moments (ops.py:186-196) + qt_bn_stats_prep outputs.  Every CTA
+// owns one channel tile (grid % ntiles == 0); per output tile the epilogue
+// warps take the tile mean and M2 of each channel from the staged tile (two
+// passes, float64) and merge them into the CTA's running (n, mean, M2) in
+// tile order (Chan et al.).  At the end each CTA publishes its (mean, M2) per
+// channel and takes a ticket; the last `nfin` CTAs wait for the rest and
+// finalize nfin disjoint channel ranges: mean = sum n_b mean_b / N,
+// M2 = sum M2_b + n_b (mean_b - mean)^2 over the CTAs b of the channel's
+// tile, in CTA order (deterministic), then var, running stats, BnConst,
+// frozen gamma/beta, step/offset and the next tape's clip counter reset.
+struct FuseParams {
+    const BnConst *bn;             // [ci] constants of THIS layer (prologue)
+    uint32_t *codes;               // packed K-bit tape, as 32-bit words
+    unsigned long long *clip;      // clip counter of this layer's tape
+    int bits;                      // 0: prologue off
+    int stats;                     // 1: epilogue statistics of the output
+    int nfin;                      // finalizer CTAs
+    double *part;                  // [grid][BN] (mean, M2)
+    double *pcnt;                  // [grid] pixel count per CTA
+    unsigned *counter;             // [2] arrivals, finalizers done (left at 0)
+    double eps;                    // next layer's BN: epsilon, gamma, beta, K
+    const float *gamma, *beta;
+    int nbits;
+    double *mean, *var, *rmean, *rvar;
+    BnConst *consts;
+    float *gcopy, *bcopy;
+    double *step;
+    int64_t *offset;
+    unsigned long long *nclip;
+};
+
 // w0 TMA, w1 TMEM + MMA, w2..w17 up to 4 split warpgroups, w18..w21 epilogue.
 // Split group g owns operand stage g and every G-th (u, chunk) stage, so G
 // stages are transformed concurrently and every mbarrier has one waiter
@@ -91,6 +136,164 @@ __device__ int g_cv_trace_cta = 0;
 constexpr int kFwdEpiWarps = 8;   // two warps per TMEM lane quarter, alternate 16-channel blocks
 constexpr int kFwdThreads = 64 + 128 * kFwdGroups + 32 * kFwdEpiWarps;
 constexpr int kFwdEpiWarp = 2 + 4 * kFwdGroups;
+
+// --- epilogue BN statistics (FuseParams.stats) ------------------------------
+constexpr int kEpiThreads = 32 * kFwdEpiWarps;
+
+// One output tile's per-channel (mean, M2) from the staged tile
+// s_out[img][BN][tpx] (valid pixels q < nvalid of the flattened 128), merged
+// into the CTA's running (n, mean, M2) per channel (first: initialise).
+// TPC = 256 / BN threads per channel (adjacent lanes); each sums a fixed,
+// bank-rotated subset in float64, the group combines by a fixed xor tree.
+template <int BN>
+__device__ __forceinline__ void epi_tile_stats(const float *s_out, int tpx_log, int nvalid,
+                                               bool nfirst, double *s_acc) {
+    constexpr int TPC = kEpiThreads / BN;      // threads per channel (adjacent lanes)
+    constexpr int PER4 = 32 / TPC;             // float4 chunks per thread (128 px / 4)
+    const int tid = (int)threadIdx.x - 32 * kFwdEpiWarp;
+    const int cc = tid / TPC, sub = tid % TPC;
+    const int tmask = (1 << tpx_log) - 1;
+    // one pass, float64, shifted by the channel's first value of the tile
+    // (|mean - shift| ~ sigma: no cancellation in M2 = Q - S^2/n); chunk
+    // r = sub + TPC * ((i + cc) mod PER4) keeps the float4 reads conflict-free
+    const double sft = (double)s_out[cc << tpx_log];
+    double S = 0.0, Q = 0.0;
+#pragma unroll 4
+    for (int i = 0; i < PER4; ++i) {
+        const int q = 4 * (sub + TPC * ((i + cc) & (PER4 - 1)));
+        if (q < nvalid) {
+            const float4 v = *reinterpret_cast<const float4 *>(
+                s_out + (((q >> tpx_log) * BN + cc) << tpx_log) + (q & tmask));
+            const double d0 = (double)v.x - sft, d1 = (double)v.y - sft;
+            const double d2 = (double)v.z - sft, d3 = (double)v.w - sft;
+            S += (d0 + d1) + (d2 + d3);
+            Q += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+        }
+    }
+#pragma unroll
+    for (int o = TPC / 2; o > 0; o >>= 1) {
+        S += __shfl_xor_sync(0xffffffffu, S, o);
+        Q += __shfl_xor_sync(0xffffffffu, Q, o);
+    }
+    if (sub == 0) {   // re-centre on the CTA's shift (its first tile's) and accumulate
+        const double n_t = (double)nvalid;
+        double *a = s_acc + 3 * cc;
+        if (nfirst) a[0] = sft;
+        const double d = sft - a[0];
+        a[1] += S + n_t * d;
+        a[2] += Q + d * (2.0 * S + n_t * d);
+    }
+}
+
+// Publish the CTA's per-channel shifted sums (shift, S, Q) and pixel count,
+// take a ticket; the last nfin CTAs wait for the rest and finalize nfin
+// disjoint channel ranges in ONE load round: every CTA's sums re-centred on
+// the first CTA's shift s0 (S' = S + n d, Q' = Q + d (2 S + n d), d = s - s0),
+// mean = s0 + sum S' / N, M2 = sum Q' - (sum S')^2 / N, in CTA order through
+// a fixed warp tree (deterministic).
+template <int BN>
+__device__ __forceinline__ void epi_stats_finalize(const FuseParams &fz, const double *s_acc,
+                                                   double cta_px, int *s_fin, int co, int ntiles) {
+    const int tid = (int)threadIdx.x - 32 * kFwdEpiWarp;
+    const int lane = tid & 31, w = tid >> 5;
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+    const int b = (int)blockIdx.x;
+    for (int c = tid; c < BN; c += kEpiThreads) {
+        double *dst = fz.part + ((size_t)b * BN + c) * 3;
+        dst[0] = s_acc[3 * c + 0];
+        dst[1] = s_acc[3 * c + 1];
+        dst[2] = s_acc[3 * c + 2];
+    }
+    if (tid == 0) fz.pcnt[b] = cta_px;
+    __threadfence();
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+    const int grid = (int)gridDim.x;
+    if (tid == 0) {
+        const unsigned t = atomicAdd(&fz.counter[0], 1u);
+        const int f = (int)t - (grid - fz.nfin);
+        if (f >= 0) {   // finalizer: wait for every CTA's partials
+            while (*(volatile unsigned *)&fz.counter[0] < (unsigned)grid) {
+            }
+            __threadfence();
+        }
+        *s_fin = f;
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+    const int f = *s_fin;
+    if (f < 0) return;
+    const int per = (co + fz.nfin - 1) / fz.nfin;
+    const int cbeg = f * per, cend = min(co, cbeg + per);
+    const int cpt = grid / ntiles;           // CTAs per channel tile
+    for (int c = cbeg + w; c < cend; c += kFwdEpiWarps) {
+        const int t = c / BN, cl = c - t * BN;
+        double nb[5], sb[5], Sb[5], Qb[5];
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {          // every load of the lane in flight at once
+            const int j = lane + 32 * k;
+            const int bb = t + (j < cpt ? j : 0) * ntiles;
+            const double *src = fz.part + ((size_t)bb * BN + cl) * 3;
+            nb[k] = j < cpt ? __ldcg(fz.pcnt + bb) : 0.0;
+            sb[k] = __ldcg(src);
+            Sb[k] = __ldcg(src + 1);
+            Qb[k] = __ldcg(src + 2);
+        }
+        const double s0 = __shfl_sync(0xffffffffu, sb[0], 0);
+        double nn = 0.0, S = 0.0, Q = 0.0;
+#pragma unroll
+        for (int k = 0; k < 5; ++k) {
+            const double d = sb[k] - s0;
+            if (nb[k] > 0.0) {
+                nn += nb[k];
+                S += Sb[k] + nb[k] * d;
+                Q += Qb[k] + d * (2.0 * Sb[k] + nb[k] * d);
+            }
+        }
+        for (int j = lane + 160; j < cpt; j += 32) {   // more than 160 CTAs per tile
+            const int bb = t + j * ntiles;
+            const double *src = fz.part + ((size_t)bb * BN + cl) * 3;
+            const double cn = __ldcg(fz.pcnt + bb);
+            const double d = __ldcg(src) - s0, Sj = __ldcg(src + 1);
+            if (cn > 0.0) {
+                nn += cn;
+                S += Sj + cn * d;
+                Q += __ldcg(src + 2) + d * (2.0 * Sj + cn * d);
+            }
+        }
+        nn = warp_sum(nn);
+        S = warp_sum(S);
+        Q = warp_sum(Q);
+        if (lane == 0) {
+            const double mean = s0 + S / nn;
+            double var = (Q - S * (S / nn)) / nn;
+            if (!(var > 0.0)) var = var != var ? var : 0.0;
+            fz.mean[c] = mean;
+            fz.var[c] = var;
+            if (fz.rmean) {   // layer.py:237-241
+                const double m = 0.9;
+                fz.rmean[c] = __dadd_rn(__dmul_rn(fz.rmean[c], m), __dmul_rn(1.0 - m, mean));
+                fz.rvar[c] = __dadd_rn(__dmul_rn(fz.rvar[c], m), __dmul_rn(1.0 - m, var));
+            }
+            const float pg = fz.gamma[c], pb = fz.beta[c];
+            const BnConst k = bn_const(mean, var, fz.eps, pg, pb, fz.nbits);
+            fz.consts[c] = k;
+            fz.gcopy[c] = pg;     // frozen tape copies (layer.py:253-255)
+            fz.bcopy[c] = pb;
+            if (fz.nbits) {
+                fz.step[c] = k.step;
+                fz.offset[c] = k.off;
+            }
+            if (c == 0 && fz.nclip) *fz.nclip = 0;
+        }
+    }
+    asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+    if (tid == 0) {   // the last finalizer re-arms the counters for the next launch
+        __threadfence();
+        if (atomicAdd(&fz.counter[1], 1u) == (unsigned)fz.nfin - 1) {
+            fz.counter[0] = 0;
+            fz.counter[1] = 0;
+        }
+    }
+}
 
 // Persistent implicit-GEMM conv: each CTA walks output tiles (128 pixels x BN
 // channels) with a grid-stride loop.
@@ -117,7 +320,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                        const __grid_constant__ CUtensorMap tmBh,
                        const __grid_constant__ CUtensorMap tmBl,
                        const __grid_constant__ CUtensorMap tmOut,
-                       const __grid_constant__ CUtensorMap tmRes, FwdGeo g, EpiParams ep) {
+                       const __grid_constant__ CUtensorMap tmRes, FwdGeo g, EpiParams ep,
+                       FuseParams fz) {
     using C = FwdCfg<BN, OWT, KC, KW>;
     const int R = g.R, NOUT = g.NOUT, G = g.G;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -135,6 +339,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     uint64_t *res_full = acc_empty + 2;
     uint64_t *w_full = res_full + 2;
     uint32_t *tmem_slot = (uint32_t *)(w_full + 1);
+    // fusion scratch (16-byte aligned): the layer's BnConst table, the CTA's
+    // running (n, mean, M2) per channel of its tile, the finalizer index
+    // (pointer arithmetic from the shared base keeps every access LDS/STS)
+    // (bars is 1 KiB aligned; this is the first 16-byte boundary past tmem_slot)
+    uint8_t *fbase = (uint8_t *)(bars + 2 * R + 2 * kFwdGroups + 8);
+    BnConst *s_bn = (BnConst *)fbase;
+    double *s_acc = (double *)(fbase + (fz.bits ? g.ci * (int)sizeof(BnConst) : 0));   // [BN][3]
+    int *s_fin = (int *)(s_acc + (fz.stats ? 3 * BN : 0));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     long long *const tr_ = (g_cv_trace && blockIdx.x == (unsigned)g_cv_trace_cta) ? g_cv_trace : nullptr;
@@ -154,6 +366,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_init(w_full, 1);
         fence_barrier_init();
     }
+    if (fz.stats && (int)threadIdx.x < 3 * BN) s_acc[threadIdx.x] = 0.0;
     if (warp == 1) tmem_alloc<512>(tmem_slot);
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
@@ -276,6 +489,17 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         int gi = grp < G ? grp : nstages;
         int s = gi % R;
         uint32_t phr = (uint32_t)(gi / R) & 1u, pho = (uint32_t)(gi / G) & 1u;
+        const int bits = fz.bits;
+        unsigned long long nclip = 0;
+        if (bits) {   // the layer's BnConst table (written by the stats kernel / producer)
+            const int st = threadIdx.x - 64;
+            const float4 *src = reinterpret_cast<const float4 *>(fz.bn);
+            float4 *dst = reinterpret_cast<float4 *>(s_bn);
+            for (int q = st; q < g.ci * 3; q += 128 * kFwdGroups) dst[q] = src[q];
+            asm volatile("bar.sync 2, %0;" ::"n"(128 * kFwdGroups) : "memory");
+        }
+        const int lpw_log = bits ? 5 - (bits == 1 ? 0 : bits == 2 ? 1 : bits == 4 ? 2 : 3) : 0;
+        const int lpw = 1 << lpw_log;                      // lanes (pixels) per 32-bit code word
         for (; gi < nstages; gi += G) {
             mbar_wait(&raw_full[s], phr);
             if (quarter == 2 && lane == 0 && gi < 64) CV_TRACE(8 * gi + 1);
@@ -283,13 +507,38 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             if (quarter == 2 && lane == 0 && gi < 64) CV_TRACE(8 * gi + 2);
             tc_fence_after();
             const uint8_t *raw = sRaw(s);
-#pragma unroll
+            // stage -> (tile, kernel row u, channel chunk c0); pixel validity
+            // (zero padding / partial flat run) and whether this stage emits
+            // the tape (centre row of the CTA's first channel tile)
+            int u = 0, c0 = 0, nimg0 = 0, pix = 0;
+            bool valid = true, emit = false;
+            if (bits) {
+                const int lt_ = gi / nst, ist = gi - lt_ * nst;
+                u = ist / kchunks;
+                c0 = (ist - u * kchunks) * KC;
+                int h0_, co0_;
+                tile_coords((int)blockIdx.x + lt_ * (int)gridDim.x, nimg0, h0_, co0_);
+                pix = (h0_ + u - g.pad) * g.w + (int)apx;
+                valid = pix >= 0 && pix < g.hw;
+                emit = (u == g.pad) && (co0_ == 0);
+                nimg0 += (int)aimg;
+            }
+#pragma unroll 1
             for (int cg = 0; cg < KC; cg += 16) {
                 uint32_t hi[16], lo[16];
+                float a2[16];
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     const uint32_t off = ((aimg * KC + cg + j) * tpx + apx) * 4;
-                    const float x = *reinterpret_cast<const float *>(raw + off);
+                    float x = *reinterpret_cast<const float *>(raw + off);
+                    if (bits) {   // A3 = relu(BN(x)), 0 outside the image
+                        const float4 k4 = *reinterpret_cast<const float4 *>(&s_bn[c0 + cg + j]);
+                        float v = __fsub_rn(x, k4.x);           // layer.py:246-249
+                        v = __fmul_rn(v, k4.y);
+                        v = __fmul_rn(v, k4.z);
+                        a2[j] = __fadd_rn(v, k4.w);
+                        x = valid ? ((a2[j] >= 0.f || a2[j] != a2[j]) ? a2[j] : 0.f) : 0.f;
+                    }
                     float h, l;
                     split_tf32(x, h, l);
                     hi[j] = __float_as_uint(h);
@@ -297,6 +546,46 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 }
                 tmem_st16(lane_base + a_col(o) + cg, hi);
                 tmem_st16(lane_base + a_col(o) + KC + cg, lo);
+                if (emit) {   // the K-bit tape of A2: lanes = consecutive pixels
+                    // phase 1: 16 independent codes; phase 2: OR-reduce each
+                    // over the lpw lanes of its word; phase 3: one lane stores
+                    const int64_t ebase = ((int64_t)nimg0 * g.ci + c0 + cg) * g.hw + pix;
+                    const uint32_t sh_l = (uint32_t)(bits * (lane & (lpw - 1)));
+                    uint32_t wv[16];
+                    uint32_t slowm = 0;
+#pragma unroll
+                    for (int j = 0; j < 16; ++j) {
+                        const BnConst &k = s_bn[c0 + cg + j];
+                        bool cl, slow;
+                        const uint32_t cj = code_fast_only(a2[j], k.s1, k.s2, k.off, bits, &cl, &slow);
+                        slowm |= slow ? (1u << j) : 0u;
+                        nclip += (valid && cl && !slow) ? 1u : 0u;
+                        wv[j] = cj << sh_l;
+                    }
+                    if (slowm) {   // rare: exact float64 recipe (codec.py:118-120)
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) {
+                            if (slowm & (1u << j)) {
+                                const BnConst &k = s_bn[c0 + cg + j];
+                                bool cl;
+                                wv[j] = code_slow(a2[j], k.scale, k.off, bits, &cl) << sh_l;
+                                nclip += (valid && cl) ? 1u : 0u;
+                            }
+                        }
+                    }
+#pragma unroll
+                    for (int sh = 1; sh < 32; sh <<= 1) {
+                        if (sh < lpw) {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) wv[j] |= __shfl_xor_sync(0xffffffffu, wv[j], sh);
+                        }
+                    }
+                    if (valid && (lane & (lpw - 1)) == 0) {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)
+                            __stcg(fz.codes + ((ebase + (int64_t)j * g.hw) >> lpw_log), wv[j]);
+                    }
+                }
             }
             tmem_wait_st();
             tc_fence_before();
@@ -305,6 +594,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             s += G;
             if (s >= R) { s -= R; phr ^= 1u; }    // R is a multiple of G
             pho ^= 1u;
+        }
+        if (bits) {   // clip count of the tape (codec.py:133-135), integer atomics
+            nclip = warp_sum(nclip);
+            if (lane == 0 && nclip) atomicAdd(fz.clip, nclip);
         }
     } else {  // ------------------------------------------------ epilogue warps
         const int quarter = warp & 3;
@@ -324,6 +617,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                         co0, n0);
         }
         int lt = 0;
+        int cta_px = 0;      // pixels this CTA's tiles contributed (statistics epilogue)
         for (int T = blockIdx.x; T < total; T += gridDim.x, ++lt) {
             int n0, h0, co0;
             tile_coords(T, n0, h0, co0);
@@ -412,8 +706,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                                 g.flat ? h1 * OWT : 0, g.flat ? 0 : h1, c1, n1);
                 }
             }
+            if (fz.stats) {   // BN statistics of this output tile (reads the staged tile)
+                const int nvalid = g.flat ? min(128, g.hw - h0 * OWT) : 128;
+                epi_tile_stats<BN>(s_out, cstride == 64 ? 6 : 7, nvalid, lt == 0, s_acc);
+                cta_px += nvalid;
+            }
         }
         if (leader) bulk_wait_read0();
+        if (fz.stats) epi_stats_finalize<BN>(fz, s_acc, (double)cta_px, s_fin, g.co, g.ntiles);
     }
     tc_fence_before();
     __syncthreads();
@@ -545,8 +845,8 @@ static int dgrad_cta_cap() {
 }
 
 template <int BN, int OWT, int KC, int KW>
-static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, int tiles, int ntiles,
-                      cudaStream_t st) {
+static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, const FuseParams &fz,
+                      int tiles, int ntiles, cudaStream_t st) {
     using C = FwdCfg<BN, OWT, KC, KW>;
     auto kern = conv_fwd_tc_kernel<BN, OWT, KC, KW>;
     static bool attr = false;
@@ -574,10 +874,18 @@ static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, int t
         gg.wres = 1;
         grid = std::max(ntiles, std::min(total, sms) / ntiles * ntiles);
     }
+    FuseParams fzl = fz;
+    if (fz.stats) {   // every CTA keeps one channel tile: grid a multiple of ntiles
+        if (ntiles > sms) return QT_EUNSUPPORTED;
+        grid = std::max(ntiles, std::min(total, sms) / ntiles * ntiles);
+        fzl.nfin = std::max(1, std::min(grid, g.co / 8));
+    }
+    const int fuse_bytes = 16 + (fz.bits ? g.ci * (int)sizeof(BnConst) : 0) +
+                           (fz.stats ? 3 * BN * 8 : 0) + 16;
     gg.slot = gg.wres ? (C::A_BYTES + 1023) / 1024 * 1024 : C::RAW_BYTES;
     gg.ntd = make_fastdiv((uint32_t)ntiles);
     gg.tpid = make_fastdiv((uint32_t)std::max(1, g.tiles_per_img));
-    const int budget = 227 * 1024 - 1024 - 512 - (gg.wres ? wbytes : 0);
+    const int budget = 227 * 1024 - 1024 - 512 - fuse_bytes - (gg.wres ? wbytes : 0);
     auto raw_fit = [&](int no) { return (budget - no * C::OUT_BYTES) / gg.slot; };
     int nout = 2;
     while (G > 1 && raw_fit(1) < G) G /= 2;
@@ -588,21 +896,22 @@ static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, int t
     gg.R = r;
     gg.NOUT = nout;
     gg.G = G;
-    const int smem = r * gg.slot + nout * C::OUT_BYTES + (gg.wres ? wbytes : 0) + 1024 + 512;
-    launch_pdl(kern, grid, kFwdThreads, smem, st, m.a, m.bh, m.bl, m.out, m.res, gg, ep);
+    const int smem = r * gg.slot + nout * C::OUT_BYTES + (gg.wres ? wbytes : 0) + 1024 + 512 +
+                     fuse_bytes;
+    launch_pdl(kern, grid, kFwdThreads, smem, st, m.a, m.bh, m.bl, m.out, m.res, gg, ep, fzl);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
 
 template <int OWT, int KC, int KW>
-static int dispatch_bn(int bn, const Maps &m, const FwdGeo &g, const EpiParams &ep, int tiles,
-                       int ntiles, cudaStream_t st) {
+static int dispatch_bn(int bn, const Maps &m, const FwdGeo &g, const EpiParams &ep,
+                       const FuseParams &fz, int tiles, int ntiles, cudaStream_t st) {
     switch (bn) {
-        case 16: return launch_fwd<16, OWT, KC, KW>(m, g, ep, tiles, ntiles, st);
-        case 32: return launch_fwd<32, OWT, KC, KW>(m, g, ep, tiles, ntiles, st);
-        case 64: return launch_fwd<64, OWT, KC, KW>(m, g, ep, tiles, ntiles, st);
+        case 16: return launch_fwd<16, OWT, KC, KW>(m, g, ep, fz, tiles, ntiles, st);
+        case 32: return launch_fwd<32, OWT, KC, KW>(m, g, ep, fz, tiles, ntiles, st);
+        case 64: return launch_fwd<64, OWT, KC, KW>(m, g, ep, fz, tiles, ntiles, st);
         case 128:
-            if constexpr (KW == 1) return launch_fwd<128, OWT, KC, KW>(m, g, ep, tiles, ntiles, st);
+            if constexpr (KW == 1) return launch_fwd<128, OWT, KC, KW>(m, g, ep, fz, tiles, ntiles, st);
             return QT_EUNSUPPORTED;
         default: return QT_EUNSUPPORTED;
     }
@@ -610,14 +919,15 @@ static int dispatch_bn(int bn, const Maps &m, const FwdGeo &g, const EpiParams &
 
 template <int OWT>
 static int dispatch_kc(int kc, int kw, int bn, const Maps &m, const FwdGeo &g,
-                       const EpiParams &ep, int tiles, int ntiles, cudaStream_t st) {
+                       const EpiParams &ep, const FuseParams &fz, int tiles, int ntiles,
+                       cudaStream_t st) {
     if (kw == 1) {
         switch (kc) {
-            case 16: return dispatch_bn<OWT, 16, 1>(bn, m, g, ep, tiles, ntiles, st);
-            case 32: return dispatch_bn<OWT, 32, 1>(bn, m, g, ep, tiles, ntiles, st);
+            case 16: return dispatch_bn<OWT, 16, 1>(bn, m, g, ep, fz, tiles, ntiles, st);
+            case 32: return dispatch_bn<OWT, 32, 1>(bn, m, g, ep, fz, tiles, ntiles, st);
         }
     } else if (kw == 3) {
-        if (kc == 16) return dispatch_bn<OWT, 16, 3>(bn, m, g, ep, tiles, ntiles, st);
+        if (kc == 16) return dispatch_bn<OWT, 16, 3>(bn, m, g, ep, fz, tiles, ntiles, st);
     }
     return QT_EUNSUPPORTED;
 }
@@ -679,9 +989,11 @@ static bool tc_shape_ok(int n, int ci, int h, int wd, int co, int kh, int kw, in
 
 // Runs out = conv_s1(x, W') with W' the (possibly transposed+flipped) kernel.
 // x: (n, ci, h, w); out: (n, co, oh, ow); weights w in the ORIGINAL layout.
+static const FuseParams kNoFuse{};
+
 static int tc_conv_s1(const float *x, const float *w, float *out, int n, int ci, int h, int wd,
                       int co, int kh, int kw, int pad, int flip, const float *res, int cr, int sr,
-                      void *ws, cudaStream_t st) {
+                      void *ws, cudaStream_t st, const FuseParams &fz = kNoFuse) {
     FwdGeo g{};
     {   // data gradient beside the side-stream weight gradients: half the SMs
         const double macs = (double)n * (h + 2 * pad - kh + 1) * (wd + 2 * pad - kw + 1) *
@@ -703,7 +1015,8 @@ static int tc_conv_s1(const float *x, const float *w, float *out, int n, int ci,
         }
     } else if (tc_flat_ok(ci, h, wd, co, kh, kw, pad)) {
         if (res && sr != 1) {   // strided shortcut: the conv, then the standalone add
-            int rc = tc_conv_s1(x, w, out, n, ci, h, wd, co, kh, kw, pad, flip, nullptr, 0, 1, ws, st);
+            if (fz.stats) return QT_EUNSUPPORTED;    // statistics must see the sum
+            int rc = tc_conv_s1(x, w, out, n, ci, h, wd, co, kh, kw, pad, flip, nullptr, 0, 1, ws, st, fz);
             if (rc) return rc;
             return qt_shortcut_add(out, res, n, co, h, wd, cr, sr, st);
         }
@@ -715,6 +1028,7 @@ static int tc_conv_s1(const float *x, const float *w, float *out, int n, int ci,
     } else {
         return QT_EUNSUPPORTED;
     }
+    if (fz.bits && (flip || g.hw % (32 / fz.bits) != 0 || ci > 512)) return QT_EUNSUPPORTED;
     const int kc = (kw == 1 && ci % 32 == 0) ? 32 : 16;
     int bn = co <= 16 ? 16 : (co <= 32 ? 32 : (co <= 64 ? 64 : 128));
     if (kw == 3 && bn > 64) bn = 64;         // stacked taps: KW * BN <= 256 (UMMA N)
@@ -750,9 +1064,9 @@ static int tc_conv_s1(const float *x, const float *w, float *out, int n, int ci,
     const int tiles = (n / g.nimg) * g.tiles_per_img;
     const int ntiles = co / bn;
     switch (g.ow) {
-        case 8: return dispatch_kc<8>(kc, kw, bn, mp, g, ep, tiles, ntiles, st);
-        case 16: return dispatch_kc<16>(kc, kw, bn, mp, g, ep, tiles, ntiles, st);
-        case 32: return dispatch_kc<32>(kc, kw, bn, mp, g, ep, tiles, ntiles, st);
+        case 8: return dispatch_kc<8>(kc, kw, bn, mp, g, ep, fz, tiles, ntiles, st);
+        case 16: return dispatch_kc<16>(kc, kw, bn, mp, g, ep, fz, tiles, ntiles, st);
+        case 32: return dispatch_kc<32>(kc, kw, bn, mp, g, ep, fz, tiles, ntiles, st);
     }
     return QT_EUNSUPPORTED;
 }
@@ -936,6 +1250,120 @@ int qt_tc_conv_s2d_forward(const float *x, const float *w, float *out, const qt:
     if (rc) return rc;
     return tc_conv_s1(xd, w, out, (int)g.n, (int)(g.ci * g.kh * g.kw), (int)g.oh, (int)g.ow,
                       (int)g.co, 1, 1, 0, 0, res, (int)cr, (int)sr, ws, s);
+}
+
+// ---------------------------------------------------------------------------
+// Fused forward (qt_conv_forward_fused): BN-apply + ReLU + K-bit tape in the
+// operand prologue and/or the next layer's BN statistics in the epilogue.
+namespace qt {
+
+// 1: stride-1 row-tiled or flat tensor-core path; 2: kernel == stride via
+// space-to-depth (stats epilogue only); 0: neither
+static int fused_route(int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co, int64_t kh,
+                       int64_t kw, int64_t stride, int64_t pad) {
+    if (tc_disabled() || n <= 0 || n > INT32_MAX || ci * h * wd > INT32_MAX) return 0;
+    if (stride == 1 && tc_shape_ok((int)n, (int)ci, (int)h, (int)wd, (int)co, (int)kh, (int)kw,
+                                   (int)pad))
+        return 1;
+    if (stride > 1 && kh == stride && kw == stride && pad == 0 && h % stride == 0 &&
+        wd % stride == 0 &&
+        tc_shape_ok((int)n, (int)(ci * kh * kw), (int)(h / stride), (int)(wd / stride), (int)co,
+                    1, 1, 0))
+        return 2;
+    return 0;
+}
+
+static bool flat_only(int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co, int64_t kh,
+                      int64_t kw, int64_t pad) {
+    return !tc_rows_ok((int)n, (int)ci, (int)h, (int)wd, (int)co, (int)kh, (int)kw, (int)pad);
+}
+
+}  // namespace qt
+
+extern "C" int64_t qt_conv_stats_workspace(int64_t co) {
+    return 256 + (int64_t)qt_sm_count() * (8 + co * 24);
+}
+
+extern "C" int qt_conv_fused_support(int64_t n, int64_t ci, int64_t h, int64_t wd, int64_t co,
+                                     int64_t kh, int64_t kw, int64_t stride, int64_t pad,
+                                     int64_t sr, int bits) {
+    const int route = fused_route(n, ci, h, wd, co, kh, kw, stride, pad);
+    if (!route) return 0;
+    int r = 0;
+    if (route == 1 && qt_bits_ok(bits) && ci <= 512 && (h * wd) % (32 / bits) == 0) r |= 1;
+    // the statistics must see the shortcut sum: the flat path adds a strided
+    // shortcut in a separate kernel
+    const int64_t oh = route == 2 ? h / stride : h + 2 * pad - kh + 1;
+    const int64_t ow = route == 2 ? wd / stride : wd + 2 * pad - kw + 1;
+    const int64_t cin = route == 2 ? ci * kh * kw : ci;
+    const bool flat = route == 2 ? flat_only(n, cin, oh, ow, co, 1, 1, 0)
+                                 : flat_only(n, ci, h, wd, co, kh, kw, pad);
+    (void)oh; (void)ow;
+    if (!(flat && sr > 1) && co % 16 == 0 && co <= 4096) r |= 2;
+    return r;
+}
+
+extern "C" int qt_conv_forward_fused(const float *x, const float *w, float *out, int64_t n,
+                                     int64_t ci, int64_t h, int64_t wd, int64_t co, int64_t kh,
+                                     int64_t kw, int64_t stride, int64_t pad, const float *res,
+                                     int64_t cr, int64_t sr, const qt_bn_prologue_t *pro,
+                                     const qt_bn_stats_epilogue_t *epi, void *ws,
+                                     qt_stream_t stream) {
+    if (!pro && !epi)
+        return qt_conv_forward(x, w, out, n, ci, h, wd, co, kh, kw, stride, pad, res, cr, sr, ws,
+                               stream);
+    QT_REQUIRE(x && out && ws && n > 0 && ci > 0 && co > 0);
+    QT_REQUIRE(!res || (cr > 0 && cr <= co && sr >= 1));
+    const int sup = qt_conv_fused_support(n, ci, h, wd, co, kh, kw, stride, pad, res ? sr : 1,
+                                          pro ? pro->bits : 4);
+    if ((pro && !(sup & 1)) || (epi && !(sup & 2))) return QT_EUNSUPPORTED;
+    FuseParams fz{};
+    if (pro) {
+        QT_REQUIRE(pro->consts && pro->codes && pro->clip_count && qt_bits_ok(pro->bits));
+        QT_REQUIRE(((uintptr_t)pro->codes & 3) == 0);
+        fz.bn = (const BnConst *)pro->consts;
+        fz.codes = (uint32_t *)pro->codes;
+        fz.clip = (unsigned long long *)pro->clip_count;
+        fz.bits = pro->bits;
+    }
+    if (epi) {
+        QT_REQUIRE(epi->ws && epi->mean && epi->var && epi->gamma && epi->beta && epi->consts &&
+                   epi->gamma_copy && epi->beta_copy);
+        QT_REQUIRE(epi->bits == 0 || (qt_bits_ok(epi->bits) && epi->step && epi->offset));
+        char *b = (char *)epi->ws;
+        fz.stats = 1;
+        fz.counter = (unsigned *)b;
+        fz.pcnt = (double *)(b + 256);
+        fz.part = fz.pcnt + qt_sm_count();
+        fz.eps = epi->eps;
+        fz.gamma = epi->gamma;
+        fz.beta = epi->beta;
+        fz.nbits = epi->bits;
+        fz.mean = epi->mean;
+        fz.var = epi->var;
+        fz.rmean = epi->running_mean;
+        fz.rvar = epi->running_var;
+        fz.consts = (BnConst *)epi->consts;
+        fz.gcopy = epi->gamma_copy;
+        fz.bcopy = epi->beta_copy;
+        fz.step = epi->step;
+        fz.offset = epi->offset;
+        fz.nclip = (unsigned long long *)epi->clip_count;
+    }
+    const cudaStream_t st = qt_s(stream);
+    if (fused_route(n, ci, h, wd, co, kh, kw, stride, pad) == 1)
+        return tc_conv_s1(x, w, out, (int)n, (int)ci, (int)h, (int)wd, (int)co, (int)kh, (int)kw,
+                          (int)pad, 0, res, (int)cr, (int)sr, ws, st, fz);
+    // kernel == stride: space-to-depth, then the 1x1 with the stats epilogue
+    QT_REQUIRE(w);
+    ConvGeo g{};
+    g.n = n; g.ci = ci; g.h = h; g.w = wd; g.co = co; g.kh = kh; g.kw = kw; g.s = stride;
+    g.pad = pad; g.oh = h / stride; g.ow = wd / stride;
+    float *xd = (float *)((char *)ws + s2d_weights_bytes(g));
+    int rc = space_depth(x, xd, g.n, g.ci, g.h, g.w, (int)g.s, true, st);
+    if (rc) return rc;
+    return tc_conv_s1(xd, w, out, (int)g.n, (int)(g.ci * g.kh * g.kw), (int)g.oh, (int)g.ow,
+                      (int)g.co, 1, 1, 0, 0, res, (int)cr, (int)sr, ws, st, fz);
 }
 
 int qt_tc_conv_s2d_dgrad(const float *gr, const float *w, float *gx, const qt::ConvGeo &g,

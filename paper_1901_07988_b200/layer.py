@@ -212,9 +212,14 @@ def _prepared(ws, p: LayerParams, dgrad: int):
     return None if ent is None else ent[dgrad]
 
 
-def _linear_forward(a3, p: LayerParams, out, residual=None, ws=None):
-    """layer.py:138-151; ``residual`` fuses the block-end shortcut add."""
+def _linear_forward(a3, p: LayerParams, out, residual=None, ws=None, epilogue=None):
+    """layer.py:138-151; ``residual`` fuses the block-end shortcut add,
+    ``epilogue`` (engine) the next layer's BN statistics."""
     if p.kind == "conv":
+        if epilogue is not None:
+            return ops.conv2d_forward_fused(a3, p.weight, p.stride, p.pad, out, residual,
+                                            ws=ws.conv, prepared=_prepared(ws, p, 0),
+                                            epilogue=epilogue)
         return ops.conv2d_forward(a3, p.weight, p.stride, p.pad, out=out, residual=residual,
                                   ws=None if ws is None else ws.conv, prepared=_prepared(ws, p, 0))
     if p.kind == "dense":
@@ -233,19 +238,28 @@ def layer_forward(a_in: torch.Tensor, p: LayerParams, mode: str = "exact",
                   bits: Optional[int] = 8, training: bool = True,
                   out: Optional[torch.Tensor] = None, work: Optional[torch.Tensor] = None,
                   slot: Optional[TapeSlot] = None, residual: Optional[torch.Tensor] = None,
-                  ws=None):
+                  ws=None, fuse: Optional[dict] = None):
     """Run the layer forward; returns (a_out, tape) (layer.py:208-266).
 
     ``work`` receives the ReLU'd activations and may not alias ``a_in``;
     ``out`` may share storage with ``a_in``.  ``slot``/``residual``/``ws`` are
-    engine hooks (preallocated tape storage, fused shortcut add, scratch)."""
+    engine hooks (preallocated tape storage, fused shortcut add, scratch).
+
+    ``fuse`` (engine hook, DESIGN.md section 3 "layer fusion"):
+      stats_done -- this layer's statistics and constants were already
+                    written into ``slot`` by the previous conv's epilogue;
+      pro        -- the conv applies BN + ReLU and writes the K-bit tape in
+                    its operand staging (no qt_bn_relu_forward, no ``work``);
+      epi        -- N.BnStatsEpilogue: the conv's epilogue computes the NEXT
+                    layer's statistics."""
     if mode not in MODES:
         raise StateError(f"unknown mode {mode!r}")
     if bits is not None and bits not in (1, 2, 4, 8):
         raise ConfigError(f"bits must be one of (1, 2, 4, 8), got {bits}")
     _dev_f32(a_in, "a_in")
+    fz = fuse or {}
     if not p.preact:
-        a_out = _linear_forward(a_in, p, out, residual, ws)
+        a_out = _linear_forward(a_in, p, out, residual, ws, epilogue=fz.get("epi"))
         return a_out, LayerTape(mode="plain", stored=None, input_ref=a_in)
 
     n, c, hw = ops.nchw(a_in)
@@ -253,12 +267,16 @@ def layer_forward(a_in: torch.Tensor, p: LayerParams, mode: str = "exact",
         raise ShapeError(f"layer expects {p.gamma.numel()} channels, got {c}")
     a_in = a_in.contiguous()
     dev = a_in.device
-    if work is None:
+    quantized = training and mode != "exact" and bits is not None
+    fused_in = bool(fz.get("pro")) and quantized and mode == "approx" and p.kind == "conv"
+    if fused_in:
+        if slot is None or ws is None:
+            raise StateError("the fused BN prologue is an engine path (slot and ws required)")
+    elif work is None:
         work = torch.empty_like(a_in)
     elif work.data_ptr() == a_in.data_ptr():
         raise StateError("work may not alias a_in")
 
-    quantized = training and mode != "exact" and bits is not None
     a2_tape = codes = step = offset = clip = consts = None
     kbits = 0
     nmode = 0
@@ -274,19 +292,23 @@ def layer_forward(a_in: torch.Tensor, p: LayerParams, mode: str = "exact",
         # one launch: moments + running stats + K1 constants + frozen gamma/beta
         # + tape step/offset + clip-counter reset (layer.py:236-255)
         mean, var, consts = slot.mean, slot.var, slot.consts
-        if ws is not None:
-            sws = ws.stats
-        else:
-            sws = ops.workspace(N.query("qt_bn_stats_workspace", n, c, hw), dev, "stats")
-        N.call("qt_bn_stats_prep", N.ptr(a_in), n, c, hw, float(p.bn_epsilon), N.ptr(p.gamma),
-               N.ptr(p.beta), kbits, N.ptr(mean), N.ptr(var), N.ptr(p.running_mean),
-               N.ptr(p.running_var), N.ptr(slot.gamma), N.ptr(slot.beta), N.ptr(step),
-               N.ptr(offset), N.ptr(clip), N.ptr(consts), N.ptr(sws))
+        if not fz.get("stats_done"):
+            if ws is not None:
+                sws = ws.stats
+            else:
+                sws = ops.workspace(N.query("qt_bn_stats_workspace", n, c, hw), dev, "stats")
+            N.call("qt_bn_stats_prep", N.ptr(a_in), n, c, hw, float(p.bn_epsilon),
+                   N.ptr(p.gamma), N.ptr(p.beta), kbits, N.ptr(mean), N.ptr(var),
+                   N.ptr(p.running_mean), N.ptr(p.running_var), N.ptr(slot.gamma),
+                   N.ptr(slot.beta), N.ptr(step), N.ptr(offset), N.ptr(clip), N.ptr(consts),
+                   N.ptr(sws))
     else:
         mean, var = p.running_mean, p.running_var
-    N.call("qt_bn_relu_forward", N.ptr(a_in), n, c, hw, N.ptr(mean), N.ptr(var),
-           float(p.bn_epsilon), N.ptr(p.gamma), N.ptr(p.beta), nmode, kbits, N.ptr(work),
-           N.ptr(a2_tape), N.ptr(codes), N.ptr(step), N.ptr(offset), N.ptr(clip), N.ptr(consts))
+    if not fused_in:
+        N.call("qt_bn_relu_forward", N.ptr(a_in), n, c, hw, N.ptr(mean), N.ptr(var),
+               float(p.bn_epsilon), N.ptr(p.gamma), N.ptr(p.beta), nmode, kbits, N.ptr(work),
+               N.ptr(a2_tape), N.ptr(codes), N.ptr(step), N.ptr(offset), N.ptr(clip),
+               N.ptr(consts))
 
     tape = None
     if training:
@@ -299,7 +321,13 @@ def layer_forward(a_in: torch.Tensor, p: LayerParams, mode: str = "exact",
         tape = LayerTape(mode=mode, stored=stored, sigma2=var, gamma=slot.gamma,
                          beta=slot.beta, bn_epsilon=p.bn_epsilon,
                          identity=(bits is None and mode != "exact"))
-    a_out = _linear_forward(work, p, out, residual, ws)
+    if fused_in:   # BN apply + ReLU + tape inside the conv's operand staging
+        pro = N.BnPrologue(N.ptr(consts), N.ptr(codes), N.ptr(clip), int(bits))
+        a_out = ops.conv2d_forward_fused(a_in, p.weight, p.stride, p.pad, out, residual,
+                                         ws=ws.conv, prepared=_prepared(ws, p, 0),
+                                         prologue=pro, epilogue=fz.get("epi"))
+    else:
+        a_out = _linear_forward(work, p, out, residual, ws, epilogue=fz.get("epi"))
     ops._check_finite(a_out)
     return a_out, tape
 

@@ -15,6 +15,8 @@ level, tests/test_parity_gpu.py):
 
 from __future__ import annotations
 
+import ctypes
+
 import os
 from typing import Optional
 
@@ -145,6 +147,29 @@ def conv2d_forward(x: torch.Tensor, k: torch.Tensor, stride: int = 1, pad: int =
     N.call("qt_conv_forward", N.ptr(x), N.ptr(wp), N.ptr(out), n, ci, x.shape[2], x.shape[3], co,
            kh, kw, stride, pad, N.ptr(residual), cr, sr, N.ptr(wsp))
     _check_finite(out)
+    return out
+
+
+def conv2d_forward_fused(x: torch.Tensor, k: torch.Tensor, stride: int, pad: int,
+                         out: torch.Tensor, residual=None, ws=None, prepared=None,
+                         prologue=None, epilogue=None) -> torch.Tensor:
+    """Engine form of the forward conv with layer fusion (qt_conv_forward_fused):
+    ``prologue`` (N.BnPrologue) makes ``x`` the layer's pre-BN input and the
+    conv apply BN + ReLU and write the K-bit tape in its operand staging;
+    ``epilogue`` (N.BnStatsEpilogue) computes the next layer's BN statistics
+    from the output.  Shapes must pass qt_conv_fused_support."""
+    n, co, oh, ow = conv2d_out_shape(tuple(x.shape), tuple(k.shape), stride, pad)
+    ci, kh, kw = k.shape[1:]
+    cr, sr = 0, 1
+    if residual is not None:
+        cr = residual.shape[1]
+        sr = residual.shape[2] // oh
+    wp, wsp = (None, prepared) if prepared is not None else \
+        (k, _conv_ws(k, ws, tuple(x.shape), stride, pad))
+    N.call("qt_conv_forward_fused", N.ptr(x), N.ptr(wp), N.ptr(out), n, ci, x.shape[2],
+           x.shape[3], co, kh, kw, stride, pad, N.ptr(residual), cr, sr,
+           None if prologue is None else ctypes.byref(prologue),
+           None if epilogue is None else ctypes.byref(epilogue), N.ptr(wsp))
     return out
 
 
