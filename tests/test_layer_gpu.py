@@ -253,3 +253,51 @@ def test_backward_given_device_tape(cfg):
     assert norm_err(host(p.grad_weight), op["grad_weight"]) < LAYER_TOL
     assert norm_err(host(p.grad_gamma), op["grad_gamma"]) < LAYER_TOL
     assert norm_err(host(p.grad_beta), op["grad_beta"]) < LAYER_TOL
+
+
+@pytest.mark.parametrize("bits", [1, 2, 4, 8, None])
+def test_reconstruct_from_tape_matches_oracle(bits):
+    """layer.reconstruct_from_tape (layer.py:269-283): A2 = decode(tape),
+    A3 = max(A2, 0), A1 = (A2 - beta) / safe_gamma(gamma) with the frozen
+    gamma / beta -- bit-exact against the oracle on the same tape, including
+    a zero gamma (floored to 1e-8), negative gammas and exact (fp32) tapes."""
+    rng = np.random.default_rng(0 if bits is None else bits)
+    c = 6
+    gamma = np.array([1.0, -0.7, 0.0, 2.5, -1e-9, 0.3], np.float32)
+    beta = rng.uniform(-1, 1, c).astype(np.float32)
+    x = dev((rng.standard_normal((3, c, 8, 8)) * 2 + 0.5).astype(np.float32))
+    p = _conv_params(c, 4, 5, gamma, beta)
+    _, t = L.layer_forward(x, p, mode="approx" if bits else "exact", bits=bits)
+    a1, a2, a3 = (host(v) for v in L.reconstruct_from_tape(t))
+    if t.is_quantized:
+        q = {"codes": host(t.stored.codes), "bits": bits, "shape": t.shape, "dtype": np.float32,
+             "step": host(t.stored.step), "offset": host(t.stored.offset)}
+        want2 = O.dequantize(q)
+    else:
+        want2 = host(t.stored)
+    want3 = np.maximum(want2, np.float32(0))
+    gs = O.safe_gamma(host(t.gamma))
+    want1 = (want2 - host(t.beta).reshape(1, -1, 1, 1)) / gs.reshape(1, -1, 1, 1)
+    for got, want in ((a1, want1), (a2, want2), (a3, want3)):
+        assert got.dtype == np.float32
+        assert np.array_equal(got.view(np.uint32), want.astype(np.float32).view(np.uint32))
+
+
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+def test_decode_threshold_is_the_sign_of_the_decode(bits):
+    """codec.decode_threshold (codec.py:165-173) equals the oracle's, and a
+    code is >= the threshold exactly when it decodes to a positive value --
+    the mask primitive the BN backward uses (bn_bwd.cu's per-code tables)."""
+    rng = np.random.default_rng(bits)
+    c = 8
+    gamma = rng.uniform(0.2, 3, c).astype(np.float32) * rng.choice([-1, 1], c).astype(np.float32)
+    beta = np.concatenate([rng.uniform(-4, 4, c - 2), [50.0, -50.0]]).astype(np.float32)
+    x = dev(rng.standard_normal((2, c, 4, 4)).astype(np.float32))
+    _, t = L.layer_forward(x, _conv_params(c, 4, 1, gamma, beta), mode="approx", bits=bits)
+    thr = host(P.codec.decode_threshold(t.stored))
+    q = {"bits": bits, "offset": host(t.stored.offset)}
+    assert np.array_equal(thr, O.decode_threshold(q))
+    codes = np.arange(1 << bits)
+    for ch in range(c):
+        dec = host(t.stored.step)[ch] * ((codes + (0.5 - (1 << (bits - 1)))) + q["offset"][ch])
+        assert np.array_equal(dec.astype(np.float32) > 0, codes >= thr[ch]), (bits, ch)
