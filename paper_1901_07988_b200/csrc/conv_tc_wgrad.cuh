@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                          const __grid_constant__ CUtensorMap tmC, WgParams p) {
     constexpr int ROWS = 32 / OW;                           // image rows per 32-pixel chunk
     constexpr int G_BYTES = BN * 128;                       // raw g tile: BN rows x 32 px fp32
-    constexpr bool FAST_OK = (BITS == 4);
+    constexpr bool FAST_OK = (BITS == 4 || BITS == 2);
     constexpr int NT = TAP ? 3 : 1;                         // column taps stacked in N
     constexpr bool STACK = TAP ? (9 * BN <= 256) : (3 * BN <= 192);   // pieces stacked in N
     constexpr int FACC = STACK ? 3 * NT * BN : NT * BN;     // FAST accumulator columns per tile
@@ -526,7 +526,59 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const uint32_t acol = acc_cols + (uint32_t)((o * p.mtg + t) * SUB + sub) * acols;
                 const int c = rc[t], u = ru[t], sh = rsh[t];
                 const int cbox = (c - c_begin) * p.cb;
-                if (FAST_OK && fast) {
+                if (FAST_OK && fast && BITS == 2) {
+                    // 2-bit codes: a row is OW/4 bytes (8 px: one halfword).
+                    // Per 8-pixel group (16 bits h): z = (h & 0xFF) | (h >> 8) << 16
+                    // puts pixel k at bits 2k and pixel k + 4 at bits 16 + 2k,
+                    // so (z >> 2k) & 0x00030003 is A word k of the group's
+                    // (k, k + 4) pixel pairing -- then the same *2 + (0x4300 + b)
+                    // and relu(x - 128) as the 4-bit path (m < 128, exact)
+                    uint32_t av[16];
+#pragma unroll
+                    for (int x = 0; x < 16; ++x) av[x] = 0u;
+                    if (rok[t]) {
+                        const uint32_t bc = s_bc[c - c_begin];
+#pragma unroll
+                        for (int seg = 0; seg < ROWS; ++seg) {
+                            const int iy = y0 + seg + u - p.pad;
+                            if (iy < 0 || iy >= p.h) continue;
+                            const uint8_t *rowp = cst + cbox + iy * p.rb - wbase;
+                            uint32_t hw[OW / 8];               // one 16-bit group per entry
+                            if (OW == 8) {
+                                uint32_t w0 = *reinterpret_cast<const uint16_t *>(rowp);
+                                w0 = sh > 0 ? (w0 >> 2) : sh < 0 ? ((w0 << 2) & 0xFFFFu) : w0;
+                                hw[0] = w0;
+                            } else {
+                                constexpr int NW = OW / 16;            // 32-bit words per row
+                                const uint32_t *cw = reinterpret_cast<const uint32_t *>(rowp);
+                                uint32_t w[NW + 2];
+                                w[0] = 0u;
+                                w[NW + 1] = 0u;
+#pragma unroll
+                                for (int q = 0; q < NW; ++q) w[q + 1] = cw[q];
+#pragma unroll
+                                for (int q = 0; q < NW; ++q) {
+                                    const uint32_t sw = sh > 0   ? __funnelshift_r(w[q + 1], w[q + 2], 2)
+                                                        : sh < 0 ? __funnelshift_l(w[q], w[q + 1], 2)
+                                                                 : w[q + 1];
+                                    hw[2 * q] = sw & 0xFFFFu;
+                                    hw[2 * q + 1] = sw >> 16;
+                                }
+                            }
+#pragma unroll
+                            for (int gq = 0; gq < OW / 8; ++gq) {
+                                const uint32_t z = (hw[gq] & 0xFFu) | ((hw[gq] >> 8) << 16);
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    av[seg * (OW / 2) + 4 * gq + k] =
+                                        bf16x2_relu_sub128(((z >> (2 * k)) & 0x00030003u) * 2u + bc);
+                            }
+                            if (sh < 0) av[seg * (OW / 2)] &= 0xFFFF0000u;          // x = 0 pads
+                            if (sh > 0) av[seg * (OW / 2) + OW / 2 - 1] &= 0x0000FFFFu;  // x = OW-1
+                        }
+                    }
+                    tmem_st16(lane_base + acol, av);
+                } else if (FAST_OK && fast && BITS == 4) {
                     constexpr int NW = OW / 8;                 // 32-bit words per row (4-bit)
                     uint32_t av[16];
 #pragma unroll

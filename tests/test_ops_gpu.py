@@ -311,3 +311,34 @@ def test_segmented_3x3_wgrad_from_codes(shape, bits):
         ref = torch.nn.grad.conv2d_weight(act.double(), (co, ci, 3, 3), g.double(), padding=1) - 0.5
         err = ((gw.double() - ref).norm() / ref.norm()).item()
         assert err < CONV_TOL, (regime, err)
+
+
+@pytest.mark.parametrize("bits", [2, 4])
+@pytest.mark.parametrize("shape", [(2, 16, 32, 16, 3), (2, 32, 16, 32, 3), (4, 64, 8, 64, 3),
+                                   (2, 16, 32, 64, 1), (2, 64, 8, 256, 1), (4, 128, 16, 32, 1),
+                                   (3, 64, 8, 16, 1)])
+def test_wgrad_from_codes_row_tiles(shape, bits):
+    """Row-tiled (8/16/32-px rows) weight gradient from 2- and 4-bit tapes:
+    the FAST decode (integer bf16 operand; the 2-bit form regroups each
+    halfword's pixel pairs) for narrow channels, GENERIC for wide ones,
+    mixed channels in one CTA -- against float64 on the dequantized tape."""
+    from paper_1901_07988_b200 import codec
+    n, ci, hw, co, k = shape
+    torch.manual_seed(bits * 100 + ci + k)
+    for regime in ("narrow", "wide", "mixed"):
+        x = torch.randn(n, ci, hw, hw, device="cuda")
+        gamma = torch.rand(ci, device="cuda") + 0.5
+        beta = torch.randn(ci, device="cuda") * 0.3
+        if regime != "narrow":
+            wide = torch.arange(ci, device="cuda") % (1 if regime == "wide" else 5) == 0
+            gamma = torch.where(wide, torch.rand(ci, device="cuda") * 0.05 + 0.05, gamma)
+            beta = torch.where(wide, torch.rand(ci, device="cuda") + 1.5, beta)
+        t = codec.quantize(x, gamma, beta, bits)
+        act = codec.dequantize(t, relu=True)
+        g = torch.randn(n, co, hw, hw, device="cuda")
+        gw = torch.full((co, ci, k, k), 0.125, device="cuda")
+        ops.conv2d_wgrad(g, (co, ci, k, k), 1, k // 2, gw, tape=t.as_native(), in_shape=(n, ci, hw, hw))
+        ref = torch.nn.grad.conv2d_weight(act.double(), (co, ci, k, k), g.double(), padding=k // 2)
+        ref = ref + 0.125
+        err = ((gw.double() - ref).norm() / ref.norm()).item()
+        assert err < CONV_TOL, (regime, err)
