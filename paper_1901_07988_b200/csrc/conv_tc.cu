@@ -314,7 +314,7 @@ __device__ __forceinline__ void epi_stats_finalize(const FuseParams &fz, const d
 //            + shortcut (TMA-prefetched) -> smem -> TMA store) overlaps tile
 //            j+1's main loop.
 // Precision: 3xTF32 (hi*hi + hi*lo + lo*hi).
-template <int BN, int OWT, int KC, int KW>
+template <int BN, int OWT, int KC, int KW, bool FUSE>
 __global__ void __launch_bounds__(kFwdThreads, 1)
     conv_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmBh,
@@ -345,8 +345,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // (bars is 1 KiB aligned; this is the first 16-byte boundary past tmem_slot)
     uint8_t *fbase = (uint8_t *)(bars + 2 * R + 2 * kFwdGroups + 8);
     BnConst *s_bn = (BnConst *)fbase;
-    double *s_acc = (double *)(fbase + (fz.bits ? g.ci * (int)sizeof(BnConst) : 0));   // [BN][3]
-    int *s_fin = (int *)(s_acc + (fz.stats ? 3 * BN : 0));
+    double *s_acc = (double *)(fbase + (FUSE && fz.bits ? g.ci * (int)sizeof(BnConst) : 0));   // [BN][3]
+    int *s_fin = (int *)(s_acc + (FUSE && fz.stats ? 3 * BN : 0));
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     long long *const tr_ = (g_cv_trace && blockIdx.x == (unsigned)g_cv_trace_cta) ? g_cv_trace : nullptr;
@@ -366,7 +366,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         mbar_init(w_full, 1);
         fence_barrier_init();
     }
-    if (fz.stats && (int)threadIdx.x < 3 * BN) s_acc[threadIdx.x] = 0.0;
+    if (FUSE && fz.stats && (int)threadIdx.x < 3 * BN) s_acc[threadIdx.x] = 0.0;
     if (warp == 1) tmem_alloc<512>(tmem_slot);
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         int gi = grp < G ? grp : nstages;
         int s = gi % R;
         uint32_t phr = (uint32_t)(gi / R) & 1u, pho = (uint32_t)(gi / G) & 1u;
-        const int bits = fz.bits;
+        const int bits = FUSE ? fz.bits : 0;
         unsigned long long nclip = 0;
         if (bits) {   // the layer's BnConst table (written by the stats kernel / producer)
             const int st = threadIdx.x - 64;
@@ -523,7 +523,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 emit = (u == g.pad) && (co0_ == 0);
                 nimg0 += (int)aimg;
             }
-#pragma unroll 1
+#pragma unroll
             for (int cg = 0; cg < KC; cg += 16) {
                 uint32_t hi[16], lo[16];
                 float a2[16];
@@ -706,14 +706,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                                 g.flat ? h1 * OWT : 0, g.flat ? 0 : h1, c1, n1);
                 }
             }
-            if (fz.stats) {   // BN statistics of this output tile (reads the staged tile)
+            if (FUSE && fz.stats) {   // BN statistics of this output tile (reads the staged tile)
                 const int nvalid = g.flat ? min(128, g.hw - h0 * OWT) : 128;
                 epi_tile_stats<BN>(s_out, cstride == 64 ? 6 : 7, nvalid, lt == 0, s_acc);
                 cta_px += nvalid;
             }
         }
         if (leader) bulk_wait_read0();
-        if (fz.stats) epi_stats_finalize<BN>(fz, s_acc, (double)cta_px, s_fin, g.co, g.ntiles);
+        if (FUSE && fz.stats) epi_stats_finalize<BN>(fz, s_acc, (double)cta_px, s_fin, g.co, g.ntiles);
     }
     tc_fence_before();
     __syncthreads();
@@ -848,11 +848,13 @@ template <int BN, int OWT, int KC, int KW>
 static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, const FuseParams &fz,
                       int tiles, int ntiles, cudaStream_t st) {
     using C = FwdCfg<BN, OWT, KC, KW>;
-    auto kern = conv_fwd_tc_kernel<BN, OWT, KC, KW>;
-    static bool attr = false;
-    if (!attr) {
+    const bool fuse = fz.bits || fz.stats;
+    auto kern = fuse ? conv_fwd_tc_kernel<BN, OWT, KC, KW, true>
+                     : conv_fwd_tc_kernel<BN, OWT, KC, KW, false>;
+    static bool attr[2] = {false, false};
+    if (!attr[fuse]) {
         cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr = true;
+        attr[fuse] = true;
     }
     FwdGeo gg = g;
     gg.mtiles = tiles;

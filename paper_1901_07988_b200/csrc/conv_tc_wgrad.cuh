@@ -484,10 +484,15 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 for (int q = tg; q < BN * 4; q += 128) {
                     const int co = q >> 2, qq = q & 3;
                     const uint32_t rrow = (uint32_t)((co * SUB + sub) * 128);
-                    const float4 x0 = *reinterpret_cast<const float4 *>(
-                        graws + swz_off<128>(rrow + qq * 32));
-                    const float4 x1 = *reinterpret_cast<const float4 *>(
-                        graws + swz_off<128>(rrow + qq * 32 + 16));
+                    // odd channels read their two 16-byte halves in the other
+                    // order: the 8 lanes of a quarter warp (2 channels x 4
+                    // groups) then hit 8 distinct swizzled chunks (no conflict)
+                    const uint32_t fl = (uint32_t)(co & 1) * 16u;
+                    const float4 y0 = *reinterpret_cast<const float4 *>(
+                        graws + swz_off<128>(rrow + qq * 32 + fl));
+                    const float4 y1 = *reinterpret_cast<const float4 *>(
+                        graws + swz_off<128>(rrow + qq * 32 + (16u - fl)));
+                    const float4 x0 = fl ? y1 : y0, x1 = fl ? y0 : y1;
                     const float xa[4] = {x0.x, x0.y, x0.z, x0.w}, xb[4] = {x1.x, x1.y, x1.z, x1.w};
                     uint32_t H[4], M[4], L[4];
 #pragma unroll
@@ -554,8 +559,13 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                                 uint32_t w[NW + 2];
                                 w[0] = 0u;
                                 w[NW + 1] = 0u;
+                                if constexpr (NW == 2) {
+                                    const uint2 v2 = *reinterpret_cast<const uint2 *>(cw);
+                                    w[1] = v2.x; w[2] = v2.y;
+                                } else {
 #pragma unroll
-                                for (int q = 0; q < NW; ++q) w[q + 1] = cw[q];
+                                    for (int q = 0; q < NW; ++q) w[q + 1] = cw[q];
+                                }
 #pragma unroll
                                 for (int q = 0; q < NW; ++q) {
                                     const uint32_t sw = sh > 0   ? __funnelshift_r(w[q + 1], w[q + 2], 2)
@@ -594,8 +604,19 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                             uint32_t w[NW + 2];
                             w[0] = 0u;
                             w[NW + 1] = 0u;
+                            // one vector load per row (rows are NW-word aligned):
+                            // lanes on different channels then spread over the
+                            // banks instead of queueing per word
+                            if constexpr (NW == 4) {
+                                const uint4 v4 = *reinterpret_cast<const uint4 *>(cw);
+                                w[1] = v4.x; w[2] = v4.y; w[3] = v4.z; w[4] = v4.w;
+                            } else if constexpr (NW == 2) {
+                                const uint2 v2 = *reinterpret_cast<const uint2 *>(cw);
+                                w[1] = v2.x; w[2] = v2.y;
+                            } else {
 #pragma unroll
-                            for (int q = 0; q < NW; ++q) w[q + 1] = cw[q];
+                                for (int q = 0; q < NW; ++q) w[q + 1] = cw[q];
+                            }
 #pragma unroll
                             for (int q = 0; q < NW; ++q) {
                                 const uint32_t sw = sh > 0   ? __funnelshift_r(w[q + 1], w[q + 2], 4)
