@@ -12,6 +12,7 @@
 // bytes.  Per-(n,c)-plane constants (mean/inv/gamma/beta/scale/offset) are
 // computed once per block into shared memory.
 #include <algorithm>
+#include <climits>
 
 #include "common.cuh"
 
@@ -322,40 +323,65 @@ __global__ void unpack_kernel(const uint8_t *packed, int64_t count, int bits, ui
 // groups per iteration with all four 128-bit loads issued before any math,
 // constants through the read-only cache -- no block prologue, no smem.
 // Codes of 8 consecutive A2 values of one channel (approx / naive modes).
-// Common path in fp32/int32 (see code_fast in common.cuh for the error
-// analysis): a*scale = p + e + a*s2, floor taken from f + floor(fr) when the
-// fraction fr is more than 2^-20 from an integer and |p| < 2^20; elements
-// failing that (non-finite, huge, near-integer products) and channels whose
-// offset is outside +-2^30 are recomputed with the exact float64 recipe.
+// Common path: ONE fp32 fma per element, y = fl(a * s1 + c) with s1 =
+// fl32(scale) and c = 2^(K-1) - offset (an exact small float).  Against the
+// reference raw = floor(fl64(a * scale)) + c (codec.py:118-120), y is off by
+// at most ulp(y)/2 + 2^-24 (|y| + |c| + 1)(1 + 2^-29) (the fma rounding, the
+// dropped low part of the scale, the float64 product's rounding), so when
+// y's fraction is farther than `marg` (twice that bound) from an integer,
+// floor(y) is exactly the reference's raw code.  Elements within marg of an
+// integer that could change the clamped code or the clip flag (y in
+// (-2, 2^K + 2)), non-finite or |y| >= 2^20 values, and channels with
+// |offset| >= 2^20 take the exact float64 recipe (rare).
+struct QuantK {
+    float s1, cf, marg;
+    bool ok;          // |offset| < 2^20: the fp32 common path applies
+    double scale;
+    int64_t off;
+};
+
 template <int BITS>
-__device__ __forceinline__ void quant8(const float (&v)[8], const BnConst &k, uint32_t (&code)[8],
-                                       uint32_t &clipmask) {
+__device__ __forceinline__ QuantK quant_consts(float s1, double scale, int64_t off) {
+    QuantK q;
+    q.ok = off > -(1ll << 20) && off < (1ll << 20);
+    q.s1 = s1;
+    q.cf = q.ok ? (float)((1 << (BITS - 1)) - (int)off) : 0.f;
+    // 2^-15 + (|c| + 2^K + 8) 2^-23 >= 2 x the bound above for |y| < 2^K + 2
+    q.marg = __fmaf_rn(__fadd_rn(fabsf(q.cf), (float)((1 << BITS) + 8)), 1.1920928955078125e-07f,
+                       3.0517578125e-05f);
+    q.scale = scale;
+    q.off = off;
+    return q;
+}
+
+template <int BITS, bool LAZY = false>
+__device__ __forceinline__ void quant8(const float (&v)[8], const QuantK &k, uint32_t (&code)[8],
+                                       uint32_t &clipmask, const float *lazy_g = nullptr,
+                                       const float *lazy_b = nullptr) {
     constexpr int top = (1 << BITS) - 1;
-    const bool chan_ok = k.off > -(1ll << 30) && k.off < (1ll << 30);
-    // u_bits = float bits of (floor(a*scale) + 1.5*2^23); raw = u_bits + bias
-    const int bias = (1 << (BITS - 1)) - (int)(chan_ok ? k.off : 0) - 0x4B400000;
-    uint32_t slow = chan_ok ? 0u : 0xFFu;
+    constexpr float mid = 0.5f * (float)top, half_span = 0.5f * (float)top + 2.0f;
+    uint32_t slow = k.ok ? 0u : 0xFFu;
     clipmask = 0u;
+    const float hi_m = __fsub_rn(1.0f, k.marg);
 #pragma unroll
     for (int j = 0; j < 8; ++j) {
-        const float p = __fmul_rn(v[j], k.s1);
-        const float e = __fmaf_rn(v[j], k.s1, -p);
-        const float corr = __fmaf_rn(v[j], k.s2, e);
-        const float f = floorf(p);
-        const float fr = __fadd_rn(__fsub_rn(p, f), corr);
-        const float dist = fabsf(__fsub_rn(fr, rintf(fr)));
-        if (!(fabsf(p) < 1048576.f && dist > 9.5367431640625e-07f)) slow |= 1u << j;
-        const float u = __fadd_rn(__fadd_rn(f, floorf(fr)), 12582912.f);
-        const int raw = __float_as_int(u) + bias;
+        const float y = __fmaf_rn(v[j], k.s1, k.cf);
+        const float f = floorf(y);
+        const float fr = __fsub_rn(y, f);              // exact
+        const bool inrange = fabsf(__fsub_rn(y, mid)) < half_span;   // y in (-2, 2^K + 2)
+        const bool near = (fr <= k.marg) | (fr >= hi_m);
+        if (!(fabsf(y) < 1048576.f) | (inrange & near)) slow |= 1u << j;
+        const int raw = __float_as_int(__fadd_rn(f, 12582912.f)) - 0x4B400000;   // |f| < 2^22
         const int c = min(max(raw, 0), top);
         code[j] = (uint32_t)c;
         clipmask |= (raw != c) ? (1u << j) : 0u;
     }
     if (slow) {
+        const double scale = LAZY ? chan_code(*lazy_g, *lazy_b, BITS).scale : k.scale;
 #pragma unroll 1
         for (int j = 0; j < 8; ++j) {
             if (!((slow >> j) & 1u)) continue;
-            const int64_t raw = raw_code(v[j], k.scale, k.off, BITS);
+            const int64_t raw = raw_code(v[j], scale, k.off, BITS);
             const bool cl = raw < 0 || raw > top;
             code[j] = (uint32_t)(raw < 0 ? 0 : (raw > top ? top : raw));
             clipmask = (clipmask & ~(1u << j)) | (cl ? (1u << j) : 0u);
@@ -406,10 +432,10 @@ __global__ void __launch_bounds__(kThreads) bn_relu_quant_stream(FwdArgs a) {
             }
             if (BITS) {
                 uint32_t code[8], clipmask;
-                quant8<BITS>(a2v, k, code, clipmask);
+                quant8<BITS>(a2v, quant_consts<BITS>(k.s1, k.scale, k.off), code, clipmask);
                 if (split) {   // second half with the next channel's constants
                     uint32_t code_b[8], clip_b;
-                    quant8<BITS>(a2v, kb, code_b, clip_b);
+                    quant8<BITS>(a2v, quant_consts<BITS>(kb.s1, kb.scale, kb.off), code_b, clip_b);
 #pragma unroll
                     for (int j = 4; j < 8; ++j) code[j] = code_b[j];
                     clipmask = (clipmask & 0x0Fu) | (clip_b & 0xF0u);
@@ -469,65 +495,162 @@ __global__ void __launch_bounds__(kThreads) bn_relu_quant_stream(FwdArgs a) {
 // float64 divide per 8 elements, L1-resident gamma/beta), the fp32 fast floor
 // with the exact float64 fallback (quant8).  Threads below C also write the
 // frozen step / offset.
-template <int BITS, bool CLIP>
+// Per-channel constants of the quantize-pack stream kernel, staged in shared
+// memory once per block (C <= kQuantTable): s1 = fl32(scale), cf = 2^(K-1) -
+// offset, lim = 1/2 - marg (see quant8), and the offset for the exact path
+// (INT_MIN: |offset| >= 2^20, the whole channel takes the exact path).
+constexpr int kQuantTable = 1024;
+struct QChan {
+    float s1, cf, lim;
+    int off;
+};
+
+template <int BITS>
+__device__ __forceinline__ QChan qchan(float gamma, float beta) {
+    const ChanCode cc = chan_code(gamma, beta, BITS);
+    const QuantK k = quant_consts<BITS>(__double2float_rn(cc.scale), cc.scale, cc.off);
+    return QChan{k.s1, k.cf, __fsub_rn(0.5f, k.marg), k.ok ? (int)cc.off : INT_MIN};
+}
+
+// Exact float64 recipe for 4 elements (rare: an element near a code
+// boundary, non-finite, huge, or a channel with a huge offset).
+template <int BITS>
+__device__ __noinline__ uint32_t quant4_exact(float4 x, float gamma, float beta, uint32_t *nclip) {
+    constexpr int top = (1 << BITS) - 1;
+    const ChanCode cc = chan_code(gamma, beta, BITS);
+    const float v[4] = {x.x, x.y, x.z, x.w};
+    uint32_t w = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const int64_t raw = raw_code(v[j], cc.scale, cc.off, BITS);
+        *nclip += (raw < 0 || raw > top) ? 1u : 0u;
+        w |= (uint32_t)(raw < 0 ? 0 : (raw > top ? top : raw)) << (j * BITS);
+    }
+    return w;
+}
+
+// Codes of 4 consecutive A2 values of one channel (4K bits), quant8's error
+// analysis with fewer instructions: the near-integer test as
+// |frac - 1/2| >= 1/2 - marg, the clamp in float, the codes packed by exact
+// float accumulation (sum fc_j 2^(jK) < 2^16 for K <= 4; two halves for K = 8).
+// Sets `slow` when any element needs the exact recipe (the caller redoes all 4).
+template <int BITS>
+__device__ __forceinline__ uint32_t quant4(const float4 &x, const QChan &q, uint32_t &nclip,
+                                           bool &slow) {
+    constexpr float top = (float)((1 << BITS) - 1);
+    constexpr float mid = 0.5f * top, half_span = 0.5f * top + 2.0f;
+    const float v[4] = {x.x, x.y, x.z, x.w};
+    float fc[4];
+    bool sl = q.off == INT_MIN;
+    uint32_t nc = 0;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const float y = __fmaf_rn(v[j], q.s1, q.cf);
+        const float f = floorf(y);
+        const float fr = __fsub_rn(y, f);
+        const bool near = fabsf(__fsub_rn(fr, 0.5f)) >= q.lim;
+        const bool inr = fabsf(__fsub_rn(y, mid)) < half_span;
+        sl |= !(fabsf(y) < 1048576.f) | (near & inr);
+        fc[j] = fminf(fmaxf(f, 0.f), top);
+        nc += (fc[j] != f) ? 1u : 0u;
+    }
+    uint32_t w;
+    if (BITS == 8) {
+        const float lo = __fmaf_rn(fc[1], 256.f, fc[0]), hi = __fmaf_rn(fc[3], 256.f, fc[2]);
+        w = (uint32_t)(__float_as_int(__fadd_rn(lo, 8388608.f)) - 0x4B000000) |
+            ((uint32_t)(__float_as_int(__fadd_rn(hi, 8388608.f)) - 0x4B000000) << 16);
+    } else {
+        constexpr float r = (float)(1 << BITS);
+        const float acc = __fmaf_rn(__fmaf_rn(__fmaf_rn(fc[3], r, fc[2]), r, fc[1]), r, fc[0]);
+        w = (uint32_t)(__float_as_int(__fadd_rn(acc, 8388608.f)) - 0x4B000000);
+    }
+    if (!sl) nclip += nc;
+    slow = sl;
+    return w;
+}
+
+// Lane-interleaved streaming layout: a warp iteration covers 32 * kSlots
+// consecutive float4; slot i of lane l is float4 32 i + l, so every load
+// and store instruction of the warp is one contiguous run.  A float4 is half
+// of an 8-element group (one channel: hw % 8 == 0); the 4K-bit code pieces of
+// 8/K adjacent lanes are OR-combined with shuffles into one 32-bit word,
+// which the first of them stores (K = 8: every lane stores its own word).
+constexpr int kSlots = 8;
+
+template <int BITS>
+__device__ __forceinline__ void store_code_piece(uint8_t *codes, int64_t f, uint32_t piece) {
+    constexpr int lpw = BITS == 8 ? 1 : 8 / BITS;        // lanes per 32-bit word
+    const int lane = threadIdx.x & 31;
+    uint32_t w = piece << (((lane & (lpw - 1)) * 4 * BITS) & 31);
+    if (lpw > 1) w |= __shfl_xor_sync(0xffffffffu, w, 1);
+    if (lpw > 2) w |= __shfl_xor_sync(0xffffffffu, w, 2);
+    if (lpw > 4) w |= __shfl_xor_sync(0xffffffffu, w, 4);
+    if ((lane & (lpw - 1)) == 0)
+        reinterpret_cast<uint32_t *>(codes)[(f * 4 * BITS) >> 5] = w;
+}
+
+template <int BITS, bool CLIP, bool TABLE>
 __global__ void __launch_bounds__(kThreads) quant_pack_stream(FwdArgs a) {
     pdl_enter();
+    __shared__ QChan s_q[TABLE ? kQuantTable : 1];
     const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (tid < a.c && a.step) {
-        const ChanCode cc = chan_code(a.gamma[tid], a.beta[tid], BITS);
-        a.step[tid] = cc.step;
-        a.offset[tid] = cc.off;
+    for (int64_t c = tid; c < a.c && a.step; c += (int64_t)gridDim.x * kThreads) {
+        const ChanCode cc = chan_code(a.gamma[c], a.beta[c], BITS);
+        a.step[c] = cc.step;
+        a.offset[c] = cc.off;
     }
-    const int64_t ngroups = a.numel >> 3;
-    const int64_t stride = (int64_t)gridDim.x * kThreads;
-    unsigned long long clip = 0;
-    for (int64_t g0 = tid; g0 < ngroups; g0 += 2 * stride) {
-        const int64_t gs[2] = {g0, g0 + stride};
-        float4 xa[2], xb[2];
+    if (TABLE) {
+        for (int c = threadIdx.x; c < a.c; c += kThreads)
+            s_q[c] = qchan<BITS>(__ldg(a.gamma + c), __ldg(a.beta + c));
+        __syncthreads();
+    }
+    // full 32-float4 warp slots in the lane-interleaved loop; the < 128-element
+    // tail (8-element groups) one group per thread
+    const int64_t nf4 = (a.numel >> 7) << 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = tid >> 5, nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+    uint32_t nclip = 0;
+    auto chan_of = [&](int64_t gg) {
+        const uint32_t plane = fast_div((uint32_t)gg, a.hw8d);
+        return plane - fast_div(plane, a.cd) * (uint32_t)a.c;
+    };
+    auto piece_of = [&](const float4 &x, uint32_t ch) {
+        const QChan q = TABLE ? s_q[ch] : qchan<BITS>(__ldg(a.gamma + ch), __ldg(a.beta + ch));
+        bool slow;
+        uint32_t p = quant4<BITS>(x, q, nclip, slow);
+        if (slow) p = quant4_exact<BITS>(x, __ldg(a.gamma + ch), __ldg(a.beta + ch), &nclip);
+        return p;
+    };
+    for (int64_t base = warp * (32 * kSlots); base < nf4; base += nwarps * (32 * kSlots)) {
+        float4 xq[kSlots];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            if (gs[u] < ngroups) {
-                const float4 *src = reinterpret_cast<const float4 *>(a.x) + 2 * gs[u];
-                xa[u] = __ldcs(src);
-                xb[u] = __ldcs(src + 1);
-            }
+        for (int i = 0; i < kSlots; ++i)
+            if (base + 32 * i < nf4) xq[i] = __ldcs(reinterpret_cast<const float4 *>(a.x) + base + 32 * i + lane);
+#pragma unroll
+        for (int i = 0; i < kSlots; ++i) {
+            if (base + 32 * i >= nf4) break;                 // warp-uniform
+            const int64_t f = base + 32 * i + lane;
+            store_code_piece<BITS>(a.codes, f, piece_of(xq[i], chan_of(f >> 1)));
         }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int64_t gg = gs[u];
-            if (gg >= ngroups) break;
-            const uint32_t plane = fast_div((uint32_t)gg, a.hw8d);
-            const uint32_t ch = plane - fast_div(plane, a.cd) * (uint32_t)a.c;
-            const ChanCode cc = chan_code(__ldg(a.gamma + ch), __ldg(a.beta + ch), BITS);
-            BnConst k;
-            k.scale = cc.scale;
-            k.step = cc.step;
-            k.off = cc.off;
-            k.s1 = __double2float_rn(cc.scale);
-            k.s2 = __double2float_rn(cc.scale - (double)k.s1);
-            const float xv[8] = {xa[u].x, xa[u].y, xa[u].z, xa[u].w, xb[u].x, xb[u].y, xb[u].z, xb[u].w};
-            uint32_t code[8], clipmask;
-            quant8<BITS>(xv, k, code, clipmask);
-            if (CLIP) clip += __popc(clipmask);
-            uint8_t *dst = a.codes + gg * BITS;
-            if (BITS == 8) {
-                uint64_t word = 0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) word |= (uint64_t)code[j] << (j * 8);
-                *reinterpret_cast<uint2 *>(dst) = make_uint2((uint32_t)word, (uint32_t)(word >> 32));
-            } else {
-                uint32_t w32 = 0;
-#pragma unroll
-                for (int j = 0; j < 8; ++j) w32 |= code[j] << (j * BITS);
-                if (BITS == 4) *reinterpret_cast<uint32_t *>(dst) = w32;
-                else if (BITS == 2) *reinterpret_cast<uint16_t *>(dst) = (uint16_t)w32;
-                else *dst = (uint8_t)w32;
-            }
+    }
+    const int64_t g_tail = nf4 >> 1, ngroups = a.numel >> 3;
+    for (int64_t gg = g_tail + tid; gg < ngroups; gg += (int64_t)gridDim.x * kThreads) {
+        const float4 *src = reinterpret_cast<const float4 *>(a.x) + 2 * gg;
+        const uint32_t ch = chan_of(gg);
+        const uint32_t p0 = piece_of(src[0], ch), p1 = piece_of(src[1], ch);
+        uint8_t *dst = a.codes + gg * BITS;
+        if (BITS == 8) {
+            *reinterpret_cast<uint2 *>(dst) = make_uint2(p0, p1);
+        } else {
+            const uint32_t w = p0 | (p1 << (4 * BITS));
+            if (BITS == 4) *reinterpret_cast<uint32_t *>(dst) = w;
+            else if (BITS == 2) *reinterpret_cast<uint16_t *>(dst) = (uint16_t)w;
+            else *dst = (uint8_t)w;
         }
     }
     if (CLIP) {
         __shared__ unsigned long long s_clip[kThreads / 32];
-        clip = warp_sum(clip);
+        unsigned long long clip = warp_sum((unsigned long long)nclip);
         if ((threadIdx.x & 31) == 0) s_clip[threadIdx.x >> 5] = clip;
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -538,50 +661,130 @@ __global__ void __launch_bounds__(kThreads) quant_pack_stream(FwdArgs a) {
     }
 }
 
+// Blocks that are co-resident for `kern` (one wave of a grid-stride kernel).
+template <typename K>
+static int64_t resident_blocks(K kern) {
+    int nb = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&nb, kern, kThreads, 0) != cudaSuccess || nb < 1)
+        nb = 1;
+    return (int64_t)nb * qt_sm_count();
+}
+
 // Unpack + dequantize (codec.dequantize, codec.py:146-156) as a streaming
-// kernel: 8 codes -> 8 fp32 (two float4 stores) per group; decode in float64
-// exactly as the reference (step * ((code + (0.5 - 2^(K-1))) + offset)).
+// kernel: 8 codes -> 8 fp32 (two float4 stores) per group.
+// The reference rounds step * z (z = code + 0.5 - 2^(K-1) + offset, exact)
+// to float64 and then to float32.  step = 6 |gamma| 2^-K has at most 26
+// significant bits (|gamma| a float32 >= 1e-8) and |z| < 2^20 at most 21,
+// so step * z is exact in float64 and the reference value is simply
+// fl32(step * z).  With step = sh + sl (sh = fl32(step), sl the <= 2-bit
+// rest), sl * z is exact in fp32 and fma(sh, z, sl * z) rounds the exact
+// product once: bit-identical, in four fp32 ops.  Channels that do not meet
+// the conditions (floored gamma, |offset| >= 2^19) decode in float64.
+struct DChan {
+    float sh, sl, zc;   // zc = offset + 0.5 - 2^(K-1)
+    int ok;
+};
+
 template <int BITS>
+__device__ __forceinline__ DChan dec_consts(double st, int64_t of) {
+    DChan d;
+    d.sh = __double2float_rn(st);
+    d.sl = __double2float_rn(st - (double)d.sh);
+    // sh + sl == step, sl <= 3 significant bits within 2^-27 of sh: step spans
+    // <= 30 bits, so step * z (|z| < 2^20) is exact in float64
+    const bool exact = ((double)d.sh + (double)d.sl == st) &&
+                       ((__float_as_uint(d.sl) & 0x1FFFFFu) == 0u) && isfinite(st) && st > 0.0 &&
+                       (d.sl == 0.f || fabsf(d.sl) >= __fmul_rn(d.sh, 7.450580596923828e-09f));
+    d.ok = exact && of > -(1ll << 19) && of < (1ll << 19);
+    d.zc = d.ok ? (float)((double)of + (0.5 - (double)(1 << (BITS - 1)))) : 0.f;
+    return d;
+}
+
+constexpr int kDecTable = 1024;
+
+// 4 codes (4K bits) of one channel -> 4 fp32 values
+template <int BITS, bool TABLE>
+__device__ __forceinline__ float4 dequant4(const DecArgs &a, const DChan *s_d, uint32_t ch,
+                                           uint32_t piece) {
+    float v[4];
+    const DChan d = TABLE ? s_d[ch] : dec_consts<BITS>(__ldg(a.step + ch), __ldg(a.offset + ch));
+    if (d.ok) {
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t code = (piece >> (j * BITS)) & ((1u << BITS) - 1u);
+            const float z = __fadd_rn((float)code, d.zc);        // exact
+            const float y = __fmaf_rn(d.sh, z, __fmul_rn(d.sl, z));
+            v[j] = a.relu ? fmaxf(y, 0.f) : y;                   // y is never 0 or NaN
+        }
+    } else {
+        const double st = __ldg(a.step + ch);
+        const int64_t of = __ldg(a.offset + ch);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const float dd = decode((piece >> (j * BITS)) & ((1u << BITS) - 1u), st, of, BITS);
+            v[j] = a.relu ? relu_np(dd) : dd;
+        }
+    }
+    return make_float4(v[0], v[1], v[2], v[3]);
+}
+
+// Lane-interleaved like quant_pack_stream: slot i of lane l is float4
+// 32 i + l of the warp's 256-float4 run, so every store instruction writes
+// one contiguous 512-byte run; a lane loads the 32-bit code word holding its
+// 4 codes (shared with 8/K - 1 neighbours: one contiguous code run per warp).
+template <int BITS, bool TABLE>
 __global__ void __launch_bounds__(kThreads) dequant_stream(DecArgs a, FastDiv hw8d, FastDiv cd) {
     pdl_enter();
+    __shared__ DChan s_d[TABLE ? kDecTable : 1];
+    if (TABLE) {
+        for (int c = threadIdx.x; c < a.c; c += kThreads)
+            s_d[c] = dec_consts<BITS>(__ldg(a.step + c), __ldg(a.offset + c));
+        __syncthreads();
+    }
+    const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    const int64_t nf4 = (a.numel >> 7) << 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = tid >> 5, nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+    auto chan_of = [&](int64_t gg) {
+        const uint32_t plane = fast_div((uint32_t)gg, hw8d);
+        return plane - fast_div(plane, cd) * (uint32_t)a.c;
+    };
+    constexpr int lpw = BITS == 8 ? 1 : 8 / BITS;
+    const uint32_t *cw = reinterpret_cast<const uint32_t *>(a.codes);
+    for (int64_t base = warp * (32 * kSlots); base < nf4; base += nwarps * (32 * kSlots)) {
+        uint32_t word[kSlots];
+#pragma unroll
+        for (int i = 0; i < kSlots; ++i) {
+            const int64_t f = base + 32 * i + lane;
+            if (base + 32 * i < nf4) word[i] = __ldcs(cw + ((f * 4 * BITS) >> 5));
+        }
+#pragma unroll
+        for (int i = 0; i < kSlots; ++i) {
+            if (base + 32 * i >= nf4) break;
+            const int64_t f = base + 32 * i + lane;
+            const uint32_t piece = BITS == 8 ? word[i] : (word[i] >> (((lane & (lpw - 1)) * 4 * BITS) & 31));
+            __stcs(reinterpret_cast<float4 *>(a.out) + f,
+                   dequant4<BITS, TABLE>(a, s_d, chan_of(f >> 1), piece));
+        }
+    }
     const int64_t ngroups = a.numel >> 3;
-    const int64_t stride = (int64_t)gridDim.x * kThreads;
-    for (int64_t g0 = (int64_t)blockIdx.x * kThreads + threadIdx.x; g0 < ngroups; g0 += 2 * stride) {
-        const int64_t gs[2] = {g0, g0 + stride};
-        uint64_t words[2] = {0, 0};
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            if (gs[u] >= ngroups) continue;
-            const uint8_t *src = a.codes + gs[u] * BITS;
-            if (BITS == 8) {
-                const uint2 w = __ldcs(reinterpret_cast<const uint2 *>(src));
-                words[u] = w.x | ((uint64_t)w.y << 32);
-            } else if (BITS == 4) {
-                words[u] = __ldcs(reinterpret_cast<const unsigned int *>(src));
-            } else if (BITS == 2) {
-                words[u] = __ldcs(reinterpret_cast<const unsigned short *>(src));
-            } else {
-                words[u] = __ldcs(reinterpret_cast<const unsigned char *>(src));
-            }
+    for (int64_t gg = (nf4 >> 1) + tid; gg < ngroups; gg += (int64_t)gridDim.x * kThreads) {
+        const uint8_t *src = a.codes + gg * BITS;
+        uint64_t w;
+        if (BITS == 8) {
+            const uint2 u = *reinterpret_cast<const uint2 *>(src);
+            w = u.x | ((uint64_t)u.y << 32);
+        } else if (BITS == 4) {
+            w = *reinterpret_cast<const unsigned int *>(src);
+        } else if (BITS == 2) {
+            w = *reinterpret_cast<const unsigned short *>(src);
+        } else {
+            w = *src;
         }
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-            const int64_t gg = gs[u];
-            if (gg >= ngroups) break;
-            const uint32_t plane = fast_div((uint32_t)gg, hw8d);
-            const uint32_t ch = plane - fast_div(plane, cd) * (uint32_t)a.c;
-            const double st = __ldg(a.step + ch);
-            const int64_t of = __ldg(a.offset + ch);
-            float v[8];
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const float d = decode((uint32_t)(words[u] >> (j * BITS)) & ((1u << BITS) - 1u), st, of, BITS);
-                v[j] = a.relu ? relu_np(d) : d;
-            }
-            float4 *dst = reinterpret_cast<float4 *>(a.out) + 2 * gg;
-            __stcs(dst, make_float4(v[0], v[1], v[2], v[3]));
-            __stcs(dst + 1, make_float4(v[4], v[5], v[6], v[7]));
-        }
+        const uint32_t ch = chan_of(gg);
+        float4 *dst = reinterpret_cast<float4 *>(a.out) + 2 * gg;
+        dst[0] = dequant4<BITS, TABLE>(a, s_d, ch, (uint32_t)(w & ((1ull << (4 * BITS)) - 1)));
+        dst[1] = dequant4<BITS, TABLE>(a, s_d, ch, (uint32_t)(w >> (4 * BITS)));
     }
 }
 
@@ -644,20 +847,27 @@ static int launch_fwd(const FwdArgs &a0, bool apply_bn, cudaStream_t s) {
         (((uintptr_t)a.x) & 15) == 0 &&
         (a.numel >> 3) < (1ll << 31)) {   // quantize-pack from A2: the streaming form
         const int64_t ngroups = a.numel >> 3;
-        int64_t blocks = std::min<int64_t>(qt_cdiv(ngroups, 2 * kThreads), qt_sm_count() * 8);
-        blocks = std::max<int64_t>(blocks, qt_cdiv(a.c, kThreads));   // constants for every channel
-        const unsigned b = (unsigned)std::max<int64_t>(blocks, 1);
         const bool clip = a.clip_count != nullptr;
+        const bool table = a.c <= kQuantTable;
+        // one wave of co-resident blocks, 4 groups per thread per iteration
+#define QT_QK(B, C, T) quant_pack_stream<B, C, T>
+#define QT_QL(B, C, T)                                                                        \
+    launch_pdl(QT_QK(B, C, T),                                                                \
+               (unsigned)std::max<int64_t>(1, std::min<int64_t>(qt_cdiv(ngroups, 4 * kThreads),     \
+                                                                resident_blocks(QT_QK(B, C, T)))), \
+               kThreads, 0, s, a)
+#define QT_QP(B)                                                                              \
+    (table ? (clip ? QT_QL(B, true, true) : QT_QL(B, false, true))                          \
+           : (clip ? QT_QL(B, true, false) : QT_QL(B, false, false)))
         switch (a.bits) {
-            case 1: clip ? launch_pdl(quant_pack_stream<1, true>, b, kThreads, 0, s, a)
-                         : launch_pdl(quant_pack_stream<1, false>, b, kThreads, 0, s, a); break;
-            case 2: clip ? launch_pdl(quant_pack_stream<2, true>, b, kThreads, 0, s, a)
-                         : launch_pdl(quant_pack_stream<2, false>, b, kThreads, 0, s, a); break;
-            case 4: clip ? launch_pdl(quant_pack_stream<4, true>, b, kThreads, 0, s, a)
-                         : launch_pdl(quant_pack_stream<4, false>, b, kThreads, 0, s, a); break;
-            case 8: clip ? launch_pdl(quant_pack_stream<8, true>, b, kThreads, 0, s, a)
-                         : launch_pdl(quant_pack_stream<8, false>, b, kThreads, 0, s, a); break;
+            case 1: QT_QP(1); break;
+            case 2: QT_QP(2); break;
+            case 4: QT_QP(4); break;
+            case 8: QT_QP(8); break;
         }
+#undef QT_QP
+#undef QT_QL
+#undef QT_QK
         QT_CHECK_LAUNCH();
         return QT_OK;
     }
@@ -747,15 +957,23 @@ extern "C" int qt_unpack_dequant(const uint8_t *codes, int64_t n, int64_t c, int
     if ((hw & 7) == 0 && hw < (1ll << 31) && c < (1ll << 31) && (((uintptr_t)out) & 15) == 0 &&
         (d.numel >> 3) < (1ll << 31)) {   // the streaming form
         const int64_t ngroups = d.numel >> 3;
-        const unsigned b = (unsigned)std::max<int64_t>(
-            std::min<int64_t>(qt_cdiv(ngroups, 2 * kThreads), qt_sm_count() * 8), 1);
         const FastDiv hw8d = make_fastdiv((uint32_t)(hw >> 3)), cd = make_fastdiv((uint32_t)c);
+        const bool table = c <= kDecTable;
+        // one wave of co-resident blocks, 4 groups per thread per iteration
+#define QT_DL(B, T)                                                                           \
+    launch_pdl(dequant_stream<B, T>,                                                          \
+               (unsigned)std::max<int64_t>(1, std::min<int64_t>(qt_cdiv(ngroups, 4 * kThreads),     \
+                                                                resident_blocks(dequant_stream<B, T>))), \
+               kThreads, 0, qt_s(stream), d, hw8d, cd)
+#define QT_DQ(B) (table ? QT_DL(B, true) : QT_DL(B, false))
         switch (bits) {
-            case 1: launch_pdl(dequant_stream<1>, b, kThreads, 0, qt_s(stream), d, hw8d, cd); break;
-            case 2: launch_pdl(dequant_stream<2>, b, kThreads, 0, qt_s(stream), d, hw8d, cd); break;
-            case 4: launch_pdl(dequant_stream<4>, b, kThreads, 0, qt_s(stream), d, hw8d, cd); break;
-            case 8: launch_pdl(dequant_stream<8>, b, kThreads, 0, qt_s(stream), d, hw8d, cd); break;
+            case 1: QT_DQ(1); break;
+            case 2: QT_DQ(2); break;
+            case 4: QT_DQ(4); break;
+            case 8: QT_DQ(8); break;
         }
+#undef QT_DQ
+#undef QT_DL
         QT_CHECK_LAUNCH();
         return QT_OK;
     }
