@@ -796,10 +796,122 @@ __global__ void __launch_bounds__(kThreads) dequant_stream(DecArgs a, FastDiv hw
     }
 }
 
+// Fused K1 (approx tapes, hw % 8 == 0, C <= kQuantTable) in the
+// lane-interleaved layout of dequant_stream: every x load and A3 store of a
+// warp is one contiguous 512-byte run; the per-channel BN and code constants
+// come from a shared table (one block prologue); the codes of a float4 go
+// through quant4 and store_code_piece.  Bit-identical to bn_relu_quant_stream.
+struct K1Chan {
+    float m32, inv32, g, b;   // BN apply (layer.py:246-249)
+    QChan q;                   // codes
+};
+
+template <int BITS, bool CLIP>
+__global__ void __launch_bounds__(kThreads) bn_relu_quant_lanes(FwdArgs a) {
+    pdl_enter();
+    __shared__ K1Chan s_k[kQuantTable];
+    for (int c = threadIdx.x; c < a.c; c += kThreads) {
+        const BnConst k = a.consts[c];
+        const QuantK qk = quant_consts<BITS>(k.s1, k.scale, k.off);
+        s_k[c] = K1Chan{k.m32, k.inv32, k.g, k.b,
+                        QChan{qk.s1, qk.cf, __fsub_rn(0.5f, qk.marg), qk.ok ? (int)k.off : INT_MIN}};
+    }
+    __syncthreads();
+    const int64_t tid = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    const int64_t nf4 = (a.numel >> 7) << 5;
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = tid >> 5, nwarps = ((int64_t)gridDim.x * kThreads) >> 5;
+    uint32_t nclip = 0;
+    auto chan_of = [&](int64_t gg) {
+        const uint32_t plane = fast_div((uint32_t)gg, a.hw8d);
+        return plane - fast_div(plane, a.cd) * (uint32_t)a.c;
+    };
+    // BN apply + ReLU of one float4 (A3 out) and its 4K-bit code piece
+    auto one = [&](const float4 &x, uint32_t ch, float4 &a3) {
+        const K1Chan k = s_k[ch];
+        const float xv[4] = {x.x, x.y, x.z, x.w};
+        float a2[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            float v = __fsub_rn(xv[j], k.m32);
+            v = __fmul_rn(v, k.inv32);
+            v = __fmul_rn(v, k.g);
+            a2[j] = __fadd_rn(v, k.b);
+        }
+        a3 = make_float4(relu_np(a2[0]), relu_np(a2[1]), relu_np(a2[2]), relu_np(a2[3]));
+        const float4 a24 = make_float4(a2[0], a2[1], a2[2], a2[3]);
+        bool slow;
+        uint32_t p = quant4<BITS>(a24, k.q, nclip, slow);
+        if (slow) p = quant4_exact<BITS>(a24, __ldg(a.gamma + ch), __ldg(a.beta + ch), &nclip);
+        return p;
+    };
+    constexpr int S = 4;
+    for (int64_t base = warp * (32 * S); base < nf4; base += nwarps * (32 * S)) {
+        float4 xq[S];
+#pragma unroll
+        for (int i = 0; i < S; ++i)
+            if (base + 32 * i < nf4) xq[i] = __ldg(reinterpret_cast<const float4 *>(a.x) + base + 32 * i + lane);
+#pragma unroll
+        for (int i = 0; i < S; ++i) {
+            if (base + 32 * i >= nf4) break;                 // warp-uniform
+            const int64_t f = base + 32 * i + lane;
+            float4 a3;
+            const uint32_t piece = one(xq[i], chan_of(f >> 1), a3);
+            reinterpret_cast<float4 *>(a.a3_out)[f] = a3;
+            store_code_piece<BITS>(a.codes, f, piece);
+        }
+    }
+    const int64_t ngroups = a.numel >> 3;
+    for (int64_t gg = (nf4 >> 1) + tid; gg < ngroups; gg += (int64_t)gridDim.x * kThreads) {
+        const float4 *src = reinterpret_cast<const float4 *>(a.x) + 2 * gg;
+        const uint32_t ch = chan_of(gg);
+        float4 a30, a31;
+        const uint32_t p0 = one(src[0], ch, a30), p1 = one(src[1], ch, a31);
+        reinterpret_cast<float4 *>(a.a3_out)[2 * gg] = a30;
+        reinterpret_cast<float4 *>(a.a3_out)[2 * gg + 1] = a31;
+        uint8_t *dst = a.codes + gg * BITS;
+        if (BITS == 8) {
+            *reinterpret_cast<uint2 *>(dst) = make_uint2(p0, p1);
+        } else {
+            const uint32_t w = p0 | (p1 << (4 * BITS));
+            if (BITS == 4) *reinterpret_cast<uint32_t *>(dst) = w;
+            else if (BITS == 2) *reinterpret_cast<uint16_t *>(dst) = (uint16_t)w;
+            else *dst = (uint8_t)w;
+        }
+    }
+    if (CLIP) {
+        __shared__ unsigned long long s_clip[kThreads / 32];
+        unsigned long long clip = warp_sum((unsigned long long)nclip);
+        if ((threadIdx.x & 31) == 0) s_clip[threadIdx.x >> 5] = clip;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            for (int w = 0; w < kThreads / 32; ++w) t += s_clip[w];
+            if (t) atomicAdd(a.clip_count, t);
+        }
+    }
+}
+
+// The lane-interleaved K1 pays a per-block table prologue: measured slower
+// on the C2 step's <= 8.4 M-element layers (1.19 vs 1.05 ms/step), so it is
+// used from QTAPE_K1_LANES elements up (default 2^24: ImageNet-sized layers).
+static bool lanes_k1(int64_t numel) {
+    static const int64_t v = qt_env_i64("QTAPE_K1_LANES", 1ll << 24);
+    return v > 0 && numel >= v;
+}
+
 template <int BITS>
 static void launch_stream(const FwdArgs &a, unsigned blocks, cudaStream_t s) {
     const bool clip = a.clip_count != nullptr;
     const bool h4 = (a.hw & 7) != 0;
+    if (!h4 && a.mode != MODE_NAIVE && a.c <= kQuantTable && !a.a2_tape && lanes_k1(a.numel)) {
+        const int64_t ngroups = a.numel >> 3;
+        auto kern = clip ? bn_relu_quant_lanes<BITS, true> : bn_relu_quant_lanes<BITS, false>;
+        const unsigned b = (unsigned)std::max<int64_t>(
+            1, std::min<int64_t>(qt_cdiv(ngroups, 4 * kThreads), resident_blocks(kern)));
+        launch_pdl(kern, b, kThreads, 0, s, a);
+        return;
+    }
 #define QT_ST(M, C)                                                                                 \
     (h4 ? launch_pdl(bn_relu_quant_stream<BITS, M, false, C, true>, blocks, kThreads, 0, s, a)       \
         : launch_pdl(bn_relu_quant_stream<BITS, M, false, C, false>, blocks, kThreads, 0, s, a))
