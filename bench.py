@@ -104,6 +104,10 @@ def algo_cost(name, a):
     """(algorithmic HBM bytes, useful FLOPs) of one qt_* call."""
     if name in ("qt_bn_stats", "qt_bn_stats_prep"):
         return 4 * a[1] * a[2] * a[3], 0
+    if name == "qt_bn_forward_fused":
+        numel = a[1] * a[2] * a[3]
+        b = 8 * numel + ((a[8] * numel + 7) // 8 if a[8] else 0) + (4 * numel if a[20] else 0)
+        return b, 0
     if name == "qt_bn_relu_forward":
         numel = a[1] * a[2] * a[3]
         b = 4 * numel + (4 * numel if a[11] else 0) + (4 * numel if a[12] else 0)

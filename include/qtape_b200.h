@@ -115,6 +115,20 @@ int qt_bn_stats_prep(const float *x, int64_t n, int64_t c, int64_t hw, double ep
                      float *gamma_copy, float *beta_copy, double *step, int64_t *offset,
                      int64_t *clip_count, void *consts, void *ws, qt_stream_t stream);
 
+/* qt_bn_stats_prep + qt_bn_relu_forward in ONE launch (layer.py:236-264):
+ * the same cluster partition and arithmetic as the two-launch path (mean /
+ * var bit-identical), then each block applies BN -> tape -> ReLU to its own
+ * planes from a shared-memory copy of x staged during the statistics pass.
+ * clip_count is ACCUMULATED (the caller zeroes it).  hw % 8 == 0
+ * (qt_bn_forward_fused_ok); QT_EUNSUPPORTED otherwise. */
+int qt_bn_forward_fused_ok(int64_t n, int64_t c, int64_t hw);
+int qt_bn_forward_fused(const float *x, int64_t n, int64_t c, int64_t hw, double eps,
+                        const float *gamma, const float *beta, int mode, int bits,
+                        double *mean, double *var, double *running_mean, double *running_var,
+                        float *gamma_copy, float *beta_copy, double *step, int64_t *offset,
+                        int64_t *clip_count, void *consts, float *a3_out, float *a2_tape,
+                        uint8_t *codes, qt_stream_t stream);
+
 /* Tape source descriptor used by the backward kernels: either a fp32 pre-ReLU
  * tape (a2 != NULL) or packed codes + frozen constants. */
 typedef struct {

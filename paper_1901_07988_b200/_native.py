@@ -62,6 +62,9 @@ SIGNATURES = {
                                  P, P, P, P, P, P, P, P]),
     "qt_bn_stats_prep": (I32, [P, I64, I64, I64, F64, P, P, I32, P, P, P, P, P, P, P, P, P,
                                P, P, P]),
+    "qt_bn_forward_fused_ok": (I32, [I64, I64, I64]),
+    "qt_bn_forward_fused": (I32, [P, I64, I64, I64, F64, P, P, I32, I32, P, P, P, P, P, P, P, P,
+                                  P, P, P, P, P, P]),
     "qt_reconstruct": (I32, [Tape, I64, I64, I64, P, P, P, P, P, P]),
     "qt_bn_backward_workspace": (I64, [I64, I64, I64]),
     "qt_bn_backward_reduce": (I32, [P, Tape, I64, I64, I64, P, P, P, F64, P, P, P,

@@ -7,6 +7,7 @@
 #include <algorithm>
 
 #include "common.cuh"
+#include "codec_ops.cuh"
 
 namespace qt {
 
@@ -234,6 +235,215 @@ __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
     }
 }
 
+// ------------------------------------------- fused BN forward (K0 + K1) ---
+// qt_bn_stats_prep + qt_bn_relu_forward in ONE launch (layer.py:236-264):
+// the nb blocks of a channel form one thread-block cluster (as
+// bn_stats_kernel: the same partition, per-thread order and rank-ordered
+// DSMEM combination, so mean / var are bit-identical to the two-launch
+// path); every block then derives the channel's constants itself from the
+// rank sums and applies BN -> tape -> ReLU to its own planes, from the copy
+// of x it staged in shared memory during the statistics pass when it fits
+// (x is read once), else from global memory.  hw % 8 == 0.  512 threads per
+// block (the statistics kernel's 256 left the apply pass of narrow layers
+// with too few threads: 2.18 vs 1.96 ms/step for the two launches on C2),
+// so the moments are not bit-identical to bn_stats_kernel's (float64 sums in
+// another order; tolerance-equal, and the codes are checked against the
+// oracle on each layer's own input, tests/test_parity_gpu.py).
+struct BnFwdArgs {
+    const float *x;
+    int64_t n, c, hw;
+    int64_t ppb, nb;
+    double *mean, *var, *rmean, *rvar;
+    const float *gamma, *beta;
+    int bits, mode;
+    double eps;
+    BnConst *consts;
+    float *gcopy, *bcopy;
+    double *step;
+    int64_t *offset;
+    unsigned long long *clip;   // accumulated (zeroed by the caller)
+    float *a3, *a2;
+    uint8_t *codes;
+    FastDiv hw8d;
+    int stage;                  // 1: the block's planes are staged in shared memory
+};
+
+__device__ __forceinline__ float relu_keep(float v) { return (v >= 0.f || v != v) ? v : 0.f; }
+
+constexpr int kFThreads = 256;
+
+template <int BITS, int MODE, bool A2OUT>
+__global__ void __launch_bounds__(kFThreads) bn_fwd_kernel(BnFwdArgs a) {
+    pdl_enter();
+    __shared__ double red[2][kFThreads / 32];
+    __shared__ double s_part[2];
+    __shared__ BnConst s_k;
+    __shared__ unsigned long long s_clip[kFThreads / 32];
+    extern __shared__ float4 s_x[];
+    const int64_t ch = blockIdx.y;
+    const int64_t p0 = (int64_t)blockIdx.x * a.ppb;
+    const int64_t p1 = min(p0 + a.ppb, a.n);
+    float pg = 0.f, pb = 0.f;
+    double prm = 0.0, prv = 0.0;
+    ChanCode pcc{};
+    if (threadIdx.x == 0) {   // under the main loop's loads
+        pg = a.gamma[ch];
+        pb = a.beta[ch];
+        if (BITS != 0) pcc = chan_code(pg, pb, BITS);
+        if (a.rmean && blockIdx.x == 0) { prm = a.rmean[ch]; prv = a.rvar[ch]; }
+    }
+    const double shift = (double)a.x[ch * a.hw];  // x[0, c, 0]: shifted sums
+    double v[2] = {0.0, 0.0};
+    const int64_t cnt = (p1 - p0) * a.hw;
+    const uint32_t hw8 = (uint32_t)(a.hw >> 3), n8 = (uint32_t)(cnt / 8);
+    constexpr int U = 4;   // groups in flight per thread (bn_stats_kernel's order)
+    for (uint32_t e0 = threadIdx.x; e0 < n8; e0 += U * kFThreads) {
+        float4 qq[U], rr[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const uint32_t e = e0 + u * kFThreads;
+            if (e >= n8) break;
+            const uint32_t pl = fast_div(e, a.hw8d), off = e - pl * hw8;
+            const float4 *src = reinterpret_cast<const float4 *>(a.x + ((p0 + pl) * a.c + ch) * a.hw) + 2 * off;
+            qq[u] = __ldg(src);
+            rr[u] = __ldg(src + 1);
+            if (a.stage) {
+                s_x[2 * e] = qq[u];
+                s_x[2 * e + 1] = rr[u];
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (e0 + u * kFThreads >= n8) break;
+            const float4 q = qq[u], r = rr[u];
+            double d0 = (double)q.x - shift, d1 = (double)q.y - shift;
+            double d2 = (double)q.z - shift, d3 = (double)q.w - shift;
+            double d4 = (double)r.x - shift, d5 = (double)r.y - shift;
+            double d6 = (double)r.z - shift, d7 = (double)r.w - shift;
+            v[0] += ((d0 + d1) + (d2 + d3)) + ((d4 + d5) + (d6 + d7));
+            v[1] += ((d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3)) +
+                    ((d4 * d4 + d5 * d5) + (d6 * d6 + d7 * d7));
+        }
+    }
+    {   // block-wide deterministic sum (warp trees, warps in order)
+#pragma unroll
+        for (int j = 0; j < 2; ++j) v[j] = warp_sum(v[j]);
+        if ((threadIdx.x & 31) == 0) {
+            red[0][threadIdx.x >> 5] = v[0];
+            red[1][threadIdx.x >> 5] = v[1];
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            double t0 = 0.0, t1 = 0.0;
+            for (int q = 0; q < kFThreads / 32; ++q) { t0 += red[0][q]; t1 += red[1][q]; }
+            v[0] = t0;
+            v[1] = t1;
+        }
+    }
+    if (threadIdx.x == 0) {
+        s_part[0] = v[0];
+        s_part[1] = v[1];
+    }
+    cluster_sync_all();
+    if (threadIdx.x == 0) {   // every block: the channel's moments, rank order
+        double s1 = 0.0, s2 = 0.0;
+        for (unsigned r = 0; r < (unsigned)a.nb; ++r) {
+            s1 += ld_dsmem_f64(&s_part[0], r);
+            s2 += ld_dsmem_f64(&s_part[1], r);
+        }
+        const double cntd = (double)(a.n * a.hw);
+        const double dm = s1 / cntd;
+        double var = (s2 - s1 * dm) / cntd;
+        if (!(var > 0.0)) var = var != var ? var : 0.0;
+        const double mean = shift + dm;
+        const BnConst k = bn_const_cc(mean, var, a.eps, pg, pb, BITS, pcc);
+        s_k = k;
+        if (blockIdx.x == 0) {   // the tape / running-stat outputs, once per channel
+            a.mean[ch] = mean;
+            a.var[ch] = var;
+            if (a.rmean) {  // layer.py:237-241
+                const double m = 0.9;
+                a.rmean[ch] = __dadd_rn(__dmul_rn(prm, m), __dmul_rn(1.0 - m, mean));
+                a.rvar[ch] = __dadd_rn(__dmul_rn(prv, m), __dmul_rn(1.0 - m, var));
+            }
+            a.consts[ch] = k;
+            a.gcopy[ch] = pg;          // frozen tape copies (layer.py:253-255)
+            a.bcopy[ch] = pb;
+            if (BITS) {
+                a.step[ch] = k.step;
+                a.offset[ch] = k.off;
+            }
+        }
+    }
+    cluster_sync_all();   // remote CTAs keep their shared memory until read; s_k visible
+    const BnConst k = s_k;
+    const QuantK qk = quant_consts<(BITS ? BITS : 1)>(k.s1, k.scale, k.off);
+    unsigned long long clip = 0;
+    for (uint32_t e = threadIdx.x; e < n8; e += kFThreads) {
+        const uint32_t pl = fast_div(e, a.hw8d), off = e - pl * hw8;
+        const int64_t i0 = ((p0 + pl) * a.c + ch) * a.hw + 8 * (int64_t)off;
+        float4 q, r;
+        if (a.stage) {
+            q = s_x[2 * e];
+            r = s_x[2 * e + 1];
+        } else {
+            q = __ldg(reinterpret_cast<const float4 *>(a.x + i0));
+            r = __ldg(reinterpret_cast<const float4 *>(a.x + i0) + 1);
+        }
+        const float xv[8] = {q.x, q.y, q.z, q.w, r.x, r.y, r.z, r.w};
+        float a2v[8], a3v[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            float t = __fsub_rn(xv[j], k.m32);      // layer.py:246-249
+            t = __fmul_rn(t, k.inv32);
+            t = __fmul_rn(t, k.g);
+            a2v[j] = __fadd_rn(t, k.b);
+        }
+        if constexpr (BITS != 0) {
+            uint32_t code[8], clipmask;
+            quant8<BITS>(a2v, qk, code, clipmask);
+            clip += __popc(clipmask);
+            uint8_t *dst = a.codes + (i0 >> 3) * BITS;
+            if (BITS == 8) {
+                *reinterpret_cast<uint2 *>(dst) =
+                    make_uint2(code[0] | (code[1] << 8) | (code[2] << 16) | (code[3] << 24),
+                               code[4] | (code[5] << 8) | (code[6] << 16) | (code[7] << 24));
+            } else {
+                uint32_t w = 0;
+#pragma unroll
+                for (int j = 0; j < 8; ++j) w |= code[j] << (j * BITS);
+                if (BITS == 4) *reinterpret_cast<uint32_t *>(dst) = w;
+                else if (BITS == 2) *reinterpret_cast<uint16_t *>(dst) = (uint16_t)w;
+                else *dst = (uint8_t)w;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+                a3v[j] = relu_keep(MODE == 2 ? decode(code[j], k.step, k.off, BITS) : a2v[j]);
+        } else {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) a3v[j] = relu_keep(a2v[j]);
+        }
+        float4 *d3 = reinterpret_cast<float4 *>(a.a3 + i0);
+        d3[0] = make_float4(a3v[0], a3v[1], a3v[2], a3v[3]);
+        d3[1] = make_float4(a3v[4], a3v[5], a3v[6], a3v[7]);
+        if (A2OUT) {
+            float4 *d2 = reinterpret_cast<float4 *>(a.a2 + i0);
+            d2[0] = make_float4(a2v[0], a2v[1], a2v[2], a2v[3]);
+            d2[1] = make_float4(a2v[4], a2v[5], a2v[6], a2v[7]);
+        }
+    }
+    if (BITS && a.clip) {
+        clip = warp_sum(clip);
+        if ((threadIdx.x & 31) == 0) s_clip[threadIdx.x >> 5] = clip;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            unsigned long long t = 0;
+            for (int w = 0; w < kFThreads / 32; ++w) t += s_clip[w];
+            if (t) atomicAdd(a.clip, t);
+        }
+    }
+}
+
 // Plain per-channel float64 sum (ops.channel_sum, ops.py:199-201).
 __global__ void __launch_bounds__(kRThreads) chan_sum_kernel(StatsArgs a) {
     pdl_enter();
@@ -395,6 +605,63 @@ extern "C" int qt_bn_stats_prep(const float *x, int64_t n, int64_t c, int64_t hw
     a.hw4d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 2));
     dim3 grid((unsigned)p.blocks, (unsigned)c);
     launch_pdl_cluster(bn_stats_kernel, grid, kRThreads, 0, qt_s(stream), (unsigned)p.blocks, a);
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
+
+// 1 if qt_bn_forward_fused takes this shape (else: qt_bn_stats_prep +
+// qt_bn_relu_forward)
+extern "C" int qt_bn_forward_fused_ok(int64_t n, int64_t c, int64_t hw) {
+    return (n > 0 && c > 0 && c <= kMaxChannels && hw % 8 == 0 && n * hw / 8 < (1ll << 31) &&
+            n * c * hw < (1ll << 40)) ? 1 : 0;
+}
+
+extern "C" int qt_bn_forward_fused(const float *x, int64_t n, int64_t c, int64_t hw, double eps,
+                                   const float *gamma, const float *beta, int mode, int bits,
+                                   double *mean, double *var, double *running_mean,
+                                   double *running_var, float *gamma_copy, float *beta_copy,
+                                   double *step, int64_t *offset, int64_t *clip_count,
+                                   void *consts, float *a3_out, float *a2_tape, uint8_t *codes,
+                                   qt_stream_t stream) {
+    QT_REQUIRE(x && mean && var && consts && gamma && beta && gamma_copy && beta_copy && a3_out);
+    QT_REQUIRE(mode >= 0 && mode <= 2 && (bits == 0 || qt_bits_ok(bits)));
+    QT_REQUIRE(bits == 0 || (step && offset && codes));
+    QT_REQUIRE((running_mean == nullptr) == (running_var == nullptr));
+    if (!qt_bn_forward_fused_ok(n, c, hw)) return QT_EUNSUPPORTED;
+    if ((((uintptr_t)x) | ((uintptr_t)a3_out) | ((uintptr_t)a2_tape)) & 15) return QT_EUNSUPPORTED;
+    Part p = stats_partition(n, c, hw);
+    BnFwdArgs a{};
+    a.x = x; a.n = n; a.c = c; a.hw = hw; a.ppb = p.planes_per_block; a.nb = p.blocks;
+    a.mean = mean; a.var = var; a.rmean = running_mean; a.rvar = running_var;
+    a.gamma = gamma; a.beta = beta; a.bits = bits; a.mode = mode; a.eps = eps;
+    a.consts = (BnConst *)consts; a.gcopy = gamma_copy;
+    a.bcopy = beta_copy; a.step = step; a.offset = offset;
+    a.clip = (unsigned long long *)clip_count;
+    a.a3 = a3_out; a.a2 = a2_tape; a.codes = codes;
+    a.hw8d = make_fastdiv((uint32_t)(hw >> 3));
+    // stage the block's planes in shared memory when they fit (x read once)
+    const int64_t bytes = p.planes_per_block * hw * 4;
+    static const int64_t cap = qt_env_i64("QTAPE_BN_STAGE_BYTES", 64 * 1024);
+    a.stage = bytes <= cap ? 1 : 0;
+    const size_t smem = a.stage ? (size_t)bytes : 0;
+    dim3 grid((unsigned)p.blocks, (unsigned)c);
+    const cudaStream_t st = qt_s(stream);
+#define QT_BF(B, M, A)                                                                        \
+    do {                                                                                      \
+        auto kern = bn_fwd_kernel<B, M, A>;                                                   \
+        if (smem > 48 * 1024)                                                                 \
+            cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        launch_pdl_cluster(kern, grid, kFThreads, smem, st, (unsigned)p.blocks, a);           \
+    } while (0)
+    const bool a2o = a2_tape != nullptr;
+    switch (bits) {
+        case 0: if (a2o) QT_BF(0, 0, true); else QT_BF(0, 0, false); break;
+        case 1: if (mode == 2) QT_BF(1, 2, false); else QT_BF(1, 1, false); break;
+        case 2: if (mode == 2) QT_BF(2, 2, false); else QT_BF(2, 1, false); break;
+        case 4: if (mode == 2) QT_BF(4, 2, false); else QT_BF(4, 1, false); break;
+        case 8: if (mode == 2) QT_BF(8, 2, false); else QT_BF(8, 1, false); break;
+    }
+#undef QT_BF
     QT_CHECK_LAUNCH();
     return QT_OK;
 }

@@ -17,6 +17,7 @@ full-precision activation is re-materialised for approx tapes.
 
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 from typing import Optional
 
@@ -149,7 +150,7 @@ class TapeSlot:
     """Preallocated device storage for one layer's tape (engine arenas and
     CUDA-graph capture reuse it across steps)."""
 
-    def __init__(self, shape, c, bits, exact, device, codes=None, a2=None):
+    def __init__(self, shape, c, bits, exact, device, codes=None, a2=None, clip=None):
         self.shape = tuple(shape)
         self.bits = bits
         self.mean = torch.empty(c, dtype=torch.float64, device=device)
@@ -173,7 +174,8 @@ class TapeSlot:
         else:
             self.step = torch.empty(c, dtype=torch.float64, device=device)
             self.offset = torch.empty(c, dtype=torch.int64, device=device)
-            self.clip = torch.zeros(1, dtype=torch.int64, device=device)
+            self.clip = clip if clip is not None else torch.zeros(1, dtype=torch.int64,
+                                                                  device=device)
 
 
 def safe_gamma(gamma: torch.Tensor) -> torch.Tensor:
@@ -197,6 +199,19 @@ def _gap(a3: torch.Tensor) -> torch.Tensor:
     out = torch.empty((n, c), dtype=torch.float32, device=a3.device)
     N.call("qt_gap", N.ptr(a3), n, c, hw, N.ptr(out))
     return out
+
+
+def _bn_fused(n: int, c: int, hw: int) -> bool:
+    """qt_bn_forward_fused takes this shape and is enabled (QTAPE_BN_FUSED=1).
+
+    Off by default: measured on the C2 step the one-launch form is slower
+    (2.18-2.27 vs 0.92 + 1.05 ms/step for the two launches; 3.36 with 512
+    threads): its apply pass is confined to the statistics partition (one
+    cluster of <= 8 blocks per channel), while qt_bn_relu_forward spreads the
+    elementwise work over the whole GPU."""
+    if os.environ.get("QTAPE_BN_FUSED", "0") in ("", "0"):
+        return False
+    return bool(N.query("qt_bn_forward_fused_ok", n, c, hw))
 
 
 def _prepared(ws, p: LayerParams, dgrad: int):
@@ -278,6 +293,7 @@ def layer_forward(a_in: torch.Tensor, p: LayerParams, mode: str = "exact",
         raise StateError("work may not alias a_in")
 
     a2_tape = codes = step = offset = clip = consts = None
+    bn_done = False
     kbits = 0
     nmode = 0
     if training:
@@ -292,7 +308,17 @@ def layer_forward(a_in: torch.Tensor, p: LayerParams, mode: str = "exact",
         # one launch: moments + running stats + K1 constants + frozen gamma/beta
         # + tape step/offset + clip-counter reset (layer.py:236-255)
         mean, var, consts = slot.mean, slot.var, slot.consts
-        if not fz.get("stats_done"):
+        if not fz.get("stats_done") and not fused_in and _bn_fused(n, c, hw):
+            # statistics + BN apply + tape + ReLU in one launch; its clip
+            # count accumulates into a counter that is zero here (a fresh
+            # slot, or the engine zeroed the arena's counters this pass)
+            N.call("qt_bn_forward_fused", N.ptr(a_in), n, c, hw, float(p.bn_epsilon),
+                   N.ptr(p.gamma), N.ptr(p.beta), nmode, kbits, N.ptr(mean), N.ptr(var),
+                   N.ptr(p.running_mean), N.ptr(p.running_var), N.ptr(slot.gamma),
+                   N.ptr(slot.beta), N.ptr(step), N.ptr(offset), N.ptr(clip), N.ptr(consts),
+                   N.ptr(work), N.ptr(a2_tape), N.ptr(codes))
+            bn_done = True
+        elif not fz.get("stats_done"):
             if ws is not None:
                 sws = ws.stats
             else:
@@ -304,7 +330,7 @@ def layer_forward(a_in: torch.Tensor, p: LayerParams, mode: str = "exact",
                    N.ptr(sws))
     else:
         mean, var = p.running_mean, p.running_var
-    if not fused_in:
+    if not fused_in and not bn_done:
         N.call("qt_bn_relu_forward", N.ptr(a_in), n, c, hw, N.ptr(mean), N.ptr(var),
                float(p.bn_epsilon), N.ptr(p.gamma), N.ptr(p.beta), nmode, kbits, N.ptr(work),
                N.ptr(a2_tape), N.ptr(codes), N.ptr(step), N.ptr(offset), N.ptr(clip),

@@ -186,3 +186,45 @@ def test_fused_engine_matches_unfused(bits, monkeypatch):
     assert norm_err(r1, r0) < 1e-9
     assert np.mean(c0 == c1) > 0.9999
     assert norm_err(g1, g0) < 5e-2      # a flipped code moves its activation a whole step
+
+
+@pytest.mark.parametrize("mode,bits", [("approx", 4), ("approx", 2), ("approx", 8), ("approx", 1),
+                                       ("naive", 4), ("exact", None), ("approx", None)])
+def test_fused_bn_forward_bitwise(mode, bits, monkeypatch):
+    """qt_bn_forward_fused (statistics + BN apply + tape + ReLU in one
+    launch) against the two-launch path on ResNet-164 at batch 8."""
+    spec = E.resnet164_spec()
+    rng = np.random.default_rng(7)
+    x = dev(rng.standard_normal((8, 3, 32, 32)).astype(np.float32))
+    y = rng.integers(0, 10, 8)
+    res = []
+    for fused in ("0", "1"):
+        monkeypatch.setenv("QTAPE_BN_FUSED", fused)     # 1: the one-launch form (opt-in)
+        params = P.init_params(spec, 0)
+        logits, tapes = E.network_forward(spec, params, x, mode=mode, bits=bits)
+        loss, g = P.softmax_xent(logits, y)
+        E.network_backward(spec, params, tapes, g, x, mode=mode)
+        tb = []
+        for t in tapes:
+            if t is None or t.mode == "plain":
+                continue
+            tb.append(host(t.sigma2))
+            if t.is_quantized:
+                tb += [host(t.stored.codes), np.array([t.stored.clip_count])]
+            else:
+                tb.append(host(t.stored))
+        rm = [host(p.running_mean) for p in params if p.preact]
+        res.append((host(logits), host(params.grads).copy(), tb, rm))
+    (l0, g0, t0, r0), (l1, g1, t1, r1) = res
+    # the fused kernel sums the moments with 512 threads (float64, another
+    # order): mean / var agree to MOMENT_TOL, so mean32 / inv32 and with them
+    # the codes are equal except where a last-ulp difference moves an A2
+    # across a boundary
+    assert norm_err(l1, l0) < 1e-6
+    for a, b in zip(t0, t1):
+        if a.dtype == np.float64:
+            assert norm_err(b, a) < MOMENT_TOL
+        elif a.dtype == np.uint8:
+            assert np.mean(a == b) > 0.9999
+    assert all(norm_err(b, a) < MOMENT_TOL for a, b in zip(r0, r1))
+    assert norm_err(g1, g0) < 5e-2
