@@ -301,7 +301,7 @@ class ClockSampler:
 
 # ---------------------------------------------------------- CPU baseline
 
-def _cpu_worker(cfg_name, batch, steps, warmup, q):
+def _cpu_worker(cfg_name, batch, steps, warmup, q, budget_s=None, seed=0):
     os.environ["OMP_NUM_THREADS"] = "1"
     os.environ["OPENBLAS_NUM_THREADS"] = "1"
     import numpy as np
@@ -309,27 +309,33 @@ def _cpu_worker(cfg_name, batch, steps, warmup, q):
     from paper_1901_07988_b200 import engine as E
     c = CONFIGS[cfg_name]
     spec = getattr(E, c["builder"])().to_json()
-    rng = np.random.default_rng(0)
+    rng = np.random.default_rng(seed)
     x = rng.standard_normal((batch,) + tuple(spec["input_shape"])).astype(np.float32)
     y = rng.integers(0, spec["num_classes"], batch)
     params = O.init_params(spec, 0)
     times = []
+    t_start = time.perf_counter()
     for i in range(warmup + steps):
         t0 = time.perf_counter()
         O.train_step(spec, params, x, y, "approx", c["bits"])
         if i >= warmup:
             times.append(time.perf_counter() - t0)
+            # time-bounded sample: at least one timed step, then stop once
+            # the budget is spent
+            if budget_s is not None and time.perf_counter() - t_start > budget_s:
+                break
     q.put(times)
 
 
-def cpu_reference(cfg_name, batch, steps, warmup, procs):
-    """Oracle port (+ reference C kernel) on `procs` single-thread replicas;
-    returns (aggregate images/s, median step seconds)."""
+def cpu_reference(cfg_name, batch, steps, warmup, procs, budget_s=None):
+    """Oracle port (+ reference C kernel) on `procs` single-thread processes,
+    each a shard of `batch` images (distinct data per process); returns
+    (aggregate images/s, median step seconds)."""
     import multiprocessing as mp
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
-    ps = [ctx.Process(target=_cpu_worker, args=(cfg_name, batch, steps, warmup, q))
-          for _ in range(procs)]
+    ps = [ctx.Process(target=_cpu_worker, args=(cfg_name, batch, steps, warmup, q, budget_s, r))
+          for r in range(procs)]
     for p in ps:
         p.start()
     res = [q.get() for _ in ps]
@@ -390,7 +396,9 @@ def main():
     ap.add_argument("--config", default="C2", choices=sorted(CONFIGS))
     ap.add_argument("--bits", type=int, default=None)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--cpu-batch", type=int, default=4)
+    ap.add_argument("--cpu-batch", type=int, default=0,
+                    help="reference arm: images per process (0: the config batch / cores); "
+                         "cpu_baseline leg: 4")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
     bits = args.bits or cfg["bits"]
@@ -409,18 +417,25 @@ def main():
             return
         procs = max(1, len(os.sched_getaffinity(0)))
         steps = max(1, args.steps)
-        ips, med = cpu_reference(args.config, args.cpu_batch, steps, max(0, min(args.warmup, 1)),
-                                 procs)
+        # the config's per-GPU batch per step, sharded over the host's cores
+        # (one single-thread process per core, local BN per shard as the
+        # data-parallel GPU path); time-bounded so the run ends in minutes
+        shard = max(1, -(-cfg["batch"] // procs)) if args.cpu_batch <= 0 else args.cpu_batch
+        budget = 120.0
+        ips, med = cpu_reference(args.config, shard, steps, max(0, min(args.warmup, 1)), procs,
+                                 budget_s=budget)
         line = {
             "metric": METRIC, "value": ips, "unit": "images/s", "impl": "reference",
             "n_gpus": args.gpus, "steps": steps, "warmup": args.warmup,
             "ms_per_step": med * 1e3, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32 (f64 accumulation)", "data": "synthetic",
-            "config": {"workload": cfg["workload"], "sample_batch_per_process": args.cpu_batch,
-                       "processes": procs},
+            "config": {"workload": cfg["workload"], "images_per_step": shard * procs,
+                       "batch_per_process": shard, "processes": procs},
             "cpu_baseline": {"value": ips, "unit": "images/s", "cores": procs, "kind": "port",
-                             "sample": f"{procs} single-thread replicas x {steps} steps of "
-                                       f"batch {args.cpu_batch} ({args.config} spec)"},
+                             "sample": f"{procs} single-thread processes x batch {shard} = "
+                                       f"{shard * procs} images per step ({args.config} spec, "
+                                       f"the config's batch {cfg['batch']} sharded over the "
+                                       f"cores), up to {steps} steps or {budget:.0f} s"},
             "e2e": {"value": ips, "unit": "images/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0},
         }
@@ -590,9 +605,10 @@ def main():
     }
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         procs = 1
-        ips, med = cpu_reference(args.config, args.cpu_batch, 2, 1, procs)
+        cb = args.cpu_batch if args.cpu_batch > 0 else 4
+        ips, med = cpu_reference(args.config, cb, 2, 1, procs)
         line["cpu_baseline"] = {"value": ips, "unit": "images/s", "cores": procs, "kind": "port",
-                                "sample": f"1 warm-up + 2 steps at batch {args.cpu_batch} of the "
+                                "sample": f"1 warm-up + 2 steps at batch {cb} of the "
                                           f"{args.config} network, oracle port + reference C "
                                           f"conv kernel, 1 thread ({med:.1f} s/step)"}
     if rank == 0:

@@ -15,10 +15,12 @@ def call(name, *args):
         return
     return real(name, *args)
 N.call = call
-spec = E.resnet164_spec() if cfg == "C2" else E.resnet1001_spec()
-tr = P.Trainer(spec, 128, mode="approx", bits=4)
+spec = {"C2": E.resnet164_spec, "C3": E.resnet1001_spec, "C4": E.resnet152_spec}[cfg]()
+nb = 64 if cfg == "C4" else 128
+tr = P.Trainer(spec, nb, mode="approx", bits=4)
 rng = np.random.default_rng(0)
-tr.load_batch(rng.standard_normal((128, 3, 32, 32)).astype(np.float32), rng.integers(0, 10, 128))
+tr.load_batch(rng.standard_normal((nb,) + tuple(spec.input_shape)).astype(np.float32),
+              rng.integers(0, spec.num_classes, nb))
 tr.capture()
 for _ in range(5):
     tr.step_device()
