@@ -308,6 +308,25 @@ int qt_softmax_xent(const float *logits, const int64_t *labels, int64_t n, int64
 int qt_sgd(float *value, float *grad, float *vel, int64_t count, float lr,
            const float *lr_dev, float momentum, float weight_decay, qt_stream_t stream);
 
+/* ------------------------------------------------------------ input data ---
+ * Device-side CIFAR-10 pipeline (data.py:45-87, :182-206), bit-identical to
+ * the reference's numpy arithmetic.
+ * qt_cifar_decode: n binary records (3073 B: label byte + 3072 channel-major
+ * pixels, data.py:20, :52-57) -> labels (int64) and images fp32 = u8 / 255;
+ * *bad_label = 1 if a label byte exceeds 9 (DataError, data.py:73-74).
+ * qt_standardize: images = (images - mean[c]) / std[c] in fp32 (data.py:84-85).
+ * qt_gather_augment: dst[i] = src[idx[i]] (idx NULL: src[i]) horizontally
+ * flipped where flip[i] != 0 (flip NULL: none), then translated to
+ * padded[:, dy:dy+h, dx:dx+w] of a zero border of `pad` pixels with
+ * (dy, dx) = offsets[2i], offsets[2i+1] (offsets NULL: no translation). */
+int qt_cifar_decode(const uint8_t *records, int64_t n, float *images, int64_t *labels,
+                    int32_t *bad_label, qt_stream_t stream);
+int qt_standardize(float *images, int64_t n, int64_t c, int64_t hw, const float *mean,
+                   const float *std_, qt_stream_t stream);
+int qt_gather_augment(const float *src, const int64_t *idx, int64_t n, int64_t c, int64_t h,
+                      int64_t w, const uint8_t *flip, const int32_t *offsets, int pad,
+                      float *dst, qt_stream_t stream);
+
 /* ------------------------------------------------------------ engine glue ---
  * res = copy(x) and shortcut add / adjoint (engine.py:262-279) as standalone
  * kernels (the fused forms live in qt_conv_forward / qt_bn_backward_apply). */

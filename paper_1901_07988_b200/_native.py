@@ -91,6 +91,9 @@ SIGNATURES = {
     "qt_gap_backward": (I32, [P, I64, I64, I64, P, P]),
     "qt_softmax_xent": (I32, [P, P, I64, I64, P, P, P, P]),
     "qt_sgd": (I32, [P, P, P, I64, F32, P, F32, F32, P]),
+    "qt_cifar_decode": (I32, [P, I64, P, P, P, P]),
+    "qt_standardize": (I32, [P, I64, I64, I64, P, P, P]),
+    "qt_gather_augment": (I32, [P, P, I64, I64, I64, I64, P, P, I32, P, P]),
     "qt_copy": (I32, [P, P, I64, P]),
     "qt_shortcut_add": (I32, [P, P, I64, I64, I64, I64, I64, I64, P]),
     "qt_shortcut_adjoint": (I32, [P, P, I64, I64, I64, I64, I64, I64, P]),

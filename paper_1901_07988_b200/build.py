@@ -28,7 +28,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O2",
           "--expt-relaxed-constexpr", f"-I{ROOT / 'include'}", "-Xptxas", "-warn-spills"]
 STRICT = ["-fmad=false", "-prec-div=true", "-prec-sqrt=true", "-ftz=false"]
-STRICT_UNITS = {"codec.cu", "bn.cu", "dense.cu"}
+STRICT_UNITS = {"codec.cu", "bn.cu", "dense.cu", "data.cu"}
 
 
 def _sources():

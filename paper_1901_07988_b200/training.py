@@ -392,6 +392,11 @@ class Trainer:
     def step(self, images, labels) -> float:
         """End-to-end iteration through the public API; returns the loss."""
         self.load_batch(images, labels)
+        return self.step_loaded()
+
+    def step_loaded(self) -> float:
+        """One iteration on the batch already in ``self.x`` / ``self.labels``
+        (the device input pipeline writes them); returns the loss."""
         self.step_device()
         self.loss_host.copy_(self.loss_buf[:1], non_blocking=True)
         torch.cuda.current_stream(self.device).synchronize()
@@ -423,9 +428,11 @@ class TrainResult:
         return np.array([r[1] for r in self.records])
 
 
-def iterate_batches(dataset, batch_size: int, total_iters: int, seed: int):
-    """Seeded epoch shuffles, partial batch dropped (training.py:147-166)."""
-    n = len(dataset.labels)
+def iterate_indices(n: int, batch_size: int, total_iters: int, seed: int):
+    """(iteration, epoch, sample indices): seeded epoch permutations, the
+    partial last batch dropped -- the reference's batch order
+    (training.py:147-166) as indices, so a device-resident dataset is
+    gathered on the GPU."""
     per_epoch = n // batch_size
     if per_epoch == 0:
         raise ConfigError("batch_size larger than dataset")
@@ -436,17 +443,43 @@ def iterate_batches(dataset, batch_size: int, total_iters: int, seed: int):
         for b in range(per_epoch):
             if it >= total_iters:
                 return
-            idx = order[b * batch_size:(b + 1) * batch_size]
-            yield it, epoch, dataset.images[idx].copy(), dataset.labels[idx]
+            yield it, epoch, order[b * batch_size:(b + 1) * batch_size]
             it += 1
         epoch += 1
 
 
-def train(spec: NetworkSpec, config: TrainConfig, dataset, params=None, augment_fn=None
-          ) -> TrainResult:
-    """Training loop with the reference's seeding and CSV log
-    (training.py:169-212).  Augmentation (host-side, out of scope for the
-    device path) is applied through ``augment_fn(images, rng)`` if given."""
+def iterate_batches(dataset, batch_size: int, total_iters: int, seed: int):
+    """(iteration, epoch, images, labels) in the reference's order
+    (training.py:147-166); images are host copies (or device gathers for a
+    device-resident dataset)."""
+    for it, epoch, idx in iterate_indices(len(dataset.labels), batch_size, total_iters, seed):
+        if isinstance(dataset.images, torch.Tensor):
+            from .data import gather_batch
+            images = gather_batch(dataset.images, idx)
+        else:
+            images = dataset.images[idx].copy()
+        yield it, epoch, images, dataset.labels[idx]
+
+
+def write_log(path: str, records: list) -> None:
+    """CSV training log (training.py:206-212)."""
+    with open(path, "w") as f:
+        f.write("iter,loss,lr,elapsed_ms\n")
+        for it, loss, lr, ms in records:
+            f.write(f"{it},{loss:.17g},{lr:.17g},{ms:.3f}\n")
+
+
+def train(spec: NetworkSpec, config: TrainConfig, dataset, params=None) -> TrainResult:
+    """Training loop with the reference's seeding, augmentation and CSV log
+    (training.py:169-212) on the captured Trainer step.
+
+    Every batch is gathered and augmented on the device straight into the
+    step's input buffer (qt_gather_augment): a device-resident dataset
+    (data.load_cifar10) never leaves HBM; a host dataset is uploaded per
+    batch.  The flips / crop offsets come from the per-batch generator
+    keyed by (seed, epoch, iteration) with the reference's draws, so runs
+    augment exactly as the reference does."""
+    from .data import gather_batch
     if params is None:
         params = init_params(spec, config.seed)
     tr = Trainer(spec, config.batch_size, mode=config.mode, bits=config.bits,
@@ -455,20 +488,35 @@ def train(spec: NetworkSpec, config: TrainConfig, dataset, params=None, augment_
     tr.capture()
     records = []
     t0 = time.perf_counter()
-    for it, epoch, images, labels in iterate_batches(dataset, config.batch_size,
-                                                     config.total_iters, config.seed):
-        if augment_fn is not None and images.ndim == 4:
-            rng = np.random.default_rng(np.random.SeedSequence((config.seed, epoch, it)))
-            images = augment_fn(images, rng)
+    augment = (config.hflip or config.translate) and len(tr.x.shape) == 4
+    dev_images = isinstance(dataset.images, torch.Tensor)
+    staging = None
+    for it, epoch, idx in iterate_indices(len(dataset.labels), config.batch_size,
+                                          config.total_iters, config.seed):
+        rng = (np.random.default_rng(np.random.SeedSequence((config.seed, epoch, it)))
+               if augment else None)
+        if dev_images:
+            src, gidx = dataset.images, idx
+        else:                          # host dataset: upload the batch, augment on the device
+            if staging is None:
+                staging = torch.empty_like(tr.x)
+            tr.x_host.copy_(torch.from_numpy(np.ascontiguousarray(dataset.images[idx],
+                                                                   dtype=np.float32)))
+            staging.copy_(tr.x_host, non_blocking=True)
+            src, gidx = staging, None
+        if augment or dev_images:
+            gather_batch(src, gidx, rng, config.hflip, config.translate, out=tr.x,
+                         n=config.batch_size)
+        else:
+            tr.x.copy_(src)
+        tr.labels_host.copy_(torch.from_numpy(np.asarray(dataset.labels[idx], dtype=np.int64)))
+        tr.labels.copy_(tr.labels_host, non_blocking=True)
         lr = lr_at(config, it)
         tr.set_lr(lr)
-        loss = tr.step(images, labels)
+        loss = tr.step_loaded()
         records.append((it, loss, lr, (time.perf_counter() - t0) * 1e3))
     if config.log_path:
-        with open(config.log_path, "w") as f:
-            f.write("iter,loss,lr,elapsed_ms\n")
-            for it, loss, lr, ms in records:
-                f.write(f"{it},{loss:.17g},{lr:.17g},{ms:.3f}\n")
+        write_log(config.log_path, records)
     return TrainResult(records=records, params=tr.params, pool=tr.pool)
 
 
@@ -478,8 +526,11 @@ def evaluate(spec: NetworkSpec, params, dataset, batch_size: int = 256) -> float
     wrong = 0
     dev = params[0].weight.device
     for s in range(0, n, batch_size):
-        x = torch.as_tensor(np.ascontiguousarray(dataset.images[s:s + batch_size],
-                                                 dtype=np.float32)).to(dev)
+        if isinstance(dataset.images, torch.Tensor):      # device-resident dataset
+            x = dataset.images[s:s + batch_size].contiguous()
+        else:
+            x = torch.as_tensor(np.ascontiguousarray(dataset.images[s:s + batch_size],
+                                                     dtype=np.float32)).to(dev)
         logits, _ = network_forward(spec, params, x, training=False)
         pred = logits.argmax(dim=1).cpu().numpy()
         wrong += int(np.count_nonzero(pred != np.asarray(dataset.labels[s:s + batch_size])))

@@ -117,10 +117,15 @@ def test_memory_report_matches_instrumented_pool():
         E.network_backward(spec, params, tapes, torch.ones_like(logits), x, mode="approx",
                            pool=pool)
         rep = E.memory_report(spec, shape, mode="approx", bits=4)
-        # the report reproduces the reference's W+1 schedule (engine.py:419-482);
-        # the device engine aliases the block input as the shortcut operand
-        # instead of copying it, so its pool never exceeds that schedule
-        assert 0 < pool.peak_live_bytes <= rep.transient_buffer_bytes
+        dev_rep = E.memory_report(spec, shape, mode="approx", bits=4, schedule="device")
+        # the default report reproduces the reference's W+1 schedule
+        # (engine.py:419-482); the device engine holds the block input as the
+        # shortcut operand instead of copying it -- its own schedule
+        # (schedule="device") equals the instrumented pool byte for byte
+        # (reference test_engine.py:246-260), and never exceeds the reference's
+        assert pool.peak_live_bytes == dev_rep.transient_buffer_bytes
+        assert pool.peak_live_count == dev_rep.peak_live_tensors
+        assert dev_rep.transient_buffer_bytes <= rep.transient_buffer_bytes
         assert pool.peak_live_count <= rep.peak_live_tensors <= spec.width() + 1
         assert rep.persistent_tape_bytes == E.measured_tape_bytes(tapes)
         assert rep.channel_overhead_bytes == E.measured_overhead_bytes(tapes)
