@@ -1471,41 +1471,50 @@ static SegDiv seg_div(const SegGeo &s, int64_t c, int64_t w) {
     return d;
 }
 
+// source of element i of a segmented plane: its (n, c, h, w) index si and
+// channel tc, or false for a zero (padding) element (MODE as seg_in_kernel)
+template <int MODE>
+__device__ __forceinline__ bool seg_src(uint32_t i, int c, int h, int w, const SegGeo &s,
+                                        const SegDiv &dv, int64_t &si, int &tc) {
+    bool ok;
+    if (s.flat) {   // c = source channels x sd^2; (h, w) = source extent
+        const uint32_t m = fast_div(i, dv.plane), p = i - m * (uint32_t)(s.hp * s.owt);
+        const uint32_t wd = (uint32_t)w / (uint32_t)s.sd;
+        ok = p < (uint32_t)h / (uint32_t)s.sd * wd;
+        if (s.sd == 1) {
+            si = (int64_t)m * (uint32_t)(h * w) + p;
+            tc = (int)(m - fast_div(m, dv.c) * (uint32_t)c);
+        } else {
+            const uint32_t nn = fast_div(m, dv.c), ch = m - nn * (uint32_t)c;
+            const uint32_t Y = fast_div(p, dv.wd), X = p - Y * wd;
+            const uint32_t sd2 = (uint32_t)(s.sd * s.sd), c0 = fast_div(ch, dv.sd2), uv = ch - c0 * sd2;
+            const uint32_t u = fast_div(uv, dv.sd), v = uv - u * (uint32_t)s.sd;
+            const uint32_t cs = (uint32_t)c / sd2;
+            si = (((int64_t)nn * cs + c0) * h + Y * s.sd + u) * w + X * s.sd + v;
+            tc = (int)c0;
+        }
+    } else {
+        const uint32_t k = i & ((uint32_t)s.owt - 1u), r = i >> dv.owt_log2;
+        const uint32_t r2 = fast_div(r, dv.hp), y = r - r2 * (uint32_t)s.hp;
+        const uint32_t m = fast_div(r2, dv.c), ch = r2 - m * (uint32_t)c;
+        const uint32_t nn = fast_div(m, dv.nseg), j = m - nn * (uint32_t)s.nseg;
+        const int col = (int)(j * s.step + k) - s.halo;
+        ok = y < (uint32_t)h && col >= 0 && col < w;
+        if (MODE == 1) ok = ok && (int)k >= s.halo && (int)k < s.halo + s.step;
+        si = (((int64_t)nn * c + ch) * h + y) * w + col;
+        tc = (int)ch;
+    }
+    return ok;
+}
+
 template <int MODE>
 __global__ void seg_in_kernel(const float *src, qt_tape_t t, float *dst, uint32_t total, int c,
                               int h, int w, SegGeo s, SegDiv dv) {
     pdl_enter();
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-        bool ok;
         int64_t si;
         int tc;
-        if (s.flat) {   // c = source channels x sd^2; (h, w) = source extent
-            const uint32_t m = fast_div(i, dv.plane), p = i - m * (uint32_t)(s.hp * s.owt);
-            const uint32_t wd = (uint32_t)w / (uint32_t)s.sd;
-            ok = p < (uint32_t)h / (uint32_t)s.sd * wd;
-            if (s.sd == 1) {
-                si = (int64_t)m * (uint32_t)(h * w) + p;
-                tc = (int)(m - fast_div(m, dv.c) * (uint32_t)c);
-            } else {
-                const uint32_t nn = fast_div(m, dv.c), ch = m - nn * (uint32_t)c;
-                const uint32_t Y = fast_div(p, dv.wd), X = p - Y * wd;
-                const uint32_t sd2 = (uint32_t)(s.sd * s.sd), c0 = fast_div(ch, dv.sd2), uv = ch - c0 * sd2;
-                const uint32_t u = fast_div(uv, dv.sd), v = uv - u * (uint32_t)s.sd;
-                const uint32_t cs = (uint32_t)c / sd2;
-                si = (((int64_t)nn * cs + c0) * h + Y * s.sd + u) * w + X * s.sd + v;
-                tc = (int)c0;
-            }
-        } else {
-            const uint32_t k = i & ((uint32_t)s.owt - 1u), r = i >> dv.owt_log2;
-            const uint32_t r2 = fast_div(r, dv.hp), y = r - r2 * (uint32_t)s.hp;
-            const uint32_t m = fast_div(r2, dv.c), ch = r2 - m * (uint32_t)c;
-            const uint32_t nn = fast_div(m, dv.nseg), j = m - nn * (uint32_t)s.nseg;
-            const int col = (int)(j * s.step + k) - s.halo;
-            ok = y < (uint32_t)h && col >= 0 && col < w;
-            if (MODE == 1) ok = ok && (int)k >= s.halo && (int)k < s.halo + s.step;
-            si = (((int64_t)nn * c + ch) * h + y) * w + col;
-            tc = (int)ch;
-        }
+        const bool ok = seg_src<MODE>(i, c, h, w, s, dv, si, tc);
         float v = 0.f;
         if (ok) {
             if (MODE != 2 || src) {
@@ -1519,6 +1528,57 @@ __global__ void seg_in_kernel(const float *src, qt_tape_t t, float *dst, uint32_
     }
 }
 
+// g_out of a segmented plane straight into the weight gradient's pre-split B
+// layout (conv_tc_wgrad.cuh, PRE-SPLIT): per (image, 32-px chunk) three
+// piece blocks [co][32 px] of bf16 hi / mid / lo (hi + mid + lo == g to fp32
+// precision), pixels pair-permuted in 8-px groups (word k = pixels k, k + 4).
+// One thread per (image, chunk, channel, 8-px group): 3 x 16-byte stores.
+__global__ void seg_pieces_kernel(const float *g, uint4 *dst, uint32_t groups, int co, int h, int w,
+                                  SegGeo s, SegDiv dv, FastDiv cod, FastDiv cpid) {
+    pdl_enter();
+    const uint32_t plane = (uint32_t)(s.hp * s.owt);
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < groups;
+         i += gridDim.x * blockDim.x) {
+        const uint32_t q = i & 3u, r = i >> 2;
+        const uint32_t r2 = fast_div(r, cod), ch = r - r2 * (uint32_t)co;    // r2 = image * cpi + chunk
+        const uint32_t nn = fast_div(r2, cpid), chunk = r2 - nn * (plane / 32u);
+        const uint32_t p0 = chunk * 32u + 8u * q;     // first pixel of the group in the plane
+        // the group's 8 pixels are one run of a source row (owt and the
+        // flat plane are multiples of 8): map the first, clip the run
+        int64_t si;
+        int klo = 0, khi = 8;
+        if (s.flat) {   // g_out planes are flat with sd == 1
+            si = (int64_t)(nn * (uint32_t)co + ch) * (uint32_t)(h * w) + p0;
+            khi = max(0, min(8, h * w - (int)p0));
+        } else {
+            const uint32_t nimg = fast_div(nn, dv.nseg), j = nn - nimg * (uint32_t)s.nseg;
+            const uint32_t y = p0 >> dv.owt_log2, k0 = p0 & ((uint32_t)s.owt - 1u);
+            const int col = (int)(j * s.step + k0) - s.halo;
+            si = (((int64_t)nimg * co + ch) * h + y) * w + col;
+            klo = max(max(0, -col), s.halo - (int)k0);
+            khi = min(min(8, w - col), s.halo + s.step - (int)k0);
+            if ((int)y >= h) khi = 0;
+        }
+        float v[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) v[k] = (k >= klo && k < khi) ? __ldg(g + si + k) : 0.f;
+        uint32_t H[4], M[4], L[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            H[k] = pack_bf16x2(v[k], v[k + 4]);
+            const float rx = __fsub_rn(v[k], bf16_lo(H[k])), ry = __fsub_rn(v[k + 4], bf16_hi(H[k]));
+            M[k] = pack_bf16x2(rx, ry);
+            L[k] = pack_bf16x2(__fsub_rn(rx, bf16_lo(M[k])), __fsub_rn(ry, bf16_hi(M[k])));
+        }
+        // [image][chunk][piece][co][4 groups of 16 B]
+        uint4 *o = dst + ((size_t)r2 * 3u * (uint32_t)co + ch) * 4u + q;
+        const size_t pstride = (size_t)co * 4u;
+        o[0] = make_uint4(H[0], H[1], H[2], H[3]);
+        o[pstride] = make_uint4(M[0], M[1], M[2], M[3]);
+        o[2 * pstride] = make_uint4(L[0], L[1], L[2], L[3]);
+    }
+}
+
 // Flat weight-gradient operand from a packed tape: codes of the (space-to-
 // depth) plane repacked into zero-padded (n, c sd^2, hp * owt) planes in the
 // same K-bit little-endian order (codec.pack_codes, codec.py:59-78), plus the
@@ -1526,7 +1586,8 @@ __global__ void seg_in_kernel(const float *src, qt_tape_t t, float *dst, uint32_
 // their g is zero, so any finite decode contributes nothing.
 __global__ void seg_codes_kernel(const uint8_t *codes, uint32_t *dst, uint32_t words, int bits,
                                  int c4, int h, int w, SegGeo s, const double *step,
-                                 const int64_t *offset, double *step4, int64_t *offset4) {
+                                 const int64_t *offset, double *step4, int64_t *offset4,
+                                 FastDiv pwd, FastDiv c4d, FastDiv nsegd) {
     pdl_enter();
     const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
     const uint32_t sd = (uint32_t)s.sd, sd2 = sd * sd;
@@ -1540,7 +1601,7 @@ __global__ void seg_codes_kernel(const uint8_t *codes, uint32_t *dst, uint32_t w
     const uint32_t cs = (uint32_t)c4 / sd2;
     const uint32_t *src32 = reinterpret_cast<const uint32_t *>(codes);   // 16-byte aligned tape
     for (uint32_t o = tid; o < words; o += gridDim.x * blockDim.x) {
-        const uint32_t m = o / pw, wi = o - m * pw;
+        const uint32_t m = fast_div(o, pwd), wi = o - m * pw;
         uint32_t acc = 0;
         // the word's codes are one contiguous run of the source tape: extract
         // its 32 bits with a funnel shift across two aligned words
@@ -1548,8 +1609,8 @@ __global__ void seg_codes_kernel(const uint8_t *codes, uint32_t *dst, uint32_t w
         if (s.flat && sd == 1) {
             if ((wi + 1) * per <= pl) run = (int64_t)m * pl + wi * per;
         } else if (!s.flat && per <= (uint32_t)s.owt) {
-            const uint32_t img = m / (uint32_t)c4, ch = m - img * (uint32_t)c4;
-            const uint32_t nn = img / (uint32_t)s.nseg, j = img - nn * (uint32_t)s.nseg;
+            const uint32_t img = fast_div(m, c4d), ch = m - img * (uint32_t)c4;
+            const uint32_t nn = fast_div(img, nsegd), j = img - nn * (uint32_t)s.nseg;
             const uint32_t p0 = wi * per, y = p0 / (uint32_t)s.owt, kx = p0 - y * (uint32_t)s.owt;
             const int col = (int)(j * s.step + kx) - s.halo;
             if (y < (uint32_t)h && col >= 0 && col + (int)per <= w)
@@ -1605,6 +1666,11 @@ __global__ void seg_pad_fix_kernel(const float *g, float *grad_w, int n, int co_
     __shared__ double red[9][256];
     __shared__ double S[9];
     const int co = blockIdx.x, tid = threadIdx.x;
+    // only channels whose code 0 decodes positive (every code positive) see
+    // the padding pixels: nothing to do for the usual tapes
+    int any = 0;
+    for (int c = tid; c < ci; c += blockDim.x) any |= decode(0u, step[c], offset[c], bits) > 0.f;
+    if (!__syncthreads_or(any)) return;
     const int L = w + 2 * (h - 1);   // last row, last column above it, first column above it
     double acc[9];
 #pragma unroll
@@ -1795,6 +1861,9 @@ int qt_tc_conv_seg_dgrad(const float *gr, const float *w, float *gx, const qt::C
 
 int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
                      const qt::ConvGeo &g, void *ws, cudaStream_t st);
+int qt_tc_conv_wgrad_pre(const void *pieces, qt_tape_t act, float *grad_w, const qt::ConvGeo &g,
+                         void *ws, cudaStream_t st);
+bool qt_tc_wgrad_pre_ok(const qt::ConvGeo &g, int bits);
 int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g);
 
 static qt::ConvGeo seg_wgrad_geo(const qt::ConvGeo &g, const SegGeo &s) {
@@ -1821,7 +1890,9 @@ int64_t qt_tc_seg_wgrad_workspace(const qt::ConvGeo &g) {
     const SegGeo s = seg_geo_wgrad(g);
     if (!s.ok) return 0;
     const int64_t part = (qt_tc_wgrad_workspace(seg_wgrad_geo(g, s)) + 255) / 256 * 256;
-    return part + 4 * seg_elems(s, g.n, g.ci * s.sd * s.sd + g.co) + g.ci * s.sd * s.sd * 16 + 1024;
+    // g_out region: fp32 (4 B) or bf16 pieces (6 B per element)
+    const int64_t gbytes = (6 * seg_elems(s, g.n, g.co) + 255) / 256 * 256;
+    return part + gbytes + 4 * seg_elems(s, g.n, g.ci * s.sd * s.sd) + g.ci * s.sd * s.sd * 16 + 1024;
 }
 
 // weight gradient: segmented g_out (zero outside each segment's own columns)
@@ -1837,17 +1908,26 @@ int qt_tc_conv_seg_wgrad(const float *gr, qt_tape_t act, const float *x_plain, f
     const int64_t part = (qt_tc_wgrad_workspace(d) + 255) / 256 * 256;
     if (part <= 0) return QT_EUNSUPPORTED;
     float *gs = (float *)((char *)ws + part);
-    float *as = gs + seg_elems(s, g.n, g.co);
+    float *as = (float *)((char *)gs + (6 * seg_elems(s, g.n, g.co) + 255) / 256 * 256);
+    // g_out is already the flat plane in the flat case: a 1x1 view of (oh, ow)
+    SegGeo sg = s;
+    if (s.flat) sg.sd = 1;
+    const int64_t gh = s.flat ? g.oh : g.h, gw = s.flat ? g.ow : g.w;
+    const bool codes = !x_plain && !act.a2 && act.codes && qt_bits_ok(act.bits);
+    bool pre = codes && qt_tc_wgrad_pre_ok(d, act.bits);
     int rc;
-    if (s.flat) {   // g_out is already the flat plane: a 1x1 view of (oh, ow)
-        SegGeo s1 = s;
-        s1.sd = 1;
-        rc = seg_in<1>(gr, qt_tape_t{}, gs, g.n, g.co, g.oh, g.ow, s1, st);
+    if (pre) {   // g_out straight into the bf16 pieces the weight gradient's TMA reads
+        const uint32_t groups = (uint32_t)(seg_elems(s, g.n, g.co) / 8);
+        const uint32_t cpi = (uint32_t)(s.hp * s.owt / 32);
+        launch_pdl(seg_pieces_kernel, seg_blocks(groups), 256, 0, st, gr, (uint4 *)gs, groups,
+                   (int)g.co, (int)gh, (int)gw, sg, seg_div(sg, g.co, gw), make_fastdiv((uint32_t)g.co),
+                   make_fastdiv(cpi));
+        QT_CHECK_LAUNCH();
     } else {
-        rc = seg_in<1>(gr, qt_tape_t{}, gs, g.n, g.co, g.h, g.w, s, st);
+        rc = seg_in<1>(gr, qt_tape_t{}, gs, g.n, g.co, gh, gw, sg, st);
+        if (rc) return rc;
     }
-    if (rc) return rc;
-    if (!x_plain && !act.a2 && act.codes && qt_bits_ok(act.bits)) {
+    if (codes) {
         // packed operand: the tensor-core path decodes it in its operand staging
         const int64_t words = seg_elems(s, g.n, cin) * act.bits / 32;
         uint32_t *cw = (uint32_t *)as;
@@ -1855,10 +1935,18 @@ int qt_tc_conv_seg_wgrad(const float *gr, qt_tape_t act, const float *x_plain, f
         int64_t *off4 = (int64_t *)(step4 + cin);
         launch_pdl(seg_codes_kernel, seg_blocks(std::max(words, cin)), 256, 0, st, act.codes, cw,
                    (uint32_t)words, act.bits, (int)cin, (int)g.h, (int)g.w, s, act.step, act.offset,
-                   step4, off4);
+                   step4, off4, make_fastdiv((uint32_t)(s.hp * s.owt * act.bits / 32)),
+                   make_fastdiv((uint32_t)cin), make_fastdiv((uint32_t)s.nseg));
         QT_CHECK_LAUNCH();
         qt_tape_t t2{nullptr, (const uint8_t *)cw, step4, off4, act.bits};
-        rc = qt_tc_conv_wgrad(gs, t2, nullptr, grad_w, d, ws, st);
+        rc = pre ? qt_tc_conv_wgrad_pre(gs, t2, grad_w, d, ws, st)
+                 : qt_tc_conv_wgrad(gs, t2, nullptr, grad_w, d, ws, st);
+        if (rc == QT_EUNSUPPORTED && pre) {   // the fp32 plane for the paths below
+            pre = false;
+            rc = seg_in<1>(gr, qt_tape_t{}, gs, g.n, g.co, gh, gw, sg, st);
+            if (rc) return rc;
+            rc = qt_tc_conv_wgrad(gs, t2, nullptr, grad_w, d, ws, st);
+        }
         if (rc != QT_EUNSUPPORTED) {
             if (rc || s.flat) return rc;
             if (s.hp == g.h && !s.halo && s.owt == g.w) return rc;   // no padding pixels

@@ -73,8 +73,11 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn_wg() {
 
 // bits > 0: the activation is a packed code tape of that width; tap: 3x3
 // with the column taps moved into N (4-bit codes, BN <= 32)
-static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = false) {
+// pre: g_out arrives as bf16 pieces (FAST-capable codes, stacked, no taps)
+static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = false,
+                      bool pre = false) {
     WgPlan pl;
+    if (pre && (tap || fbox || !(bits == 2 || bits == 4))) return pl;
     if (g.s != 1) return pl;
     const int64_t ow = g.ow, oh = g.oh;
     if (ow != 8 && ow != 16 && ow != 32) return pl;
@@ -90,6 +93,19 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = 
     // pieces and a four-deep operand ring fit only up to 64 -- the A decode
     // is repeated per block, cheap for the narrow-input expand layers
     if (bn > 64 && g.co % 64 == 0 && !tap) bn = 64;
+    // pre-split pieces: the B tile is TMA traffic, not operand work -- wide
+    // outputs take 128-channel blocks (three N = 128 MMAs per K step, one
+    // accumulator) and both m-tiles of a pair, so each byte of B read from
+    // L2 feeds twice the MMA work (the L2 -> SM rate bounds the stacked form)
+    const int64_t mt0 = (g.ci * g.kh * g.kw + 127) / 128;
+    if (pre && g.co % 128 == 0 && mt0 >= 2) bn = 128;
+    if (pre) {
+        static const int bn_env = [] {
+            const char *e = getenv("QTAPE_WG_PRE_BN");
+            return e ? atoi(e) : 0;
+        }();
+        if (bn_env >= 16 && bn_env <= 128 && g.co % bn_env == 0) bn = bn_env;   // tuning
+    }
     if (g.co % bn) return pl;
     pl.bn = bn;
     pl.nblk = (int)(g.co / bn);
@@ -103,7 +119,10 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = 
     const bool stack = tap ? 9 * bn <= 256 : 3 * bn <= 192;
     const int facc = stack ? 3 * nt * bn : nt * bn;      // FAST accumulator columns per tile
     const int gacc = nt * bn;                            // GENERIC accumulator columns per tile
-    const int opb = std::max(3 * nt * bn * 64, 2 * nt * bn * 128);   // operand bytes per chunk
+    // operand bytes per chunk: FAST 3 bf16 pieces (only 2/4-bit codes take
+    // FAST), GENERIC TF32 (hi, lo); the two modes share one smem region
+    const int opb_g = 2 * nt * bn * 128;
+    const int opb_f = (bits == 2 || bits == 4) ? 3 * nt * bn * 64 : opb_g;
     // TMEM (512 columns): FAST needs mtg*facc + ops*mtg*SUB*16, GENERIC
     // mtg*BN + ops_g*mtg*SUB*64; ring depths are powers of two (see kWgGroups)
     constexpr int SUB = kWgSub;
@@ -111,11 +130,14 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = 
     // still leaves four operand stages in TMEM and the tiles are not one of
     // three or more (measured: mtg 1 wins for mt >= 3 and for ops < 4)
     int mtg = (int)std::min<int64_t>(mt, 2);
-    if (mtg == 2 && (mt >= 3 || 2 * facc + 4 * 2 * SUB * 16 > 512)) mtg = 1;
+    if (mtg == 2 && ((!pre && mt >= 3) || 2 * facc + 4 * 2 * SUB * 16 > 512)) mtg = 1;
     if (const char *e = getenv("QTAPE_WG_MTG")) mtg = std::max(1, std::min(mtg, atoi(e)));   // tuning
     while (mtg > 1 && (mtg * gacc + mtg * SUB * 64 > 512 || mtg * facc + 2 * mtg * SUB * 16 > 512))
         --mtg;
     if (mtg * gacc + mtg * SUB * 64 > 512 || mtg * facc + 2 * mtg * SUB * 16 > 512) return WgPlan{};
+    // GENERIC-PRE keeps three bf16 A pieces (48 columns per chunk) in TMEM
+    while (pre && mtg > 1 && mtg * facc + mtg * SUB * 48 > 512) --mtg;
+    if (pre && mtg * facc + mtg * SUB * 48 > 512) return WgPlan{};
     pl.mtg = mtg;
     pl.mgroups = (int)((mt + mtg - 1) / mtg);
     pl.ops = 4;
@@ -132,7 +154,8 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = 
         if (pl.cb > 256 || pl.nch > kWgMaxCh) return WgPlan{};
         if (pl.nch * (1 << bits) > kWgLutEntries) return WgPlan{};
         pl.cbytes = pl.cb * pl.nch;
-        pl.lut_floats = pl.nch * ((2 << bits) + 2);      // padded channel stride
+        // padded channel stride: (hi, lo) pairs, or (pre) the value itself
+        pl.lut_floats = pl.nch * (pre ? (1 << bits) + 1 : (2 << bits) + 2);
     } else if (fbox) {   // fp32 box per stage: the chunk rows plus the pad rows of each channel
         const int kk = pl.rpc;
         pl.nch = (int)std::min<int64_t>(g.ci, (mtg * 128 + kk - 1) / kk + (kk > 1 ? 1 : 0));
@@ -142,19 +165,45 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = 
         pl.cbytes = pl.cb * pl.nch;
         pl.fbox = 1;
     }
-    gbytes = (SUB * gbytes0 + pl.cbytes + 1023) & ~1023;    // one raw stage
+    gbytes = ((pre ? 0 : SUB * gbytes0) + pl.cbytes + 1023) & ~1023;    // one raw stage
     pl.slot = gbytes;
     const int fixed = pl.lut_floats * 4 + kWgMaxCh * 4 + 1024 + 512;
     const int budget = 227 * 1024 - fixed;
-    const int sraw = gbytes, sop = SUB * opb;                 // bytes per raw / operand stage
-    while (pl.ops > 1 && pl.ops * (sraw + sop) > budget) pl.ops /= 2;
-    if (pl.ops * (sraw + sop) > budget) return WgPlan{};
+    if (pre) {
+        // raw ring = code boxes only (owned by the FAST groups: a multiple of
+        // ops), B ring = the pieces (MMA warp only, any depth >= 2); no smem
+        // operand region (A lives in TMEM in both modes)
+        pl.pre = 1;
+        // A stages live only in TMEM: up to two per operand group
+        pl.ops = 8;
+        while (pl.ops > 2 && mtg * facc + pl.ops * mtg * SUB * 16 > 512) pl.ops /= 2;
+        pl.ops_g = std::min(pl.ops, 4);
+        while (pl.ops_g > 1 && mtg * facc + pl.ops_g * mtg * SUB * 48 > 512) pl.ops_g /= 2;
+        const int bstage = SUB * 3 * bn * 64;
+        const int G = std::min(pl.ops, 4);                // active FAST groups
+        pl.rg = std::max(pl.ops, std::min(8, budget / 3 / gbytes) / G * G);
+        pl.bring = std::min(8, (budget - pl.rg * gbytes) / bstage);
+        if (pl.bring < 2) return WgPlan{};
+        pl.opreg = pl.bring * bstage;
+        pl.smem = pl.rg * gbytes + pl.opreg + fixed;
+    } else {
+    const int sraw = gbytes;                                  // bytes per raw stage
     pl.ops_g = pl.ops;
     while (pl.ops_g > 1 && mtg * gacc + pl.ops_g * mtg * SUB * 64 > 512) pl.ops_g /= 2;
+    // operand region: ops FAST stages or ops_g GENERIC stages (a CTA takes
+    // one mode), at least one raw stage per FAST operand stage beside it
+    auto region = [&] { return std::max(pl.ops * SUB * opb_f, pl.ops_g * SUB * opb_g); };
+    while (pl.ops > 1 && region() + pl.ops * sraw > budget) {
+        pl.ops /= 2;
+        pl.ops_g = std::min(pl.ops_g, pl.ops);
+    }
+    if (region() + pl.ops * sraw > budget) return WgPlan{};
     // raw ring: the largest multiple of ops up to 8 stages that fits
-    pl.rg = std::min(8, (budget - pl.ops * sop) / sraw) / pl.ops * pl.ops;
+    pl.rg = std::min(8, (budget - region()) / sraw) / pl.ops * pl.ops;
     if (pl.rg < pl.ops) return WgPlan{};
-    pl.smem = pl.rg * sraw + pl.ops * sop + fixed;
+    pl.opreg = region();
+    pl.smem = pl.rg * sraw + pl.opreg + fixed;
+    }
     pl.total = (int)(g.n * oh * ow / 32);
     // split-K count: one CTA per SM (one is resident per SM: a second wave
     // would pay setup, pipeline fill and epilogue again), at least one
@@ -178,7 +227,7 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = 
     // CTA at least one stage per group: the kernel takes about as long on
     // fewer SMs (latency-bound), leaves the rest to the input-gradient chain
     // running beside it, and writes fewer partials
-    want = std::min(want, std::max(1, pl.total / (SUB * pl.ops)));
+    want = std::min(want, std::max(1, pl.total / (SUB * std::min(pl.ops, 4))));
     const double gbytes_all = 128.0 * g.co * pl.total;
     const double part_cap = std::max(4.0 * gbytes_all, 32.0 * 1024 * 1024);
     want = std::min(want, std::max(1, (int)(part_cap / (4.0 * (double)Rout * g.co))));
@@ -293,6 +342,10 @@ int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g) {
         WgPlan q = wg_plan(g, bits);
         sp = std::max(sp, (int64_t)(q.ok ? q.splits : 0));
     }
+    for (int bits : {2, 4}) {      // the pre-split pieces path
+        WgPlan q = wg_plan(g, bits, false, false, true);
+        sp = std::max(sp, (int64_t)(q.ok ? q.splits : 0));
+    }
     return sp * g.co * g.ci * g.kh * g.kw * (int64_t)sizeof(float);
 }
 
@@ -319,11 +372,13 @@ int qt_tc_wgrad_reduce(const float *partial, int64_t splits, int64_t count, floa
     return QT_OK;
 }
 
-int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
-                     const qt::ConvGeo &g0, void *ws, cudaStream_t st) {
+// gr: fp32 g_out, or (pieces != NULL) its bf16 pieces in the wg_pieces layout
+static int wgrad_tc(const float *gr, const void *pieces, qt_tape_t act, const float *x_plain,
+                    float *grad_w, const qt::ConvGeo &g0, void *ws, cudaStream_t st) {
     if (tcw_disabled()) return QT_EUNSUPPORTED;
     const ConvGeo g = wg_flat_shape(g0) ? wg_flat_geo(g0) : g0;
     const bool codes = !x_plain && !act.a2;
+    if (pieces && (!codes || ((uintptr_t)pieces & 15))) return QT_EUNSUPPORTED;
     // 3x3 on 4-bit codes with the column taps in N: correct (tested) but not
     // yet faster than the (ci, u, v)-row form -- its g split triples -- so
     // opt-in with QTAPE_WG_TAP=1
@@ -332,7 +387,11 @@ int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float
         return e && *e && *e != '0';
     }();
     WgPlan pl{};
-    if (codes && use_tap) pl = wg_plan(g, act.bits, true);
+    if (pieces) {
+        pl = wg_plan(g, act.bits, false, false, true);
+        if (!pl.ok) return QT_EUNSUPPORTED;
+    }
+    if (!pl.ok && codes && use_tap) pl = wg_plan(g, act.bits, true);
     if (!pl.ok && !codes) pl = wg_plan(g, 0, false, true);   // fp32 rows staged by TMA
     if (!pl.ok) pl = wg_plan(g, codes ? act.bits : 0);
     if (!pl.ok) return QT_EUNSUPPORTED;
@@ -345,15 +404,28 @@ int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float
     // swizzle span is padded per row by TMA, so rows of 8/16 px cannot be
     // stacked into one swizzle row.)
     CUtensorMap m;
+    cuuint32_t es[5] = {1, 1, 1, 1, 1};
+    if (pieces) {
+        // 5D (32 px, co, piece, chunk, n) bf16: one box = SUB chunks x 3
+        // pieces x BN channels of 64-byte rows, SW64 -- the FAST B layout
+        const cuuint64_t cpi = (cuuint64_t)(g.oh * g.ow / 32), row = 64;
+        cuuint64_t dims[5] = {32, (cuuint64_t)g.co, 3, cpi, (cuuint64_t)g.n};
+        cuuint64_t strides[4] = {row, row * g.co, row * g.co * 3, row * g.co * 3 * cpi};
+        cuuint32_t box[5] = {32, (cuuint32_t)pl.bn, 3, (cuuint32_t)kWgSub, 1};
+        if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, const_cast<void *>(pieces), dims, strides,
+                box, es, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+            return QT_EUNSUPPORTED;
+    } else {
     // 4D (32 px, chunk, c, n): one box = SUB consecutive chunks x BN channels
     cuuint64_t dims[4] = {32, (cuuint64_t)(g.oh * g.ow / 32), (cuuint64_t)g.co, (cuuint64_t)g.n};
     cuuint64_t strides[3] = {128, (cuuint64_t)g.oh * g.ow * 4, (cuuint64_t)g.co * g.oh * g.ow * 4};
     cuuint32_t box[4] = {32, (cuuint32_t)kWgSub, (cuuint32_t)pl.bn, 1};
-    cuuint32_t es[4] = {1, 1, 1, 1};
     if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 4, (void *)gr, dims, strides, box, es,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
             CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
         return QT_EUNSUPPORTED;
+    }
     CUtensorMap mc = m;   // codes (n, ci, plane bytes) as 3D (byte, c, n)
     if (codes) {
         const int64_t plane = g.h * g.w * act.bits / 8;
@@ -398,6 +470,9 @@ int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float
     p.RG = pl.rg;
     p.OPS = pl.ops;
     p.OPS_G = pl.ops_g;
+    p.opreg = pl.opreg;
+    p.pre = pl.pre;
+    p.RB = pl.bring;
     p.lut_floats = pl.lut_floats;
     p.slot = pl.slot;
     p.cb = pl.cb;
@@ -417,6 +492,27 @@ int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float
     }
     if (rc) return rc;
     return qt_tc_wgrad_reduce((const float *)ws, pl.splits, g.co * p.Rout, grad_w, st);
+}
+
+int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
+                     const qt::ConvGeo &g, void *ws, cudaStream_t st) {
+    return wgrad_tc(gr, nullptr, act, x_plain, grad_w, g, ws, st);
+}
+
+// weight gradient with g_out already split into bf16 pieces (wg_pieces layout)
+int qt_tc_conv_wgrad_pre(const void *pieces, qt_tape_t act, float *grad_w, const qt::ConvGeo &g,
+                         void *ws, cudaStream_t st) {
+    return wgrad_tc(nullptr, pieces, act, nullptr, grad_w, g, ws, st);
+}
+
+// the pieces path is planned for this (32-px-row) geometry and code width
+bool qt_tc_wgrad_pre_ok(const qt::ConvGeo &g, int bits) {
+    if (tcw_disabled()) return false;
+    static const bool off = [] {
+        const char *e = getenv("QTAPE_WG_PRE");
+        return e && *e == '0';
+    }();
+    return !off && wg_plan(wg_flat_shape(g) ? wg_flat_geo(g) : g, bits, false, false, true).ok;
 }
 
 // 2x2/s2 weight gradient from a packed code tape through the rearranged tape

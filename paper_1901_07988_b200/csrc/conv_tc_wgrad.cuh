@@ -37,6 +37,14 @@
 //     TF32 (hi, lo) and three kind::tf32 passes hi*hi + hi*lo + lo*hi.
 // Each MMA issues in ~46 cycles for N <= 64 (kind::f16 K=16 and kind::tf32
 // K=8 alike), so pixels per instruction is the throughput lever.
+// PRE-SPLIT (p.pre, FAST-capable codes, stacked pieces): g_out comes as the
+//   three bf16 pieces already, in the FAST B layout (wg_pieces: per image,
+//   chunk: [piece][co][32 px, pair-permuted]); one TMA box per stage lands
+//   in a B ring read only by the MMA warp, so the operand warps only decode
+//   A.  A CTA whose offsets leave the FAST range (GENERIC-PRE) splits the
+//   reference's fp32 relu(decode) into three bf16 pieces in TMEM as well and
+//   issues A_hi*[hi mid lo] + A_mid*[hi mid] + A_lo*[hi] (the six products
+//   above 2^-24 relative), summed by the same three-group epilogue.
 // Split-K over CTAs (contiguous pixel ranges), fp32 partials, then a
 // deterministic fixed-order float64 reduction into grad_w (layer.py:167).
 #include <cudaTypedefs.h>
@@ -86,6 +94,9 @@ struct WgParams {
     long long *trace;        // debug timeline buffer (qt_debug_wgrad_trace) or NULL
     int trace_cta;
     int Rout;                // rows of dW = ci*kh*kw (partial row stride)
+    int opreg;               // operand ring bytes (FAST and GENERIC strides share it)
+    int pre;                 // g_out arrives pre-split: tmG maps the bf16 pieces
+    int RB;                  // pre: B-piece ring depth (stages of SUB * 3 * BN rows of 64 B)
     FastDiv cpid;            // / chunks_per_img
 };
 
@@ -132,6 +143,16 @@ __device__ __forceinline__ void generic_px(const WgParams &p, const uint8_t *cst
     lv = ok ? __float_as_uint(ll) : 0u;
 }
 
+// x -> three bf16 pieces hi + mid + lo (== x to fp32 precision), packed with
+// a second value y in the high halves (pair words of the FAST layouts)
+__device__ __forceinline__ void split3_bf16x2(float x, float y, uint32_t &H, uint32_t &M,
+                                             uint32_t &L) {
+    H = pack_bf16x2(x, y);
+    const float rx = __fsub_rn(x, bf16_lo(H)), ry = __fsub_rn(y, bf16_hi(H));
+    M = pack_bf16x2(rx, ry);
+    L = pack_bf16x2(__fsub_rn(rx, bf16_lo(M)), __fsub_rn(ry, bf16_hi(M)));
+}
+
 // Operand warps form up to 4 warpgroups (one warp per TMEM lane quarter).
 // With an operand ring of `ops` stages (a power of two <= 4), groups
 // 0..ops-1 are active and group g owns chunks g, g+ops, ... -- so each ring
@@ -156,8 +177,9 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     constexpr int FACC = STACK ? 3 * NT * BN : NT * BN;     // FAST accumulator columns per tile
     constexpr int GACC = NT * BN;                           // GENERIC accumulator columns per tile
     // operand bytes per 32-px chunk: FAST 3 pieces x NT*BN rows x 64 B,
-    // GENERIC (hi, lo) x NT*BN rows x 128 B
-    constexpr int OPB = (3 * NT * BN * 64 > 2 * NT * BN * 128) ? 3 * NT * BN * 64 : 2 * NT * BN * 128;
+    // GENERIC (hi, lo) x NT*BN rows x 128 B (one shared region, p.opreg)
+    constexpr int OPB_F = 3 * NT * BN * 64;
+    constexpr int OPB_G = 2 * NT * BN * 128;
     constexpr int SUB = kWgSub;                             // 32-px chunks per pipeline stage
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1 KiB alignment by pointer arithmetic on the __shared__ array (keeps
@@ -167,13 +189,14 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     // raw ring stage: g box [co][sub][32 px] (SW128 rows of 128 B), then the
     // code box [channel][cb bytes] covering the stage's SUB chunks
     uint8_t *graw = smem;                                   // RG x slot
-    uint8_t *gop = graw + RG * p.slot;                      // OPS x SUB x OPB operands
-    float *s_lut = (float *)(gop + p.OPS * SUB * OPB);      // GENERIC code table (hi, lo)
+    uint8_t *gop = graw + RG * p.slot;                      // operand ring (p.opreg bytes)
+    float *s_lut = (float *)(gop + p.opreg);                // GENERIC code table (hi, lo)
     uint32_t *s_bc = (uint32_t *)(s_lut + p.lut_floats);    // FAST: 0x4300 + b per channel
     uint64_t *bars = (uint64_t *)(s_bc + kWgMaxCh);
     uint64_t *raw_full = bars, *raw_empty = bars + RG;
     uint64_t *op_full = raw_empty + RG, *op_empty = op_full + p.OPS;
-    uint64_t *done = op_empty + p.OPS;
+    uint64_t *b_full = op_empty + p.OPS, *b_empty = b_full + p.RB;   // pre: B-piece ring
+    uint64_t *done = b_empty + p.RB;
     uint32_t *tmem_slot = (uint32_t *)(done + 1);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -190,11 +213,11 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     const int nk = k1 - k0;                                 // chunks of this split
     const int nst = (nk + SUB - 1) / SUB;                   // pipeline stages
     long long *const tr_ =
-        (p.trace && blockIdx.x == (unsigned)p.trace_cta && blockIdx.y == 0) ? p.trace : nullptr;
+        (p.trace && blockIdx.x == (unsigned)p.trace_cta && blockIdx.y == 0 && blockIdx.z == 0) ? p.trace : nullptr;
     if (threadIdx.x == 0) WG_TRACE(0);
     if (threadIdx.x == 0 && tr_)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_[332]));
-    if (threadIdx.x == 0 && p.trace && blockIdx.y == 0 && blockIdx.x < 1024) {
+    if (threadIdx.x == 0 && p.trace && blockIdx.y == 0 && blockIdx.z == 0 && blockIdx.x < 1024) {
         uint32_t sm;
         asm volatile("mov.u32 %0, %%smid;" : "=r"(sm));
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(p.trace[600 + 3 * blockIdx.x]));
@@ -204,6 +227,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     if (threadIdx.x == 0) {
         for (int s = 0; s < RG; ++s) { mbar_init(&raw_full[s], 1); mbar_init(&raw_empty[s], 128); }
         for (int s = 0; s < p.OPS; ++s) { mbar_init(&op_full[s], 128); mbar_init(&op_empty[s], 1); }
+        for (int s = 0; s < p.RB; ++s) { mbar_init(&b_full[s], 1); mbar_init(&b_empty[s], 1); }
         mbar_init(done, 1);
         fence_barrier_init();
     }
@@ -257,6 +281,10 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const int cc = c_begin + e / ncode, code = e % ncode;
                 float a = decode((uint32_t)code, p.tape.step[cc], p.tape.offset[cc], bits);
                 a = (a >= 0.f || isnan(a)) ? a : 0.f;
+                if (p.pre) {   // GENERIC-PRE: the value itself, channel stride 2^K + 1
+                    s_lut[(e / ncode) * (ncode + 1) + code] = a;
+                    continue;
+                }
                 // channel stride 2^(K+1) + 2 floats: lanes on different
                 // channels reading the same code hit different banks
                 float *q = s_lut + (e / ncode) * ((2 << bits) + 2) + 2 * code;
@@ -270,10 +298,27 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     if (threadIdx.x == 64 && tr_)   // an operand thread (warp 0 does not take part in the vote)
         tr_[525] = fast;
     const int ops = fast ? p.OPS : p.OPS_G;
-    const uint32_t acc_cols = (uint32_t)(p.mtg * (fast ? FACC : GACC));
-    const uint32_t acols = fast ? 16u : 64u;                // A columns per tile per stage
+    const bool pre = p.pre != 0;                            // B pieces by TMA (STACK, !TAP)
+    const bool pieces = fast || pre;                        // three-piece accumulator groups
+    const int OPB = pieces ? OPB_F : OPB_G;                 // operand stride per chunk
+    const uint32_t acc_cols = (uint32_t)(p.mtg * (pieces ? FACC : GACC));
+    const uint32_t acols = fast ? 16u : (pre ? 48u : 64u);  // A columns per tile per stage
 
     if (warp == 0) {
+        if (lane == 1 && pre) {  // ------------- TMA producer of the B pieces (pre-split)
+            // its own lane: the code boxes run ahead of the B ring's depth
+            int nn = k0 / p.chunks_per_img, yc = k0 % p.chunks_per_img;
+            int sb = 0;
+            uint32_t phb = 0;
+            for (int st = 0; st < nst; ++st) {
+                mbar_wait(&b_empty[sb], phb ^ 1u);
+                mbar_expect_tx(&b_full[sb], SUB * OPB_F);
+                tma_load_5d(gop + sb * (SUB * OPB_F), &tmG, &b_full[sb], 0, co0, 0, yc, nn);
+                if (++sb == p.RB) { sb = 0; phb ^= 1u; }
+                yc += SUB;
+                if (yc >= p.chunks_per_img) { yc -= p.chunks_per_img; ++nn; }
+            }
+        }
         if (lane == 0) {  // ----------------------------- TMA producer (g_out + codes)
             // one g box and one code box per stage: its SUB chunks are
             // consecutive pixel runs of one image (cps, cpi multiples of SUB)
@@ -285,6 +330,10 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 if (st < 64) WG_TRACE(2 + 5 * st);
                 const int y0 = yc * p.rows_per_chunk;
                 uint8_t *slot = graw + s * p.slot;
+                if (pre) {   // codes -> raw ring (the B pieces: lane 1)
+                    mbar_expect_tx(&raw_full[s], p.cbytes);
+                    tma_load_3d(slot, &tmC, &raw_full[s], ((y0 - p.pad) * p.rb) & ~15, c_begin, nn);
+                } else {
                 mbar_expect_tx(&raw_full[s], SUB * G_BYTES + (p.dbg_nocodes ? 0 : p.cbytes));
                 tma_load_4d(slot, &tmG, &raw_full[s], 0, yc, co0, nn);
                 if (p.lut && !p.dbg_nocodes)   // 16-byte aligned window of input rows y0-pad ..
@@ -293,6 +342,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 else if (p.fbox)               // fp32 rows y0-pad .. (OOB rows zero-filled)
                     tma_load_3d(slot + SUB * G_BYTES, &tmC, &raw_full[s], (y0 - p.pad) * p.ow,
                                 c_begin, nn);
+                }
                 yc += SUB;
                 if (yc >= p.chunks_per_img) { yc -= p.chunks_per_img; ++nn; }
                 if (st < 64) WG_TRACE(336 + 3 * st);
@@ -304,14 +354,15 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         // address field (all operand tiles lie below 256 KiB); the loops are
         // unrolled over the compile-time maxima with predicates, so an MMA
         // costs a couple of uniform adds
-        int o = 0;
-        uint32_t ph = 0;
+        int o = 0, sb = 0;
+        uint32_t ph = 0, phb = 0;
         const uint32_t gop_base = smem_u32(gop);
         const uint64_t dfast = smem_desc(gop_base, 16, 512, 4);    // bf16 SW64 K-major
         const uint64_t dgen = smem_desc(gop_base, 16, 1024, 2);    // tf32 SW128 K-major
         const uint32_t mtg = (uint32_t)p.mtg;
         for (int st = 0; st < nst; ++st) {
             mbar_wait(&op_full[o], ph);
+            if (pre) mbar_wait(&b_full[sb], phb);
             if (lane == 0 && st < 64) WG_TRACE(6 + 5 * st);
             tc_fence_after();
             const int nsub = min(SUB, nk - st * SUB);
@@ -322,7 +373,8 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 #pragma unroll
                     for (int sub = 0; sub < SUB; ++sub) {
                         if (sub >= nsub) break;
-                        const uint32_t off16 = (uint32_t)(((o * SUB + sub) * OPB) >> 4);
+                        const uint32_t off16 =
+                            (uint32_t)((((pre ? sb : o) * SUB + sub) * OPB) >> 4);
                         const uint32_t a =
                             tmem + acc_cols + (((uint32_t)o * mtg + t) * SUB + sub) * acols;
                         const uint32_t first = (st | sub) ? 1u : 0u;   // 0: zero-init D
@@ -342,6 +394,36 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                                                     idesc, (first | j | pc) ? 1u : 0u);
                                 }
                             }
+                        } else if (!STACK && !TAP && pre) {
+                            // GENERIC-PRE, one accumulator: the six products above
+                            // 2^-24 relative, each N = BN
+                            constexpr uint32_t id1 = instr_desc(128, BN, 1, 0, 0);
+                            const uint32_t d = tmem + (uint32_t)(t * FACC);
+                            constexpr uint32_t pb = (BN * 64) >> 4;   // piece block (desc units)
+#pragma unroll
+                            for (int j = 0; j < 2; ++j) {
+                                const uint64_t bh = dfast + off16 + j * 2;
+                                mma_bf16_ts(d, a + j * 8, bh, id1, (first | j) ? 1u : 0u);
+                                mma_bf16_ts(d, a + j * 8, bh + pb, id1, 1u);
+                                mma_bf16_ts(d, a + 16 + j * 8, bh, id1, 1u);
+                                mma_bf16_ts(d, a + 16 + j * 8, bh + pb, id1, 1u);
+                                mma_bf16_ts(d, a + j * 8, bh + 2 * pb, id1, 1u);
+                                mma_bf16_ts(d, a + 32 + j * 8, bh, id1, 1u);
+                            }
+                        } else if (STACK && !TAP && pre) {
+                            // GENERIC-PRE: A pieces (hi, mid, lo) at +0/16/32 columns
+                            // against the stacked B rows [hi | mid | lo]
+                            constexpr uint32_t id3 = instr_desc(128, 3 * BN, 1, 0, 0);
+                            constexpr uint32_t id2 = instr_desc(128, 2 * BN, 1, 0, 0);
+                            constexpr uint32_t id1 = instr_desc(128, BN, 1, 0, 0);
+                            const uint32_t d = tmem + (uint32_t)(t * FACC);
+#pragma unroll
+                            for (int j = 0; j < 2; ++j) {
+                                mma_bf16_ts(d, a + j * 8, dfast + off16 + j * 2, id3,
+                                            (first | j) ? 1u : 0u);
+                                mma_bf16_ts(d, a + 16 + j * 8, dfast + off16 + j * 2, id2, 1u);
+                                mma_bf16_ts(d, a + 32 + j * 8, dfast + off16 + j * 2, id1, 1u);
+                            }
                         } else {
                             constexpr uint32_t idesc = instr_desc(128, GACC, 2, 0, 0);
                             const uint32_t d = tmem + (uint32_t)(t * GACC);
@@ -357,11 +439,13 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     }
                 }
                 mma_commit(&op_empty[o]);
+                if (pre) mma_commit(&b_empty[sb]);
                 if (st == nst - 1) mma_commit(done);
             }
             __syncwarp();
             if (lane == 0 && st < 64) WG_TRACE(401 + 2 * st);
             if (++o == ops) { o = 0; ph ^= 1u; }
+            if (pre && ++sb == p.RB) { sb = 0; phb ^= 1u; }
         }
         if (nst == 0 && lane == 0) mbar_arrive(done);
     } else {  // ---------------------- operand warpgroups + epilogue
@@ -369,7 +453,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         const int quarter = warp & 3;        // TMEM lanes 32*quarter .. +31
         const int tg = threadIdx.x - 64 - 128 * grp;        // 0..127 within the group
         const uint32_t lane_base = tmem + ((uint32_t)(32 * quarter) << 16);
-        const int lut_stride = p.lut ? (2 << p.tape.bits) + 2 : 0;
+        const int lut_stride = !p.lut ? 0 : (p.pre ? (1 << p.tape.bits) + 1 : (2 << p.tape.bits) + 2);
         // this thread's act rows: tile t -> local row t*128 + 32*quarter + lane
         int rc[2], ru[2], rsh[2];
         bool rok[2];
@@ -389,12 +473,16 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         // four groups share every stage -- pixel quads and g items dealt
         // round-robin -- and meet at a named barrier before group 0 arrives.
         const bool coop = !fast;
-        const int sstep = coop ? 1 : ops;
+        // FAST: group g takes stages g, g + G, ... (G = active groups); with
+        // an operand ring deeper than G (pre-split: A only in TMEM, up to 8)
+        // it alternates between op stages g and g + G -- raw slots and op
+        // stages of one group never alias another's (RG, ops multiples of G)
+        const int sstep = coop ? 1 : min(ops, kWgGroups);
         const int gsplit = coop ? grp : 0, gstride = coop ? kWgGroups : 1;
         int st = coop ? 0 : (grp < ops ? grp : nst);   // FAST groups beyond the ring idle
         int s = st % RG;
-        int o = coop ? 0 : grp;               // operand ring stage
-        uint32_t phr = (uint32_t)(st / RG) & 1u, pho = 0u;
+        int o = coop ? 0 : st % ops;          // operand ring stage
+        uint32_t phr = (uint32_t)(st / RG) & 1u, pho = (uint32_t)(st / ops) & 1u;
         for (; st < nst; st += sstep) {
             mbar_wait(&raw_full[s], phr);
             if (tg == 0 && st < 64) WG_TRACE(3 + 5 * st);
@@ -406,13 +494,15 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             const int nn = (int)fast_div((uint32_t)kc0, p.cpid);
             const int ys = (kc0 - nn * p.chunks_per_img) * p.rows_per_chunk;
             const uint8_t *graws = graw + s * p.slot;
-            const uint8_t *cst = graws + SUB * G_BYTES;               // code box
+            const uint8_t *cst = graws + (pre ? 0 : SUB * G_BYTES);   // code box
             const int wbase = p.fbox ? (ys - p.pad) * p.rb                // its first byte
                                      : ((ys - p.pad) * p.rb) & ~15;
             for (int sub = 0; sub < nsub; ++sub) {
             const int y0 = ys + sub * p.rows_per_chunk;
             uint8_t *opb = gop + (o * SUB + sub) * OPB;
-            if (TAP) {
+            if (pre) {
+                // B pieces arrive by TMA (B ring)
+            } else if (TAP) {
                 // g -> the three column-shifted copies B_v[x] = g[x - v + 1]
                 // (zero outside the image row); FAST: bf16 pieces, rows
                 // (piece, v, co), pair-permuted K; GENERIC: TF32 (hi, lo),
@@ -633,6 +723,37 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     }
                     if (tg == 0 && st < 64 && t == 0) WG_TRACE(3701 + 4 * st + 2 * sub);
                     tmem_st16(lane_base + acol, av);
+                } else if (FAST_OK && !TAP && pre) {
+                    // GENERIC-PRE: the reference's fp32 relu(decode) (table hi +
+                    // lo, exact) as three bf16 pieces in pair words (k, k + 4)
+                    // like the B rows; each group takes one 8-pixel group
+                    const float *lut = s_lut + (size_t)(c - c_begin) * lut_stride;
+                    const bool live = rok[t];
+#pragma unroll 1
+                    for (int q8 = gsplit; q8 < 4; q8 += gstride) {
+                        float a8[8];
+#pragma unroll
+                        for (int k = 0; k < 8; ++k) {
+                            const int i = 8 * q8 + k;
+                            const int seg = i / OW, x = i - seg * OW;
+                            const int iy = y0 + seg + u - p.pad, sx = x + sh;
+                            float a = 0.f;
+                            if (live && iy >= 0 && iy < p.h && sx >= 0 && sx < OW) {
+                                const uint32_t *cw = reinterpret_cast<const uint32_t *>(cst);
+                                const int bp = (cbox + iy * p.rb - wbase) * 8 + sx * BITS;
+                                const uint32_t code = __funnelshift_r(cw[bp >> 5], cw[(bp >> 5) + 1],
+                                                                      bp & 31) & ((1u << BITS) - 1u);
+                                a = lut[code];
+                            }
+                            a8[k] = a;
+                        }
+                        uint32_t H[4], M[4], L[4];
+#pragma unroll
+                        for (int k = 0; k < 4; ++k) split3_bf16x2(a8[k], a8[k + 4], H[k], M[k], L[k]);
+                        tmem_st4(lane_base + acol + 4 * q8, H[0], H[1], H[2], H[3]);
+                        tmem_st4(lane_base + acol + 16 + 4 * q8, M[0], M[1], M[2], M[3]);
+                        tmem_st4(lane_base + acol + 32 + 4 * q8, L[0], L[1], L[2], L[3]);
+                    }
                 } else {
                     // a compact loop of 4-pixel quads (x4 TMEM stores): the
                     // fully unrolled form overflows the instruction cache
@@ -674,12 +795,9 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 mbar_arrive(&op_full[o]);
             }
             s += sstep;
-            if (s >= RG) { s -= RG; phr ^= 1u; }   // RG is a multiple of ops
-            if (coop) {
-                if (++o == ops) { o = 0; pho ^= 1u; }
-            } else {
-                pho ^= 1u;                          // same stage (o == grp), next round
-            }
+            if (s >= RG) { s -= RG; phr ^= 1u; }   // RG is a multiple of sstep
+            o += sstep;
+            if (o >= ops) { o -= ops; pho ^= 1u; }
         }
         // epilogue: all four groups drain TMEM -- items (tile, tap, 16-column
         // chunk) dealt round-robin over the groups, each warp its lane
@@ -709,9 +827,9 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             const bool ok = rl < nrows;
             const int r = row0 + rl;
             const int rout = TAP ? r * 3 + v : r;            // dW row (ci, u, v); TAP rows (ci, u)
-            const uint32_t tbase = lane_base + (uint32_t)t * (fast ? FACC : GACC);
+            const uint32_t tbase = lane_base + (uint32_t)t * (pieces ? FACC : GACC);
             uint32_t r0[16], r1[16], r2[16];
-            if (fast && STACK) {
+            if (pieces && STACK) {
                 tmem_ld16(tbase + (0 * NT + v) * BN + cb, r0);
                 tmem_ld16(tbase + (1 * NT + v) * BN + cb, r1);
                 tmem_ld16(tbase + (2 * NT + v) * BN + cb, r2);
@@ -725,7 +843,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 #pragma unroll
                 for (int j = 0; j < 16; ++j) {
                     float acc = __uint_as_float(r0[j]);
-                    if (fast && STACK)   // hi + (mid + lo): the small pieces first
+                    if (pieces && STACK)   // hi + (mid + lo): the small pieces first
                         acc = __fadd_rn(acc, __fadd_rn(__uint_as_float(r1[j]), __uint_as_float(r2[j])));
                     const float val = fast ? __fmul_rn(acc, sc) : acc;
                     if (co0 + cb + j < p.co) dst[(int64_t)j * p.Rout] = val;
@@ -738,7 +856,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     if (threadIdx.x == 0) WG_TRACE(331);
     if (threadIdx.x == 0 && tr_)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(tr_[333]));
-    if (threadIdx.x == 0 && p.trace && blockIdx.y == 0 && blockIdx.x < 1024)
+    if (threadIdx.x == 0 && p.trace && blockIdx.y == 0 && blockIdx.z == 0 && blockIdx.x < 1024)
         asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(p.trace[601 + 3 * blockIdx.x]));
     if (warp == 1) {
         tc_fence_after();
@@ -752,6 +870,8 @@ struct WgPlan {
     int ops = 0, ops_g = 0;                               // FAST / GENERIC operand stages
     int nch = 0, rb = 0, cb = 0, cbytes = 0, slot = 0;    // code box (codes tapes)
     int lut_floats = 0;
+    int opreg = 0;                                        // operand region bytes
+    int pre = 0, bring = 0;                               // pieces by TMA; B ring depth
     int tap = 0, rpc = 0;                                 // column taps in N; A rows per channel
     int fbox = 0;                                         // fp32 source boxed per stage
     int nblk = 1;                                         // output-channel blocks of BN

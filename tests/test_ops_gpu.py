@@ -265,20 +265,25 @@ def test_transition_wgrad_from_codes(shape, bits):
                                    (2, 64, 8, 320, 1), (2, 16, 56, 32, 1), (1, 64, 24, 64, 1),
                                    (2, 16, 56, 32, 3), (2, 64, 14, 64, 3), (2, 64, 7, 128, 3),
                                    (2, 32, 28, 32, 3), (2, 64, 14, 64, 1), (2, 32, 7, 64, 1),
-                                   (2, 16, 28, 32, 1)])
-def test_wgrad_from_codes_channel_blocks(shape):
-    """Weight gradient from a 4-bit tape for outputs wider than one 64-channel
-    block (grid z) -- FAST and GENERIC CTAs -- against float64."""
+                                   (2, 16, 28, 32, 1), (2, 256, 14, 256, 1), (2, 128, 7, 256, 3),
+                                   (1, 512, 7, 128, 1)])
+@pytest.mark.parametrize("bits", [2, 4])
+def test_wgrad_from_codes_channel_blocks(shape, bits):
+    """Weight gradient from a 2-/4-bit tape for outputs wider than one
+    64-channel block (grid z) -- FAST and GENERIC CTAs, and on the segmented
+    planes (14/7/28 px) the pre-split g_out pieces path (FAST-PRE and
+    GENERIC-PRE) -- against float64."""
     from paper_1901_07988_b200 import codec
     n, ci, hw, co, k = shape
-    torch.manual_seed(co + k)
-    for regime in ("narrow", "wide"):
+    torch.manual_seed(co + k + bits)
+    for regime in ("narrow", "wide", "mixed"):
         x = torch.randn(n, ci, hw, hw, device="cuda")
-        if regime == "narrow":
-            gamma, beta = torch.rand(ci, device="cuda") + 0.5, torch.randn(ci, device="cuda") * 0.1
-        else:
-            gamma, beta = torch.rand(ci, device="cuda") * 0.05 + 0.05, torch.rand(ci, device="cuda") + 1.5
-        t = codec.quantize(x, gamma, beta, 4)
+        gamma, beta = torch.rand(ci, device="cuda") + 0.5, torch.randn(ci, device="cuda") * 0.1
+        if regime != "narrow":
+            wide = torch.arange(ci, device="cuda") % (1 if regime == "wide" else 7) == 0
+            gamma = torch.where(wide, torch.rand(ci, device="cuda") * 0.05 + 0.05, gamma)
+            beta = torch.where(wide, torch.rand(ci, device="cuda") + 1.5, beta)
+        t = codec.quantize(x, gamma, beta, bits)
         act = codec.dequantize(t, relu=True)
         g = torch.randn(n, co, hw, hw, device="cuda")
         gw = torch.zeros(co, ci, k, k, device="cuda")
