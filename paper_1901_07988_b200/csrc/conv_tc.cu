@@ -1864,7 +1864,26 @@ int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float
 int qt_tc_conv_wgrad_pre(const void *pieces, qt_tape_t act, float *grad_w, const qt::ConvGeo &g,
                          void *ws, cudaStream_t st);
 bool qt_tc_wgrad_pre_ok(const qt::ConvGeo &g, int bits);
+int qt_tc_conv_wgrad_fp32(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
+                          const qt::ConvGeo &g, void *ws, cudaStream_t st);
 int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g);
+int64_t qt_tc_wgrad_partial_workspace(const qt::ConvGeo &g);
+
+// g_out (n, co, h, w) of an unsegmented plane (h * w % 32 == 0) into the
+// weight gradient's bf16 pieces (seg_pieces_kernel on a flat geometry)
+int qt_tc_wgrad_pieces(const float *g, void *dst, int64_t n, int64_t co, int64_t h, int64_t w,
+                       cudaStream_t st) {
+    if ((h * w) % 32 || ((uintptr_t)dst & 15) || n * co * h * w >= (1ll << 31)) return QT_EUNSUPPORTED;
+    SegGeo s{};
+    s.ok = 1; s.flat = 1; s.sd = 1; s.owt = 32; s.halo = 0; s.nseg = 1; s.step = 32;
+    s.hp = (int)(h * w / 32);
+    const uint32_t groups = (uint32_t)(n * co * h * w / 8);
+    launch_pdl(seg_pieces_kernel, seg_blocks(groups), 256, 0, st, g, (uint4 *)dst, groups, (int)co,
+               (int)h, (int)w, s, seg_div(s, co, w), make_fastdiv((uint32_t)co),
+               make_fastdiv((uint32_t)(h * w / 32)));
+    QT_CHECK_LAUNCH();
+    return QT_OK;
+}
 
 static qt::ConvGeo seg_wgrad_geo(const qt::ConvGeo &g, const SegGeo &s) {
     qt::ConvGeo d = g;
@@ -1889,7 +1908,7 @@ static SegGeo seg_geo_wgrad(const qt::ConvGeo &g) {
 int64_t qt_tc_seg_wgrad_workspace(const qt::ConvGeo &g) {
     const SegGeo s = seg_geo_wgrad(g);
     if (!s.ok) return 0;
-    const int64_t part = (qt_tc_wgrad_workspace(seg_wgrad_geo(g, s)) + 255) / 256 * 256;
+    const int64_t part = (qt_tc_wgrad_partial_workspace(seg_wgrad_geo(g, s)) + 255) / 256 * 256;
     // g_out region: fp32 (4 B) or bf16 pieces (6 B per element)
     const int64_t gbytes = (6 * seg_elems(s, g.n, g.co) + 255) / 256 * 256;
     return part + gbytes + 4 * seg_elems(s, g.n, g.ci * s.sd * s.sd) + g.ci * s.sd * s.sd * 16 + 1024;
@@ -1905,7 +1924,7 @@ int qt_tc_conv_seg_wgrad(const float *gr, qt_tape_t act, const float *x_plain, f
     const int64_t cin = g.ci * (s.flat ? s.sd * s.sd : 1);
     if (!seg_fits(s, g.n, cin, g.h, g.w) || !seg_fits(s, g.n, g.co, g.h, g.w)) return QT_EUNSUPPORTED;
     const qt::ConvGeo d = seg_wgrad_geo(g, s);
-    const int64_t part = (qt_tc_wgrad_workspace(d) + 255) / 256 * 256;
+    const int64_t part = (qt_tc_wgrad_partial_workspace(d) + 255) / 256 * 256;
     if (part <= 0) return QT_EUNSUPPORTED;
     float *gs = (float *)((char *)ws + part);
     float *as = (float *)((char *)gs + (6 * seg_elems(s, g.n, g.co) + 255) / 256 * 256);
@@ -1940,12 +1959,12 @@ int qt_tc_conv_seg_wgrad(const float *gr, qt_tape_t act, const float *x_plain, f
         QT_CHECK_LAUNCH();
         qt_tape_t t2{nullptr, (const uint8_t *)cw, step4, off4, act.bits};
         rc = pre ? qt_tc_conv_wgrad_pre(gs, t2, grad_w, d, ws, st)
-                 : qt_tc_conv_wgrad(gs, t2, nullptr, grad_w, d, ws, st);
+                 : qt_tc_conv_wgrad_fp32(gs, t2, nullptr, grad_w, d, ws, st);
         if (rc == QT_EUNSUPPORTED && pre) {   // the fp32 plane for the paths below
             pre = false;
             rc = seg_in<1>(gr, qt_tape_t{}, gs, g.n, g.co, gh, gw, sg, st);
             if (rc) return rc;
-            rc = qt_tc_conv_wgrad(gs, t2, nullptr, grad_w, d, ws, st);
+            rc = qt_tc_conv_wgrad_fp32(gs, t2, nullptr, grad_w, d, ws, st);
         }
         if (rc != QT_EUNSUPPORTED) {
             if (rc || s.flat) return rc;
@@ -1958,5 +1977,5 @@ int qt_tc_conv_seg_wgrad(const float *gr, qt_tape_t act, const float *x_plain, f
     }
     rc = seg_in<2>(x_plain, act, as, g.n, cin, g.h, g.w, s, st);
     if (rc) return rc;
-    return qt_tc_conv_wgrad(gs, qt_tape_t{}, as, grad_w, d, ws, st);
+    return qt_tc_conv_wgrad_fp32(gs, qt_tape_t{}, as, grad_w, d, ws, st);
 }

@@ -328,12 +328,8 @@ static int64_t wg_s2d_bytes(const ConvGeo &g, int bits) {   // codes' + step' + 
 
 }  // namespace qt
 
-int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g) {
-    if (wg_flat_shape(g)) return qt_tc_wgrad_workspace(wg_flat_geo(g));
-    if (wg_s2d_shape(g, 8)) {   // the 2x2/s2 rearranged-codes path (widest code width)
-        const ConvGeo d = wg_s2d_geo(g);
-        return wg_s2d_bytes(g, 8) + qt_tc_wgrad_workspace(d);
-    }
+// fp32 split-K partials of every plan this geometry may take
+static int64_t wg_partial_bytes(const ConvGeo &g) {
     WgPlan a = wg_plan(g, 4), b = wg_plan(g, 0), c = wg_plan(g, 4, true), e = wg_plan(g, 0, false, true);
     int64_t sp = std::max(a.ok ? a.splits : 0, b.ok ? b.splits : 0);
     sp = std::max(sp, (int64_t)(c.ok ? c.splits : 0));
@@ -347,6 +343,41 @@ int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g) {
         sp = std::max(sp, (int64_t)(q.ok ? q.splits : 0));
     }
     return sp * g.co * g.ci * g.kh * g.kw * (int64_t)sizeof(float);
+}
+
+// direct (unsegmented) planes: the in-kernel split stays the default -- an
+// extra pieces pass measured slower on every C2 layer (e.g. 64->16 1x1 at
+// 32x32: 13.9 -> 18.9 us) and on the C4 56x56 layers; QTAPE_WG_PRE_DIRECT=1
+// opts in
+static bool wg_direct_pre_on() {
+    static const bool on = [] {
+        const char *e = getenv("QTAPE_WG_PRE_DIRECT");
+        return e && *e && *e != '0';
+    }();
+    return on;
+}
+
+static bool wg_direct_pre(const ConvGeo &g, int bits) {
+    if (!wg_direct_pre_on() || (g.oh * g.ow) % 32) return false;
+    return wg_plan(g, bits, false, false, true).ok;
+}
+
+static int64_t wg_pieces_bytes(const ConvGeo &g) { return 6 * g.n * g.co * g.oh * g.ow; }
+
+int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g) {
+    if (wg_flat_shape(g)) return qt_tc_wgrad_workspace(wg_flat_geo(g));
+    if (wg_s2d_shape(g, 8)) {   // the 2x2/s2 rearranged-codes path (widest code width)
+        const ConvGeo d = wg_s2d_geo(g);
+        return wg_s2d_bytes(g, 8) + qt_tc_wgrad_workspace(d);
+    }
+    int64_t b = wg_partial_bytes(g);
+    if (wg_direct_pre(g, 4) || wg_direct_pre(g, 2)) b = (b + 255) / 256 * 256 + wg_pieces_bytes(g);
+    return b;
+}
+
+// partials only: the segmented path keeps its own planes behind them
+int64_t qt_tc_wgrad_partial_workspace(const qt::ConvGeo &g) {
+    return wg_partial_bytes(wg_flat_shape(g) ? wg_flat_geo(g) : g);
 }
 
 // debug hook (not part of the public ABI): buf = 600 + 3*1024 int64 stamps or NULL
@@ -494,8 +525,25 @@ static int wgrad_tc(const float *gr, const void *pieces, qt_tape_t act, const fl
     return qt_tc_wgrad_reduce((const float *)ws, pl.splits, g.co * p.Rout, grad_w, st);
 }
 
+int qt_tc_wgrad_pieces(const float *g, void *dst, int64_t n, int64_t co, int64_t h, int64_t w,
+                       cudaStream_t st);
+
 int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
-                     const qt::ConvGeo &g, void *ws, cudaStream_t st) {
+                     const qt::ConvGeo &g0, void *ws, cudaStream_t st) {
+    const ConvGeo g = wg_flat_shape(g0) ? wg_flat_geo(g0) : g0;
+    if (!x_plain && !act.a2 && act.codes && ws && wg_direct_pre(g, act.bits)) {
+        void *pieces = (char *)ws + (wg_partial_bytes(g) + 255) / 256 * 256;
+        int rc = qt_tc_wgrad_pieces(gr, pieces, g.n, g.co, g.oh, g.ow, st);
+        if (rc) return rc;
+        rc = wgrad_tc(nullptr, pieces, act, nullptr, grad_w, g, ws, st);
+        if (rc != QT_EUNSUPPORTED) return rc;
+    }
+    return wgrad_tc(gr, nullptr, act, x_plain, grad_w, g0, ws, st);
+}
+
+// the fp32 g_out path only (the segmented path's planes follow the partials)
+int qt_tc_conv_wgrad_fp32(const float *gr, qt_tape_t act, const float *x_plain, float *grad_w,
+                          const qt::ConvGeo &g, void *ws, cudaStream_t st) {
     return wgrad_tc(gr, nullptr, act, x_plain, grad_w, g, ws, st);
 }
 

@@ -234,6 +234,45 @@ print("ok")
     assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
 
 
+def test_wgrad_direct_pieces_form_matches():
+    """The opt-in pre-split g_out pieces on unsegmented planes
+    (QTAPE_WG_PRE_DIRECT=1, read once per process): 1x1 / 3x3 on 8/16/32-px
+    rows and a 56x56 flat plane, 2- and 4-bit tapes, narrow / wide / mixed
+    channels, against float64."""
+    import os
+    import subprocess
+    import sys
+    code = r'''
+import torch
+from paper_1901_07988_b200 import codec, ops
+torch.manual_seed(1)
+for bits in (2, 4):
+    for regime in ("narrow", "wide", "mixed"):
+        for n, ci, hw, co, k in ((2, 16, 32, 64, 1), (2, 32, 16, 32, 3), (4, 256, 8, 64, 1),
+                                 (2, 64, 8, 256, 1), (1, 64, 56, 128, 1)):
+            x = torch.randn(n, ci, hw, hw, device="cuda")
+            gamma, beta = torch.rand(ci, device="cuda") + 0.5, torch.randn(ci, device="cuda") * 0.1
+            if regime != "narrow":
+                wide = torch.arange(ci, device="cuda") % (1 if regime == "wide" else 3) == 0
+                gamma = torch.where(wide, torch.rand(ci, device="cuda") * 0.05 + 0.05, gamma)
+                beta = torch.where(wide, torch.rand(ci, device="cuda") + 1.5, beta)
+            t = codec.quantize(x, gamma, beta, bits)
+            act = codec.dequantize(t, relu=True)
+            g = torch.randn(n, co, hw, hw, device="cuda")
+            gw = torch.zeros(co, ci, k, k, device="cuda")
+            ops.conv2d_wgrad(g, (co, ci, k, k), 1, k // 2, gw, tape=t.as_native(), in_shape=(n, ci, hw, hw))
+            ref = torch.nn.grad.conv2d_weight(act.double(), (co, ci, k, k), g.double(), padding=k // 2)
+            err = ((gw.double() - ref).norm() / ref.norm()).item()
+            assert err < 1e-5, (bits, regime, ci, co, k, err)
+print("ok")
+'''
+    env = dict(os.environ, QTAPE_WG_PRE_DIRECT="1")
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", code], env=env, cwd=root, capture_output=True,
+                       text=True, timeout=300)
+    assert r.returncode == 0 and "ok" in r.stdout, r.stderr[-2000:]
+
+
 @pytest.mark.parametrize("bits", [1, 2, 4, 8])
 @pytest.mark.parametrize("shape", [(2, 32, 32, 32), (4, 64, 16, 64), (2, 16, 8, 16),
                                    (2, 32, 56, 64), (2, 64, 14, 32), (2, 3, 224, 64, 4),
