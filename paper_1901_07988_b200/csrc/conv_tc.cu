@@ -1600,28 +1600,43 @@ __global__ void seg_codes_kernel(const uint8_t *codes, uint32_t *dst, uint32_t w
     const uint32_t wd = (uint32_t)w / sd, pl = (uint32_t)h / sd * wd;
     const uint32_t cs = (uint32_t)c4 / sd2;
     const uint32_t *src32 = reinterpret_cast<const uint32_t *>(codes);   // 16-byte aligned tape
+    const uint32_t owt_log2 = s.owt == 8 ? 3u : (s.owt == 16 ? 4u : 5u);
     for (uint32_t o = tid; o < words; o += gridDim.x * blockDim.x) {
         const uint32_t m = fast_div(o, pwd), wi = o - m * pw;
         uint32_t acc = 0;
-        // the word's codes are one contiguous run of the source tape: extract
-        // its 32 bits with a funnel shift across two aligned words
-        int64_t run = -1;
+        // the word's codes are one run of a source row (flat plane, or a
+        // segment row: owt is a multiple of the codes per word): the valid
+        // codes [klo, khi) come out of two aligned source words with one
+        // funnel shift, the rest of the word is zero padding
+        int64_t row = 0;              // code index of the word's first position
+        int klo = 0, khi = 0;         // its valid positions (none: all padding)
+        const bool run = (s.flat && sd == 1) || (!s.flat && per <= (uint32_t)s.owt);
         if (s.flat && sd == 1) {
-            if ((wi + 1) * per <= pl) run = (int64_t)m * pl + wi * per;
+            row = (int64_t)m * pl + wi * per;
+            khi = min((int)per, (int)pl - (int)(wi * per));
         } else if (!s.flat && per <= (uint32_t)s.owt) {
             const uint32_t img = fast_div(m, c4d), ch = m - img * (uint32_t)c4;
             const uint32_t nn = fast_div(img, nsegd), j = img - nn * (uint32_t)s.nseg;
-            const uint32_t p0 = wi * per, y = p0 / (uint32_t)s.owt, kx = p0 - y * (uint32_t)s.owt;
+            const uint32_t p0 = wi * per, y = p0 >> owt_log2, kx = p0 & ((uint32_t)s.owt - 1u);
             const int col = (int)(j * s.step + kx) - s.halo;
-            if (y < (uint32_t)h && col >= 0 && col + (int)per <= w)
-                run = (((int64_t)nn * c4 + ch) * h + y) * w + col;
+            if (y < (uint32_t)h) {
+                row = (((int64_t)nn * c4 + ch) * h + y) * w + col;
+                klo = max(0, -col);
+                khi = min((int)per, w - col);
+            }
         }
-        if (run >= 0) {
-            const int64_t bit = run * bits;
-            const int64_t q = bit >> 5;
-            const uint32_t sh = (uint32_t)(bit & 31);
-            const uint32_t lo = __ldg(src32 + q);
-            dst[o] = sh ? __funnelshift_r(lo, __ldg(src32 + q + 1), sh) : lo;
+        if (run) {
+            if (khi > klo) {
+                const int64_t bit = (row + klo) * bits;
+                const int64_t q = bit >> 5;
+                const uint32_t sh = (uint32_t)(bit & 31);
+                const uint32_t lo = __ldg(src32 + q);
+                uint32_t v = sh ? __funnelshift_r(lo, __ldg(src32 + q + 1), sh) : lo;
+                const int nv = khi - klo;
+                if (nv * bits < 32) v &= (1u << (nv * bits)) - 1u;
+                acc = v << (klo * bits);
+            }
+            dst[o] = acc;
             continue;
         }
         if (s.flat) {
