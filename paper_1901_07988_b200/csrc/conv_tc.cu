@@ -1507,6 +1507,80 @@ __device__ __forceinline__ bool seg_src(uint32_t i, int c, int h, int w, const S
     return ok;
 }
 
+// Four consecutive elements i0..i0+3 of a segmented plane (i0 % 4 == 0: owt
+// and the flat plane are multiples of 4, so they share one source row): the
+// source index of the first and the valid positions [klo, khi); false for
+// the space-to-depth flat form (sd > 1), which maps element by element.
+template <int MODE>
+__device__ __forceinline__ bool seg_src4(uint32_t i0, int c, int h, int w, const SegGeo &s,
+                                         const SegDiv &dv, int64_t &si, int &tc, int &klo,
+                                         int &khi) {
+    klo = 0;
+    khi = 4;
+    if (s.flat) {
+        if (s.sd != 1) return false;
+        const uint32_t m = fast_div(i0, dv.plane), p = i0 - m * (uint32_t)(s.hp * s.owt);
+        si = (int64_t)m * (uint32_t)(h * w) + p;
+        tc = (int)(m - fast_div(m, dv.c) * (uint32_t)c);
+        khi = max(0, min(4, h * w - (int)p));
+        return true;
+    }
+    const uint32_t k = i0 & ((uint32_t)s.owt - 1u), r = i0 >> dv.owt_log2;
+    const uint32_t r2 = fast_div(r, dv.hp), y = r - r2 * (uint32_t)s.hp;
+    const uint32_t m = fast_div(r2, dv.c), ch = r2 - m * (uint32_t)c;
+    const uint32_t nn = fast_div(m, dv.nseg), j = m - nn * (uint32_t)s.nseg;
+    const int col = (int)(j * s.step + k) - s.halo;
+    si = (((int64_t)nn * c + ch) * h + y) * w + col;
+    tc = (int)ch;
+    klo = max(0, -col);
+    khi = min(4, w - col);
+    if (MODE == 1) {
+        klo = max(klo, s.halo - (int)k);
+        khi = min(khi, s.halo + s.step - (int)k);
+    }
+    if (y >= (uint32_t)h) khi = 0;
+    return true;
+}
+
+template <int MODE>
+__global__ void seg_in4_kernel(const float *src, qt_tape_t t, float *dst, uint32_t total, int c,
+                               int h, int w, SegGeo s, SegDiv dv) {
+    pdl_enter();
+    const uint32_t quads = total >> 2;
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < quads; q += gridDim.x * blockDim.x) {
+        int64_t si;
+        int tc, klo, khi;
+        float v[4] = {0.f, 0.f, 0.f, 0.f};
+        if (seg_src4<MODE>(4 * q, c, h, w, s, dv, si, tc, klo, khi)) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (k < klo || k >= khi) continue;
+                if (MODE != 2 || src) {
+                    v[k] = __ldg(src + si + k);
+                } else {
+                    const float a = tape_value(t, si + k, tc);
+                    v[k] = (a >= 0.f || isnan(a)) ? a : 0.f;
+                }
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                int64_t sk;
+                int tk;
+                if (seg_src<MODE>(4 * q + k, c, h, w, s, dv, sk, tk)) {
+                    if (MODE != 2 || src) {
+                        v[k] = __ldg(src + sk);
+                    } else {
+                        const float a = tape_value(t, sk, tk);
+                        v[k] = (a >= 0.f || isnan(a)) ? a : 0.f;
+                    }
+                }
+            }
+        }
+        reinterpret_cast<float4 *>(dst)[q] = make_float4(v[0], v[1], v[2], v[3]);
+    }
+}
+
 template <int MODE>
 __global__ void seg_in_kernel(const float *src, qt_tape_t t, float *dst, uint32_t total, int c,
                               int h, int w, SegGeo s, SegDiv dv) {
@@ -1728,30 +1802,54 @@ __global__ void seg_pad_fix_kernel(const float *g, float *grad_w, int n, int co_
 
 // out (n, c, h, w) [+ shortcut res (n, cr, h*sr, w*sr), engine.py:262-269]
 // from the segmented conv result (n*nseg, c, hp, owt)
-__global__ void seg_out_kernel(const float *src, float *out, uint32_t total, int c, int h, int w,
-                               SegGeo s, const float *res, int cr, int sr) {
+// Unsegment: out (n, c, h, w) from the segmented / flattened plane (+ the
+// shortcut add).  Four pixels x0..x0+3 of one output row per thread (rows
+// padded to whole quads in the index space), FastDiv index math.
+__global__ void seg_out4_kernel(const float *src, float *out, uint32_t quads, int c, int h, int w,
+                                SegGeo s, const float *res, int cr, int sr, FastDiv gprd,
+                                FastDiv hd, FastDiv cd, FastDiv stepd, FastDiv sdd) {
     pdl_enter();
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-        const uint32_t x = i % (uint32_t)w, r = i / (uint32_t)w;
-        const uint32_t y = r % (uint32_t)h, r2 = r / (uint32_t)h;
-        const uint32_t ch = r2 % (uint32_t)c, nn = r2 / (uint32_t)c;
-        float v;
-        if (s.flat) {   // src (n, c sd^2, hp * owt): flattened (space-to-depth) plane
-            const uint32_t sd = (uint32_t)s.sd, Y = y / sd, u = y - Y * sd, X = x / sd, vv = x - X * sd;
-            const uint32_t cs = (ch * sd + u) * sd + vv;
-            v = __ldg(src + ((size_t)nn * c * sd * sd + cs) * ((size_t)s.hp * s.owt) +
-                      Y * ((uint32_t)w / sd) + X);
-        } else {
-            const uint32_t j = x / (uint32_t)s.step, k = x - j * s.step + s.halo;
-            const uint32_t m = nn * s.nseg + j;
-            v = __ldg(src + (((size_t)m * c + ch) * s.hp + y) * s.owt + k);
+    const uint32_t gpr = (uint32_t)(w + 3) >> 2;
+    const size_t plane_s = (size_t)s.hp * s.owt;
+    for (uint32_t q = blockIdx.x * blockDim.x + threadIdx.x; q < quads; q += gridDim.x * blockDim.x) {
+        const uint32_t r = fast_div(q, gprd), xq = q - r * gpr;
+        const uint32_t r2 = fast_div(r, hd), y = r - r2 * (uint32_t)h;
+        const uint32_t nn = fast_div(r2, cd), ch = r2 - nn * (uint32_t)c;
+        const size_t obase = ((size_t)r2 * h + y) * w;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const uint32_t x = 4 * xq + k;
+            if (x >= (uint32_t)w) break;
+            float v;
+            if (s.flat) {
+                const uint32_t sd = (uint32_t)s.sd;
+                const uint32_t Y = fast_div(y, sdd), u = y - Y * sd, X = fast_div(x, sdd), vv = x - X * sd;
+                const uint32_t cs = (ch * sd + u) * sd + vv;
+                v = __ldg(src + ((size_t)nn * c * sd * sd + cs) * plane_s + Y * ((uint32_t)w / sd) + X);
+            } else {
+                const uint32_t j = fast_div(x, stepd), kk = x - j * s.step + s.halo;
+                const uint32_t m = nn * s.nseg + j;
+                v = __ldg(src + (((size_t)m * c + ch) * s.hp + y) * s.owt + kk);
+            }
+            if (res && (int)ch < cr)
+                v = __fadd_rn(v, __ldg(res + (((size_t)nn * cr + ch) * h * sr + (size_t)y * sr) * w * sr +
+                                       (size_t)x * sr));
+            out[obase + x] = v;
         }
-        if (res && (int)ch < cr)
-            v = __fadd_rn(v, __ldg(res + (((size_t)nn * cr + ch) * h * sr + (size_t)y * sr) * w * sr +
-                                   (size_t)x * sr));
-        out[i] = v;
     }
 }
+
+static unsigned seg_blocks(int64_t total);
+
+static void launch_seg_out(const float *src, float *out, int64_t n, int64_t c, int64_t h, int64_t w,
+                           const SegGeo &s, const float *res, int64_t cr, int64_t sr, cudaStream_t st) {
+    const int64_t gpr = (w + 3) / 4, quads = n * c * h * gpr;
+    launch_pdl(seg_out4_kernel, seg_blocks(quads), 256, 0, st, src, out, (uint32_t)quads, (int)c,
+               (int)h, (int)w, s, res, (int)cr, (int)sr, make_fastdiv((uint32_t)gpr),
+               make_fastdiv((uint32_t)h), make_fastdiv((uint32_t)c),
+               make_fastdiv((uint32_t)std::max(1, s.step)), make_fastdiv((uint32_t)std::max(1, s.sd)));
+}
+
 
 static int64_t seg_elems(const SegGeo &s, int64_t n, int64_t c) {
     return n * s.nseg * c * s.hp * s.owt;
@@ -1765,8 +1863,12 @@ template <int MODE>
 static int seg_in(const float *src, qt_tape_t t, float *dst, int64_t n, int64_t c, int64_t h,
                   int64_t w, const SegGeo &s, cudaStream_t st) {
     const int64_t total = seg_elems(s, n, c);
-    launch_pdl(seg_in_kernel<MODE>, seg_blocks(total), 256, 0, st, src, t, dst, (uint32_t)total,
-               (int)c, (int)h, (int)w, s, seg_div(s, c, w));
+    if (total % 4 == 0 && ((uintptr_t)dst & 15) == 0)   // one float4 per thread
+        launch_pdl(seg_in4_kernel<MODE>, seg_blocks(total / 4), 256, 0, st, src, t, dst,
+                   (uint32_t)total, (int)c, (int)h, (int)w, s, seg_div(s, c, w));
+    else
+        launch_pdl(seg_in_kernel<MODE>, seg_blocks(total), 256, 0, st, src, t, dst, (uint32_t)total,
+                   (int)c, (int)h, (int)w, s, seg_div(s, c, w));
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -1794,9 +1896,7 @@ static int seg_conv(const float *x, const float *w, float *out, int64_t n, int64
     rc = tc_conv_s1(xs, w, os, (int)(n * s.nseg), (int)ci, s.hp, s.owt, (int)co, 3, 3, 1, flip,
                     nullptr, 0, 1, ws, st);
     if (rc) return rc;
-    const int64_t total = n * co * h * wd;
-    launch_pdl(seg_out_kernel, seg_blocks(total), 256, 0, st, (const float *)os, out,
-               (uint32_t)total, (int)co, (int)h, (int)wd, s, res, (int)cr, (int)sr);
+    launch_seg_out(os, out, n, co, h, wd, s, res, cr, sr, st);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
@@ -1825,17 +1925,13 @@ static int seg_conv_flat(const float *src, const float *w, float *dst, int64_t n
         if (rc) return rc;
         rc = tc_conv_s1(xs, w, os, (int)n, (int)c4, s.hp, s.owt, (int)co, 1, 1, 0, 0, nullptr, 0, 1, ws, st);
         if (rc) return rc;
-        const int64_t total = n * co * oh * ow;
-        launch_pdl(seg_out_kernel, seg_blocks(total), 256, 0, st, (const float *)os, dst,
-                   (uint32_t)total, (int)co, (int)oh, (int)ow, s1, res, (int)cr, (int)sr);
+        launch_seg_out(os, dst, n, co, oh, ow, s1, res, cr, sr, st);
     } else {
         rc = seg_in<0>(src, qt_tape_t{}, xs, n, co, oh, ow, s1, st);
         if (rc) return rc;
         rc = tc_conv_s1(xs, w, os, (int)n, (int)co, s.hp, s.owt, (int)c4, 1, 1, 0, 1, nullptr, 0, 1, ws, st);
         if (rc) return rc;
-        const int64_t total = n * ci * h * wd;
-        launch_pdl(seg_out_kernel, seg_blocks(total), 256, 0, st, (const float *)os, dst,
-                   (uint32_t)total, (int)ci, (int)h, (int)wd, s, nullptr, 0, 1);
+        launch_seg_out(os, dst, n, ci, h, wd, s, nullptr, 0, 1, st);
     }
     QT_CHECK_LAUNCH();
     return QT_OK;
