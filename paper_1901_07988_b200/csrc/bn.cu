@@ -107,6 +107,7 @@ struct StatsArgs {
     int64_t *clip;
     FastDiv hw8d;       // hw / 8 (vectorized stats loop)
     FastDiv hw4d;       // hw / 4 (4-pixel groups, hw % 8 == 4)
+    FastDiv hwd;        // hw (scalar loop of odd planes, e.g. 7x7)
 };
 
 __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
@@ -180,6 +181,28 @@ __global__ void __launch_bounds__(kRThreads) bn_stats_kernel(StatsArgs a) {
                 double d2 = (double)q.z - shift, d3 = (double)q.w - shift;
                 v[0] += (d0 + d1) + (d2 + d3);
                 v[1] += (d0 * d0 + d1 * d1) + (d2 * d2 + d3 * d3);
+            }
+        }
+    } else if (cnt < (1ll << 31) && a.hw < (1ll << 31)) {
+        // odd planes (7x7): the same per-thread order as the loop below,
+        // FastDiv indexing and U loads in flight
+        const uint32_t hw = (uint32_t)a.hw, n1 = (uint32_t)cnt;
+        constexpr int U = 4;
+        for (uint32_t e0 = threadIdx.x; e0 < n1; e0 += U * kRThreads) {
+            float xv[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const uint32_t e = e0 + u * kRThreads;
+                if (e >= n1) break;
+                const uint32_t pl = fast_div(e, a.hwd), off = e - pl * hw;
+                xv[u] = __ldg(a.x + ((p0 + pl) * a.c + ch) * a.hw + off);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                if (e0 + u * kRThreads >= n1) break;
+                const double d = (double)xv[u] - shift;
+                v[0] += d;
+                v[1] += d * d;
             }
         }
     } else {
@@ -581,6 +604,7 @@ extern "C" int qt_bn_stats(const float *x, int64_t n, int64_t c, int64_t hw, dou
                 nullptr, nullptr, 0, 0.0, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
     a.hw8d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 3));
     a.hw4d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 2));
+    a.hwd = make_fastdiv((uint32_t)std::max<int64_t>(1, std::min<int64_t>(hw, INT32_MAX)));
     dim3 grid((unsigned)p.blocks, (unsigned)c);
     launch_pdl_cluster(bn_stats_kernel, grid, kRThreads, 0, qt_s(stream), (unsigned)p.blocks, a);
     QT_CHECK_LAUNCH();
@@ -603,6 +627,7 @@ extern "C" int qt_bn_stats_prep(const float *x, int64_t n, int64_t c, int64_t hw
                 clip_count};
     a.hw8d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 3));
     a.hw4d = make_fastdiv((uint32_t)std::max<int64_t>(1, hw >> 2));
+    a.hwd = make_fastdiv((uint32_t)std::max<int64_t>(1, std::min<int64_t>(hw, INT32_MAX)));
     dim3 grid((unsigned)p.blocks, (unsigned)c);
     launch_pdl_cluster(bn_stats_kernel, grid, kRThreads, 0, qt_s(stream), (unsigned)p.blocks, a);
     QT_CHECK_LAUNCH();

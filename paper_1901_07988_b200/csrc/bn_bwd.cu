@@ -75,6 +75,7 @@ struct BwdArgs {
     unsigned *counter;
     float *lut;      // [C][2][256]: mask, a1 per code
     FastDiv gppd;    // hw / 8
+    FastDiv hwd;     // hw (scalar loop of odd planes)
 };
 
 // mask (1/0) and a1 for one code of channel ch (layer.py:354-366)
@@ -222,8 +223,10 @@ __global__ void __launch_bounds__(kBT) bn_bwd_reduce_kernel(BwdArgs a) {
     } else {
         build_lut();
         const int64_t cnt = (p1 - p0) * a.hw;
+        const bool fd = cnt < (1ll << 31) && a.hw < (1ll << 31);   // FastDiv indexing
         for (int64_t e = threadIdx.x; e < cnt; e += kBT) {
-            const int64_t pl = e / a.hw, off = e - pl * a.hw;
+            const int64_t pl = fd ? (int64_t)fast_div((uint32_t)e, a.hwd) : e / a.hw;
+            const int64_t off = e - pl * a.hw;
             const int64_t i = ((p0 + pl) * a.c + ch) * a.hw + off;
             float m;
             double a1d;
@@ -432,6 +435,7 @@ extern "C" int qt_bn_backward_reduce(const float *g3, qt_tape_t tape, int64_t n,
     // and code width only, never on the tape type
     const int G = bn_group(hw, hw);
     a.gppd = make_fastdiv((uint32_t)std::max<int64_t>(1, hw / (G > 0 ? G : 8)));
+    a.hwd = make_fastdiv((uint32_t)std::max<int64_t>(1, std::min<int64_t>(hw, INT32_MAX)));
     dim3 grid((unsigned)p.nb, (unsigned)c);
     cudaStream_t s = qt_s(stream);
 #define QT_RED(GG)                                                                                \
