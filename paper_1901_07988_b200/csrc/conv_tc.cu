@@ -59,7 +59,8 @@ struct FwdGeo {
     int flat;                       // 1x1 on any plane: 128-pixel runs of the flattened plane
     int mtiles, ntiles;             // output tiles along pixels / channels
     int R, NOUT;                    // raw ring and output staging depths
-    int G;                          // split warpgroups = operand ring depth (1, 2, 4)
+    int G;                          // split warpgroups (1, 2)
+    int OPS;                        // operand ring depth in TMEM (a multiple of G, <= kFwdMaxOps)
     int wres;                       // 1: the CTA's weight tiles stay resident in smem
     int slot;                       // raw ring slot bytes (A box [+ B tiles])
     FastDiv ntd, tpid;              // / ntiles, / tiles_per_img (no runtime IDIV)
@@ -122,6 +123,10 @@ struct FuseParams {
 // stages are transformed concurrently and every mbarrier has one waiter
 // group that consumes its phases in order (R is a multiple of G).
 constexpr int kFwdGroups = 2;
+// Operand (TMEM A) ring depth: up to kFwdMaxOps stages, a multiple of the
+// split groups -- group g alternates over stages g, g + G, ... so it can
+// transform stage gi while the MMAs of gi - G still read theirs
+constexpr int kFwdMaxOps = 8;
 
 // debug timeline (qt_debug_conv_trace): clock64 stamps of CTA trace_cta.
 // Per stage gi < 64: [8*gi + 0] producer issue, +1 split raw_full ok, +2 split
@@ -334,8 +339,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     uint8_t *wres_base = (uint8_t *)out_base + NOUT * C::OUT_BYTES;
     uint64_t *bars = (uint64_t *)(wres_base + (g.wres ? g.kh * (g.ci / KC) * 2 * C::B_SLOT : 0));
     uint64_t *raw_full = bars, *raw_empty = bars + R;
-    uint64_t *op_full = bars + 2 * R, *op_empty = op_full + kFwdGroups;
-    uint64_t *acc_full = op_empty + kFwdGroups, *acc_empty = acc_full + 2;
+    uint64_t *op_full = bars + 2 * R, *op_empty = op_full + kFwdMaxOps;
+    uint64_t *acc_full = op_empty + kFwdMaxOps, *acc_empty = acc_full + 2;
     uint64_t *res_full = acc_empty + 2;
     uint64_t *w_full = res_full + 2;
     uint32_t *tmem_slot = (uint32_t *)(w_full + 1);
@@ -343,7 +348,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     // running (n, mean, M2) per channel of its tile, the finalizer index
     // (pointer arithmetic from the shared base keeps every access LDS/STS)
     // (bars is 1 KiB aligned; this is the first 16-byte boundary past tmem_slot)
-    uint8_t *fbase = (uint8_t *)(bars + 2 * R + 2 * kFwdGroups + 8);
+    uint8_t *fbase = (uint8_t *)(bars + 2 * R + 2 * kFwdMaxOps + 8);
     BnConst *s_bn = (BnConst *)fbase;
     double *s_acc = (double *)(fbase + (FUSE && fz.bits ? g.ci * (int)sizeof(BnConst) : 0));   // [BN][3]
     int *s_fin = (int *)(s_acc + (FUSE && fz.stats ? 3 * BN : 0));
@@ -351,13 +356,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     long long *const tr_ = (g_cv_trace && blockIdx.x == (unsigned)g_cv_trace_cta) ? g_cv_trace : nullptr;
     if (threadIdx.x == 0) CV_TRACE(1000);
+    if (threadIdx.x == 0 && tr_) { tr_[990] = R; tr_[991] = G; tr_[992] = g.OPS; }
     const int kchunks = g.ci / KC;
     const int nst = g.kh * kchunks;             // (u, channel chunk) stages per tile
     const int total = g.mtiles * g.ntiles;
 
     if (threadIdx.x == 0) {
         for (int s = 0; s < R; ++s) { mbar_init(&raw_full[s], 1); mbar_init(&raw_empty[s], 1); }
-        for (int s = 0; s < G; ++s) { mbar_init(&op_full[s], 128); mbar_init(&op_empty[s], 1); }
+        for (int s = 0; s < g.OPS; ++s) { mbar_init(&op_full[s], 128); mbar_init(&op_empty[s], 1); }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&acc_full[a], 1);
             mbar_init(&acc_empty[a], 32 * kFwdEpiWarps);
@@ -449,8 +455,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             tc_fence_after();
             const uint32_t d = tmem + (uint32_t)(acc * C::NM);
             for (int i = 0; i < nst; ++i) {
-                mbar_wait(&op_full[o], pho);
                 const int gi_ = lt * nst + i;
+                if (lane == 0 && gi_ < 64) CV_TRACE(8 * gi_ + 6);
+                mbar_wait(&op_full[o], pho);
                 if (lane == 0 && gi_ < 64) CV_TRACE(8 * gi_ + 4);
                 tc_fence_after();
                 if (elect_one()) {
@@ -471,7 +478,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 __syncwarp();
                 if (lane == 0 && gi_ < 64) CV_TRACE(8 * gi_ + 5);
                 if (++s == R) { s = 0; phs ^= 1u; }
-                if (++o == G) { o = 0; pho ^= 1u; }
+                if (++o == g.OPS) { o = 0; pho ^= 1u; }
             }
         }
     } else if (warp < kFwdEpiWarp) {  // ------------ split warpgroups -> TMEM (A operand)
@@ -485,10 +492,10 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         // stages of this CTA: (its tiles) x nst, in MMA order
         const int my_tiles = (int)blockIdx.x < total ? (total - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
         const int nstages = my_tiles * nst;
-        const int o = grp;
         int gi = grp < G ? grp : nstages;
         int s = gi % R;
-        uint32_t phr = (uint32_t)(gi / R) & 1u, pho = (uint32_t)(gi / G) & 1u;
+        int o = gi % g.OPS;                           // operand stage of stage gi
+        uint32_t phr = (uint32_t)(gi / R) & 1u, pho = (uint32_t)(gi / g.OPS) & 1u;
         const int bits = FUSE ? fz.bits : 0;
         unsigned long long nclip = 0;
         if (bits) {   // the layer's BnConst table (written by the stats kernel / producer)
@@ -590,10 +597,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             tmem_wait_st();
             tc_fence_before();
             if (quarter == 2 && lane == 0 && gi < 64) CV_TRACE(8 * gi + 3);
+            if (quarter == 0 && lane == 0 && gi < 64) CV_TRACE(8 * gi + 7);
             mbar_arrive(&op_full[o]);
             s += G;
             if (s >= R) { s -= R; phr ^= 1u; }    // R is a multiple of G
-            pho ^= 1u;
+            o += G;
+            if (o >= g.OPS) { o -= g.OPS; pho ^= 1u; }   // OPS is a multiple of G
         }
         if (bits) {   // clip count of the tape (codec.py:133-135), integer atomics
             nclip = warp_sum(nclip);
@@ -898,6 +907,13 @@ static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, const
     gg.R = r;
     gg.NOUT = nout;
     gg.G = G;
+    static const int ops_env = [] {
+        const char *e = getenv("QTAPE_FWD_OPS");
+        return e ? atoi(e) : 0;
+    }();
+    int ops = std::min(kFwdMaxOps, (512 - C::ACC_COLS) / C::OP_COLS) / G * G;
+    if (ops_env > 0) ops = std::max(G, std::min(ops, ops_env / G * G));   // tuning
+    gg.OPS = std::max(G, ops);
     const int smem = r * gg.slot + nout * C::OUT_BYTES + (gg.wres ? wbytes : 0) + 1024 + 512 +
                      fuse_bytes;
     launch_pdl(kern, grid, kFwdThreads, smem, st, m.a, m.bh, m.bl, m.out, m.res, gg, ep, fzl);

@@ -26,10 +26,10 @@ fn(None, 0)
 b = buf.cpu().tolist()
 t0 = b[1000]
 rel = lambda v: (v - t0) if v else -1
-print(f"CTA 0: total {b[1001] - t0} cycles")
-print("  gi  prod  s_raw  s_empty  s_done  mma_go  mma_done")
+print(f"CTA 0: total {b[1001] - t0} cycles  R={b[990]} G={b[991]} OPS={b[992]}")
+print("  gi  prod  s_raw  s_empty  s_done(q2)  mma_go  mma_issued  mma_pre_wait  s_done(q0)")
 for gi in range(64):
-    r = b[8 * gi: 8 * gi + 6]
+    r = b[8 * gi: 8 * gi + 8]
     if not any(r):
         break
     print(f"{gi:4d} " + " ".join(f"{rel(v):7d}" for v in r))
