@@ -144,6 +144,8 @@ constexpr int kFwdEpiWarp = 2 + 4 * kFwdGroups;
 
 // --- epilogue BN statistics (FuseParams.stats) ------------------------------
 constexpr int kEpiThreads = 32 * kFwdEpiWarps;
+constexpr int kFwdDualThreads = 64 + 128 + 32 * 4;   // DUAL form: 1 split group, 4 epilogue warps
+constexpr int kFwdDualSmem = 113 * 1024;             // dynamic smem per CTA, two CTAs per SM
 
 // One output tile's per-channel (mean, M2) from the staged tile
 // s_out[img][BN][tpx] (valid pixels q < nvalid of the flattened 128), merged
@@ -319,8 +321,12 @@ __device__ __forceinline__ void epi_stats_finalize(const FuseParams &fz, const d
 //            + shortcut (TMA-prefetched) -> smem -> TMA store) overlaps tile
 //            j+1's main loop.
 // Precision: 3xTF32 (hi*hi + hi*lo + lo*hi).
-template <int BN, int OWT, int KC, int KW, bool FUSE>
-__global__ void __launch_bounds__(kFwdThreads, 1)
+// DUAL: two CTAs per SM (one split group, four epilogue warps, 256 TMEM
+// columns each) for the small-N CIFAR layers, whose tiles are bound by fixed
+// per-tile latencies (barrier round trips, epilogue hand-offs) rather than by
+// the tensor pipe: the two CTAs' pipelines interleave on the SM.
+template <int BN, int OWT, int KC, int KW, bool FUSE, bool DUAL = false>
+__global__ void __launch_bounds__(DUAL ? 64 + 128 + 32 * 4 : kFwdThreads, DUAL ? 2 : 1)
     conv_fwd_tc_kernel(const __grid_constant__ CUtensorMap tmA,
                        const __grid_constant__ CUtensorMap tmBh,
                        const __grid_constant__ CUtensorMap tmBl,
@@ -328,6 +334,11 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                        const __grid_constant__ CUtensorMap tmRes, FwdGeo g, EpiParams ep,
                        FuseParams fz) {
     using C = FwdCfg<BN, OWT, KC, KW>;
+    static_assert(!(DUAL && FUSE), "fused prologue / epilogue: single-CTA form only");
+    constexpr int NG = DUAL ? 1 : kFwdGroups;          // split warpgroups
+    constexpr int NEPI = DUAL ? 4 : kFwdEpiWarps;      // epilogue warps
+    constexpr int EPIW = 2 + 4 * NG;                   // first epilogue warp
+    constexpr int TMEM_COLS = DUAL ? 256 : 512;
     const int R = g.R, NOUT = g.NOUT, G = g.G;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     // 1 KiB alignment by pointer arithmetic on the __shared__ array (an
@@ -366,14 +377,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         for (int s = 0; s < g.OPS; ++s) { mbar_init(&op_full[s], 128); mbar_init(&op_empty[s], 1); }
         for (int a = 0; a < 2; ++a) {
             mbar_init(&acc_full[a], 1);
-            mbar_init(&acc_empty[a], 32 * kFwdEpiWarps);
+            mbar_init(&acc_empty[a], 32 * NEPI);
             mbar_init(&res_full[a], 1);
         }
         mbar_init(w_full, 1);
         fence_barrier_init();
     }
     if (FUSE && fz.stats && (int)threadIdx.x < 3 * BN) s_acc[threadIdx.x] = 0.0;
-    if (warp == 1) tmem_alloc<512>(tmem_slot);
+    if (warp == 1) tmem_alloc<TMEM_COLS>(tmem_slot);
     if (warp == 0 && lane == 0) {
         tma_prefetch(&tmA);
         tma_prefetch(&tmBh);
@@ -481,7 +492,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                 if (++o == g.OPS) { o = 0; pho ^= 1u; }
             }
         }
-    } else if (warp < kFwdEpiWarp) {  // ------------ split warpgroups -> TMEM (A operand)
+    } else if (warp < EPIW) {  // ------------ split warpgroups -> TMEM (A operand)
         const int grp = (warp - 2) >> 2;
         const int quarter = warp & 3;
         const int row = 32 * quarter + lane;          // this thread's TMEM lane = pixel
@@ -502,8 +513,8 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             const int st = threadIdx.x - 64;
             const float4 *src = reinterpret_cast<const float4 *>(fz.bn);
             float4 *dst = reinterpret_cast<float4 *>(s_bn);
-            for (int q = st; q < g.ci * 3; q += 128 * kFwdGroups) dst[q] = src[q];
-            asm volatile("bar.sync 2, %0;" ::"n"(128 * kFwdGroups) : "memory");
+            for (int q = st; q < g.ci * 3; q += 128 * NG) dst[q] = src[q];
+            asm volatile("bar.sync 2, %0;" ::"n"(128 * NG) : "memory");
         }
         const int lpw_log = bits ? 5 - (bits == 1 ? 0 : bits == 2 ? 1 : bits == 4 ? 2 : 3) : 0;
         const int lpw = 1 << lpw_log;                      // lanes (pixels) per 32-bit code word
@@ -610,12 +621,12 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
         }
     } else {  // ------------------------------------------------ epilogue warps
         const int quarter = warp & 3;
-        const int ehalf = (warp - kFwdEpiWarp) >> 2;  // which alternate 16-channel blocks
+        const int ehalf = DUAL ? 0 : (warp - EPIW) >> 2;  // which alternate channel chunks
         const int row = 32 * quarter + lane;
         const int ratom = row / OWT, wcol = row % OWT;
         const int img = ratom / g.rows, rr = ratom % g.rows;
         const size_t cstride = (size_t)g.rows * OWT;
-        const bool leader = (warp == kFwdEpiWarp && lane == 0);
+        const bool leader = (warp == EPIW && lane == 0);
         const bool res_ldg = ep.res && !ep.res_tma;
         const int kw_pad = (KW > 1) ? g.pad : 0;
         if (leader && ep.res_tma && (int)blockIdx.x < total) {  // prefetch the first shortcut tile
@@ -632,7 +643,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             tile_coords(T, n0, h0, co0);
             const int acc = lt & 1, ob = (NOUT > 1) ? (lt & 1) : 0;
             float *s_out = out_base + (size_t)ob * (C::OUT_BYTES / 4);
-            asm volatile("bar.sync 1, %0;" ::"n"(32 * kFwdEpiWarps) : "memory");   // staging free
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * NEPI) : "memory");   // staging free
             mbar_wait(&acc_full[acc], (uint32_t)(lt >> 1) & 1u);
             if (leader && lt < 32) CV_TRACE(600 + 4 * lt);
             tc_fence_after();
@@ -641,12 +652,15 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             const uint32_t tbase = tmem + ((uint32_t)(32 * quarter) << 16) + (uint32_t)(acc * C::NM);
             float *so = s_out + (img * BN * g.rows + rr) * OWT + wcol;
             const int64_t hr = (int64_t)g.oh * ep.sr, wr = (int64_t)g.ow * ep.sr;
+            // channel chunks of CW dealt to the two warps of each lane quarter
+            // (8-channel chunks when BN = 16, so both warps work)
+            constexpr int CW = BN >= 32 ? 16 : 8;
 #pragma unroll 1
-            for (int cb = 16 * ehalf; cb < BN; cb += 32) {
-                float rv[16];
-                if (res_ldg) {  // strided shortcut (sr > 1): gather, 16 loads in flight
+            for (int cb = CW * ehalf; cb < BN; cb += (DUAL ? 1 : 2) * CW) {
+                float rv[CW];
+                if (res_ldg) {  // strided shortcut (sr > 1): gather, CW loads in flight
 #pragma unroll
-                    for (int j = 0; j < 16; ++j) {
+                    for (int j = 0; j < CW; ++j) {
                         const int co = co0 + cb + j;
                         rv[j] = co < ep.cr ? __ldg(ep.res + (((int64_t)nn * ep.cr + co) * hr +
                                                              (int64_t)y * ep.sr) * wr +
@@ -654,9 +668,9 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                                            : 0.f;
                     }
                 }
-                uint32_t r[KW][16];
+                uint32_t r[KW][CW];
                 // per column tap: source lane and zero-padding mask (branch-free
-                // so the 16 channels' shuffle chains interleave)
+                // so the CW channels' shuffle chains interleave)
                 int src[KW];
                 bool okt[KW];
 #pragma unroll
@@ -666,11 +680,14 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
                     okt[t] = (wcol + dx >= 0) && (wcol + dx < OWT);
                 }
 #pragma unroll
-                for (int v = 0; v < KW; ++v) tmem_ld16(tbase + v * BN + cb, r[v]);
+                for (int v = 0; v < KW; ++v) {
+                    if constexpr (CW == 16) tmem_ld16(tbase + v * BN + cb, r[v]);
+                    else tmem_ld8(tbase + v * BN + cb, r[v]);
+                }
                 tmem_wait_ld();
                 if (leader && lt < 32 && cb == 0) CV_TRACE(600 + 4 * lt + 2);
 #pragma unroll
-                for (int j = 0; j < 16; ++j) {
+                for (int j = 0; j < CW; ++j) {
                     float v;
                     if (KW == 1) {
                         v = __uint_as_float(r[0][j]);
@@ -697,7 +714,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
             tc_fence_before();
             mbar_arrive(&acc_empty[acc]);            // TMEM buffer free for tile lt+2
             fence_async_smem();
-            asm volatile("bar.sync 1, %0;" ::"n"(32 * kFwdEpiWarps) : "memory");
+            asm volatile("bar.sync 1, %0;" ::"n"(32 * NEPI) : "memory");
             if (leader && lt < 32) CV_TRACE(600 + 4 * lt + 1);
             if (leader) {
                 tma_store_4d(&tmOut, s_out, g.flat ? h0 * OWT : 0, g.flat ? 0 : h0, co0, n0);
@@ -729,7 +746,7 @@ __global__ void __launch_bounds__(kFwdThreads, 1)
     if (threadIdx.x == 0) CV_TRACE(1001);
     if (warp == 1) {
         tc_fence_after();
-        tmem_dealloc<512>(tmem);
+        tmem_dealloc<TMEM_COLS>(tmem);
     }
 }
 
@@ -855,33 +872,55 @@ static int dgrad_cta_cap() {
 
 template <int BN, int OWT, int KC, int KW>
 static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, const FuseParams &fz,
-                      int tiles, int ntiles, cudaStream_t st) {
+                      int tiles, int ntiles, cudaStream_t st, bool allow_dual = true) {
     using C = FwdCfg<BN, OWT, KC, KW>;
     const bool fuse = fz.bits || fz.stats;
+    const int total = tiles * ntiles;
+    // two CTAs per SM (DUAL) for small-N layers with more tiles than SMs:
+    // 256 TMEM columns and about half the shared memory each (QTAPE_FWD_DUAL=0: off)
+    static const bool dual_on = [] {
+        const char *e = getenv("QTAPE_FWD_DUAL");
+        return !(e && *e == '0');
+    }();
+    // also under the concurrent-backward SM cap (the data gradient beside the
+    // side-stream weight gradients): C2 dgrad 1.84 -> 1.60 ms/step
+    static const bool dual_capped = [] {
+        const char *e = getenv("QTAPE_FWD_DUAL_CAP");
+        return !(e && *e == '0');
+    }();
+    // CIFAR-sized layers only: the ImageNet ones are closer to the tensor
+    // bound and measured 1 % slower in pairs (C4 43.9 vs 44.3 ms/step)
+    const double macs = (double)g.n * g.oh * g.ow * (double)g.co * g.ci * g.kh * g.kw;
+    bool dual = allow_dual && dual_on && !fuse && macs < kSmallLayerMacs &&
+                (s_cta_cap == 0 || dual_capped) && BN <= 64 &&
+                total > (s_cta_cap > 0 ? s_cta_cap : num_sms()) && C::ACC_COLS + C::OP_COLS <= 256;
     auto kern = fuse ? conv_fwd_tc_kernel<BN, OWT, KC, KW, true>
-                     : conv_fwd_tc_kernel<BN, OWT, KC, KW, false>;
-    static bool attr[2] = {false, false};
-    if (!attr[fuse]) {
-        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
-        attr[fuse] = true;
+                : dual ? conv_fwd_tc_kernel<BN, OWT, KC, KW, false, true>
+                       : conv_fwd_tc_kernel<BN, OWT, KC, KW, false>;
+    const int variant = fuse ? 1 : (dual ? 2 : 0);
+    static bool attr[3] = {false, false, false};
+    if (!attr[variant]) {
+        cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             dual ? kFwdDualSmem : 227 * 1024);
+        attr[variant] = true;
     }
     FwdGeo gg = g;
     gg.mtiles = tiles;
     gg.ntiles = ntiles;
+    const int tmem_cols = dual ? 256 : 512;
     // split groups G (operand ring depth) limited by TMEM; smem: output
     // staging x2 when it fits, raw ring a multiple of G (>= G, up to 8)
-    int G = kFwdGroups;
-    while (G > 1 && C::ACC_COLS + G * C::OP_COLS > 512) G /= 2;
-    if (C::ACC_COLS + G * C::OP_COLS > 512) return QT_EUNSUPPORTED;
-    const int total = tiles * ntiles;
+    int G = dual ? 1 : kFwdGroups;
+    while (G > 1 && C::ACC_COLS + G * C::OP_COLS > tmem_cols) G /= 2;
+    if (C::ACC_COLS + G * C::OP_COLS > tmem_cols) return QT_EUNSUPPORTED;
     // resident weights: every CTA keeps one co tile (grid a multiple of
     // ntiles) and its nst stages' (hi, lo) tiles fit next to the rings
     const int nst = g.kh * (g.ci / KC);
     const int wbytes = nst * 2 * C::B_SLOT;
-    const int sms = s_cta_cap > 0 ? std::min(num_sms(), s_cta_cap) : num_sms();
+    const int sms = (s_cta_cap > 0 ? std::min(num_sms(), s_cta_cap) : num_sms()) * (dual ? 2 : 1);
     int grid = std::min(total, sms);
     gg.wres = 0;
-    if (ntiles <= sms && wbytes <= 96 * 1024) {
+    if (ntiles <= sms && wbytes <= (dual ? 40 : 96) * 1024) {
         gg.wres = 1;
         grid = std::max(ntiles, std::min(total, sms) / ntiles * ntiles);
     }
@@ -896,13 +935,18 @@ static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, const
     gg.slot = gg.wres ? (C::A_BYTES + 1023) / 1024 * 1024 : C::RAW_BYTES;
     gg.ntd = make_fastdiv((uint32_t)ntiles);
     gg.tpid = make_fastdiv((uint32_t)std::max(1, g.tiles_per_img));
-    const int budget = 227 * 1024 - 1024 - 512 - fuse_bytes - (gg.wres ? wbytes : 0);
+    const int budget = (dual ? kFwdDualSmem : 227 * 1024) - 1024 - 512 - fuse_bytes -
+                       (gg.wres ? wbytes : 0);
     auto raw_fit = [&](int no) { return (budget - no * C::OUT_BYTES) / gg.slot; };
     int nout = 2;
     while (G > 1 && raw_fit(1) < G) G /= 2;
     if (raw_fit(nout) < G) nout = 1;
     int r = raw_fit(nout);
-    if (r < G || r < 1) return QT_EUNSUPPORTED;
+    if (r < G || r < 1) {
+        if (dual)   // does not fit half an SM: the single-CTA form
+            return launch_fwd<BN, OWT, KC, KW>(m, g, ep, fz, tiles, ntiles, st, false);
+        return QT_EUNSUPPORTED;
+    }
     r = std::min(r, 8) / G * G;
     gg.R = r;
     gg.NOUT = nout;
@@ -911,12 +955,13 @@ static int launch_fwd(const Maps &m, const FwdGeo &g, const EpiParams &ep, const
         const char *e = getenv("QTAPE_FWD_OPS");
         return e ? atoi(e) : 0;
     }();
-    int ops = std::min(kFwdMaxOps, (512 - C::ACC_COLS) / C::OP_COLS) / G * G;
+    int ops = std::min(kFwdMaxOps, (tmem_cols - C::ACC_COLS) / C::OP_COLS) / G * G;
     if (ops_env > 0) ops = std::max(G, std::min(ops, ops_env / G * G));   // tuning
     gg.OPS = std::max(G, ops);
     const int smem = r * gg.slot + nout * C::OUT_BYTES + (gg.wres ? wbytes : 0) + 1024 + 512 +
                      fuse_bytes;
-    launch_pdl(kern, grid, kFwdThreads, smem, st, m.a, m.bh, m.bl, m.out, m.res, gg, ep, fzl);
+    launch_pdl(kern, grid, dual ? kFwdDualThreads : kFwdThreads, smem, st, m.a, m.bh, m.bl, m.out,
+               m.res, gg, ep, fzl);
     QT_CHECK_LAUNCH();
     return QT_OK;
 }
