@@ -44,7 +44,9 @@ def _digest() -> str:
     for p in sorted(list(CSRC.glob("*")) + [ROOT / "include" / "qtape_b200.h"]):
         h.update(p.name.encode())
         h.update(p.read_bytes())
-    h.update(" ".join(ARCH + COMMON + STRICT).encode())
+    # flags without the checkout's absolute path: a build (and a traffic
+    # capture stamped with this digest) is the same wherever the repo lives
+    h.update(" ".join(ARCH + COMMON + STRICT).replace(str(ROOT), "<root>").encode())
     return h.hexdigest()[:16]
 
 
