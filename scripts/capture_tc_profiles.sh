@@ -20,6 +20,7 @@ run c2_dgrad_s1 C2 dgrad 1 conv_fwd_tc_kernel
 run c4_fwd_s14 C4 fwd 14 conv_fwd_tc_kernel
 run c4_dgrad_s14 C4 dgrad 14 conv_fwd_tc_kernel
 run c4_wgrad_s14 C4 wgrad 14 conv_wgrad_tc_kernel
+run c4_wgrad_s12 C4 wgrad 12 conv_wgrad_tc_kernel
 ls $out
 # summaries (the .ncu-rep files exceed what gpurun copies back)
 for r in $out/*.ncu-rep; do
@@ -29,6 +30,6 @@ for r in $out/*.ncu-rep; do
   ncu -i $r --page source --csv --print-source sass > $b.sass.csv 2>/dev/null
 done
 mkdir -p gpurun_out/tc_keep
-mv $out/c2_wgrad_s7.ncu-rep gpurun_out/tc_keep/ 2>/dev/null
+rm -rf gpurun_out/tc_keep
 rm -f $out/*.ncu-rep
 du -sh $out
