@@ -2,7 +2,7 @@
 // other warps hammer TMEM with tcgen05.st (split-warp pattern) and/or
 // tcgen05.ld (epilogue pattern), or spin on mbarrier try_wait.
 #include <cstdio>
-#include "../paper_1901_07988_b200/csrc/tc_common.cuh"
+#include "../../paper_1901_07988_b200/csrc/tc_common.cuh"
 using namespace qt::tc;
 template <int MODE>   // 0 none, 1 st, 2 ld, 3 st+ld, 4 spin, 5 st+ld+spin
 __global__ void k(long long *out, int iters, volatile int *stop) {

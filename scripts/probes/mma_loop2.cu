@@ -2,7 +2,7 @@
 // part of a stage costs.  VARIANT bits: 1 mbar_wait per stage, 2 clock64
 // trace stores, 4 per-stage descriptor build, 8 (i|j) accumulate predicate.
 #include <cstdio>
-#include "../paper_1901_07988_b200/csrc/tc_common.cuh"
+#include "../../paper_1901_07988_b200/csrc/tc_common.cuh"
 using namespace qt::tc;
 template <int VARIANT>
 __global__ void k(long long *out, long long *tr, int iters) {

@@ -1,26 +1,26 @@
-// Throughput of back-to-back tcgen05.mma kind::f16 (bf16), M=128, K=16, A in TMEM or SMEM.
+// Throughput of back-to-back tcgen05.mma kind::tf32 (A in TMEM or SMEM), M=128.
 #include <cstdio>
-#include "../paper_1901_07988_b200/csrc/tc_common.cuh"
+#include "../../paper_1901_07988_b200/csrc/tc_common.cuh"
 using namespace qt::tc;
 template <int N, bool TS>
 __global__ void k(long long *out, int iters) {
   extern __shared__ __align__(1024) uint8_t sm_raw[];
   uint8_t *sb = (uint8_t *)(((uintptr_t)sm_raw + 1023) & ~(uintptr_t)1023);
   __shared__ uint64_t bar; __shared__ uint32_t slot;
-  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) ((uint32_t *)sb)[i] = 0x3f803f80u;
+  for (int i = threadIdx.x; i < 64 * 1024 / 4; i += blockDim.x) ((float *)sb)[i] = 1.0f;
   fence_async_smem();
   if (threadIdx.x == 0) { mbar_init(&bar, 1); fence_barrier_init(); }
   if (threadIdx.x < 32) tmem_alloc<512>(&slot);
   tc_fence_before(); __syncthreads(); tc_fence_after();
   uint32_t tmem = slot;
   if (threadIdx.x == 0) {
-    uint32_t idesc = instr_desc(128, N, 1, 0, 0);
-    uint64_t db = smem_desc(smem_u32(sb), 16, 512, 4);
-    uint64_t da = smem_desc(smem_u32(sb) + 32768, 16, 512, 4);
+    uint32_t idesc = instr_desc(128, N, 2, 0, 0);
+    uint64_t db = smem_desc(smem_u32(sb), 16, 1024, 2);
+    uint64_t da = smem_desc(smem_u32(sb) + 32768, 16, 1024, 2);
     long long t0 = clock64();
     for (int i = 0; i < iters; ++i) {
-      if (TS) mma_bf16_ts(tmem, tmem + 256 + (i & 1) * 8, db + (i & 1) * 2, idesc, 1);
-      else mma_bf16(tmem, da + (i & 1) * 2, db + (i & 1) * 2, idesc, 1);
+      if (TS) mma_tf32_ts(tmem, tmem + 256, db, idesc, 1);
+      else mma_tf32(tmem, da, db, idesc, 1);
     }
     mma_commit(&bar);
     mbar_wait(&bar, 0);
@@ -33,10 +33,10 @@ __global__ void k(long long *out, int iters) {
 template <int N, bool TS> void run() {
   long long *d; cudaMalloc(&d, 8);
   cudaFuncSetAttribute(k<N, TS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 70000);
-  for (int it : {64, 512}) {
+  for (int it : {1, 64, 512}) {
     k<N, TS><<<1, 128, 70000>>>(d, it); cudaDeviceSynchronize();
     long long h; cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
-    printf("bf16 N=%3d %s iters=%4d per-mma=%.1f cyc  (128xNx16 MAC / 4096 = %d)\n", N, TS ? "A=TMEM" : "A=SMEM", it, (double)h / it, 128 * N * 16 / 4096);
+    printf("N=%3d %s iters=%4d cycles=%lld  per-mma=%.1f  (ideal %d)\n", N, TS ? "A=TMEM" : "A=SMEM", it, h, (double)h / it, 128 * N / 256 * 2);
   }
 }
-int main() { run<64, true>(); run<64, false>(); run<128, true>(); run<128, false>(); run<192, true>(); run<192, false>(); run<256, true>(); run<256, false>(); return 0; }
+int main() { run<16, true>(); run<16, false>(); run<48, true>(); run<64, true>(); run<64, false>(); run<128, true>(); run<256, true>(); return 0; }

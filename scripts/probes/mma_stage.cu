@@ -1,7 +1,7 @@
 // Per-"stage" cost of the conv MMA issue loop: wait a completed mbarrier,
 // fence, 6 x tcgen05.mma kind::tf32 (A in TMEM, N = 48 / 96), 2 commits.
 #include <cstdio>
-#include "../paper_1901_07988_b200/csrc/tc_common.cuh"
+#include "../../paper_1901_07988_b200/csrc/tc_common.cuh"
 using namespace qt::tc;
 template <int N, int NMMA, int NCOMMIT>
 __global__ void k(long long *out, int iters) {

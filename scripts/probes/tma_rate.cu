@@ -2,7 +2,7 @@
 // destinations, one mbarrier), cycles per issue; box rows x 128 B.
 #include <cstdio>
 #include <cudaTypedefs.h>
-#include "../paper_1901_07988_b200/csrc/tc_common.cuh"
+#include "../../paper_1901_07988_b200/csrc/tc_common.cuh"
 using namespace qt::tc;
 
 __global__ void k(const __grid_constant__ CUtensorMap m, long long *out, int n, int rows) {

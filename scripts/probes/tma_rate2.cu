@@ -2,7 +2,7 @@
 // and B 3D (ci=16, co=16, taps=3), interleaved as in the producer loop.
 #include <cstdio>
 #include <cudaTypedefs.h>
-#include "../paper_1901_07988_b200/csrc/tc_common.cuh"
+#include "../../paper_1901_07988_b200/csrc/tc_common.cuh"
 using namespace qt::tc;
 
 __global__ void k(const __grid_constant__ CUtensorMap ma, const __grid_constant__ CUtensorMap mb,
