@@ -119,34 +119,63 @@ def write_cifar10_file(path: str, images_u8: np.ndarray, labels: np.ndarray) -> 
     out.tofile(path)
 
 
-def synth_cifar_images(seed: int, n: int, classes: int = 10, noise: float = 32.0):
+def _class_grids(rng, classes: int, style: str) -> np.ndarray:
+    """(K, 3, 8, 8) per-class level grids of the three corpus styles the
+    reference's acceptance tests use (data.py:120-147): "smooth" uniform
+    levels, "sparse" a dark field with five bright cells (heavy-tailed
+    post-normalization activations), "natural" mid-range levels with four
+    highlights (mild tails)."""
+    if style == "smooth":
+        return rng.uniform(40.0, 215.0, size=(classes, 3, 8, 8))
+    if style not in ("sparse", "natural"):
+        raise DataError(f"unknown style {style!r}")
+    sparse = style == "sparse"
+    grid = np.full((classes, 3, 8, 8), 25.0) if sparse else rng.uniform(40.0, 160.0, size=(classes, 3, 8, 8))
+    for k in range(classes):
+        for _ in range(5 if sparse else 4):
+            ch, yy, xx = rng.integers(0, 3), rng.integers(0, 8), rng.integers(0, 8)
+            if sparse:
+                grid[k, ch, yy, xx] = 235.0
+            else:
+                grid[k, ch, yy, xx] += 140.0
+    return grid
+
+
+def synth_cifar_images(seed: int, n: int, classes: int = 10, noise: float = 32.0,
+                       style: str = "bilinear"):
     """A learnable synthetic corpus in the CIFAR record format: every class
-    is a smooth random RGB pattern (an 8x8 grid of levels, bilinearly
-    upsampled), every sample that pattern cyclically shifted by up to 3
-    pixels plus Gaussian pixel noise, clipped to uint8.  (The reference's
-    generator, data.py:114-165, serves the same purpose; the exact images
-    differ.)"""
+    is a random RGB pattern (an 8x8 grid of levels, upsampled to 32x32:
+    bilinearly for the default "bilinear" style, as 4x4 blocks for the
+    reference's "smooth" / "sparse" / "natural" styles), every sample that
+    pattern cyclically shifted by up to 3 pixels plus Gaussian pixel noise,
+    clipped to uint8.  The block styles draw the reference generator's
+    random numbers in its order (data.py:114-165), so a seed gives the
+    reference's corpus; "bilinear" is this package's own smooth variant."""
     rng = np.random.default_rng(seed)
-    grid = rng.uniform(40.0, 215.0, size=(classes, 3, 8, 8))
-    t = (np.arange(32) + 0.5) / 4.0 - 0.5                # sample points on the 8x8 grid
-    i0 = np.clip(np.floor(t).astype(int), 0, 7)
-    i1 = np.clip(i0 + 1, 0, 7)
-    f = np.clip(t - i0, 0.0, 1.0)
-    rows = grid[:, :, i0, :] * (1 - f)[None, None, :, None] + grid[:, :, i1, :] * f[None, None, :, None]
-    pat = rows[:, :, :, i0] * (1 - f) + rows[:, :, :, i1] * f          # (K,3,32,32)
+    if style == "bilinear":
+        grid = rng.uniform(40.0, 215.0, size=(classes, 3, 8, 8))
+        t = (np.arange(32) + 0.5) / 4.0 - 0.5                # sample points on the 8x8 grid
+        i0 = np.clip(np.floor(t).astype(int), 0, 7)
+        i1 = np.clip(i0 + 1, 0, 7)
+        f = np.clip(t - i0, 0.0, 1.0)
+        rows = grid[:, :, i0, :] * (1 - f)[None, None, :, None] + grid[:, :, i1, :] * f[None, None, :, None]
+        pat = rows[:, :, :, i0] * (1 - f) + rows[:, :, :, i1] * f          # (K,3,32,32)
+    else:
+        pat = _class_grids(rng, classes, style).repeat(4, axis=2).repeat(4, axis=3)
     labels = rng.permutation(np.arange(n) % classes).astype(np.int64)
-    dy, dx = rng.integers(-3, 4, size=(2, n))
-    imgs = np.stack([np.roll(pat[labels[i]], (dy[i], dx[i]), axis=(1, 2)) for i in range(n)])
+    shift = rng.integers(-3, 4, size=(n, 2))             # (dy, dx) per sample
+    imgs = np.stack([np.roll(pat[labels[i]], tuple(shift[i]), axis=(1, 2)) for i in range(n)])
     imgs = imgs + rng.standard_normal(imgs.shape) * noise
     return np.clip(imgs, 0, 255).astype(np.uint8), labels
 
 
 def make_synthetic_cifar_dir(dir_path: str, seed: int = 0, train_n: int = 5000,
-                             test_n: int = 1000, noise: float = 32.0) -> str:
+                             test_n: int = 1000, noise: float = 32.0,
+                             style: str = "bilinear") -> str:
     """A synthetic corpus written in the CIFAR-10 binary layout, read back
     through the real parser (data.py:168-179)."""
     os.makedirs(dir_path, exist_ok=True)
-    images, labels = synth_cifar_images(seed, train_n + test_n, noise=noise)
+    images, labels = synth_cifar_images(seed, train_n + test_n, noise=noise, style=style)
     write_cifar10_file(os.path.join(dir_path, TRAIN_FILES[0]), images[:train_n], labels[:train_n])
     write_cifar10_file(os.path.join(dir_path, TEST_FILE), images[train_n:], labels[train_n:])
     return dir_path
@@ -203,3 +232,23 @@ def augment_batch(batch, rng: np.random.Generator, hflip: bool = True,
         batch = torch.from_numpy(np.ascontiguousarray(arr, dtype=np.float32)).cuda()
     N.require_cuda(batch, "batch")
     return gather_batch(batch.contiguous(), None, rng, hflip, translate)
+
+
+def synth_blobs(seed: int, n: int, classes: int, shape, separation: float = 3.0,
+                device=None) -> Dataset:
+    """Gaussian clusters, balanced classes (data.py:100-116): class centres
+    of norm ``separation`` in the flattened input space plus unit noise;
+    the images are uploaded to the device."""
+    if n < classes:
+        raise DataError("need at least one sample per class")
+    rng = np.random.default_rng(seed)
+    shape = (shape,) if isinstance(shape, int) else tuple(shape)
+    dim = int(np.prod(shape))
+    centres = rng.standard_normal((classes, dim))
+    centres *= separation / np.linalg.norm(centres, axis=1, keepdims=True)
+    labels = np.arange(n) % classes
+    rng.shuffle(labels)
+    x = (centres[labels] + rng.standard_normal((n, dim))).reshape((n,) + shape).astype(np.float32)
+    dev = torch.device(device) if device is not None else torch.device("cuda", torch.cuda.current_device())
+    return Dataset(images=torch.from_numpy(x).to(dev), labels=labels.astype(np.int64),
+                   num_classes=classes)

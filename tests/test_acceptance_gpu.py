@@ -1,0 +1,213 @@
+"""The reference's acceptance suite (/root/reference/pkg/tests/test_acceptance.py),
+criterion by criterion, on the device engine.
+
+Same workloads: a 20-layer residual net (8 base channels) on 5000-image
+synthetic corpora written in the CIFAR-10 binary layout and read through the
+parser ("sparse": heavy-tailed, for training parity and the depth sweep;
+"natural": mild statistics, for gradient error vs SGD noise), the same
+schedules, batch 16, 2000 parity iterations.  The corpora come from this
+package's generator, which draws the reference generator's random numbers
+in its order: they are the reference's corpora byte for byte
+(tests/test_host.py::test_synth_styles_match_reference).
+
+Criterion 6 averages ten seeds instead of three.  Its final training losses
+(~0.01-0.06 per seed on this corpus) scatter so widely that a three-seed
+mean carries a standard error of ~35 %, above the criterion's 10 %: with
+seeds 0-2 this engine gives exact 0.0239 / K=8 0.0254 / K=4 0.0211, the
+reference's own CPU run 0.0087 / 0.0107 / 0.0604 for exact alone.  The
+device trains ten seeds of all four configurations in under a minute.
+
+Criterion 3 (central differences in float64) is not restated: the device
+path is float32; its gradients are held to the oracle's float64 analytic
+gradients in tests/test_parity_gpu.py and tests/test_engine_gpu.py (the
+oracle follows the reference, whose gradients criterion 3 validates).
+"""
+
+import json
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+import paper_1901_07988_b200 as P  # noqa: E402
+from paper_1901_07988_b200 import data as D, diag, engine as E, layer as L  # noqa: E402
+from paper_1901_07988_b200 import training as T  # noqa: E402
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+SCHEDULE = [[0, 0.01], [400, 0.1], [1200, 0.01], [1600, 0.001]]
+BATCH = 16
+SEEDS = tuple(range(10))
+PARITY_ITERS = 2000
+
+
+@pytest.fixture(scope="module")
+def accept_dir(tmp_path_factory):
+    d = tmp_path_factory.mktemp("accept-data")
+    D.make_synthetic_cifar_dir(str(d), seed=5, train_n=5000, test_n=500, noise=96.0, style="sparse")
+    return str(d)
+
+
+@pytest.fixture(scope="module")
+def accept_data(accept_dir):
+    return D.load_cifar10(accept_dir)
+
+
+@pytest.fixture(scope="module")
+def mild_data(tmp_path_factory):
+    d = tmp_path_factory.mktemp("mild-data")
+    D.make_synthetic_cifar_dir(str(d), seed=5, train_n=5000, test_n=500, noise=64.0, style="natural")
+    return D.load_cifar10(str(d))
+
+
+@pytest.fixture(scope="module")
+def accept_spec():
+    spec = E.make_residual_spec(base_channels=8, blocks_per_stage=3, stages=3)
+    assert len(spec.layers) == 20
+    return spec
+
+
+def test_criterion_1_quantizer_bound_and_sign():
+    for bits in (1, 2, 4, 8):
+        r = diag.quantizer_check(bits, n=1_000_000, seed=bits)
+        assert r["error_bound_ok"] and r["sign_ok"], (bits, r)
+        assert r["pack_roundtrip_ok"] and r["storage_ok"], (bits, r)
+
+
+def test_criterion_2_identity_quantizer_equivalence():
+    layers = [E.LayerSpec("conv", 8, 3, 1, 1, preact=False)]
+    blocks = []
+    for _ in range(3):
+        first = len(layers)
+        layers += [E.LayerSpec("conv", 8, 3, 1, 1), E.LayerSpec("conv", 8, 3, 1, 1)]
+        blocks.append((first, first + 1))
+    layers.append(E.LayerSpec("gap_dense", 4))
+    spec = E.NetworkSpec(input_shape=(3, 12, 12), num_classes=4, layers=layers, blocks=blocks)
+    data = D.synth_blobs(0, 160, 4, (3, 12, 12), separation=4.0)
+    base = dict(batch_size=8, total_iters=100, seed=3, lr_schedule=SCHEDULE, hflip=True, translate=True)
+    exact = T.train(spec, T.TrainConfig(mode="exact", **base), data)
+    bypass = T.train(spec, T.TrainConfig(mode="approx", bits=None, **base), data)
+    assert np.array_equal(exact.losses(), bypass.losses())
+    for pe, pb in zip(exact.params, bypass.params):
+        assert torch.equal(pe.weight, pb.weight)
+        if pe.preact:
+            assert torch.equal(pe.gamma, pb.gamma) and torch.equal(pe.beta, pb.beta)
+
+
+def test_criterion_4_exactness_decomposition():
+    rng = np.random.default_rng(4)
+    gamma = rng.uniform(0.8, 1.2, 16).astype(np.float32)
+    beta = rng.uniform(-0.2, 0.2, 16).astype(np.float32)
+    w0 = (np.random.default_rng(4).standard_normal((16, 16, 3, 3)) * 0.3).astype(np.float32)
+
+    def make_params():
+        return L.LayerParams(kind="conv", weight=torch.from_numpy(w0).cuda(), stride=1, pad=1,
+                             gamma=torch.from_numpy(gamma).cuda(), beta=torch.from_numpy(beta).cuda())
+
+    x = torch.from_numpy(rng.standard_normal((4, 16, 8, 8)).astype(np.float32)).cuda()
+    p = make_params()
+    out, tape_exact = L.layer_forward(x, p, mode="exact")
+    _, tape_quant = L.layer_forward(x, p, mode="approx", bits=8)
+    g_out = torch.from_numpy(rng.standard_normal(tuple(out.shape)).astype(np.float32)).cuda()
+    int_e, int_a = {}, {}
+    pe, pa = make_params(), make_params()
+    g_in_exact = L.layer_backward(g_out, tape_exact, pe, internals=int_e)
+    g_in_approx = L.layer_backward(g_out, tape_quant, pa, internals=int_a)
+    assert torch.equal(int_e["mask"], int_a["mask"])
+    assert torch.equal(int_e["grad_linear_in"], int_a["grad_linear_in"])
+    assert torch.equal(pe.grad_beta, pa.grad_beta)
+    assert torch.equal(int_e["grad_normalized"], int_a["grad_normalized"])
+    assert not torch.equal(g_in_exact, g_in_approx)
+    g_in_sub = L.layer_backward(g_out, tape_quant, make_params(), variance_a1=int_e["a1"])
+    assert torch.equal(g_in_sub, g_in_exact)
+
+
+def test_criterion_5_gradient_error_vs_sgd_noise(accept_spec, mild_data):
+    cfg = T.TrainConfig(mode="exact", bits=None, batch_size=BATCH, total_iters=500, seed=0,
+                        lr_schedule=[[0, 0.01], [400, 0.1]])
+    params = T.train(accept_spec, cfg, mild_data).params
+    report = diag.grad_error_report(accept_spec, params, mild_data, bits=8, batches=50,
+                                    batch_size=BATCH, seed=1)
+    worst = max(r["ratio"] for r in report.rows if r["ratio"] is not None)
+    assert worst < 0.1, [(r["layer"], r["ratio"]) for r in report.rows]
+
+
+def test_criterion_6_training_parity(accept_spec, accept_data):
+    tails = {}
+    for mode, bits in (("exact", None), ("approx", 8), ("approx", 4), ("naive", 8)):
+        per_seed = []
+        for seed in SEEDS:
+            cfg = T.TrainConfig(mode=mode, bits=bits, batch_size=BATCH, total_iters=PARITY_ITERS,
+                                seed=seed, lr_schedule=SCHEDULE)
+            per_seed.append(float(T.train(accept_spec, cfg, accept_data).losses()[-100:].mean()))
+        tails[(mode, bits)] = float(np.mean(per_seed))
+    exact, k8, k4 = tails[("exact", None)], tails[("approx", 8)], tails[("approx", 4)]
+    naive = tails[("naive", 8)]
+    print(f"\n[criterion 6] exact {exact:.4f}  K=8 {k8:.4f}  K=4 {k4:.4f}  naive {naive:.4f}")
+    assert abs(k8 - exact) <= 0.10 * exact, (k8, exact)
+    assert abs(k4 - exact) <= 0.10 * exact, (k4, exact)
+    assert naive >= 1.5 * exact, (naive, exact)
+
+
+def test_criterion_7_memory_formula(accept_spec, accept_data):
+    cfg = T.TrainConfig(mode="approx", bits=4, batch_size=BATCH, total_iters=20, seed=0,
+                        lr_schedule=[[0, 0.01]])
+    result = T.train(accept_spec, cfg, accept_data)
+    width = accept_spec.width()
+    assert result.pool.peak_live_count <= width + 1
+    # the report of this engine's schedule equals its instrumented pool (the
+    # reference's schedule copies the block input: schedule="reference")
+    rep = E.memory_report(accept_spec, (BATCH,) + tuple(accept_spec.input_shape), mode="approx",
+                          bits=4, schedule="device")
+    pool = E.BufferPool(width + 1)
+    batch = accept_data.images[:BATCH].contiguous()
+    logits, tapes = E.network_forward(accept_spec, result.params, batch, mode="approx", bits=4,
+                                      pool=pool)
+    E.network_backward(accept_spec, result.params, tapes, torch.ones_like(logits), batch,
+                       mode="approx", pool=pool)
+    assert rep.transient_buffer_bytes == pool.peak_live_bytes
+    assert rep.peak_live_tensors == pool.peak_live_count
+    assert rep.persistent_tape_bytes == E.measured_tape_bytes(tapes)
+    assert rep.channel_overhead_bytes == E.measured_overhead_bytes(tapes)
+    uni = E.make_uniform_spec(164)
+    urep = E.memory_report(uni, (2, 8, 16, 16), mode="approx", bits=4)
+    assert abs(urep.ratio_vs_exact - (3 / 164 + 1 / 8)) < 0.01
+
+
+def test_criterion_8_depth_sweep(accept_data):
+    rows = diag.naive_vs_proposed_depth_sweep([4, 8, 16, 32], bits=8, dataset=accept_data, seed=0,
+                                              batches=20, batch_size=BATCH)
+    by_depth = {r["depth"]: r for r in rows}
+    for depth in (16, 32):
+        assert by_depth[depth]["naive_error"] > by_depth[depth]["proposed_error"], by_depth[depth]
+    assert by_depth[32]["naive_error"] > by_depth[4]["naive_error"]
+
+
+def test_criterion_9_csv_determinism(accept_dir, tmp_path):
+    spec = E.make_residual_spec(base_channels=4, blocks_per_stage=1, stages=2)
+    cfg = T.TrainConfig(mode="approx", bits=8, batch_size=8, total_iters=5, seed=7,
+                        lr_schedule=[[0, 0.01]])
+    config = tmp_path / "cfg.json"
+    config.write_text(json.dumps({"network": spec.to_json(), "train": cfg.to_json()}))
+
+    def cli(*args):
+        r = subprocess.run([sys.executable, "-m", "paper_1901_07988_b200", *args], cwd=ROOT,
+                           capture_output=True, text=True, timeout=600)
+        assert r.returncode == 0, r.stderr[-2000:]
+
+    grads, sweeps, trains = [], [], []
+    for run in ("a", "b"):
+        g, s, t = (tmp_path / f"{k}_{run}.csv" for k in ("grad", "sweep", "train"))
+        cli("gradcheck", "--config", str(config), "--data", accept_dir, "--bits", "8",
+            "--batches", "3", "--out", str(g))
+        cli("sweep", "--depths", "3,4", "--bits", "8", "--batches", "2", "--data", accept_dir,
+            "--out", str(s))
+        cli("train", "--config", str(config), "--data", accept_dir, "--out", str(t))
+        grads.append(g.read_bytes())
+        sweeps.append(s.read_bytes())
+        trains.append([",".join(line.split(",")[:3]) for line in t.read_text().splitlines()])
+    assert grads[0] == grads[1] and sweeps[0] == sweeps[1] and trains[0] == trains[1]

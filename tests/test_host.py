@@ -122,3 +122,20 @@ def test_conv_out_shape_rule():
     assert conv2d_out_shape((2, 3, 32, 32), (8, 3, 2, 2), 2, 0) == (2, 8, 16, 16)
     with pytest.raises(ShapeError):
         conv2d_out_shape((2, 3, 32, 32), (8, 3, 3, 3), 2, 1)
+
+
+def test_synth_styles_match_reference():
+    """The block-style corpora (sparse / natural / smooth) draw the reference
+    generator's random numbers in its order: byte-identical to
+    qtape.data.synth_cifar_like (digests from tests/golden/make_golden_synth.py)."""
+    import hashlib
+    import json
+    import os
+
+    from paper_1901_07988_b200 import data as D
+    path = os.path.join(os.path.dirname(__file__), "golden", "synth_styles.json")
+    for case in json.load(open(path)):
+        images, labels = D.synth_cifar_images(case["seed"], case["n"], noise=case["noise"],
+                                              style=case["style"])
+        h = hashlib.sha256(images.tobytes() + labels.astype("int64").tobytes()).hexdigest()
+        assert h == case["sha256"], case["style"]
