@@ -511,7 +511,6 @@ static int wgrad_tc(const float *gr, const void *pieces, qt_tape_t act, const fl
     p.rb = pl.rb;
     p.lut = codes ? 1 : 0;
     p.fbox = pl.fbox;
-    p.dbg_nocodes = getenv("QTAPE_WG_NOCODES") ? 1 : 0;
     int rc;
     switch (pl.bn) {
         case 16: rc = wg_launch_bn16(m, mc, p, pl, st); break;

@@ -89,7 +89,6 @@ struct WgParams {
     int cb;                  // code box bytes per channel (16-byte multiple)
     int cbytes;              // code box bytes per stage (cb x channels)
     int rb;                  // packed bytes per input row (ow*bits/8)
-    int dbg_nocodes;         // debug timing experiment: skip the code box loads
     int rpc;                 // A rows per input channel (kh*kw, or kh with column taps in N)
     long long *trace;        // debug timeline buffer (qt_debug_wgrad_trace) or NULL
     int trace_cta;
@@ -334,9 +333,9 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     mbar_expect_tx(&raw_full[s], p.cbytes);
                     tma_load_3d(slot, &tmC, &raw_full[s], ((y0 - p.pad) * p.rb) & ~15, c_begin, nn);
                 } else {
-                mbar_expect_tx(&raw_full[s], SUB * G_BYTES + (p.dbg_nocodes ? 0 : p.cbytes));
+                mbar_expect_tx(&raw_full[s], SUB * G_BYTES + p.cbytes);
                 tma_load_4d(slot, &tmG, &raw_full[s], 0, yc, co0, nn);
-                if (p.lut && !p.dbg_nocodes)   // 16-byte aligned window of input rows y0-pad ..
+                if (p.lut)   // 16-byte aligned window of input rows y0-pad ..
                     tma_load_3d(slot + SUB * G_BYTES, &tmC, &raw_full[s],
                                 ((y0 - p.pad) * p.rb) & ~15, c_begin, nn);
                 else if (p.fbox)               // fp32 rows y0-pad .. (OOB rows zero-filled)
