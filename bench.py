@@ -403,6 +403,12 @@ def main():
     cfg = CONFIGS[args.config]
     bits = args.bits or cfg["bits"]
     if "WORLD_SIZE" not in os.environ and args.gpus > 1:
+        if args.impl != "reference":
+            import torch
+            if torch.cuda.device_count() < args.gpus:
+                print(json.dumps({"error": f"--gpus {args.gpus} but {torch.cuda.device_count()} "
+                                           f"GPU(s) visible"}), flush=True)
+                sys.exit(2)
         _spawn_ranks(args.gpus)            # re-exec under torchrun: one rank per GPU
         return
     world = int(os.environ.get("WORLD_SIZE", "1"))
