@@ -386,3 +386,49 @@ def test_wgrad_from_codes_row_tiles(shape, bits):
         ref = ref + 0.125
         err = ((gw.double() - ref).norm() / ref.norm()).item()
         assert err < CONV_TOL, (regime, err)
+
+
+_DUAL_SHAPES = [(128, 16, 32, 16, 3), (128, 16, 32, 64, 1), (128, 64, 32, 16, 1), (128, 32, 16, 32, 3),
+                (128, 128, 16, 32, 1), (128, 64, 8, 64, 3)]
+
+_DUAL_CODE = r'''
+import sys, torch
+from paper_1901_07988_b200 import ops
+out = []
+for n, ci, hw, co, k in SHAPES:
+    g = torch.Generator(device="cuda").manual_seed(ci * 1000 + co + k)
+    x = torch.randn(n, ci, hw, hw, device="cuda", generator=g)
+    w = torch.randn(co, ci, k, k, device="cuda", generator=g) * 0.1
+    gy = torch.randn(n, co, hw, hw, device="cuda", generator=g)
+    y = ops.conv2d_forward(x, w, 1, k // 2)
+    gx = torch.empty_like(x)
+    ops.conv2d_dgrad(gy, w, tuple(x.shape), 1, k // 2, gx)
+    out.append((y.cpu(), gx.cpu()))
+torch.save(out, sys.argv[1])
+'''
+
+
+def test_two_cta_conv_form_bit_identical(tmp_path):
+    """The two-CTAs-per-SM conv form (CIFAR-sized layers with more tiles than
+    SMs) against the single-CTA form (QTAPE_FWD_DUAL=0, read once per
+    process): forward and data gradient bit-identical (the same per-output
+    summation), and within CONV_TOL of float64."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    code = "SHAPES = " + repr(_DUAL_SHAPES) + "\n" + _DUAL_CODE
+    res = {}
+    for dual in ("1", "0"):
+        path = tmp_path / f"dual{dual}.pt"
+        r = subprocess.run([sys.executable, "-c", code, str(path)], cwd=root, capture_output=True,
+                           text=True, timeout=300, env=dict(os.environ, QTAPE_FWD_DUAL=dual))
+        assert r.returncode == 0, r.stderr[-2000:]
+        res[dual] = torch.load(path)
+    for (n, ci, hw, co, k), (y1, gx1), (y0, gx0) in zip(_DUAL_SHAPES, res["1"], res["0"]):
+        assert torch.equal(y1, y0) and torch.equal(gx1, gx0), (ci, co, k)
+        g = torch.Generator(device="cuda").manual_seed(ci * 1000 + co + k)
+        x = torch.randn(n, ci, hw, hw, device="cuda", generator=g)
+        w = torch.randn(co, ci, k, k, device="cuda", generator=g) * 0.1
+        ref = torch.nn.functional.conv2d(x.double(), w.double(), padding=k // 2).cpu()
+        assert ((y1.double() - ref).norm() / ref.norm()).item() < CONV_TOL
