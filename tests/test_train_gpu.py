@@ -150,3 +150,27 @@ def test_trainer_odd_channel_widths(co):
     assert abs(lo - loss) < STEP_TOL * abs(lo)
     for p, r in zip(tr.params, ref):
         assert norm_err(host(p.weight), r["weight"]) < 10 * STEP_TOL
+
+
+def test_evaluate_after_train_matches_fresh_params():
+    """Inference after train() sees the trained weights, never the Trainer's
+    prepared tensor-core operands of a stale step: the
+    logits of the returned params equal those of a fresh copy."""
+    from paper_1901_07988_b200 import data as D
+    spec = E.make_residual_spec(base_channels=16, blocks_per_stage=1, stages=2)
+    images, labels = D.synth_cifar_images(0, 64)
+    x = torch.from_numpy(((images.astype(np.float32) / 255.0) - 0.5) / 0.25).cuda()
+    ds = D.Dataset(images=x, labels=labels, num_classes=10)
+    cfg = P.TrainConfig(mode="approx", bits=4, batch_size=32, total_iters=6, seed=1,
+                        lr_schedule=[[0, 0.1]])
+    res = P.train(spec, cfg, ds)
+    fresh = P.init_params(spec, 99)
+    for a, b in zip(fresh, res.params):
+        a.weight.copy_(b.weight)
+        if a.preact:
+            for name in ("gamma", "beta", "running_mean", "running_var"):
+                getattr(a, name).copy_(getattr(b, name))
+    la, _ = E.network_forward(spec, res.params, x[:32].contiguous(), training=False)
+    lb, _ = E.network_forward(spec, fresh, x[:32].contiguous(), training=False)
+    assert torch.equal(la, lb)
+    assert P.evaluate(spec, res.params, ds) == P.evaluate(spec, fresh, ds)
