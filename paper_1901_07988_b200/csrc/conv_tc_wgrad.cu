@@ -77,7 +77,7 @@ static PFN_cuTensorMapEncodeTiled_v12000 encode_fn_wg() {
 static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = false,
                       bool pre = false) {
     WgPlan pl;
-    if (pre && (tap || fbox || !(bits == 2 || bits == 4))) return pl;
+    if (pre && (tap || fbox || !(bits == 1 || bits == 2 || bits == 4))) return pl;
     if (g.s != 1) return pl;
     const int64_t ow = g.ow, oh = g.oh;
     if (ow != 8 && ow != 16 && ow != 32) return pl;
@@ -122,7 +122,7 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = 
     // operand bytes per chunk: FAST 3 bf16 pieces (only 2/4-bit codes take
     // FAST), GENERIC TF32 (hi, lo); the two modes share one smem region
     const int opb_g = 2 * nt * bn * 128;
-    const int opb_f = (bits == 2 || bits == 4) ? 3 * nt * bn * 64 : opb_g;
+    const int opb_f = (bits == 1 || bits == 2 || bits == 4) ? 3 * nt * bn * 64 : opb_g;
     // TMEM (512 columns): FAST needs mtg*facc + ops*mtg*SUB*16, GENERIC
     // mtg*BN + ops_g*mtg*SUB*64; ring depths are powers of two (see kWgGroups)
     constexpr int SUB = kWgSub;

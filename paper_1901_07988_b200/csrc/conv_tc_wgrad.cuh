@@ -170,7 +170,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                          const __grid_constant__ CUtensorMap tmC, WgParams p) {
     constexpr int ROWS = 32 / OW;                           // image rows per 32-pixel chunk
     constexpr int G_BYTES = BN * 128;                       // raw g tile: BN rows x 32 px fp32
-    constexpr bool FAST_OK = (BITS == 4 || BITS == 2);
+    constexpr bool FAST_OK = (BITS == 4 || BITS == 2 || BITS == 1);
     constexpr int NT = TAP ? 3 : 1;                         // column taps stacked in N
     constexpr bool STACK = TAP ? (9 * BN <= 256) : (3 * BN <= 192);   // pieces stacked in N
     constexpr int FACC = STACK ? 3 * NT * BN : NT * BN;     // FAST accumulator columns per tile
@@ -620,7 +620,43 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const uint32_t acol = acc_cols + (uint32_t)((o * p.mtg + t) * SUB + sub) * acols;
                 const int c = rc[t], u = ru[t], sh = rsh[t];
                 const int cbox = (c - c_begin) * p.cb;
-                if (FAST_OK && fast && BITS == 2) {
+                if (FAST_OK && fast && BITS == 1) {
+                    // 1-bit codes: a row of OW <= 32 px is one 8/16/32-bit field
+                    // (bit x = pixel x).  Per 8-pixel group (byte b):
+                    // z = (b & 0xF) | (b >> 4) << 16 puts pixel k at bit k and
+                    // pixel k + 4 at bit 16 + k, so (z >> k) & 0x00010001 is A
+                    // word k of the (k, k + 4) pairing -- then the same
+                    // *2 + (0x4300 + b) and relu(x - 128) as the 4-bit path
+                    uint32_t av[16];
+#pragma unroll
+                    for (int x = 0; x < 16; ++x) av[x] = 0u;
+                    if (rok[t]) {
+                        const uint32_t bc = s_bc[c - c_begin];
+#pragma unroll
+                        for (int seg = 0; seg < ROWS; ++seg) {
+                            const int iy = y0 + seg + u - p.pad;
+                            if (iy < 0 || iy >= p.h) continue;
+                            const uint8_t *rowp = cst + cbox + iy * p.rb - wbase;
+                            uint32_t w = OW == 32 ? *reinterpret_cast<const uint32_t *>(rowp)
+                                       : OW == 16 ? (uint32_t)*reinterpret_cast<const uint16_t *>(rowp)
+                                                  : (uint32_t)*rowp;
+                            constexpr uint32_t rmask = OW == 32 ? 0xFFFFFFFFu : ((1u << OW) - 1u);
+                            w = sh > 0 ? (w >> 1) : sh < 0 ? ((w << 1) & rmask) : w;
+#pragma unroll
+                            for (int gq = 0; gq < OW / 8; ++gq) {
+                                const uint32_t b8 = (w >> (8 * gq)) & 0xFFu;
+                                const uint32_t z = (b8 & 0xFu) | ((b8 >> 4) << 16);
+#pragma unroll
+                                for (int k = 0; k < 4; ++k)
+                                    av[seg * (OW / 2) + 4 * gq + k] =
+                                        bf16x2_relu_sub128(((z >> k) & 0x00010001u) * 2u + bc);
+                            }
+                            if (sh < 0) av[seg * (OW / 2)] &= 0xFFFF0000u;          // x = 0 pads
+                            if (sh > 0) av[seg * (OW / 2) + OW / 2 - 1] &= 0x0000FFFFu;  // x = OW-1
+                        }
+                    }
+                    tmem_st16(lane_base + acol, av);
+                } else if (FAST_OK && fast && BITS == 2) {
                     // 2-bit codes: a row is OW/4 bytes (8 px: one halfword).
                     // Per 8-pixel group (16 bits h): z = (h & 0xFF) | (h >> 8) << 16
                     // puts pixel k at bits 2k and pixel k + 4 at bits 16 + 2k,
@@ -901,6 +937,7 @@ static int launch_wg1(const CUtensorMap &m, const CUtensorMap &mc, const WgParam
     switch (p.lut ? p.tape.bits : 0) {
         case 4: return launch_wg2<BN, OW, 4>(m, mc, p, pl, st);
         case 2: return launch_wg2<BN, OW, 2>(m, mc, p, pl, st);
+        case 1: return launch_wg2<BN, OW, 1>(m, mc, p, pl, st);
         case 8: return launch_wg2<BN, OW, 8>(m, mc, p, pl, st);
         default: return launch_wg2<BN, OW, 0>(m, mc, p, pl, st);
     }

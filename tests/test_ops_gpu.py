@@ -246,7 +246,7 @@ def test_wgrad_direct_pieces_form_matches():
 import torch
 from paper_1901_07988_b200 import codec, ops
 torch.manual_seed(1)
-for bits in (2, 4):
+for bits in (1, 2, 4):
     for regime in ("narrow", "wide", "mixed"):
         for n, ci, hw, co, k in ((2, 16, 32, 64, 1), (2, 32, 16, 32, 3), (4, 256, 8, 64, 1),
                                  (2, 64, 8, 256, 1), (1, 64, 56, 128, 1)):
@@ -306,7 +306,7 @@ def test_transition_wgrad_from_codes(shape, bits):
                                    (2, 32, 28, 32, 3), (2, 64, 14, 64, 1), (2, 32, 7, 64, 1),
                                    (2, 16, 28, 32, 1), (2, 256, 14, 256, 1), (2, 128, 7, 256, 3),
                                    (1, 512, 7, 128, 1)])
-@pytest.mark.parametrize("bits", [2, 4])
+@pytest.mark.parametrize("bits", [1, 2, 4])
 def test_wgrad_from_codes_channel_blocks(shape, bits):
     """Weight gradient from a 2-/4-bit tape for outputs wider than one
     64-channel block (grid z) -- FAST and GENERIC CTAs, and on the segmented
@@ -357,14 +357,14 @@ def test_segmented_3x3_wgrad_from_codes(shape, bits):
         assert err < CONV_TOL, (regime, err)
 
 
-@pytest.mark.parametrize("bits", [2, 4])
+@pytest.mark.parametrize("bits", [1, 2, 4])
 @pytest.mark.parametrize("shape", [(2, 16, 32, 16, 3), (2, 32, 16, 32, 3), (4, 64, 8, 64, 3),
                                    (2, 16, 32, 64, 1), (2, 64, 8, 256, 1), (4, 128, 16, 32, 1),
                                    (3, 64, 8, 16, 1)])
 def test_wgrad_from_codes_row_tiles(shape, bits):
-    """Row-tiled (8/16/32-px rows) weight gradient from 2- and 4-bit tapes:
-    the FAST decode (integer bf16 operand; the 2-bit form regroups each
-    halfword's pixel pairs) for narrow channels, GENERIC for wide ones,
+    """Row-tiled (8/16/32-px rows) weight gradient from 1-, 2- and 4-bit
+    tapes: the FAST decode (integer bf16 operand; the 1- and 2-bit forms
+    regroup each byte's / halfword's pixel pairs) for narrow channels, GENERIC for wide ones,
     mixed channels in one CTA -- against float64 on the dequantized tape."""
     from paper_1901_07988_b200 import codec
     n, ci, hw, co, k = shape
