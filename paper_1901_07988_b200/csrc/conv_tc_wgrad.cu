@@ -122,7 +122,7 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = 
     // operand bytes per chunk: FAST 3 bf16 pieces (only 2/4-bit codes take
     // FAST), GENERIC TF32 (hi, lo); the two modes share one smem region
     const int opb_g = 2 * nt * bn * 128;
-    const int opb_f = (bits == 1 || bits == 2 || bits == 4) ? 3 * nt * bn * 64 : opb_g;
+    const int opb_f = (bits == 1 || bits == 2 || bits == 4 || bits == 8) ? 3 * nt * bn * 64 : opb_g;
     // TMEM (512 columns): FAST needs mtg*facc + ops*mtg*SUB*16, GENERIC
     // mtg*BN + ops_g*mtg*SUB*64; ring depths are powers of two (see kWgGroups)
     constexpr int SUB = kWgSub;
@@ -152,10 +152,16 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = 
         pl.rb = (int)(ow * bits / 8);
         pl.cb = (((int)(32 / ow) * SUB + 2 * (int)g.pad) * pl.rb + 15 + 15) & ~15;
         if (pl.cb > 256 || pl.nch > kWgMaxCh) return WgPlan{};
-        if (pl.nch * (1 << bits) > kWgLutEntries) return WgPlan{};
         pl.cbytes = pl.cb * pl.nch;
-        // padded channel stride: (hi, lo) pairs, or (pre) the value itself
-        pl.lut_floats = pl.nch * (pre ? (1 << bits) + 1 : (2 << bits) + 2);
+        // padded channel stride: (hi, lo) pairs, or (pre) the value itself;
+        // a table past kWgLutEntries (8-bit codes over wide channel blocks)
+        // is computed inline by the GENERIC operand instead
+        if (pl.nch * (1 << bits) > kWgLutEntries) {
+            if (pre) return WgPlan{};
+            pl.nolut = 1;
+        } else {
+            pl.lut_floats = pl.nch * (pre ? (1 << bits) + 1 : (2 << bits) + 2);
+        }
     } else if (fbox) {   // fp32 box per stage: the chunk rows plus the pad rows of each channel
         const int kk = pl.rpc;
         pl.nch = (int)std::min<int64_t>(g.ci, (mtg * 128 + kk - 1) / kk + (kk > 1 ? 1 : 0));
@@ -203,6 +209,11 @@ static WgPlan wg_plan(const ConvGeo &g, int bits, bool tap = false, bool fbox = 
     if (pl.rg < pl.ops) return WgPlan{};
     pl.opreg = region();
     pl.smem = pl.rg * sraw + pl.opreg + fixed;
+    // FAST2 (two A pieces, 32 TMEM columns per chunk): the deepest ring
+    // within the FAST one that fits beside the accumulators
+    if (bits > 0 && !tap)
+        for (int o2 = pl.ops; o2 >= 1 && !pl.ops2; o2 /= 2)
+            if (mtg * facc + o2 * mtg * SUB * 32 <= 512) pl.ops2 = o2;
     }
     pl.total = (int)(g.n * oh * ow / 32);
     // split-K count: one CTA per SM (one is resident per SM: a second wave
@@ -501,10 +512,21 @@ static int wgrad_tc(const float *gr, const void *pieces, qt_tape_t act, const fl
     p.RG = pl.rg;
     p.OPS = pl.ops;
     p.OPS_G = pl.ops_g;
+    static const int fast2_env = [] {   // 0: m < 2048 channels take INT (tests)
+        const char *e = getenv("QTAPE_WG_FAST2");
+        return e ? atoi(e) : 1;
+    }();
+    p.OPS2 = fast2_env ? pl.ops2 : 0;
     p.opreg = pl.opreg;
     p.pre = pl.pre;
     p.RB = pl.bring;
     p.lut_floats = pl.lut_floats;
+    p.nolut = pl.nolut;
+    static const int int_env = [] {   // 0: wide channels take the table GENERIC (tests)
+        const char *e = getenv("QTAPE_WG_INT");
+        return e ? atoi(e) : 1;
+    }();
+    p.intok = int_env;
     p.slot = pl.slot;
     p.cb = pl.cb;
     p.cbytes = pl.cbytes;

@@ -51,6 +51,7 @@
 
 #include <algorithm>
 #include <mutex>
+#include <type_traits>
 
 #include "common.cuh"
 #include "tc_common.cuh"
@@ -71,6 +72,25 @@ constexpr int kWgMaxCh = 256;     // channels per CTA row group (code box / FAST
         if (tr_) tr_[idx] = clock64();     \
     } while (0)
 
+// FAST operand pair word from x = codes (pixel k | pixel k + 4 << 16):
+// FAST: relu(m) for m = 2x + b (bc = 0x4300 + b; 8-bit: bf16x2_relu_m8);
+// FAST2 (m < 2048): bc = (b + 2048) x 0x10001, v = max(2x + bc, 2048) per
+// half, m = v & 0x7FF as the exact bf16 pieces (m & 0x7F0) + (m & 0xF) --
+// 0x4500 + t is the bf16 pattern of 2048 + 16 t, 0x4300 + t of 128 + t
+template <int BITS, bool TWO>
+__device__ __forceinline__ void fast_pair(uint32_t x, uint32_t bc, uint32_t &a1, uint32_t &a2) {
+    uint32_t v = x * 2u + bc;
+    if constexpr (!TWO) {
+        a1 = BITS == 8 ? bf16x2_relu_m8(v) : bf16x2_relu_sub128(v);
+        return;
+    } else {
+    asm("max.u16x2 %0, %1, %2;" : "=r"(v) : "r"(v), "r"(0x08000800u));
+    const uint32_t p1 = ((v >> 4) & 0x007F007Fu) | 0x45004500u, p2 = (v & 0x000F000Fu) | 0x43004300u;
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(a1) : "r"(p1), "r"(0x3F803F80u), "r"(0xC500C500u));
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(a2) : "r"(p2), "r"(0x3F803F80u), "r"(0xC300C300u));
+    }
+}
+
 struct WgParams {
     qt_tape_t tape;          // codes (+step/offset) or a2 (relu) ...
     const float *plain;      // ... or the plain input (no relu)
@@ -82,9 +102,12 @@ struct WgParams {
     int chunks_per_img;      // oh*ow/32
     int total_chunks, chunks_per_split, splits;
     int RG, OPS, OPS_G;      // raw ring, operand ring (FAST), operand ring (GENERIC)
+    int OPS2;                // operand ring (FAST2: two bf16 A pieces per chunk), 0: none
     int lut;                 // codes: smem code table in use
     int fbox;                // fp32 source (plain input / exact tape) staged per stage by TMA
     int lut_floats;          // smem table size (floats)
+    int nolut;               // codes without the table (8-bit, wide channel blocks): decode inline
+    int intok;               // INT mode allowed (QTAPE_WG_INT, default on)
     int slot;                // raw ring slot stride: g tile + code box (bytes)
     int cb;                  // code box bytes per channel (16-byte multiple)
     int cbytes;              // code box bytes per stage (cb x channels)
@@ -128,9 +151,15 @@ __device__ __forceinline__ void generic_px(const WgParams &p, const uint8_t *cst
         const int bp = (cbox + iy * p.rb - wbase) * 8 + sx * bits;
         const uint32_t code =
             __funnelshift_r(cw[bp >> 5], cw[(bp >> 5) + 1], bp & 31) & ((1u << bits) - 1u);
-        const float2 e = *reinterpret_cast<const float2 *>(lut + 2 * code);
-        hh = e.x;
-        ll = e.y;
+        if (p.nolut) {   // the table entry, computed: relu(decode(code)) as (hi, lo)
+            float a = decode(code, __ldg(p.tape.step + c), __ldg(p.tape.offset + c), bits);
+            a = (a >= 0.f || isnan(a)) ? a : 0.f;
+            split_tf32(a, hh, ll);
+        } else {
+            const float2 e = *reinterpret_cast<const float2 *>(lut + 2 * code);
+            hh = e.x;
+            ll = e.y;
+        }
     } else if (p.fbox) {
         float a = *reinterpret_cast<const float *>(cst + cbox + iy * p.rb - wbase + sx * 4);
         if (!p.plain) a = (a >= 0.f || isnan(a)) ? a : 0.f;   // exact tape: ReLU
@@ -170,7 +199,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                          const __grid_constant__ CUtensorMap tmC, WgParams p) {
     constexpr int ROWS = 32 / OW;                           // image rows per 32-pixel chunk
     constexpr int G_BYTES = BN * 128;                       // raw g tile: BN rows x 32 px fp32
-    constexpr bool FAST_OK = (BITS == 4 || BITS == 2 || BITS == 1);
+    constexpr bool FAST_OK = (BITS == 4 || BITS == 2 || BITS == 1 || BITS == 8);
     constexpr int NT = TAP ? 3 : 1;                         // column taps stacked in N
     constexpr bool STACK = TAP ? (9 * BN <= 256) : (3 * BN <= 192);   // pieces stacked in N
     constexpr int FACC = STACK ? 3 * NT * BN : NT * BN;     // FAST accumulator columns per tile
@@ -248,16 +277,25 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     // the previous kernel, then wait for that kernel's results
     pdl_wait();
     pdl_trigger();
-    int fast = 0;
+    int fast = 0, fast2 = 0, intm = 0;
     if (warp != 0) {
         constexpr int kRest = kWgThreads - 32;     // warps 1..17
-        int narrow = 1;
+        int narrow = 1, inarrow = 1;
         const int nc = c_end - c_begin;
         if (FAST_OK && p.lut && threadIdx.x >= 64) {
             const int bits = p.tape.bits;
             for (int e = threadIdx.x - 64; e < nc; e += kWgThreads - 64) {
                 const int64_t off = p.tape.offset[c_begin + e];
                 const int64_t top = (1 << bits) - 1;            // m at the largest code
+                if (off > (2047 - top) / 2) inarrow = 0;        // INT: m < 2048, exact in TF32
+                if (BITS == 8) {
+                    // m = 2c + b up to 255 + 2 off: exact in bf16 for off <= 0
+                    // (decode bf16x2_relu_m8); off < -128 leaves every m < 0
+                    if (off > 0) narrow = 0;
+                    const int64_t b = 1 - (1 << bits) + 2 * max(off, (int64_t)-128);
+                    s_bc[e] = (uint32_t)(0x4300 + b) * 0x10001u;
+                    continue;
+                }
                 if (off > (127 - top) / 2) narrow = 0;          // m could reach 128
                 const int64_t b = 1 - (1 << bits) + 2 * max(off, (int64_t)-64);
                 s_bc[e] = (uint32_t)(0x4300 + max(b, (int64_t)-64)) * 0x10001u;
@@ -273,8 +311,31 @@ __global__ void __launch_bounds__(kWgThreads, 1)
             : "r"((uint32_t)narrow), "n"(kRest)
             : "memory");
         fast = (all != 0) && FAST_OK && p.lut;
+        if (!fast && FAST_OK && p.lut && p.intok && p.pre == 0 && !TAP) {
+            asm volatile(
+                "{\n\t.reg .pred p, q;\n\t"
+                "setp.ne.u32 q, %1, 0;\n\t"
+                "bar.red.and.pred p, 1, %2, q;\n\t"
+                "selp.u32 %0, 1, 0, p;\n\t}"
+                : "=r"(all)
+                : "r"((uint32_t)inarrow), "n"(kRest)
+                : "memory");
+            // m < 2048: FAST2 (two bf16 A pieces) when its ring fits TMEM,
+            // else INT (TF32 A)
+            fast2 = (all != 0) && p.OPS2 > 0;
+            intm = (all != 0) && !fast2;
+        }
+        // INT: s_bc holds b = 1 - 2^K + 2 off; FAST2: (max(b, -2048) + 2048) x 0x10001
+        if ((intm || fast2) && threadIdx.x >= 64) {
+            const int bits = p.tape.bits;
+            for (int e = threadIdx.x - 64; e < nc; e += kWgThreads - 64) {
+                const int64_t off = max(p.tape.offset[c_begin + e], (int64_t)-4096);
+                const int32_t b = (int32_t)(1 - (1 << bits) + 2 * off);
+                s_bc[e] = fast2 ? (uint32_t)(max(b, -2048) + 2048) * 0x10001u : (uint32_t)b;
+            }
+        }
         // the GENERIC table only when this CTA takes the GENERIC path
-        if (!fast && p.lut && threadIdx.x >= 64) {
+        if (!fast && !fast2 && !intm && p.lut && !p.nolut && threadIdx.x >= 64) {
             const int bits = p.tape.bits, ncode = 1 << bits;
             for (int e = threadIdx.x - 64; e < nc * ncode; e += kWgThreads - 64) {
                 const int cc = c_begin + e / ncode, code = e % ncode;
@@ -295,13 +356,14 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     }
     if (threadIdx.x == 0) WG_TRACE(1);
     if (threadIdx.x == 64 && tr_)   // an operand thread (warp 0 does not take part in the vote)
-        tr_[525] = fast;
-    const int ops = fast ? p.OPS : p.OPS_G;
+        tr_[525] = fast, tr_[526] = intm, tr_[527] = fast2;
+    const bool fastb = fast || fast2;                       // bf16 integer A, g pieces in smem
+    const int ops = fast ? p.OPS : fast2 ? p.OPS2 : p.OPS_G;
     const bool pre = p.pre != 0;                            // B pieces by TMA (STACK, !TAP)
-    const bool pieces = fast || pre;                        // three-piece accumulator groups
+    const bool pieces = fastb || pre;                       // three-piece accumulator groups
     const int OPB = pieces ? OPB_F : OPB_G;                 // operand stride per chunk
     const uint32_t acc_cols = (uint32_t)(p.mtg * (pieces ? FACC : GACC));
-    const uint32_t acols = fast ? 16u : (pre ? 48u : 64u);  // A columns per tile per stage
+    const uint32_t acols = fast ? 16u : fast2 ? 32u : (pre ? 48u : 64u);  // A columns per tile per stage
 
     if (warp == 0) {
         if (lane == 1 && pre) {  // ------------- TMA producer of the B pieces (pre-split)
@@ -377,20 +439,25 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                         const uint32_t a =
                             tmem + acc_cols + (((uint32_t)o * mtg + t) * SUB + sub) * acols;
                         const uint32_t first = (st | sub) ? 1u : 0u;   // 0: zero-init D
-                        if (fast) {
+                        if (fastb) {
+                            // FAST2: the second A piece (16 columns on) against the same B
                             constexpr uint32_t idesc = instr_desc(128, FACC, 1, 0, 0);
                             const uint32_t d = tmem + (uint32_t)(t * FACC);
 #pragma unroll
                             for (int j = 0; j < 2; ++j) {
-                                if (STACK) {
-                                    mma_bf16_ts(d, a + j * 8, dfast + off16 + j * 2, idesc,
-                                                (first | j) ? 1u : 0u);
-                                } else {
 #pragma unroll
-                                    for (int pc = 0; pc < 3; ++pc)
-                                        mma_bf16_ts(d, a + j * 8,
-                                                    dfast + off16 + ((pc * NT * BN * 64) >> 4) + j * 2,
-                                                    idesc, (first | j | pc) ? 1u : 0u);
+                                for (int ap = 0; ap < 2; ++ap) {
+                                    if (ap && !fast2) break;
+                                    if (STACK) {
+                                        mma_bf16_ts(d, a + 16 * ap + j * 8, dfast + off16 + j * 2, idesc,
+                                                    (first | j | ap) ? 1u : 0u);
+                                    } else {
+#pragma unroll
+                                        for (int pc = 0; pc < 3; ++pc)
+                                            mma_bf16_ts(d, a + 16 * ap + j * 8,
+                                                        dfast + off16 + ((pc * NT * BN * 64) >> 4) + j * 2,
+                                                        idesc, (first | j | pc | ap) ? 1u : 0u);
+                                    }
                                 }
                             }
                         } else if (!STACK && !TAP && pre) {
@@ -432,7 +499,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                                 const uint64_t dgl = dgh + ((NT * BN * 128) >> 4);
                                 mma_tf32_ts(d, a + j * 8, dgh, idesc, (first | j) ? 1u : 0u);
                                 mma_tf32_ts(d, a + j * 8, dgl, idesc, 1u);
-                                mma_tf32_ts(d, a + 32 + j * 8, dgh, idesc, 1u);
+                                if (!intm) mma_tf32_ts(d, a + 32 + j * 8, dgh, idesc, 1u);
                             }
                         }
                     }
@@ -471,7 +538,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
         // (coop): the TF32 A operand limits the ring to 1-2 stages, so all
         // four groups share every stage -- pixel quads and g items dealt
         // round-robin -- and meet at a named barrier before group 0 arrives.
-        const bool coop = !fast;
+        const bool coop = !fastb;
         // FAST: group g takes stages g, g + G, ... (G = active groups); with
         // an operand ring deeper than G (pre-split: A only in TMEM, up to 8)
         // it alternates between op stages g and g + G -- raw slots and op
@@ -567,7 +634,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                         }
                     }
                 }
-            } else if (fast) {
+            } else if (fastb) {
                 // g -> bf16 (hi, mid, lo), K-major SW64, 8-pixel groups
                 // permuted (pair word k = pixels k and k+4)
                 for (int q = tg; q < BN * 4; q += 128) {
@@ -620,16 +687,21 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 const uint32_t acol = acc_cols + (uint32_t)((o * p.mtg + t) * SUB + sub) * acols;
                 const int c = rc[t], u = ru[t], sh = rsh[t];
                 const int cbox = (c - c_begin) * p.cb;
-                if (FAST_OK && fast && BITS == 1) {
+                if (FAST_OK && fastb) {
+                    // FAST / FAST2 rows; the A piece count is a compile-time
+                    // branch so the FAST loops carry none of FAST2's decode
+                    auto rows = [&](auto two_c) {
+                    [[maybe_unused]] constexpr bool TWO = decltype(two_c)::value;
+                    if constexpr (BITS == 1) {
                     // 1-bit codes: a row of OW <= 32 px is one 8/16/32-bit field
                     // (bit x = pixel x).  Per 8-pixel group (byte b):
                     // z = (b & 0xF) | (b >> 4) << 16 puts pixel k at bit k and
                     // pixel k + 4 at bit 16 + k, so (z >> k) & 0x00010001 is A
                     // word k of the (k, k + 4) pairing -- then the same
                     // *2 + (0x4300 + b) and relu(x - 128) as the 4-bit path
-                    uint32_t av[16];
+                    uint32_t av[16], av2[16];
 #pragma unroll
-                    for (int x = 0; x < 16; ++x) av[x] = 0u;
+                    for (int x = 0; x < 16; ++x) av[x] = av2[x] = 0u;
                     if (rok[t]) {
                         const uint32_t bc = s_bc[c - c_begin];
 #pragma unroll
@@ -648,24 +720,85 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                                 const uint32_t z = (b8 & 0xFu) | ((b8 >> 4) << 16);
 #pragma unroll
                                 for (int k = 0; k < 4; ++k)
-                                    av[seg * (OW / 2) + 4 * gq + k] =
-                                        bf16x2_relu_sub128(((z >> k) & 0x00010001u) * 2u + bc);
+                                    fast_pair<BITS, TWO>((z >> k) & 0x00010001u, bc,
+                                                    av[seg * (OW / 2) + 4 * gq + k],
+                                                    av2[seg * (OW / 2) + 4 * gq + k]);
                             }
-                            if (sh < 0) av[seg * (OW / 2)] &= 0xFFFF0000u;          // x = 0 pads
-                            if (sh > 0) av[seg * (OW / 2) + OW / 2 - 1] &= 0x0000FFFFu;  // x = OW-1
+                            if (sh < 0)   // x = 0 pads
+                                av[seg * (OW / 2)] &= 0xFFFF0000u, av2[seg * (OW / 2)] &= TWO ? 0xFFFF0000u : 0u;
+                            if (sh > 0)   // x = OW-1
+                                av[seg * (OW / 2) + OW / 2 - 1] &= 0x0000FFFFu,
+                                    av2[seg * (OW / 2) + OW / 2 - 1] &= TWO ? 0x0000FFFFu : 0u;
                         }
                     }
                     tmem_st16(lane_base + acol, av);
-                } else if (FAST_OK && fast && BITS == 2) {
+                    if (TWO) tmem_st16(lane_base + acol + 16, av2);
+                    } else if constexpr (BITS == 8) {
+                    // 8-bit codes: a row is OW bytes (8 px: two words lo, hi).
+                    // A word k of a group pairs byte k of lo and of hi
+                    // (pixels k, k + 4), then *2 + (0x4300 + b) and the
+                    // 8-bit relu decode (m <= 255: exact in bf16)
+                    constexpr int NW = OW / 4;                 // 32-bit words per row
+                    uint32_t av[16], av2[16];
+#pragma unroll
+                    for (int x = 0; x < 16; ++x) av[x] = av2[x] = 0u;
+                    if (rok[t]) {
+                        const uint32_t bc = s_bc[c - c_begin];
+#pragma unroll
+                        for (int seg = 0; seg < ROWS; ++seg) {
+                            const int iy = y0 + seg + u - p.pad;
+                            if (iy < 0 || iy >= p.h) continue;
+                            const uint8_t *rowp = cst + cbox + iy * p.rb - wbase;
+                            uint32_t w[NW + 2];
+                            w[0] = 0u;
+                            w[NW + 1] = 0u;
+                            if constexpr (NW == 2) {
+                                const uint2 v2 = *reinterpret_cast<const uint2 *>(rowp);
+                                w[1] = v2.x; w[2] = v2.y;
+                            } else {
+#pragma unroll
+                                for (int q = 0; q < NW / 4; ++q) {
+                                    const uint4 v4 = reinterpret_cast<const uint4 *>(rowp)[q];
+                                    w[4 * q + 1] = v4.x; w[4 * q + 2] = v4.y;
+                                    w[4 * q + 3] = v4.z; w[4 * q + 4] = v4.w;
+                                }
+                            }
+                            uint32_t sw[NW];
+#pragma unroll
+                            for (int q = 0; q < NW; ++q)
+                                sw[q] = sh > 0   ? __funnelshift_r(w[q + 1], w[q + 2], 8)
+                                        : sh < 0 ? __funnelshift_l(w[q], w[q + 1], 8)
+                                                 : w[q + 1];
+#pragma unroll
+                            for (int gq = 0; gq < OW / 8; ++gq) {
+#pragma unroll
+                                for (int k = 0; k < 4; ++k) {
+                                    const uint32_t z =
+                                        __byte_perm(sw[2 * gq], sw[2 * gq + 1], k | (4u + k) << 8);
+                                    fast_pair<BITS, TWO>(z & 0x00FF00FFu, bc,
+                                                    av[seg * (OW / 2) + 4 * gq + k],
+                                                    av2[seg * (OW / 2) + 4 * gq + k]);
+                                }
+                            }
+                            if (sh < 0)   // x = 0 pads
+                                av[seg * (OW / 2)] &= 0xFFFF0000u, av2[seg * (OW / 2)] &= TWO ? 0xFFFF0000u : 0u;
+                            if (sh > 0)   // x = OW-1
+                                av[seg * (OW / 2) + OW / 2 - 1] &= 0x0000FFFFu,
+                                    av2[seg * (OW / 2) + OW / 2 - 1] &= TWO ? 0x0000FFFFu : 0u;
+                        }
+                    }
+                    tmem_st16(lane_base + acol, av);
+                    if (TWO) tmem_st16(lane_base + acol + 16, av2);
+                    } else if constexpr (BITS == 2) {
                     // 2-bit codes: a row is OW/4 bytes (8 px: one halfword).
                     // Per 8-pixel group (16 bits h): z = (h & 0xFF) | (h >> 8) << 16
                     // puts pixel k at bits 2k and pixel k + 4 at bits 16 + 2k,
                     // so (z >> 2k) & 0x00030003 is A word k of the group's
                     // (k, k + 4) pixel pairing -- then the same *2 + (0x4300 + b)
                     // and relu(x - 128) as the 4-bit path (m < 128, exact)
-                    uint32_t av[16];
+                    uint32_t av[16], av2[16];
 #pragma unroll
-                    for (int x = 0; x < 16; ++x) av[x] = 0u;
+                    for (int x = 0; x < 16; ++x) av[x] = av2[x] = 0u;
                     if (rok[t]) {
                         const uint32_t bc = s_bc[c - c_begin];
 #pragma unroll
@@ -705,19 +838,24 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                                 const uint32_t z = (hw[gq] & 0xFFu) | ((hw[gq] >> 8) << 16);
 #pragma unroll
                                 for (int k = 0; k < 4; ++k)
-                                    av[seg * (OW / 2) + 4 * gq + k] =
-                                        bf16x2_relu_sub128(((z >> (2 * k)) & 0x00030003u) * 2u + bc);
+                                    fast_pair<BITS, TWO>((z >> (2 * k)) & 0x00030003u, bc,
+                                                    av[seg * (OW / 2) + 4 * gq + k],
+                                                    av2[seg * (OW / 2) + 4 * gq + k]);
                             }
-                            if (sh < 0) av[seg * (OW / 2)] &= 0xFFFF0000u;          // x = 0 pads
-                            if (sh > 0) av[seg * (OW / 2) + OW / 2 - 1] &= 0x0000FFFFu;  // x = OW-1
+                            if (sh < 0)   // x = 0 pads
+                                av[seg * (OW / 2)] &= 0xFFFF0000u, av2[seg * (OW / 2)] &= TWO ? 0xFFFF0000u : 0u;
+                            if (sh > 0)   // x = OW-1
+                                av[seg * (OW / 2) + OW / 2 - 1] &= 0x0000FFFFu,
+                                    av2[seg * (OW / 2) + OW / 2 - 1] &= TWO ? 0x0000FFFFu : 0u;
                         }
                     }
                     tmem_st16(lane_base + acol, av);
-                } else if (FAST_OK && fast && BITS == 4) {
+                    if (TWO) tmem_st16(lane_base + acol + 16, av2);
+                    } else if constexpr (BITS == 4) {
                     constexpr int NW = OW / 8;                 // 32-bit words per row (4-bit)
-                    uint32_t av[16];
+                    uint32_t av[16], av2[16];
 #pragma unroll
-                    for (int x = 0; x < 16; ++x) av[x] = 0u;
+                    for (int x = 0; x < 16; ++x) av[x] = av2[x] = 0u;
                     if (rok[t]) {
                         const uint32_t bc = s_bc[c - c_begin];
 #pragma unroll
@@ -749,15 +887,24 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                                                              : w[q + 1];
 #pragma unroll
                                 for (int k = 0; k < 4; ++k)
-                                    av[seg * (OW / 2) + 4 * q + k] =
-                                        bf16x2_relu_sub128(((sw >> (4 * k)) & 0x000F000Fu) * 2u + bc);
+                                    fast_pair<BITS, TWO>((sw >> (4 * k)) & 0x000F000Fu, bc,
+                                                    av[seg * (OW / 2) + 4 * q + k],
+                                                    av2[seg * (OW / 2) + 4 * q + k]);
                             }
-                            if (sh < 0) av[seg * (OW / 2)] &= 0xFFFF0000u;          // x = 0 pads
-                            if (sh > 0) av[seg * (OW / 2) + OW / 2 - 1] &= 0x0000FFFFu;  // x = OW-1
+                            if (sh < 0)   // x = 0 pads
+                                av[seg * (OW / 2)] &= 0xFFFF0000u, av2[seg * (OW / 2)] &= TWO ? 0xFFFF0000u : 0u;
+                            if (sh > 0)   // x = OW-1
+                                av[seg * (OW / 2) + OW / 2 - 1] &= 0x0000FFFFu,
+                                    av2[seg * (OW / 2) + OW / 2 - 1] &= TWO ? 0x0000FFFFu : 0u;
                         }
                     }
                     if (tg == 0 && st < 64 && t == 0) WG_TRACE(3701 + 4 * st + 2 * sub);
                     tmem_st16(lane_base + acol, av);
+                    if (TWO) tmem_st16(lane_base + acol + 16, av2);
+                    }
+                    };
+                    if (fast2) rows(std::true_type{});
+                    else rows(std::false_type{});
                 } else if (FAST_OK && !TAP && pre) {
                     // GENERIC-PRE: the reference's fp32 relu(decode) (table hi +
                     // lo, exact) as three bf16 pieces in pair words (k, k + 4)
@@ -797,7 +944,24 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 #pragma unroll 1
                     for (int q4 = gsplit; q4 < 8; q4 += gstride) {
                         uint32_t h[4] = {0u, 0u, 0u, 0u}, l[4] = {0u, 0u, 0u, 0u};
-                        if (live) {
+                        if (live && intm) {
+                            // INT: relu(m) = max(2 code + b, 0) < 2048, exact in TF32
+                            // (no lo piece, no A_lo pass); step / 2 in the epilogue
+                            const int b = (int)s_bc[c - c_begin];
+                            const uint32_t *cw = reinterpret_cast<const uint32_t *>(cst);
+#pragma unroll
+                            for (int k = 0; k < 4; ++k) {
+                                const int i = 4 * q4 + k;
+                                const int seg = i / OW, x = i - seg * OW;
+                                const int iy = y0 + seg + u - p.pad, sx = x + sh;
+                                const int bp = (cbox + iy * p.rb - wbase) * 8 + sx * BITS;
+                                const uint32_t code = __funnelshift_r(cw[bp >> 5], cw[(bp >> 5) + 1],
+                                                                      bp & 31) & ((1u << BITS) - 1u);
+                                const bool in = iy >= 0 && iy < p.h && sx >= 0 && sx < OW;
+                                const int m = max(2 * (int)code + b, 0);
+                                h[k] = in ? __float_as_uint((float)m) : 0u;
+                            }
+                        } else if (live) {
 #pragma unroll
                             for (int k = 0; k < 4; ++k) {
                                 const int i = 4 * q4 + k;
@@ -807,7 +971,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                             }
                         }
                         tmem_st4(lane_base + acol + 4 * q4, h[0], h[1], h[2], h[3]);
-                        tmem_st4(lane_base + acol + 32 + 4 * q4, l[0], l[1], l[2], l[3]);
+                        if (!intm) tmem_st4(lane_base + acol + 32 + 4 * q4, l[0], l[1], l[2], l[3]);
                     }
                 }
             }
@@ -850,7 +1014,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
 #pragma unroll
         for (int t = 0; t < 2; ++t) {
             const int rl = t * 128 + 32 * quarter + lane;
-            scale[t] = (fast && rl < nrows) ? (float)(0.5 * p.tape.step[(row0 + rl) / kk]) : 1.f;
+            scale[t] = ((fastb || intm) && rl < nrows) ? (float)(0.5 * p.tape.step[(row0 + rl) / kk]) : 1.f;
         }
 #pragma unroll 1
         for (int it = grp; it < items; it += kWgGroups) {
@@ -880,7 +1044,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     float acc = __uint_as_float(r0[j]);
                     if (pieces && STACK)   // hi + (mid + lo): the small pieces first
                         acc = __fadd_rn(acc, __fadd_rn(__uint_as_float(r1[j]), __uint_as_float(r2[j])));
-                    const float val = fast ? __fmul_rn(acc, sc) : acc;
+                    const float val = (fastb || intm) ? __fmul_rn(acc, sc) : acc;
                     if (co0 + cb + j < p.co) dst[(int64_t)j * p.Rout] = val;
                 }
             }
@@ -904,9 +1068,10 @@ struct WgPlan {
     int bn = 0, mtg = 0, mgroups = 0, splits = 0, cps = 0, total = 0, rg = 0, smem = 0;
     int ops = 0, ops_g = 0;                               // FAST / GENERIC operand stages
     int nch = 0, rb = 0, cb = 0, cbytes = 0, slot = 0;    // code box (codes tapes)
-    int lut_floats = 0;
+    int lut_floats = 0, nolut = 0;                        // nolut: GENERIC decodes inline
     int opreg = 0;                                        // operand region bytes
     int pre = 0, bring = 0;                               // pieces by TMA; B ring depth
+    int ops2 = 0;                                         // FAST2 operand stages (0: INT)
     int tap = 0, rpc = 0;                                 // column taps in N; A rows per channel
     int fbox = 0;                                         // fp32 source boxed per stage
     int nblk = 1;                                         // output-channel blocks of BN

@@ -330,6 +330,15 @@ __device__ __forceinline__ uint32_t bf16x2_relu_sub128(uint32_t x) {
     asm("fma.rn.relu.bf16x2 %0, %1, %2, %3;" : "=r"(r) : "r"(x), "r"(0x3F803F80u), "r"(0xC300C300u));
     return r;
 }
+// 8-bit form: the pattern 0x4300 + m is 128 + m below m = 128 and 2m from
+// 128 to 256, so min(relu(x - 128), x / 2) is max(m, 0) for m in [-0x4300, 256]
+__device__ __forceinline__ uint32_t bf16x2_relu_m8(uint32_t x) {
+    uint32_t a, h, r;
+    asm("fma.rn.relu.bf16x2 %0, %1, %2, %3;" : "=r"(a) : "r"(x), "r"(0x3F803F80u), "r"(0xC300C300u));
+    asm("fma.rn.bf16x2 %0, %1, %2, %3;" : "=r"(h) : "r"(x), "r"(0x3F003F00u), "r"(0x80008000u));
+    asm("min.bf16x2 %0, %1, %2;" : "=r"(r) : "r"(a), "r"(h));
+    return r;
+}
 
 }  // namespace tc
 }  // namespace qt

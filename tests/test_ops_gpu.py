@@ -306,7 +306,7 @@ def test_transition_wgrad_from_codes(shape, bits):
                                    (2, 32, 28, 32, 3), (2, 64, 14, 64, 1), (2, 32, 7, 64, 1),
                                    (2, 16, 28, 32, 1), (2, 256, 14, 256, 1), (2, 128, 7, 256, 3),
                                    (1, 512, 7, 128, 1)])
-@pytest.mark.parametrize("bits", [1, 2, 4])
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
 def test_wgrad_from_codes_channel_blocks(shape, bits):
     """Weight gradient from a 2-/4-bit tape for outputs wider than one
     64-channel block (grid z) -- FAST and GENERIC CTAs, and on the segmented
@@ -315,10 +315,12 @@ def test_wgrad_from_codes_channel_blocks(shape, bits):
     from paper_1901_07988_b200 import codec
     n, ci, hw, co, k = shape
     torch.manual_seed(co + k + bits)
-    for regime in ("narrow", "wide", "mixed"):
+    for regime in ("narrow", "nonpos", "wide", "mixed"):
         x = torch.randn(n, ci, hw, hw, device="cuda")
         gamma, beta = torch.rand(ci, device="cuda") + 0.5, torch.randn(ci, device="cuda") * 0.1
-        if regime != "narrow":
+        if regime == "nonpos":   # offsets <= 0: the 8-bit FAST range too (K < 8: 0,
+            beta = -beta.abs() if bits == 8 else torch.zeros_like(beta)   # else all decode <= 0)
+        elif regime != "narrow":
             wide = torch.arange(ci, device="cuda") % (1 if regime == "wide" else 7) == 0
             gamma = torch.where(wide, torch.rand(ci, device="cuda") * 0.05 + 0.05, gamma)
             beta = torch.where(wide, torch.rand(ci, device="cuda") + 1.5, beta)
@@ -357,23 +359,27 @@ def test_segmented_3x3_wgrad_from_codes(shape, bits):
         assert err < CONV_TOL, (regime, err)
 
 
-@pytest.mark.parametrize("bits", [1, 2, 4])
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
 @pytest.mark.parametrize("shape", [(2, 16, 32, 16, 3), (2, 32, 16, 32, 3), (4, 64, 8, 64, 3),
                                    (2, 16, 32, 64, 1), (2, 64, 8, 256, 1), (4, 128, 16, 32, 1),
                                    (3, 64, 8, 16, 1)])
 def test_wgrad_from_codes_row_tiles(shape, bits):
-    """Row-tiled (8/16/32-px rows) weight gradient from 1-, 2- and 4-bit
+    """Row-tiled (8/16/32-px rows) weight gradient from 1-, 2-, 4- and 8-bit
     tapes: the FAST decode (integer bf16 operand; the 1- and 2-bit forms
-    regroup each byte's / halfword's pixel pairs) for narrow channels, GENERIC for wide ones,
-    mixed channels in one CTA -- against float64 on the dequantized tape."""
+    regroup each byte's / halfword's pixel pairs, the 8-bit form pairs bytes
+    of two words) for narrow channels (8-bit: offsets <= 0), GENERIC for wide
+    ones (8-bit over wide channel blocks: decoded inline, no table), mixed
+    channels in one CTA -- against float64 on the dequantized tape."""
     from paper_1901_07988_b200 import codec
     n, ci, hw, co, k = shape
     torch.manual_seed(bits * 100 + ci + k)
-    for regime in ("narrow", "wide", "mixed"):
+    for regime in ("narrow", "nonpos", "wide", "mixed"):
         x = torch.randn(n, ci, hw, hw, device="cuda")
         gamma = torch.rand(ci, device="cuda") + 0.5
         beta = torch.randn(ci, device="cuda") * 0.3
-        if regime != "narrow":
+        if regime == "nonpos":
+            beta = -beta.abs() if bits == 8 else torch.zeros_like(beta)
+        elif regime != "narrow":
             wide = torch.arange(ci, device="cuda") % (1 if regime == "wide" else 5) == 0
             gamma = torch.where(wide, torch.rand(ci, device="cuda") * 0.05 + 0.05, gamma)
             beta = torch.where(wide, torch.rand(ci, device="cuda") + 1.5, beta)
@@ -432,3 +438,61 @@ def test_two_cta_conv_form_bit_identical(tmp_path):
         w = torch.randn(co, ci, k, k, device="cuda", generator=g) * 0.1
         ref = torch.nn.functional.conv2d(x.double(), w.double(), padding=k // 2).cpu()
         assert ((y1.double() - ref).norm() / ref.norm()).item() < CONV_TOL
+
+
+
+_MODE_CODE = r'''
+import ctypes, sys, torch
+from paper_1901_07988_b200 import _native as N, codec, ops
+bits, regime, k, ci = int(sys.argv[1]), sys.argv[2], int(sys.argv[3]), int(sys.argv[4])
+n, hw, co = 4, 16, 64
+torch.manual_seed(bits * 10 + k)
+x = torch.randn(n, ci, hw, hw, device="cuda")
+gamma = torch.rand(ci, device="cuda") + 0.5
+if regime == "narrow":   # 8-bit FAST: offsets <= 0 (K < 8: zero, else every decode <= 0)
+    beta = -torch.rand(ci, device="cuda") * 0.3 if bits == 8 else torch.zeros(ci, device="cuda")
+else:   # offsets beta * 2^K / (6 gamma) in [130, 800] (past FAST, inside INT: m < 2048)
+    lo, hi = (130, 800) if regime == "wide" else (3000, 5000)   # "huge": past INT too
+    beta = (torch.rand(ci, device="cuda") * (hi - lo) + lo + 0.5) * 6 * gamma / 2 ** bits
+t = codec.quantize(x, gamma, beta, bits)
+act = codec.dequantize(t, relu=True)
+g = torch.randn(n, co, hw, hw, device="cuda")
+gw = torch.zeros(co, ci, k, k, device="cuda")
+fn = N.lib().qt_debug_wgrad_trace
+fn.argtypes = [ctypes.c_void_p, ctypes.c_int]
+buf = torch.zeros(4000, dtype=torch.int64, device="cuda")
+fn(buf.data_ptr(), 0)
+ops.conv2d_wgrad(g, (co, ci, k, k), 1, k // 2, gw, tape=t.as_native(), in_shape=(n, ci, hw, hw))
+torch.cuda.synchronize()
+fn(None, 0)
+ref = torch.nn.grad.conv2d_weight(act.double(), (co, ci, k, k), g.double(), padding=k // 2)
+err = ((gw.double() - ref).norm() / ref.norm()).item()
+print("MODE", int(buf[525].item()), int(buf[526].item()), int(buf[527].item()), "ERR", err)
+'''
+
+
+@pytest.mark.parametrize("bits", [1, 2, 4, 8])
+@pytest.mark.parametrize("k,ci", [(3, 64), (1, 128)])
+def test_wgrad_decode_mode_selected(bits, k, ci):
+    """Which operand decode a CTA takes, read from the kernel's debug
+    timeline (trace slots 525 FAST, 526 INT, 527 FAST2), and its accuracy:
+    FAST (one bf16 integer A piece) for narrow channels at every code width
+    (8-bit: offsets <= 0), FAST2 (two bf16 pieces of m < 2048) for wide ones,
+    INT (TF32 integer A, two passes) with QTAPE_WG_FAST2=0, the table GENERIC
+    past m = 2048 or with QTAPE_WG_INT=0 (8-bit over 128 channels: the
+    table decoded inline)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    cases = (("narrow", {}, "MODE 1 0 0"), ("wide", {}, "MODE 0 0 1"),
+             ("wide", {"QTAPE_WG_FAST2": "0"}, "MODE 0 1 0"), ("huge", {}, "MODE 0 0 0"),
+             ("wide", {"QTAPE_WG_INT": "0"}, "MODE 0 0 0"))
+    for regime, env, want in cases:
+        r = subprocess.run([sys.executable, "-c", _MODE_CODE, str(bits), regime, str(k), str(ci)],
+                           cwd=root, capture_output=True, text=True, timeout=300,
+                           env={**os.environ, **env})
+        assert r.returncode == 0, r.stderr[-2000:]
+        assert want in r.stdout, (bits, regime, env, r.stdout)
+        err = float(r.stdout.split("ERR")[1])
+        assert err < CONV_TOL, (bits, regime, env, err)
