@@ -200,6 +200,10 @@ __global__ void __launch_bounds__(kWgThreads, 1)
     constexpr int ROWS = 32 / OW;                           // image rows per 32-pixel chunk
     constexpr int G_BYTES = BN * 128;                       // raw g tile: BN rows x 32 px fp32
     constexpr bool FAST_OK = (BITS == 4 || BITS == 2 || BITS == 1 || BITS == 8);
+    // FAST2 is compiled for 8-bit codes only, where positive offsets are the
+    // common case; narrower codes reach m >= 128 only past offset ~56 and take
+    // INT there (the extra decode variant cost the FAST kernels ~3 %)
+    constexpr bool kFast2 = BITS == 8;
     constexpr int NT = TAP ? 3 : 1;                         // column taps stacked in N
     constexpr bool STACK = TAP ? (9 * BN <= 256) : (3 * BN <= 192);   // pieces stacked in N
     constexpr int FACC = STACK ? 3 * NT * BN : NT * BN;     // FAST accumulator columns per tile
@@ -322,7 +326,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                 : "memory");
             // m < 2048: FAST2 (two bf16 A pieces) when its ring fits TMEM,
             // else INT (TF32 A)
-            fast2 = (all != 0) && p.OPS2 > 0;
+            fast2 = (all != 0) && p.OPS2 > 0 && kFast2;
             intm = (all != 0) && !fast2;
         }
         // INT: s_bc holds b = 1 - 2^K + 2 off; FAST2: (max(b, -2048) + 2048) x 0x10001
@@ -447,7 +451,7 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                             for (int j = 0; j < 2; ++j) {
 #pragma unroll
                                 for (int ap = 0; ap < 2; ++ap) {
-                                    if (ap && !fast2) break;
+                                    if (ap && (!kFast2 || !fast2)) break;
                                     if (STACK) {
                                         mma_bf16_ts(d, a + 16 * ap + j * 8, dfast + off16 + j * 2, idesc,
                                                     (first | j | ap) ? 1u : 0u);
@@ -903,8 +907,12 @@ __global__ void __launch_bounds__(kWgThreads, 1)
                     if (TWO) tmem_st16(lane_base + acol + 16, av2);
                     }
                     };
-                    if (fast2) rows(std::true_type{});
-                    else rows(std::false_type{});
+                    if constexpr (kFast2) {
+                        if (fast2) rows(std::true_type{});
+                        else rows(std::false_type{});
+                    } else {
+                        rows(std::false_type{});
+                    }
                 } else if (FAST_OK && !TAP && pre) {
                     // GENERIC-PRE: the reference's fp32 relu(decode) (table hi +
                     // lo, exact) as three bf16 pieces in pair words (k, k + 4)

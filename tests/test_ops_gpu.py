@@ -477,15 +477,17 @@ def test_wgrad_decode_mode_selected(bits, k, ci):
     """Which operand decode a CTA takes, read from the kernel's debug
     timeline (trace slots 525 FAST, 526 INT, 527 FAST2), and its accuracy:
     FAST (one bf16 integer A piece) for narrow channels at every code width
-    (8-bit: offsets <= 0), FAST2 (two bf16 pieces of m < 2048) for wide ones,
-    INT (TF32 integer A, two passes) with QTAPE_WG_FAST2=0, the table GENERIC
+    (8-bit: offsets <= 0), for wide ones FAST2 (two bf16 pieces of m < 2048)
+    at 8 bits and INT (TF32 integer A, two passes) below 8 bits or with
+    QTAPE_WG_FAST2=0, the table GENERIC
     past m = 2048 or with QTAPE_WG_INT=0 (8-bit over 128 channels: the
     table decoded inline)."""
     import os
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    cases = (("narrow", {}, "MODE 1 0 0"), ("wide", {}, "MODE 0 0 1"),
+    wide = "MODE 0 0 1" if bits == 8 else "MODE 0 1 0"   # FAST2 is compiled for 8-bit only
+    cases = (("narrow", {}, "MODE 1 0 0"), ("wide", {}, wide),
              ("wide", {"QTAPE_WG_FAST2": "0"}, "MODE 0 1 0"), ("huge", {}, "MODE 0 0 0"),
              ("wide", {"QTAPE_WG_INT": "0"}, "MODE 0 0 0"))
     for regime, env, want in cases:
