@@ -60,8 +60,11 @@ static inline int64_t qt_env_i64(const char *name, int64_t dflt) {
     const char *e = getenv(name);
     return (e && *e) ? (int64_t)atoll(e) : dflt;
 }
+// elements per reduction block before the >= 2 blocks / SM cap (n*c / DIV)
+// decides: measured 8192 -> 32768 (plateau to 2^20) C2 8.55 -> 8.42 ms/step,
+// C3 50.9 -> 50.4, C4 43.5 -> 42.8 (BN statistics and backward reduce)
 static inline int64_t qt_red_target() {
-    static int64_t v = qt_env_i64("QTAPE_RED_TGT", 8192);
+    static int64_t v = qt_env_i64("QTAPE_RED_TGT", 32768);
     return v;
 }
 static inline int64_t qt_red_div() {
