@@ -50,6 +50,10 @@ def _c4_width():
 
 CASES = {
     "C2-resnet164-b4-k4": (E.resnet164_spec, 4, 4, 2e-4),
+    # 1- and 8-bit tapes (FAST 1-bit / 8-bit decodes); "-bn": gamma, beta drawn
+    # off their init so 8-bit offsets take both signs (FAST and FAST2 CTAs)
+    "C2-resnet164-b4-k1": (E.resnet164_spec, 4, 1, 2e-4),
+    "C2-resnet164-b4-k8-bn": (E.resnet164_spec, 4, 8, 2e-4),
     "C3-resnet1001-b2-k2": (E.resnet1001_spec, 2, 2, 2e-4),
     "C3-resnet1001-b2-k4": (E.resnet1001_spec, 2, 4, 2e-4),
     "C4w-bottleneck1121-224-b2-k4": (_c4_width, 2, 4, 1e-4),
@@ -144,6 +148,38 @@ def _force_oracle_tapes(tapes, rtapes):
         t.sigma2.copy_(torch.from_numpy(np.ascontiguousarray(r["sigma2"], dtype=np.float64)))
 
 
+def _bn_draws(ref, name):
+    """(gamma, beta) per BN layer for the "-bn" cases: gamma ~ U(0.7, 1.3),
+    beta ~ U(-0.2, 0.2) (8-bit offsets floor(beta * 2^8 / (6 gamma)) of
+    either sign, up to ~12); None elsewhere."""
+    if not name.endswith("-bn"):
+        return None
+    rng = np.random.default_rng(11)
+    out = []
+    for p in ref:
+        if p["gamma"] is None:
+            out.append(None)
+            continue
+        c = len(p["gamma"])
+        out.append((rng.uniform(0.7, 1.3, c).astype(p["gamma"].dtype),
+                    rng.uniform(-0.2, 0.2, c).astype(p["beta"].dtype)))
+    return out
+
+
+def _set_bn(draws, oracle_params=None, device_params=None):
+    if draws is None:
+        return
+    for j, d in enumerate(draws):
+        if d is None:
+            continue
+        if oracle_params is not None:
+            oracle_params[j]["gamma"][...] = d[0]
+            oracle_params[j]["beta"][...] = d[1]
+        if device_params is not None:
+            device_params[j].gamma.copy_(torch.from_numpy(d[0]))
+            device_params[j].beta.copy_(torch.from_numpy(d[1]))
+
+
 @pytest.mark.parametrize("name", list(CASES))
 def test_headline_network_step(name):
     build, n, bits, wd = CASES[name]
@@ -156,6 +192,8 @@ def test_headline_network_step(name):
 
     # ---- oracle: one step (forward keeps A2 / layer inputs for the analysis)
     ref = O.init_params(sj, 0)
+    draws = _bn_draws(ref, name)
+    _set_bn(draws, oracle_params=ref)
     rlog, rtapes = O.net_fwd(sj, ref, x, "approx", bits, keep_a2=True)
     rloss, rg = O.softmax_xent(rlog, y)
     O.net_bwd(sj, ref, rtapes, rg)
@@ -168,6 +206,7 @@ def test_headline_network_step(name):
     xd = dev(x)
     params = P.init_params(spec, 0)
     fresh = O.init_params(sj, 0)
+    _set_bn(draws, oracle_params=fresh, device_params=params)
     rows, stat = [], {"flips": 0, "local_max": 0.0}
 
     def check(j, xin, yout, res, t):
@@ -217,9 +256,11 @@ def test_headline_network_step(name):
     # every parameter gradient is within drift_tol(depth) of the
     # oracle's backward pass
     params = P.init_params(spec, 0)
+    _set_bn(draws, device_params=params)
     _, tapes = E.network_forward(spec, params, xd, mode="approx", bits=bits)
     _force_oracle_tapes(tapes, rtapes)
     fresh_b = O.init_params(sj, 0)
+    _set_bn(draws, oracle_params=fresh_b)
     shapes = spec.layer_shapes(n)
     bstat = {"local_max": 0.0}
 
