@@ -470,8 +470,10 @@ def main():
     if group is not None:
         D.broadcast_(tr.params.values, 0)
     rng = np.random.default_rng(rank)
-    x_host = rng.standard_normal((n,) + tuple(spec.input_shape)).astype(np.float32)
-    y_host = rng.integers(0, spec.num_classes, n).astype(np.int64)
+    # the host batch lives in pinned memory (the e2e contract's source); the
+    # Trainer copies it to the device directly, no staging memcpy
+    x_host = torch.from_numpy(rng.standard_normal((n,) + tuple(spec.input_shape)).astype(np.float32)).pin_memory()
+    y_host = torch.from_numpy(rng.integers(0, spec.num_classes, n).astype(np.int64)).pin_memory()
     tr.load_batch(x_host, y_host)
     tr.capture()
 

@@ -174,3 +174,23 @@ def test_evaluate_after_train_matches_fresh_params():
     lb, _ = E.network_forward(spec, fresh, x[:32].contiguous(), training=False)
     assert torch.equal(la, lb)
     assert P.evaluate(spec, res.params, ds) == P.evaluate(spec, fresh, ds)
+
+
+def test_trainer_step_from_pinned_host_tensors():
+    """Trainer.step straight from pinned host tensors (no staging copy; the
+    bench's e2e source) == the same steps from numpy arrays, bit for bit."""
+    spec = E.make_residual_spec()
+    rng = np.random.default_rng(3)
+    x = rng.standard_normal((8, 3, 32, 32)).astype(np.float32)
+    y = rng.integers(0, 10, 8).astype(np.int64)
+    losses = []
+    for src in ("numpy", "pinned"):
+        tr = P.Trainer(spec, 8, mode="approx", bits=4, lr=0.1)
+        tr.capture()
+        if src == "numpy":
+            xs, ys = x, y
+        else:
+            xs, ys = torch.from_numpy(x).pin_memory(), torch.from_numpy(y).pin_memory()
+        losses.append([tr.step(xs, ys) for _ in range(3)])
+    assert losses[0] == losses[1], losses
+
