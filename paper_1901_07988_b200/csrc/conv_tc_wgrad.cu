@@ -375,6 +375,33 @@ static bool wg_direct_pre(const ConvGeo &g, int bits) {
 
 static int64_t wg_pieces_bytes(const ConvGeo &g) { return 6 * g.n * g.co * g.oh * g.ow; }
 
+// 1-bit tapes whose planes are not 16-byte multiples (8x8: 8 bytes) cannot
+// be boxed by TMA, but their 2-bit widening can: code c stays c and the
+// offset becomes offset + 1, so m = 2c + 1 - 2^K + 2 offset and the fp64
+// decode (c + 0.5 - 2^(K-1)) + offset are unchanged (codec.py:146-156).
+static bool wg_widen1(const ConvGeo &g0, int bits) {
+    const ConvGeo g = wg_flat_shape(g0) ? wg_flat_geo(g0) : g0;
+    return bits == 1 && !wg_plan(g, 1).ok && wg_plan(g, 2).ok && g.n * g.ci * g.h * g.w / 16 < (1ll << 31);
+}
+static int64_t wg_widen1_bytes(const ConvGeo &g) {   // 2-bit codes + offset'
+    return (g.n * g.ci * g.h * g.w / 4 + 255) / 256 * 256 + (g.ci * 8 + 255) / 256 * 256;
+}
+
+__global__ void widen_1to2_kernel(const uint16_t *codes1, uint32_t *codes2, uint32_t words,
+                                  const int64_t *offset, int64_t *offset2, uint32_t c) {
+    pdl_enter();
+    const uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    if (tid < c) offset2[tid] = offset[tid] + 1;
+    for (uint32_t o = tid; o < words; o += gridDim.x * blockDim.x) {
+        uint32_t x = __ldg(codes1 + o);       // 16 one-bit codes -> 16 two-bit codes
+        x = (x | (x << 8)) & 0x00FF00FFu;
+        x = (x | (x << 4)) & 0x0F0F0F0Fu;
+        x = (x | (x << 2)) & 0x33333333u;
+        x = (x | (x << 1)) & 0x55555555u;
+        codes2[o] = x;
+    }
+}
+
 int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g) {
     if (wg_flat_shape(g)) return qt_tc_wgrad_workspace(wg_flat_geo(g));
     if (wg_s2d_shape(g, 8)) {   // the 2x2/s2 rearranged-codes path (widest code width)
@@ -383,6 +410,7 @@ int64_t qt_tc_wgrad_workspace(const qt::ConvGeo &g) {
     }
     int64_t b = wg_partial_bytes(g);
     if (wg_direct_pre(g, 4) || wg_direct_pre(g, 2)) b = (b + 255) / 256 * 256 + wg_pieces_bytes(g);
+    if (wg_widen1(g, 1)) b = std::max(b, (wg_partial_bytes(g) + 255) / 256 * 256 + wg_widen1_bytes(g));
     return b;
 }
 
@@ -558,6 +586,23 @@ int qt_tc_conv_wgrad(const float *gr, qt_tape_t act, const float *x_plain, float
         if (rc) return rc;
         rc = wgrad_tc(nullptr, pieces, act, nullptr, grad_w, g, ws, st);
         if (rc != QT_EUNSUPPORTED) return rc;
+    }
+    if (!x_plain && !act.a2 && act.codes && ws && wg_widen1(g0, act.bits) &&
+        ((g.n * g.ci * g.h * g.w) & 15) == 0 && ((uintptr_t)act.codes & 1) == 0) {
+        char *base = (char *)ws + (wg_partial_bytes(g) + 255) / 256 * 256;
+        uint32_t *codes2 = (uint32_t *)base;
+        int64_t *offset2 = (int64_t *)(base + (g.n * g.ci * g.h * g.w / 4 + 255) / 256 * 256);
+        const uint32_t words = (uint32_t)(g.n * g.ci * g.h * g.w / 16);
+        const uint32_t need = std::max(words, (uint32_t)g.ci);
+        const unsigned blocks = (unsigned)std::min<int64_t>(qt_cdiv(need, 256), qt_sm_count() * 8);
+        launch_pdl(widen_1to2_kernel, blocks, 256, 0, st, (const uint16_t *)act.codes, codes2, words,
+                   act.offset, offset2, (uint32_t)g.ci);
+        QT_CHECK_LAUNCH();
+        qt_tape_t t2 = act;
+        t2.codes = (const uint8_t *)codes2;
+        t2.offset = offset2;
+        t2.bits = 2;
+        return wgrad_tc(gr, nullptr, t2, nullptr, grad_w, g0, ws, st);
     }
     return wgrad_tc(gr, nullptr, act, x_plain, grad_w, g0, ws, st);
 }
